@@ -1,0 +1,329 @@
+/*
+ * recon_b200.h — C-ABI of the B200-native atom-reconfiguration core.
+ *
+ * This is the drop-in boundary between the reference's C++ API
+ * (the headers under /root/reference/proj/include/recon, unchanged) and the sm_100a
+ * kernels in paper_2504_06182_b200/csrc.  Every entry point takes plain
+ * pointers and sizes; no C++ or torch types cross it.  The reference-side
+ * binding (the C++ shim that re-implements the reference's free functions on
+ * top of these calls) is paper_2504_06182_b200/shim/recon_shim.cpp and is
+ * described in INTEGRATION.md.
+ *
+ * Which reference interface each entry point replaces:
+ *
+ *   recon_redrec_solve         Solution red_rec(const Problem&, std::vector<RedRecEvent>*)
+ *                                  reference proj/include/recon/redrec.hpp:67-68,
+ *                                  proj/src/redrec.cpp:205-232
+ *   recon_bird_solve           Solution bird(const Problem&, std::vector<int>*)
+ *                                  bird.hpp:40-41, bird.cpp:107-123
+ *   recon_occupancy_dag        MoveDag occupancy_dag(const std::vector<Path>&)
+ *                                  virtual_line.hpp:104, virtual_line.cpp:241-268
+ *   recon_assign_1d            Matching1D assign_1d(int, std::vector<int>, std::vector<int>)
+ *                                  exact1d.hpp:21, exact1d.cpp:342-372
+ *   recon_assign_1d_generalized Matching1D assign_1d_generalized(const Generalized1DInstance&)
+ *                                  exact1d.hpp:39, exact1d.cpp:374-407
+ *   recon_solve_1d             Solution solve_1d(int, const std::vector<int>&, const std::vector<int>&)
+ *                                  exact1d.hpp:82, exact1d.cpp:564-572
+ *   recon_batch_moves          BatchSchedule batch_moves(const Problem&, const Solution&, const BatchOptions&)
+ *                                  batching.hpp:58-59, batching.cpp:28-159
+ *
+ * plus batched device-resident variants (recon_*_batch) that take `count`
+ * independent instances already in HBM and write per-instance outputs at a
+ * fixed stride, and host-buffer batched variants (recon_*_batch_host) that
+ * include the host<->device copies.
+ *
+ * Occupancy layout ("occ bits"): column-major bit planes.  A W x H grid uses
+ * words_per_column = (H + 63) / 64 uint64 words per column; the token on
+ * vertex (x, y) (y counted from the bottom row, vertex id x*H + y, reference
+ * geometry.hpp:89-92) is bit (y % 64) of word [x * words_per_column + y / 64].
+ * A chain of n vertices is the W = n, H = 1 case written densely: bit v of
+ * word v / 64 (words_per_chain = (n + 63) / 64).
+ *
+ * Errors: every call returns a recon_status that maps 1:1 onto the reference
+ * exception types (geometry.hpp:18-30 plus std::logic_error from
+ * redrec.cpp:82-84); *detail selects the exact reference message, available
+ * from recon_detail_message().  Per-instance statuses of batched calls use the
+ * same codes.
+ *
+ * Threading: no hidden global mutable state.  A recon_ctx owns a CUDA stream
+ * and a device workspace; calls on distinct contexts may run concurrently.
+ * Passing ctx == NULL uses a context private to the calling host thread.
+ */
+#ifndef RECON_B200_H
+#define RECON_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RECON_ABI_VERSION 1
+
+typedef enum recon_status {
+    RECON_OK = 0,
+    RECON_ERR_INPUT = 1,      /* recon::InputError */
+    RECON_ERR_INFEASIBLE = 2, /* recon::InfeasibleError */
+    RECON_ERR_COLLISION = 3,  /* recon::CollisionError */
+    RECON_ERR_LOGIC = 4,      /* std::logic_error */
+    RECON_ERR_CAPACITY = 5,   /* a caller buffer is too small; the *_count out-param holds the need */
+    RECON_ERR_CUDA = 6,       /* CUDA runtime failure (no device, launch failure, ...) */
+    RECON_ERR_ARGUMENT = 7    /* null pointer / nonsensical size passed to the C-ABI */
+} recon_status;
+
+/* Exact reference messages (file:line of the throw in the reference). */
+typedef enum recon_detail {
+    RECON_D_NONE = 0,
+    RECON_D_FEWER_SOURCES = 1,         /* "fewer sources than targets (|S| < |T|)" problem.hpp:115, exact1d.cpp:311 */
+    RECON_D_BAND_NOT_CENTERED = 2,     /* "targets must form a centered full-width band" virtual_line.cpp:32-45 */
+    RECON_D_BAND_HEIGHT = 3,           /* "target band height must be in (0, H)" virtual_line.cpp:48-49 */
+    RECON_D_BAND_EMPTY = 4,            /* "target band is empty" virtual_line.cpp:25 */
+    RECON_D_NO_DEFICIT = 5,            /* "select_best_pair: no deficit column remains" redrec.cpp:82 */
+    RECON_D_NO_DONOR = 6,              /* "select_best_pair: deficit column with no admissible donor" redrec.cpp:83-84 */
+    RECON_D_BATCH_NO_PROGRESS = 7,     /* "batching made no progress (blocked dependency structure)" batching.cpp:127-128 */
+    RECON_D_BATCH_CYCLIC = 8,          /* "batching requires an acyclic dependency dag" batching.cpp:34 */
+    RECON_D_CHAIN_LENGTH = 9,          /* "chain length must be positive" exact1d.cpp:300 */
+    RECON_D_SOURCE_OOB = 10,           /* "source vertex out of bounds" exact1d.cpp:303-304 */
+    RECON_D_SOURCE_ORDER = 11,         /* "source vertices must be strictly increasing" exact1d.cpp:305-306 */
+    RECON_D_TARGET_OOB = 12,           /* "target vertex out of bounds" */
+    RECON_D_TARGET_ORDER = 13,         /* "target vertices must be strictly increasing" */
+    RECON_D_GEN_MULTIPLICITY = 14,     /* "source multiplicity must be at least 1" exact1d.cpp:379 */
+    RECON_D_GEN_MIN_USE = 15,          /* "source min_use outside [0, multiplicity]" exact1d.cpp:380-381 */
+    RECON_D_GEN_SOURCE_ORDER = 16,     /* "source positions must be strictly increasing" exact1d.cpp:382-383 */
+    RECON_D_GEN_TARGET_ORDER = 17,     /* "target positions must be strictly increasing" exact1d.cpp:389 */
+    RECON_D_GEN_SUPPLY = 18,           /* "insufficient tokens for targets" exact1d.cpp:391 */
+    RECON_D_GEN_MANDATORY = 19,        /* "mandatory draws exceed target count" exact1d.cpp:392 */
+    RECON_D_GEN_NO_ASSIGNMENT = 20,    /* "no assignment satisfies the usage bounds" exact1d.cpp:395 */
+    RECON_D_DAG_EDGE_RANGE = 21,       /* "dag edge endpoint out of range" path_system.cpp:12 */
+    RECON_D_GRID_DIMENSIONS = 22,      /* "grid dimensions must be positive" geometry.hpp */
+    RECON_D_INFEASIBLE_SUPPLY = 23,    /* "fewer sources than targets" exact1d.cpp:70 (certifier) */
+    RECON_D_CUDA = 24                  /* CUDA runtime failure; see recon_last_cuda_error() */
+} recon_detail;
+
+const char *recon_detail_message(int32_t detail);
+const char *recon_last_cuda_error(void);
+int32_t recon_abi_version(void);
+
+/* ------------------------------------------------------------------------- */
+/* Contexts                                                                   */
+/* ------------------------------------------------------------------------- */
+
+typedef struct recon_ctx recon_ctx;
+
+/* Creates a context bound to CUDA device `device` with its own stream. */
+recon_status recon_ctx_create(int32_t device, recon_ctx **out);
+void recon_ctx_destroy(recon_ctx *ctx);
+/* The context's cudaStream_t (as void*). */
+void *recon_ctx_stream(recon_ctx *ctx);
+/* Number of kernel launches this context has issued (for bench accounting). */
+int64_t recon_ctx_launch_count(recon_ctx *ctx);
+
+/* ------------------------------------------------------------------------- */
+/* Grid solvers (red-rec, bird): single instance, host buffers                */
+/* ------------------------------------------------------------------------- */
+
+/*
+ * Paths come out in the reference's canonical order (the path order of
+ * Solution::path_system, which is also the schedule order: red_rec/bird use
+ * the identity path order, virtual_line.cpp:270-277).  Each path is a
+ * one-bend staircase fully determined by (src, dst): horizontal along the
+ * source row to the destination column, then vertical (virtual_line.cpp:150-173).
+ * Every grid path has length > 0.
+ *
+ * `path_capacity` >= width * h_prime always suffices.
+ * `events`: red-rec writes 4 int32 per event {event_id, column, donor,
+ * mark_destination} (redrec.hpp:56-65); bird writes 1 int32 per event, the
+ * filled column (the solved_order of bird.hpp:41).  Both emit exactly
+ * `width` events; capacity counts int32 elements.  May be NULL.
+ * `dag_*`: optional occupancy DAG (virtual_line.cpp:241-268), edges sorted by
+ * (src, dst); pass dag_src == NULL to skip.  On RECON_ERR_CAPACITY the
+ * required edge count is in dag_count.
+ */
+typedef struct recon_grid_solution {
+    int32_t *path_src;
+    int32_t *path_dst;
+    int32_t *path_event; /* may be NULL */
+    int64_t path_capacity;
+    int64_t path_count;           /* out */
+    int64_t displaced_tokens;     /* out: SolutionStats::displaced_tokens */
+    int64_t total_displacement;   /* out: SolutionStats::total_displacement */
+    int32_t *events;              /* may be NULL */
+    int32_t event_capacity;
+    int32_t event_count;          /* out (number of events, not int32s) */
+    int32_t *dag_src;             /* may be NULL */
+    int32_t *dag_dst;
+    int64_t dag_capacity;
+    int64_t dag_count;            /* out */
+} recon_grid_solution;
+
+recon_status recon_redrec_solve(recon_ctx *ctx, const uint64_t *occ, int32_t width,
+                                int32_t height, int32_t h_prime, recon_grid_solution *out,
+                                int32_t *detail);
+recon_status recon_bird_solve(recon_ctx *ctx, const uint64_t *occ, int32_t width,
+                              int32_t height, int32_t h_prime, recon_grid_solution *out,
+                              int32_t *detail);
+
+/* occupancy_dag over an explicit path list given as (src, dst) one-bend paths
+ * on a width x height grid.  Edges sorted by (src, dst). */
+recon_status recon_occupancy_dag(recon_ctx *ctx, int32_t width, int32_t height,
+                                 const int32_t *path_src, const int32_t *path_dst,
+                                 int64_t path_count, int32_t *dag_src, int32_t *dag_dst,
+                                 int64_t dag_capacity, int64_t *dag_count, int32_t *detail);
+
+/* ------------------------------------------------------------------------- */
+/* Grid solvers: batched, device-resident                                     */
+/* ------------------------------------------------------------------------- */
+
+/*
+ * `count` independent instances of one (width, height, h_prime) shape.  All
+ * pointers are device pointers.  Instance i reads occ + i*width*wpc and writes
+ * its paths at [i * path_stride, i * path_stride + path_count[i]) with
+ * path_stride = width * h_prime.
+ */
+typedef struct recon_grid_batch {
+    const uint64_t *occ;
+    int32_t count;
+    int32_t width;
+    int32_t height;
+    int32_t h_prime;
+    int32_t *path_src;           /* [count * width * h_prime] */
+    int32_t *path_dst;           /* [count * width * h_prime] */
+    int32_t *path_event;         /* may be NULL */
+    int32_t *path_count;         /* [count] */
+    int64_t *total_displacement; /* [count] */
+    int32_t *status;             /* [count] recon_status */
+    int32_t *detail;             /* [count] recon_detail */
+    int32_t *events;             /* may be NULL: red-rec [count*width*4], bird [count*width] */
+} recon_grid_batch;
+
+recon_status recon_redrec_solve_batch(recon_ctx *ctx, const recon_grid_batch *batch);
+recon_status recon_bird_solve_batch(recon_ctx *ctx, const recon_grid_batch *batch);
+
+/* Same, but every pointer in `batch` is HOST memory (pinned or pageable): the
+ * call copies the inputs in, solves, and copies the outputs back. */
+recon_status recon_redrec_solve_batch_host(recon_ctx *ctx, const recon_grid_batch *batch);
+recon_status recon_bird_solve_batch_host(recon_ctx *ctx, const recon_grid_batch *batch);
+
+/* ------------------------------------------------------------------------- */
+/* Exact 1D                                                                   */
+/* ------------------------------------------------------------------------- */
+
+/*
+ * assign_1d: S and T need not be sorted (the reference sorts them,
+ * exact1d.cpp:343-344).  Outputs: weight; pairs (src, dst) sorted by target,
+ * exactly nt of them; use_count[ns] indexed by the SORTED S.
+ */
+recon_status recon_assign_1d(recon_ctx *ctx, int32_t n, const int32_t *S, int32_t ns,
+                             const int32_t *T, int32_t nt, int64_t *weight, int64_t *pair_src,
+                             int64_t *pair_dst, int32_t *use_count, int32_t *detail);
+
+/* assign_1d_generalized: sources as parallel arrays (pos strictly increasing),
+ * targets strictly increasing; pairs [nt], use_count [nsrc]. */
+recon_status recon_assign_1d_generalized(recon_ctx *ctx, int32_t nsrc, const int64_t *pos,
+                                         const int32_t *multiplicity, const int32_t *min_use,
+                                         int32_t nt, const int64_t *targets, int64_t *weight,
+                                         int64_t *pair_src, int64_t *pair_dst,
+                                         int32_t *use_count, int32_t *detail);
+
+/*
+ * solve_1d: paths in the reference's path order (the order of
+ * paths_from_matching after resolve_nesting, exact1d.cpp:564-572), i.e. one
+ * straight path per target including zero-length ones; path_order is
+ * order_moves_1d's execution order (exact1d.cpp:517-528); the DAG is the
+ * span-overlap edge list in the reference's emission order
+ * (exact1d.cpp:529-560).  dag_src == NULL skips the DAG; on
+ * RECON_ERR_CAPACITY dag_count holds the need.
+ */
+recon_status recon_solve_1d(recon_ctx *ctx, int32_t n, const int32_t *S, int32_t ns,
+                            const int32_t *T, int32_t nt, int32_t *path_src, int32_t *path_dst,
+                            int32_t *path_order, int32_t *dag_src, int32_t *dag_dst,
+                            int64_t dag_capacity, int64_t *dag_count,
+                            int64_t *total_displacement, int32_t *displaced, int32_t *detail);
+
+/*
+ * Batched chains, device-resident: `count` chains of length n, sources given
+ * as dense bits (words_per_chain = (n+63)/64 per chain), targets the
+ * contiguous band [t_lo, t_hi] shared by every chain.  Instance i writes its
+ * nt = t_hi - t_lo + 1 paths at [i*nt, (i+1)*nt) in solve_1d path order
+ * (target ascending); its DAG stays implicit (span overlap, exact1d.cpp:529-560).
+ */
+typedef struct recon_chain_batch {
+    const uint64_t *occ;
+    int32_t count;
+    int32_t n;
+    int32_t t_lo;
+    int32_t t_hi;
+    int32_t *path_src;           /* [count * nt] */
+    int32_t *path_dst;           /* [count * nt] */
+    int64_t *total_displacement; /* [count] */
+    int32_t *displaced;          /* [count] */
+    int32_t *status;             /* [count] */
+    int32_t *detail;             /* [count] */
+} recon_chain_batch;
+
+recon_status recon_solve_1d_batch(recon_ctx *ctx, const recon_chain_batch *batch);
+recon_status recon_solve_1d_batch_host(recon_ctx *ctx, const recon_chain_batch *batch);
+
+/* ------------------------------------------------------------------------- */
+/* Batching                                                                   */
+/* ------------------------------------------------------------------------- */
+
+typedef enum recon_preset {
+    RECON_PRESET_NONE = 0,             /* ConstraintPreset::none */
+    RECON_PRESET_COLUMN_DIRECTION = 1  /* ConstraintPreset::column_direction */
+} recon_preset;
+
+/*
+ * batch_moves over an explicit solution: initial occupancy (problem.sources)
+ * as occ bits, paths as a CSR vertex list (path_offsets[P+1], int64), DAG
+ * edges.  Output: move_batch[path_offsets[P] - P] — for path p, its k-th move
+ * (vertices[k] -> vertices[k+1]) lands at index path_offsets[p] - p + k and
+ * receives its batch number.  Batch b holds the moves tagged b in ascending
+ * path id (batching.cpp:107-125); axis/dir tags follow from the batch's first
+ * move when preset != none (batching.cpp:150-155).
+ */
+recon_status recon_batch_moves(recon_ctx *ctx, int32_t width, int32_t height,
+                               const uint64_t *occ, int32_t path_count,
+                               const int64_t *path_offsets, const int32_t *path_vertices,
+                               int64_t edge_count, const int32_t *edge_src,
+                               const int32_t *edge_dst, int32_t preset, int32_t edge_level,
+                               int32_t *move_batch, int64_t *batch_count, int32_t *detail);
+
+/*
+ * Fused grid pipeline, device-resident: solve (red-rec or bird) + occupancy
+ * DAG + batching for `count` instances.  Outputs of the solve as in
+ * recon_grid_batch; move_batch holds, per instance, one batch index per
+ * elementary move in canonical schedule order (path-major), at stride
+ * move_stride; batch_count[i] = number of batches.
+ */
+typedef struct recon_pipeline_batch {
+    recon_grid_batch grid;
+    int32_t solver;              /* 0 = red-rec, 1 = bird */
+    int32_t preset;              /* recon_preset */
+    int64_t move_stride;         /* >= max total displacement per instance */
+    int32_t *move_batch;         /* [count * move_stride] */
+    int32_t *batch_count;        /* [count] */
+} recon_pipeline_batch;
+
+recon_status recon_pipeline_batch_run(recon_ctx *ctx, const recon_pipeline_batch *batch);
+/* Same with every pointer in `batch` in host memory. */
+recon_status recon_pipeline_batch_run_host(recon_ctx *ctx, const recon_pipeline_batch *batch);
+
+/* ------------------------------------------------------------------------- */
+/* Synthetic inputs (host)                                                    */
+/* ------------------------------------------------------------------------- */
+
+/*
+ * Instance i = Rng(seed_base + i).sample_without_replacement(width*height, k)
+ * (reference rng.hpp:14-59, bit-identical), packed as occ bits: layout 0 =
+ * grid (column-major words), layout 1 = dense chain (height must be 1).
+ * threads <= 0 uses every hardware thread.
+ */
+recon_status recon_sample_occ(uint64_t seed_base, int32_t count, int32_t width, int32_t height,
+                              int64_t k, int32_t layout, uint64_t *occ, int32_t threads);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RECON_B200_H */
