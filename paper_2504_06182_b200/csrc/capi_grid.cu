@@ -1,0 +1,254 @@
+// C-ABI: grid solvers (red-rec, bird) and the occupancy DAG.
+//
+// recon_redrec_solve / recon_bird_solve replace red_rec / bird
+// (reference redrec.hpp:67-68, bird.hpp:40-41); recon_occupancy_dag replaces
+// occupancy_dag (virtual_line.hpp:104).
+
+#include <algorithm>
+#include <cstring>
+
+#include "capi_internal.cuh"
+#include "dag.cuh"
+#include "grid_solver.cuh"
+
+using namespace rb;
+
+namespace {
+
+constexpr int kWarps = 8;
+
+#define CK(call, where)                                   \
+    do {                                                  \
+        cudaError_t e_ = (call);                          \
+        if (e_ != cudaSuccess) return cuda_fail(e_, where, detail); \
+    } while (0)
+
+recon_status validate_grid(int W, int H, int hp, int32_t *detail) {
+    if (W <= 0 || H <= 0) {  // Geometry::grid (geometry.hpp:72-73)
+        if (detail) *detail = RECON_D_GRID_DIMENSIONS;
+        return RECON_ERR_INPUT;
+    }
+    if (hp <= 0 || hp >= H) {  // TargetRegion::expand (problem.hpp:82-83)
+        if (detail) *detail = RECON_D_BAND_HEIGHT;
+        return RECON_ERR_INPUT;
+    }
+    return RECON_OK;
+}
+
+int grid_blocks(Ctx *c, int solver, const GridShape &s, int count) {
+    const int occ = std::max(1, grid_occupancy(solver, s));
+    return std::max(1, std::min(count, occ * c->sms));
+}
+
+// runs the DAG over `P` device-resident paths; copies edges to host arrays
+recon_status run_dag(Ctx *c, int W, int H, const int32_t *d_src, const int32_t *d_dst, int64_t P,
+                     int32_t *h_a, int32_t *h_b, int64_t cap, int64_t *count, int32_t *detail) {
+    DagArgs d{};
+    d.W = W;
+    d.H = H;
+    d.P = (int)P;
+    d.src = d_src;
+    d.dst = d_dst;
+    d.source_of = c->dev<int32_t>(S_SRCOF, (size_t)W * H);
+    d.target_of = c->dev<int32_t>(S_TGTOF, (size_t)W * H);
+    d.cnt = c->dev<int32_t>(S_DCNT, (size_t)P + 1);
+    d.off = c->dev<int64_t>(S_DOFF, (size_t)P + 2);
+    d.temp_bytes = dag_temp_bytes(1, (int)P + 1);
+    d.temp = c->get(S_TEMP, d.temp_bytes);
+    if (!d.source_of || !d.target_of || !d.cnt || !d.off || !d.temp)
+        return cuda_fail(cudaErrorMemoryAllocation, "dag workspace", detail);
+    int64_t n = 0;
+    CK(dag_count(d, c->stream, &n), "dag_count");
+    c->launches += 4;
+    *count = n;
+    if (n > cap) return RECON_ERR_CAPACITY;
+    if (n == 0) return RECON_OK;
+    d.keys = c->dev<unsigned long long>(S_KEYS, (size_t)n);
+    d.keys_alt = c->dev<unsigned long long>(S_KEYS2, (size_t)n);
+    d.temp_bytes = dag_temp_bytes(n, (int)P + 1);
+    d.temp = c->get(S_TEMP, d.temp_bytes);
+    int32_t *ea = c->dev<int32_t>(S_EA, (size_t)n), *eb = c->dev<int32_t>(S_EB, (size_t)n);
+    if (!d.keys || !d.keys_alt || !d.temp || !ea || !eb)
+        return cuda_fail(cudaErrorMemoryAllocation, "dag workspace", detail);
+    CK(dag_emit(d, n, c->stream, ea, eb), "dag_emit");
+    c->launches += 3;
+    CK(cudaMemcpyAsync(h_a, ea, (size_t)n * 4, cudaMemcpyDeviceToHost, c->stream), "dag D2H");
+    CK(cudaMemcpyAsync(h_b, eb, (size_t)n * 4, cudaMemcpyDeviceToHost, c->stream), "dag D2H");
+    CK(cudaStreamSynchronize(c->stream), "dag sync");
+    return RECON_OK;
+}
+
+recon_status grid_single(int solver, recon_ctx *ctx, const uint64_t *occ, int W, int H, int hp,
+                         recon_grid_solution *out, int32_t *detail) {
+    if (detail) *detail = 0;
+    if (!occ || !out) return RECON_ERR_ARGUMENT;
+    recon_status st = validate_grid(W, H, hp, detail);
+    if (st != RECON_OK) return st;
+    Ctx *c = resolve(ctx);
+    if (!c) {
+        if (detail) *detail = RECON_D_CUDA;
+        return RECON_ERR_CUDA;
+    }
+    CK(cudaSetDevice(c->device), "cudaSetDevice");
+    GridShape s;
+    if (!grid_shape(W, H, hp, kWarps, s)) return RECON_ERR_ARGUMENT;
+    const size_t words = (size_t)W * s.wpd, stride = (size_t)W * hp;
+    GridParams p{};
+    p.shape = s;
+    p.count = 1;
+    uint64_t *d_occ = c->dev<uint64_t>(S_OCC, words);
+    p.occ = d_occ;
+    p.path_src = c->dev<int32_t>(S_PSRC, stride);
+    p.path_dst = c->dev<int32_t>(S_PDST, stride);
+    p.path_event = c->dev<int32_t>(S_PEV, stride);
+    p.path_count = c->dev<int32_t>(S_PCNT, 1);
+    p.total_displacement = c->dev<int64_t>(S_TDISP, 1);
+    p.status = c->dev<int32_t>(S_STATUS, 1);
+    p.detail = c->dev<int32_t>(S_DETAIL, 1);
+    p.events = c->dev<int32_t>(S_EVENTS, (size_t)W * 4);
+    if (!d_occ || !p.path_src || !p.path_dst || !p.path_event || !p.path_count || !p.total_displacement ||
+        !p.status || !p.detail || !p.events)
+        return cuda_fail(cudaErrorMemoryAllocation, "grid workspace", detail);
+    CK(cudaMemcpyAsync(d_occ, occ, words * 8, cudaMemcpyHostToDevice, c->stream), "occ H2D");
+    CK(launch_grid_solver(solver, p, 1, c->stream), "grid kernel launch");
+    c->launches += 1;
+    int32_t h_cnt = 0, h_st = 0, h_det = 0;
+    int64_t h_td = 0;
+    CK(cudaMemcpyAsync(&h_cnt, p.path_count, 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    CK(cudaMemcpyAsync(&h_st, p.status, 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    CK(cudaMemcpyAsync(&h_det, p.detail, 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    CK(cudaMemcpyAsync(&h_td, p.total_displacement, 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    CK(cudaStreamSynchronize(c->stream), "grid kernel");
+    if (h_st != RECON_OK) {
+        if (detail) *detail = h_det;
+        return (recon_status)h_st;
+    }
+    out->path_count = h_cnt;
+    out->displaced_tokens = h_cnt;  // every grid path has length > 0 (virtual_line.cpp:219)
+    out->total_displacement = h_td;
+    out->event_count = W;
+    if (out->path_capacity < h_cnt) return RECON_ERR_CAPACITY;
+    if (h_cnt > 0) {
+        CK(cudaMemcpyAsync(out->path_src, p.path_src, (size_t)h_cnt * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        CK(cudaMemcpyAsync(out->path_dst, p.path_dst, (size_t)h_cnt * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        if (out->path_event)
+            CK(cudaMemcpyAsync(out->path_event, p.path_event, (size_t)h_cnt * 4, cudaMemcpyDeviceToHost, c->stream),
+               "D2H");
+    }
+    if (out->events) {
+        const int per = solver == 0 ? 4 : 1;
+        if (out->event_capacity < W * per) return RECON_ERR_CAPACITY;
+        CK(cudaMemcpyAsync(out->events, p.events, (size_t)W * per * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    }
+    CK(cudaStreamSynchronize(c->stream), "D2H");
+    if (out->dag_src) {
+        return run_dag(c, W, H, p.path_src, p.path_dst, h_cnt, out->dag_src, out->dag_dst, out->dag_capacity,
+                       &out->dag_count, detail);
+    }
+    return RECON_OK;
+}
+
+recon_status grid_batch(int solver, recon_ctx *ctx, const recon_grid_batch *b, bool host) {
+    int32_t *detail = nullptr;
+    if (!b || !b->occ || !b->path_src || !b->path_dst || !b->path_count || !b->total_displacement || !b->status)
+        return RECON_ERR_ARGUMENT;
+    int32_t dummy = 0;
+    recon_status st = validate_grid(b->width, b->height, b->h_prime, &dummy);
+    if (st != RECON_OK) return st;
+    if (b->count <= 0) return RECON_OK;
+    Ctx *c = resolve(ctx);
+    if (!c) return RECON_ERR_CUDA;
+    CK(cudaSetDevice(c->device), "cudaSetDevice");
+    GridShape s;
+    if (!grid_shape(b->width, b->height, b->h_prime, kWarps, s)) return RECON_ERR_ARGUMENT;
+    const size_t n = (size_t)b->count, words = (size_t)b->width * s.wpd, stride = (size_t)b->width * b->h_prime;
+    const int per = solver == 0 ? 4 : 1;
+    GridParams p{};
+    p.shape = s;
+    p.count = b->count;
+    if (!host) {
+        p.occ = b->occ;
+        p.path_src = b->path_src;
+        p.path_dst = b->path_dst;
+        p.path_event = b->path_event;
+        p.path_count = b->path_count;
+        p.total_displacement = b->total_displacement;
+        p.status = b->status;
+        p.detail = b->detail;
+        p.events = b->events;
+        CK(launch_grid_solver(solver, p, grid_blocks(c, solver, s, b->count), c->stream), "grid kernel launch");
+        c->launches += 1;
+        return RECON_OK;
+    }
+    uint64_t *d_occ = c->dev<uint64_t>(S_OCC, n * words);
+    p.occ = d_occ;
+    p.path_src = c->dev<int32_t>(S_PSRC, n * stride);
+    p.path_dst = c->dev<int32_t>(S_PDST, n * stride);
+    p.path_event = b->path_event ? c->dev<int32_t>(S_PEV, n * stride) : nullptr;
+    p.path_count = c->dev<int32_t>(S_PCNT, n);
+    p.total_displacement = c->dev<int64_t>(S_TDISP, n);
+    p.status = c->dev<int32_t>(S_STATUS, n);
+    p.detail = c->dev<int32_t>(S_DETAIL, n);
+    p.events = b->events ? c->dev<int32_t>(S_EVENTS, n * b->width * per) : nullptr;
+    if (!d_occ || !p.path_src || !p.path_dst || (b->path_event && !p.path_event) || !p.path_count ||
+        !p.total_displacement || !p.status || !p.detail || (b->events && !p.events))
+        return cuda_fail(cudaErrorMemoryAllocation, "grid batch workspace", detail);
+    CK(cudaMemcpyAsync(d_occ, b->occ, n * words * 8, cudaMemcpyHostToDevice, c->stream), "occ H2D");
+    CK(launch_grid_solver(solver, p, grid_blocks(c, solver, s, b->count), c->stream), "grid kernel launch");
+    c->launches += 1;
+    CK(cudaMemcpyAsync(b->path_src, p.path_src, n * stride * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    CK(cudaMemcpyAsync(b->path_dst, p.path_dst, n * stride * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    if (b->path_event)
+        CK(cudaMemcpyAsync(b->path_event, p.path_event, n * stride * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    CK(cudaMemcpyAsync(b->path_count, p.path_count, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    CK(cudaMemcpyAsync(b->total_displacement, p.total_displacement, n * 8, cudaMemcpyDeviceToHost, c->stream),
+       "D2H");
+    CK(cudaMemcpyAsync(b->status, p.status, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    if (b->detail) CK(cudaMemcpyAsync(b->detail, p.detail, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    if (b->events)
+        CK(cudaMemcpyAsync(b->events, p.events, n * b->width * per * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    CK(cudaStreamSynchronize(c->stream), "grid batch");
+    return RECON_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+recon_status recon_redrec_solve(recon_ctx *ctx, const uint64_t *occ, int32_t width, int32_t height,
+                                int32_t h_prime, recon_grid_solution *out, int32_t *detail) {
+    return grid_single(0, ctx, occ, width, height, h_prime, out, detail);
+}
+
+recon_status recon_bird_solve(recon_ctx *ctx, const uint64_t *occ, int32_t width, int32_t height,
+                              int32_t h_prime, recon_grid_solution *out, int32_t *detail) {
+    return grid_single(1, ctx, occ, width, height, h_prime, out, detail);
+}
+
+recon_status recon_redrec_solve_batch(recon_ctx *ctx, const recon_grid_batch *b) { return grid_batch(0, ctx, b, false); }
+recon_status recon_bird_solve_batch(recon_ctx *ctx, const recon_grid_batch *b) { return grid_batch(1, ctx, b, false); }
+recon_status recon_redrec_solve_batch_host(recon_ctx *ctx, const recon_grid_batch *b) { return grid_batch(0, ctx, b, true); }
+recon_status recon_bird_solve_batch_host(recon_ctx *ctx, const recon_grid_batch *b) { return grid_batch(1, ctx, b, true); }
+
+recon_status recon_occupancy_dag(recon_ctx *ctx, int32_t width, int32_t height, const int32_t *path_src,
+                                 const int32_t *path_dst, int64_t path_count, int32_t *dag_src, int32_t *dag_dst,
+                                 int64_t dag_capacity, int64_t *dag_count, int32_t *detail) {
+    if (detail) *detail = 0;
+    if (!dag_count || (path_count > 0 && (!path_src || !path_dst))) return RECON_ERR_ARGUMENT;
+    if (width <= 0 || height <= 0) {
+        if (detail) *detail = RECON_D_GRID_DIMENSIONS;
+        return RECON_ERR_INPUT;
+    }
+    *dag_count = 0;
+    if (path_count == 0) return RECON_OK;
+    Ctx *c = resolve(ctx);
+    if (!c) return RECON_ERR_CUDA;
+    CK(cudaSetDevice(c->device), "cudaSetDevice");
+    int32_t *ds = c->dev<int32_t>(S_PSRC, (size_t)path_count), *dd = c->dev<int32_t>(S_PDST, (size_t)path_count);
+    if (!ds || !dd) return cuda_fail(cudaErrorMemoryAllocation, "dag paths", detail);
+    CK(cudaMemcpyAsync(ds, path_src, (size_t)path_count * 4, cudaMemcpyHostToDevice, c->stream), "H2D");
+    CK(cudaMemcpyAsync(dd, path_dst, (size_t)path_count * 4, cudaMemcpyHostToDevice, c->stream), "H2D");
+    return run_dag(c, width, height, ds, dd, path_count, dag_src, dag_dst, dag_capacity, dag_count, detail);
+}
+
+}  // extern "C"

@@ -1,0 +1,50 @@
+// Internal host-side context for the C-ABI implementation.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "recon_b200.h"
+
+namespace rb {
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+struct HostBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+
+// Workspace slots (grow-only device buffers owned by a context).
+enum Slot {
+    S_OCC, S_PSRC, S_PDST, S_PEV, S_PCNT, S_TDISP, S_STATUS, S_DETAIL, S_EVENTS,
+    S_SRCOF, S_TGTOF, S_DCNT, S_DOFF, S_KEYS, S_KEYS2, S_TEMP, S_EA, S_EB,
+    S_CHAIN_A, S_CHAIN_B, S_CHAIN_C, S_CHAIN_D, S_CHAIN_E,
+    S_BM_OFF, S_BM_VERT, S_BM_ES, S_BM_ED, S_BM_OUT, S_BM_AUX0, S_BM_AUX1, S_BM_AUX2, S_BM_AUX3,
+    S_BM_AUX4, S_BM_AUX5, S_BM_AUX6,
+    S_NSLOTS
+};
+
+struct Ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+    DevBuf buf[S_NSLOTS];
+    HostBuf hbuf[8];
+    void *get(int slot, size_t bytes);
+    void *host(int slot, size_t bytes);
+    template <class T>
+    T *dev(int slot, size_t count) {
+        return static_cast<T *>(get(slot, count * sizeof(T)));
+    }
+    ~Ctx();
+};
+
+Ctx *resolve(recon_ctx *ctx);
+void set_cuda_error(cudaError_t e, const char *where);
+recon_status cuda_fail(cudaError_t e, const char *where, int32_t *detail);
+
+}  // namespace rb

@@ -1,0 +1,40 @@
+// Host/device interface of the grid-solver kernels (grid_solver.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rb {
+
+// Instance shape and derived sizes (host computes, device reads).
+struct GridShape {
+    int W, H, k;      // width, height, band height h'
+    int wpd;          // u64 words per column
+    int B;            // bits per lane chunk in warp engines (8/16/32)
+    int LK;           // list capacity (k + 2)
+    int LT, LB;       // level-table sizes (top / bottom), multiples of 64
+    int nchunk;       // 32-slot chunks covering 2W-1 group-order slots
+    int nwarps;
+    int64_t smem_bytes;
+};
+
+struct GridSmem {
+    int64_t dep, keys, bal, sigma, ev_count, ev_off, lvl_t, lvl_b, scal, lists, plists, mark_dest, ev_col,
+        ev_aux, ev_a, ev_type, solved, total;
+};
+
+struct GridParams {
+    GridShape shape;
+    const uint64_t *occ;
+    int count;
+    int32_t *path_src, *path_dst, *path_event;
+    int32_t *path_count;
+    int64_t *total_displacement;
+    int32_t *status, *detail, *events;
+};
+
+bool grid_shape(int W, int H, int k, int nwarps, GridShape &s);
+cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaStream_t stream);
+int grid_occupancy(int solver, const GridShape &s);
+
+}  // namespace rb
