@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200 atom-reconfiguration core.
+
+Metric (BASELINE.json): "red-rec/bird solve µs per 256×256 grid; grids/sec at
+1/2/4/8 B200".  One step = one batched red-rec solve (recon_redrec_solve_batch)
+of B independent 256×256 grids, h'=153 (ε-critical: ~113 deficit columns, the
+pairing loop runs), 39,322 atoms each (ε=0.6), seeds 0x25600000 + global index,
+all resident in HBM.  value = grids/s over all ranks (weak scaling: each rank
+solves its own B grids; instances are independent, so no collective runs on
+the data path — torch.distributed only carries the timing max).
+
+Side measurements on the same line: bird on the same grids, single-grid
+latency (µs) for red-rec at h'=128 / 153 (C4), the roofline of the solve
+kernel against MEASURED_PEAKS.json, e2e through the host-buffer C-ABI call
+(recon_redrec_solve_batch_host: H2D of the grids + D2H of the paths inside the
+timed region), and the reference CPU implementation (oracle/_ref, compiled
+from the reference's own sources) timed on this host.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+W = H = 256
+HP = 153
+ATOMS = 39322
+SEED_BASE = 0x25600000
+METRIC = "red-rec/bird solve µs per 256×256 grid; grids/sec at 1/2/4/8 B200"
+REF_LIB = os.path.join(ROOT, "oracle", "_ref", "librecon_ref.so")
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def gen_inputs(rank: int, batch: int):
+    from paper_2504_06182_b200.inputs import sample_grids
+    return sample_grids(SEED_BASE + rank * batch, batch, W, H, ATOMS)
+
+
+def algorithmic_bytes(path_counts: np.ndarray) -> int:
+    # B = ceil(W*H/8) input bits + 8*P path list + 32 stats (no batching here)
+    n = len(path_counts)
+    return int(n * (W * H // 8) + 8 * int(path_counts.sum()) + 32 * n)
+
+
+def cpu_reference(occ: np.ndarray, count: int, solver: str = "redrec"):
+    """Times the compiled reference (oracle/_ref) on `count` grids with every host thread."""
+    from paper_2504_06182_b200.abi import ReconLib
+    ref = ReconLib(REF_LIB, "ref")
+    cores = os.cpu_count() or 1
+    os.environ["RECON_REF_THREADS"] = str(cores)
+    wpc = (H + 63) // 64
+    sub = np.ascontiguousarray(occ[: count * W * wpc])
+    t0 = time.perf_counter()
+    out = ref.grid_solve_batch(solver, sub, count, W, H, HP, host=True, with_events=False)
+    dt = time.perf_counter() - t0
+    assert (out["status"] == 0).all()
+    return count / dt, cores, out
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if ws > 1 and rank != 0:
+        return
+    sample = args.ref_sample
+    occ = gen_inputs(0, sample)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, cores, _ = cpu_reference(occ, sample)
+        if i >= args.warmup:
+            vals.append(v)
+    v = statistics.median(vals)
+    line = {
+        "metric": METRIC, "value": v, "unit": "grids/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * sample / v, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"red-rec {W}x{H} h'={HP} {ATOMS} atoms, batch of {sample} per step (bounded CPU sample)",
+                   "seeds": hex(SEED_BASE)},
+        "cpu_baseline": {"value": v, "unit": "grids/s", "cores": cores, "kind": "reference",
+                         "sample": f"{sample} grids per step, std::thread pool over all host threads"},
+        "e2e": {"value": v, "unit": "grids/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=2048, help="grids per GPU per step")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--ref-sample", type=int, default=64)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    from paper_2504_06182_b200 import load_native
+    from paper_2504_06182_b200.abi import GridBatch
+    import ctypes as C
+
+    lib = load_native()
+    lib.ctx(local)
+    stream_ptr = lib.lib.recon_ctx_stream(lib.ctx())
+    stream = torch.cuda.ExternalStream(stream_ptr)
+
+    B = args.batch
+    wpc = (H + 63) // 64
+    occ_h = gen_inputs(rank, B)
+    dev = torch.device("cuda", local)
+    occ_d = torch.from_numpy(occ_h.view(np.int64)).to(dev)
+    stride = W * HP
+    bufs = {k: torch.empty(B * stride, dtype=torch.int32, device=dev) for k in ("src", "dst")}
+    pcount = torch.empty(B, dtype=torch.int32, device=dev)
+    tdisp = torch.empty(B, dtype=torch.int64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    detail = torch.empty(B, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
+
+    def batch_struct():
+        return GridBatch(occ_d.data_ptr(), B, W, H, HP, bufs["src"].data_ptr(), bufs["dst"].data_ptr(), None,
+                         pcount.data_ptr(), tdisp.data_ptr(), status.data_ptr(), detail.data_ptr(), None)
+
+    gb = batch_struct()
+
+    def solve(fn):
+        st = fn(lib.ctx(), C.byref(gb))
+        if st != 0:
+            raise RuntimeError(f"solve failed {st}: {lib.last_cuda_error()}")
+
+    def timed(fn, steps, warmup):
+        times = []
+        for i in range(warmup + steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(i)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            solve(fn)
+            e1.record(stream)
+            e1.synchronize()
+            if i >= warmup:
+                times.append(e0.elapsed_time(e1))
+        return times
+
+    # warm-up + correctness status
+    solve(lib.lib.recon_redrec_solve_batch)
+    torch.cuda.synchronize()
+    assert int((status != 0).sum()) == 0, "solver statuses"
+
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.launch_count()
+    with Clocks(local) as clk:
+        times = timed(lib.lib.recon_redrec_solve_batch, args.steps, args.warmup)
+    launches = lib.launch_count() - launches0
+    torch.cuda.synchronize()
+    ms = sum(times) / len(times)
+    if ws > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    counts = pcount.cpu().numpy()
+    alg_bytes = algorithmic_bytes(counts)
+    hbm_peak, peak_kind = peaks()
+    achieved_gbs = alg_bytes / (ms * 1e-3) / 1e9
+    value = ws * B / (ms * 1e-3)
+
+    # bird on the same grids (secondary)
+    bird_times = timed(lib.lib.recon_bird_solve_batch, max(2, args.steps // 2), 1)
+    bird_ms = sum(bird_times) / len(bird_times)
+
+    # e2e through the host-buffer C-ABI call (pinned host memory)
+    pin = {k: torch.empty(B * stride, dtype=torch.int32).pin_memory() for k in ("src", "dst")}
+    occ_pin = torch.from_numpy(occ_h.view(np.int64)).pin_memory()
+    h_cnt = torch.empty(B, dtype=torch.int32).pin_memory()
+    h_td = torch.empty(B, dtype=torch.int64).pin_memory()
+    h_st = torch.empty(B, dtype=torch.int32).pin_memory()
+    h_det = torch.empty(B, dtype=torch.int32).pin_memory()
+    hb = GridBatch(occ_pin.data_ptr(), B, W, H, HP, pin["src"].data_ptr(), pin["dst"].data_ptr(), None,
+                   h_cnt.data_ptr(), h_td.data_ptr(), h_st.data_ptr(), h_det.data_ptr(), None)
+    e2e = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        st = lib.lib.recon_redrec_solve_batch_host(lib.ctx(), C.byref(hb))
+        dt = time.perf_counter() - t0
+        assert st == 0
+        if i >= args.warmup:
+            e2e.append(dt)
+    e2e_s = statistics.median(e2e)
+    if ws > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = B * W * wpc * 8
+    d2h = B * stride * 4 * 2 + B * (4 + 8 + 4 + 4)
+
+    # single-grid latency (C4: one instance per launch)
+    lat = {}
+    for hp, seed in ((128, 256), (153, 257)):
+        from paper_2504_06182_b200.inputs import sample_grids
+        o1 = torch.from_numpy(sample_grids(seed, 1, W, H, ATOMS).view(np.int64)).to(dev)
+        g1 = GridBatch(o1.data_ptr(), 1, W, H, hp, bufs["src"].data_ptr(), bufs["dst"].data_ptr(), None,
+                       pcount.data_ptr(), tdisp.data_ptr(), status.data_ptr(), detail.data_ptr(), None)
+        ts = []
+        for i in range(8):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            assert lib.lib.recon_redrec_solve_batch(lib.ctx(), C.byref(g1)) == 0
+            e1.record(stream)
+            e1.synchronize()
+            if i >= 3:
+                ts.append(e0.elapsed_time(e1) * 1000.0)
+        lat[f"h{hp}_seed{seed}_us"] = statistics.median(ts)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        v, cores, _ = cpu_reference(occ_h, args.ref_sample)
+        cpu = {"value": v, "unit": "grids/s", "cores": cores, "kind": "reference",
+               "sample": f"first {args.ref_sample} grids of the batch, compiled reference red_rec "
+                         f"(oracle/_ref), std::thread pool over all host threads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "grids/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": f"red-rec {W}x{H} h'={HP}, {ATOMS} atoms (eps=0.6), batch {B} grids/GPU/step",
+                       "seeds": f"{hex(SEED_BASE)} + global index", "parallelism": f"instances sharded over {ws} GPU(s)",
+                       "l2": "flushed between steps (256 MiB write)"},
+            "us_per_grid": ms * 1000.0 / B,
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved_gbs / hbm_peak, "traffic": None, "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_step": alg_bytes},
+            "e2e": {"value": ws * B / e2e_s, "unit": "grids/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "bird": {"grids_per_s": ws * B / (bird_ms * 1e-3), "ms_per_step": bird_ms},
+            "latency_single_grid": lat,
+            "clocks": clk.summary(),
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -159,7 +159,7 @@ EXPORTED_SYMBOLS = [
     "recon_redrec_solve_batch_host", "recon_bird_solve_batch_host",
     "recon_assign_1d", "recon_assign_1d_generalized", "recon_solve_1d",
     "recon_solve_1d_batch", "recon_solve_1d_batch_host",
-    "recon_batch_moves", "recon_pipeline_batch_run",
+    "recon_batch_moves", "recon_pipeline_batch_run", "recon_pipeline_batch_run_host",
 ]
 
 
@@ -244,8 +244,10 @@ class ReconLib:
                                         I32P, C.c_int64, I32P, I32P, C.c_int32, C.c_int32, I32P,
                                         I64P, I32P]
         L.recon_batch_moves.restype = C.c_int
-        L.recon_pipeline_batch_run.argtypes = [C.c_void_p, C.POINTER(PipelineBatch)]
-        L.recon_pipeline_batch_run.restype = C.c_int
+        for fn in ("recon_pipeline_batch_run", "recon_pipeline_batch_run_host"):
+            f = getattr(L, fn)
+            f.argtypes = [C.c_void_p, C.POINTER(PipelineBatch)]
+            f.restype = C.c_int
         self._ctx = None
 
     # -- context -----------------------------------------------------------
@@ -482,6 +484,6 @@ class ReconLib:
                       _vp(out["status"]).value, _vp(out["detail"]).value, None)
         pb = PipelineBatch(g, 1 if solver == "bird" else 0, preset, move_stride,
                            _vp(out["move_batch"]).value, _vp(out["batch_count"]).value)
-        st = self.lib.recon_pipeline_batch_run(self.ctx(), C.byref(pb))
+        st = self.lib.recon_pipeline_batch_run_host(self.ctx(), C.byref(pb))
         self._check(st, 0)
         return out

@@ -1,0 +1,550 @@
+// batch_moves on sm_100a: one WARP per instance.
+//
+// Reference: /root/reference/proj/src/batching.cpp:28-159 (Alg. 4).
+//
+// State per instance (global scratch): occupancy bitmap, per-path next edge,
+// per-path blocker counts, a SORTED ready list (the reference's std::set).
+// Each batch:
+//   1. the ready list is scanned in ascending id, 32 candidates per step; a
+//      candidate's next move (from -> to) needs `to` free in the PRE-batch
+//      occupancy, no vertex shared with an accepted move, and the constraint
+//      predicate against every accepted move (batching.cpp:107-125).  Inside
+//      a step the greedy ascending acceptance is resolved with a 32-round
+//      shuffle over per-lane conflict masks; earlier steps are seen through
+//      an in-batch vertex bitmap and the batch's first move;
+//   2. no acceptance while moves remain -> InputError "batching made no
+//      progress" (batching.cpp:127-128);
+//   3. atomic application (sources vacated, then destinations filled);
+//   4. finished paths release successors, which join the ready list for the
+//      NEXT batch (batching.cpp:138-148): ready = (ready - finished) merged
+//      with the sorted newly-released ids, by rank.
+// The batch index of every move is written at its path-major slot.
+
+#include <algorithm>
+#include <cub/device/device_scan.cuh>
+
+#include "batching.cuh"
+#include "common.cuh"
+
+namespace rb {
+
+struct ExplicitPaths {
+    const int64_t *off;
+    const int32_t *verts;
+    __device__ __forceinline__ int len(int p) const { return (int)(off[p + 1] - off[p] - 1); }
+    __device__ __forceinline__ int32_t v(int p, int k) const { return verts[off[p] + k]; }
+    __device__ __forceinline__ int64_t move_base(int p) const { return off[p] - p; }
+};
+
+// one-bend staircase: horizontal along the source row, then vertical
+// (virtual_line.cpp:150-173)
+struct ImplicitPaths {
+    const int32_t *src, *dst;
+    const int64_t *base;  // [P] path-major move offsets (minus base0)
+    int64_t base0;
+    int H;
+    __device__ __forceinline__ int len(int p) const {
+        const int s = src[p], t = dst[p];
+        return abs(s / H - t / H) + abs(s % H - t % H);
+    }
+    __device__ __forceinline__ int32_t v(int p, int k) const {
+        const int s = src[p], t = dst[p];
+        const int xs = s / H, ys = s % H, xt = t / H, yt = t % H;
+        const int dx = abs(xt - xs);
+        if (k <= dx) return (xs + (xt > xs ? k : -k)) * H + ys;
+        const int m = k - dx;
+        return xt * H + ys + (yt > ys ? m : -m);
+    }
+    __device__ __forceinline__ int64_t move_base(int p) const { return base[p] - base0; }
+};
+
+__device__ __forceinline__ bool bit_get(const uint32_t *bm, int v) { return (bm[v >> 5] >> (v & 31)) & 1u; }
+__device__ __forceinline__ void bit_set(uint32_t *bm, int v) { atomicOr(&bm[v >> 5], 1u << (v & 31)); }
+__device__ __forceinline__ void bit_clr(uint32_t *bm, int v) { atomicAnd(&bm[v >> 5], ~(1u << (v & 31))); }
+
+// move_dir (batching.cpp:9-15): 0 up, 1 down, 2 left, 3 right
+__device__ __forceinline__ int move_dir(int H, int32_t a, int32_t b) {
+    const int ay = a % H, by = b % H;
+    if (by > ay) return 0;
+    if (by < ay) return 1;
+    if (b / H < a / H) return 2;
+    return 3;
+}
+
+// ConstraintSet::compatible (batching.cpp:17-24)
+__device__ __forceinline__ bool compatible(int preset, int H, int32_t af, int32_t at, int32_t bf, int32_t bt) {
+    if (preset == 0) return true;
+    const int da = move_dir(H, af, at), db = move_dir(H, bf, bt);
+    if (da != db) return false;
+    if (da <= 1) return af / H == bf / H;
+    return af % H == bf % H;
+}
+
+template <class Paths>
+__device__ void batch_warp(const BatchJob &J, const Paths &paths) {
+    const int lane = lane_id();
+    const int P = J.P, H = J.H;
+    BatchScratch s = J.s;
+    // ---- init: next = 0, blockers = in-degree (given), finish zero-length paths
+    long long left = 0;
+    for (int p = lane; p < P; p += 32) {
+        s.next[p] = 0;
+        s.done[p] = 0;
+        left += paths.len(p);
+    }
+    left = warp_sum64(left);
+    __syncwarp();
+    for (int p = lane; p < P; p += 32)
+        if (paths.len(p) == 0) {
+            s.done[p] = 1;
+            for (int64_t q = J.soff[p]; q < J.soff[p + 1]; ++q) atomicSub(&s.blockers[J.succ[q]], 1);
+        }
+    __syncwarp();
+    __threadfence_block();
+    int nready = 0;
+    for (int p0 = 0; p0 < P; p0 += 32) {
+        const int p = p0 + lane;
+        const bool r = p < P && !s.done[p] && s.blockers[p] == 0;
+        const unsigned m = __ballot_sync(FULL, r);
+        if (r) s.ready[nready + __popc(m & lanemask_lt())] = p;
+        nready += __popc(m);
+    }
+    __syncwarp();
+    int32_t *ready = s.ready, *ready2 = s.ready2;
+    int nb = 0, status = RECON_OK;
+    while (left > 0) {
+        // ---- 1. candidate scan (ascending id), greedy acceptance
+        int nacc = 0;
+        int32_t f_from = -1, f_to = -1;  // first accepted move of the batch
+        if (J.edge_level) {
+            // queue = every unfinished path whose edge-level release holds
+            // (batching.cpp:84-102); rebuilt in ascending id
+            nready = 0;
+            for (int p0 = 0; p0 < P; p0 += 32) {
+                const int p = p0 + lane;
+                bool ok = p < P && !s.done[p];
+                if (ok)
+                    for (int64_t q = J.in_off[p]; q < J.in_off[p + 1] && ok; ++q) {
+                        const int pred = J.in_src[q];
+                        if (!s.done[pred] && s.next[pred] < J.in_need[q]) ok = false;
+                    }
+                const unsigned m = __ballot_sync(FULL, ok);
+                if (ok) ready[nready + __popc(m & lanemask_lt())] = p;
+                nready += __popc(m);
+            }
+            __syncwarp();
+        }
+        for (int c0 = 0; c0 < nready; c0 += 32) {
+            const int idx = c0 + lane;
+            const bool valid = idx < nready;
+            int p = -1, k = 0;
+            int32_t fr = -1, to = -1;
+            bool cand = false;
+            if (valid) {
+                p = ready[idx];
+                k = s.next[p];
+                fr = paths.v(p, k);
+                to = paths.v(p, k + 1);
+                cand = !bit_get(s.occ, to) && !bit_get(s.inb, fr) && !bit_get(s.inb, to);
+                if (cand && f_from >= 0) cand = compatible(J.preset, H, fr, to, f_from, f_to);
+            }
+            // conflicts with earlier lanes of this step
+            unsigned cm = 0;
+            for (int i = 0; i < 32; ++i) {
+                const int32_t ofr = __shfl_sync(FULL, fr, i), oto = __shfl_sync(FULL, to, i);
+                if (i < lane && valid && ofr >= 0) {
+                    const bool share = ofr == fr || ofr == to || oto == fr || oto == to;
+                    if (share || !compatible(J.preset, H, fr, to, ofr, oto)) cm |= 1u << i;
+                }
+            }
+            unsigned acc = 0;
+            for (int i = 0; i < 32; ++i) {
+                const bool a = __shfl_sync(FULL, cand && !(cm & acc), i);
+                if (a) acc |= 1u << i;
+            }
+            if ((acc >> lane) & 1u) {
+                bit_set(s.inb, fr);
+                bit_set(s.inb, to);
+                const int slot = nacc + __popc(acc & lanemask_lt());
+                s.mem[slot] = p;
+                s.mfr[slot] = fr;
+                s.mto[slot] = to;
+            }
+            if (acc && f_from < 0) {
+                const int first = __ffs(acc) - 1;
+                f_from = __shfl_sync(FULL, fr, first);
+                f_to = __shfl_sync(FULL, to, first);
+            }
+            nacc += __popc(acc);
+            __syncwarp();
+        }
+        if (nacc == 0) {
+            status = RECON_ERR_INPUT;  // batching.cpp:127-128
+            break;
+        }
+        // ---- 3. atomic application
+        for (int i = lane; i < nacc; i += 32) {
+            bit_clr(s.occ, s.mfr[i]);
+            bit_clr(s.inb, s.mfr[i]);
+            bit_clr(s.inb, s.mto[i]);
+        }
+        __syncwarp();
+        for (int i = lane; i < nacc; i += 32) bit_set(s.occ, s.mto[i]);
+        __syncwarp();
+        // ---- 4. advance, finish, release (newly -> next batch)
+        int nnew = 0, nfin = 0;
+        for (int i0 = 0; i0 < nacc; i0 += 32) {
+            const int i = i0 + lane;
+            bool fin = false;
+            int p = -1;
+            if (i < nacc) {
+                p = s.mem[i];
+                const int k = s.next[p];
+                J.move_batch[paths.move_base(p) + k] = nb;
+                s.next[p] = k + 1;
+                fin = k + 1 == paths.len(p);
+                if (fin) s.done[p] = 1;
+            }
+            const unsigned fm = __ballot_sync(FULL, fin);
+            nfin += __popc(fm);
+            // release successors of finished members
+            if (fin)
+                for (int64_t q = J.soff[p]; q < J.soff[p + 1]; ++q) {
+                    const int sc = J.succ[q];
+                    if (atomicSub(&s.blockers[sc], 1) == 1) {
+                        const int slot = atomicAdd(&s.counter[0], 1);
+                        s.newly[slot] = sc;
+                    }
+                }
+            __syncwarp();
+        }
+        left -= nacc;
+        __syncwarp();
+        nnew = s.counter[0];
+        __syncwarp();
+        if (lane == 0) s.counter[0] = 0;
+        if (!J.edge_level && (nfin > 0 || nnew > 0)) {
+            // ready' = (ready - finished) U newly, sorted: merge by rank
+            int nkeep = 0;
+            for (int c0 = 0; c0 < nready; c0 += 32) {
+                const int idx = c0 + lane;
+                const bool keep = idx < nready && !s.done[ready[idx]];
+                const unsigned m = __ballot_sync(FULL, keep);
+                if (keep) {
+                    const int x = ready[idx];
+                    int lt = 0;
+                    for (int q = 0; q < nnew; ++q) lt += s.newly[q] < x;
+                    ready2[nkeep + __popc(m & lanemask_lt()) + lt] = x;
+                }
+                nkeep += __popc(m);
+            }
+            __syncwarp();
+            for (int q = lane; q < nnew; q += 32) {
+                const int x = s.newly[q];
+                int lt = 0;
+                for (int r = 0; r < nnew; ++r) lt += s.newly[r] < x;
+                // kept ready ids below x: binary search is not possible on ready2
+                // (interleaved), count in the pre-merge list instead
+                int a = 0, b = nready, kept_lt = 0;
+                (void)a;
+                (void)b;
+                for (int r = 0; r < nready; ++r) {
+                    const int y = ready[r];
+                    if (y >= x) break;
+                    kept_lt += !s.done[y];
+                }
+                ready2[kept_lt + lt] = x;
+            }
+            __syncwarp();
+            int32_t *t = ready;
+            ready = ready2;
+            ready2 = t;
+            nready = nkeep + nnew;
+        }
+        ++nb;
+    }
+    if (lane == 0) {
+        *J.batch_count = status == RECON_OK ? nb : 0;
+        *J.status = status;
+        if (J.detail) *J.detail = status == RECON_OK ? 0 : RECON_D_BATCH_NO_PROGRESS;
+    }
+}
+
+__global__ void batch_explicit_kernel(BatchJob J, ExplicitPaths paths) {
+    if (threadIdx.x < 32) batch_warp(J, paths);
+}
+
+cudaError_t launch_batch_explicit(const BatchJob &J, const int64_t *off, const int32_t *verts, cudaStream_t st) {
+    ExplicitPaths ep{off, verts};
+    batch_explicit_kernel<<<1, 32, 0, st>>>(J, ep);
+    return cudaGetLastError();
+}
+
+// ---- DAG preparation for the general call: CSR by source, blockers, range
+// and acyclicity check (MoveDag::is_acyclic, path_system.cpp:7-39)
+
+__global__ void edges_check_kernel(int P, int64_t E, const int32_t *es, const int32_t *ed, int32_t *bad,
+                                   int32_t *outdeg, int32_t *indeg) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+        const int a = es[e], b = ed[e];
+        if (a < 0 || a >= P || b < 0 || b >= P) {
+            atomicExch(bad, 1);
+            continue;
+        }
+        atomicAdd(&outdeg[a], 1);
+        atomicAdd(&indeg[b], 1);
+    }
+}
+
+__global__ void csr_fill_kernel(int64_t E, const int32_t *key, const int32_t *val, const int64_t *off, int32_t *fill,
+                                int32_t *out, const int64_t *need_in, int64_t *need_out) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+        const int a = key[e];
+        const int slot = atomicAdd(&fill[a], 1);
+        out[off[a] + slot] = val[e];
+        if (need_out) need_out[off[a] + slot] = need_in[e];
+    }
+}
+
+// layered Kahn on one CTA: counts processed nodes
+__global__ void kahn_kernel(int P, const int64_t *soff, const int32_t *succ, int32_t *indeg, int32_t *frontier,
+                            int32_t *next_frontier, int32_t *processed) {
+    __shared__ int nf, nn, tot;
+    if (threadIdx.x == 0) {
+        nf = 0;
+        tot = 0;
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < P; p += blockDim.x)
+        if (indeg[p] == 0) frontier[atomicAdd(&nf, 1)] = p;
+    __syncthreads();
+    while (nf > 0) {
+        if (threadIdx.x == 0) {
+            nn = 0;
+            tot += nf;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+            const int p = frontier[i];
+            for (int64_t q = soff[p]; q < soff[p + 1]; ++q)
+                if (atomicSub(&indeg[succ[q]], 1) == 1) next_frontier[atomicAdd(&nn, 1)] = succ[q];
+        }
+        __syncthreads();
+        int32_t *t = frontier;
+        frontier = next_frontier;
+        next_frontier = t;
+        if (threadIdx.x == 0) nf = nn;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *processed = tot;
+}
+
+// edge-level release thresholds (batching.cpp:38-59): for dag edge i->j, the
+// number of edges of P_i up to its last edge touching a vertex of P_j
+__global__ void need_kernel(int64_t E, const int32_t *es, const int32_t *ed, const int64_t *off,
+                            const int32_t *verts, int64_t *need) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+        const int i = es[e], j = ed[e];
+        const int64_t li = off[i + 1] - off[i] - 1;
+        int64_t nd = 0;
+        for (int64_t k = 0; k < li; ++k) {
+            const int32_t a = verts[off[i] + k], b = verts[off[i] + k + 1];
+            bool touch = false;
+            for (int64_t q = off[j]; q < off[j + 1] && !touch; ++q) touch = verts[q] == a || verts[q] == b;
+            if (touch) nd = k + 1;
+        }
+        need[e] = nd;
+    }
+}
+
+
+// --------------------------------------------------------------------------
+// fused pipeline: per-instance occupancy DAG as a successor CSR + batching
+// --------------------------------------------------------------------------
+
+__global__ void occ_to_vertex_bits(int count, int W, int H, const uint64_t *occ, uint32_t *bits) {
+    const int wpc = (H + 63) / 64;
+    const int64_t nw = ((int64_t)W * H + 31) / 32;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)count * nw;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t inst = t / nw, w = t % nw;
+        uint32_t out = 0;
+        for (int b = 0; b < 32; ++b) {
+            const int64_t v = w * 32 + b;
+            if (v >= (int64_t)W * H) break;
+            const int x = (int)(v / H), y = (int)(v % H);
+            const uint64_t word = occ[(inst * W + x) * wpc + y / 64];
+            out |= (uint32_t)((word >> (y % 64)) & 1ull) << b;
+        }
+        bits[t] = out;
+    }
+}
+
+__device__ __forceinline__ bool on_path2(int H, int32_t s, int32_t t, int32_t v) {
+    const int xs = s / H, ys = s % H, xt = t / H, yt = t % H, x = v / H, y = v % H;
+    if (y == ys && x >= min(xs, xt) && x <= max(xs, xt)) return true;
+    if (x == xt && y >= min(ys, yt) && y <= max(ys, yt)) return true;
+    return false;
+}
+
+__global__ void pl_mark_kernel(PipelineArgs a) {
+    const int64_t S = (int64_t)a.W * a.k, WH = (int64_t)a.W * a.H;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)a.count * S;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t inst = t / S;
+        const int p = (int)(t % S);
+        if (a.solve_status[inst] != 0 || p >= a.path_count[inst]) continue;
+        a.source_of[inst * WH + a.path_src[t]] = p;
+        a.target_of[inst * WH + a.path_dst[t]] = p;
+    }
+}
+
+// pass 0: degrees + path lengths; pass 1: successor fill (virtual_line.cpp:241-268 edge rules)
+template <int PASS>
+__global__ void pl_walk_kernel(PipelineArgs a) {
+    const int64_t S = (int64_t)a.W * a.k, WH = (int64_t)a.W * a.H;
+    const int H = a.H;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)a.count * S;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t inst = t / S;
+        const int i = (int)(t % S);
+        if (a.solve_status[inst] != 0 || i >= a.path_count[inst]) {
+            if (PASS == 0) a.mbase[t] = 0;
+            continue;
+        }
+        const int32_t *src = a.path_src + inst * S, *dst = a.path_dst + inst * S;
+        const int32_t *so = a.source_of + inst * WH, *to = a.target_of + inst * WH;
+        const int32_t s = src[i], tt = dst[i];
+        const int xs = s / H, ys = s % H, xt = tt / H, yt = tt % H;
+        if (PASS == 0) a.mbase[t] = abs(xt - xs) + abs(yt - ys);
+        const int dx = xt > xs ? 1 : -1, dy = yt > ys ? 1 : -1;
+        int x = xs, y = ys;
+        for (;;) {
+            const int32_t v = x * H + y;
+            const int32_t pa = so[v];
+            if (pa >= 0 && pa != i) {  // (pa, i)
+                if (PASS == 0) {
+                    atomicAdd(&a.outdeg[inst * S + pa], 1);
+                    atomicAdd(&a.indeg[t], 1);
+                } else {
+                    const int slot = atomicAdd(&a.fill[inst * S + pa], 1);
+                    a.succ[a.soff[inst * S + pa] + slot] = i;
+                }
+            }
+            const int32_t pb = to[v];
+            if (pb >= 0 && pb != i && !on_path2(H, src[pb], dst[pb], s)) {  // (i, pb), not already rule 1
+                if (PASS == 0) {
+                    atomicAdd(&a.outdeg[t], 1);
+                    atomicAdd(&a.indeg[inst * S + pb], 1);
+                } else {
+                    const int slot = atomicAdd(&a.fill[t], 1);
+                    a.succ[a.soff[t] + slot] = pb;
+                }
+            }
+            if (x != xt) x += dx;
+            else if (y != yt) y += dy;
+            else break;
+        }
+    }
+}
+
+__global__ void widen32_kernel(int64_t n, const int32_t *in, int64_t *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[i];
+}
+
+size_t pipeline_temp_bytes(int64_t n) {
+    size_t t = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, t, (int64_t *)nullptr, (int64_t *)nullptr, (int)n);
+    return t;
+}
+
+cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *edges_host) {
+    const int64_t S = (int64_t)a.W * a.k, WH = (int64_t)a.W * a.H, N = (int64_t)a.count * S;
+    cudaMemsetAsync(a.source_of, 0xff, (size_t)a.count * WH * 4, st);
+    cudaMemsetAsync(a.target_of, 0xff, (size_t)a.count * WH * 4, st);
+    cudaMemsetAsync(a.outdeg, 0, (size_t)N * 4, st);
+    cudaMemsetAsync(a.indeg, 0, (size_t)N * 4, st);
+    cudaMemsetAsync(a.fill, 0, (size_t)N * 4, st);
+    const int blocks = 148 * 8;
+    pl_mark_kernel<<<blocks, 256, 0, st>>>(a);
+    pl_walk_kernel<0><<<blocks, 256, 0, st>>>(a);
+    // soff = exclusive scan of outdeg (global edge index); mbase = exclusive scan of lengths
+    widen32_kernel<<<blocks, 256, 0, st>>>(N, a.outdeg, a.soff);
+    cudaMemsetAsync(a.soff + N, 0, 8, st);
+    size_t tb = a.temp_bytes;
+    cub::DeviceScan::ExclusiveSum(a.temp, tb, a.soff, a.soff, (int)(N + 1), st);
+    cudaMemsetAsync(a.mbase + N, 0, 8, st);
+    tb = a.temp_bytes;
+    cub::DeviceScan::ExclusiveSum(a.temp, tb, a.mbase, a.mbase, (int)(N + 1), st);
+    cudaError_t e = cudaMemcpyAsync(edges_host, a.soff + N, 8, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return e;
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+__global__ void batch_pipeline_kernel(PipelineArgs a) {
+    const int64_t S = (int64_t)a.W * a.k, nwb = ((int64_t)a.W * a.H + 31) / 32;
+    const int nw = blockDim.x >> 5;
+    for (int inst = blockIdx.x * nw + warp_id(); inst < a.count; inst += gridDim.x * nw) {
+        if (a.solve_status[inst] != 0) {
+            if (lane_id() == 0) {
+                a.status[inst] = a.solve_status[inst];
+                a.batch_count[inst] = 0;
+            }
+            continue;
+        }
+        const int64_t o = (int64_t)inst * S;
+        const int64_t moves = a.mbase[o + a.path_count[inst]] - a.mbase[o];
+        if (moves > a.move_stride) {
+            if (lane_id() == 0) {
+                a.status[inst] = RECON_ERR_CAPACITY;
+                a.batch_count[inst] = 0;
+            }
+            continue;
+        }
+        BatchJob J{};
+        J.P = a.path_count[inst];
+        J.W = a.W;
+        J.H = a.H;
+        J.preset = a.preset;
+        J.edge_level = 0;
+        J.soff = a.soff + o;
+        J.succ = a.succ;
+        J.s.occ = a.occ + inst * nwb;
+        J.s.inb = a.inb + inst * nwb;
+        J.s.next = a.next + o;
+        J.s.blockers = a.indeg + o;
+        J.s.done = a.done + o;
+        J.s.ready = a.ready + o;
+        J.s.ready2 = a.ready2 + o;
+        J.s.newly = a.newly + o;
+        J.s.mem = a.mem + o;
+        J.s.mfr = a.mfr + o;
+        J.s.mto = a.mto + o;
+        J.s.counter = a.counter + inst;
+        J.move_batch = a.move_batch + (int64_t)inst * a.move_stride;
+        J.batch_count = a.batch_count + inst;
+        J.status = a.status + inst;
+        J.detail = a.detail ? a.detail + inst : nullptr;
+        ImplicitPaths ip{a.path_src + o, a.path_dst + o, a.mbase + o, a.mbase[o], a.H};
+        batch_warp(J, ip);
+    }
+}
+
+cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t st) {
+    const int64_t S = (int64_t)a.W * a.k, N = (int64_t)a.count * S, nwb = ((int64_t)a.W * a.H + 31) / 32;
+    const int blocks = 148 * 8;
+    pl_walk_kernel<1><<<blocks, 256, 0, st>>>(a);
+    occ_to_vertex_bits<<<blocks, 256, 0, st>>>(a.count, a.W, a.H, a.grid_occ, a.occ);
+    cudaMemsetAsync(a.inb, 0, (size_t)a.count * nwb * 4, st);
+    cudaMemsetAsync(a.counter, 0, (size_t)a.count * 4, st);
+    (void)N;
+    const int warps = 4;
+    const int grid = (int)std::min<int64_t>(((int64_t)a.count + warps - 1) / warps, (int64_t)sms * 16);
+    batch_pipeline_kernel<<<grid, warps * 32, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace rb

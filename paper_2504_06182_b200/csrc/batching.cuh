@@ -1,0 +1,77 @@
+// batch_moves kernels (batching.cu) and the fused solve -> DAG -> batching
+// pipeline (pipeline.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rb {
+
+// per-instance device scratch of the batching warp
+struct BatchScratch {
+    uint32_t *occ;      // W*H bits (vertex id), initialised from the sources
+    uint32_t *inb;      // W*H bits, zero
+    int32_t *next;      // [P]
+    int32_t *blockers;  // [P] initialised to the in-degree
+    uint8_t *done;      // [P]
+    int32_t *ready, *ready2, *newly, *mem, *mfr, *mto;  // [P] each
+    int32_t *counter;   // [1], zero
+};
+
+struct BatchJob {
+    int P, W, H, preset, edge_level;
+    const int64_t *soff;  // [P+1] successor CSR offsets (global edge index)
+    const int32_t *succ;
+    const int64_t *in_off;  // edge-level only: incoming CSR
+    const int32_t *in_src;
+    const int64_t *in_need;
+    BatchScratch s;
+    int32_t *move_batch;  // path-major, one per elementary move
+    int32_t *batch_count, *status, *detail;
+};
+
+cudaError_t launch_batch_explicit(const BatchJob &J, const int64_t *off, const int32_t *verts, cudaStream_t st);
+
+// kernels used by the general C-ABI call
+__global__ void edges_check_kernel(int P, int64_t E, const int32_t *es, const int32_t *ed, int32_t *bad,
+                                   int32_t *outdeg, int32_t *indeg);
+__global__ void csr_fill_kernel(int64_t E, const int32_t *key, const int32_t *val, const int64_t *off, int32_t *fill,
+                                int32_t *out, const int64_t *need_in, int64_t *need_out);
+__global__ void kahn_kernel(int P, const int64_t *soff, const int32_t *succ, int32_t *indeg, int32_t *frontier,
+                            int32_t *next_frontier, int32_t *processed);
+__global__ void need_kernel(int64_t E, const int32_t *es, const int32_t *ed, const int64_t *off, const int32_t *verts,
+                            int64_t *need);
+
+// fused pipeline over `count` grid instances already solved on the device
+struct PipelineArgs {
+    int count, W, H, k, preset;
+    const int32_t *path_src, *path_dst;  // [count * W*k] (instance stride W*k)
+    const int32_t *path_count;           // [count]
+    const int32_t *solve_status;         // [count]
+    int64_t move_stride;
+    int32_t *move_batch;                 // [count * move_stride]
+    int32_t *batch_count, *status, *detail;
+    // scratch (device), per instance strides: maps W*H, paths W*k
+    int32_t *source_of, *target_of;      // [count * W*H]
+    int32_t *outdeg, *indeg, *fill;      // [count * W*k]
+    int64_t *soff;                       // [count * W*k + 1]
+    int64_t *mbase;                      // [count * W*k + 1]
+    int32_t *succ;                       // [edge capacity]
+    int64_t edge_capacity;
+    uint32_t *occ, *inb;                 // [count * ceil(W*H/32)]
+    int32_t *next, *ready, *ready2, *newly, *mem, *mfr, *mto;  // [count * W*k]
+    uint8_t *done;                       // [count * W*k]
+    int32_t *counter;                    // [count]
+    const uint64_t *grid_occ;            // [count * W * wpc] initial occupancy (occ bits)
+    void *temp;
+    size_t temp_bytes;
+};
+
+size_t pipeline_temp_bytes(int64_t n);
+cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *edges_host);
+cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t st);
+
+// occ bits (column-major, bit y) -> vertex-id bitmap
+__global__ void occ_to_vertex_bits(int count, int W, int H, const uint64_t *occ, uint32_t *bits);
+
+}  // namespace rb

@@ -1,0 +1,281 @@
+// C-ABI: batch_moves (batching.hpp:58-59) and the fused solve -> DAG ->
+// batching pipeline over device-resident instances.
+
+#include <algorithm>
+#include <cub/device/device_scan.cuh>
+#include <vector>
+
+#include "batching.cuh"
+#include "capi_internal.cuh"
+#include "grid_solver.cuh"
+
+using namespace rb;
+
+namespace {
+
+#define CK(call, where)                                             \
+    do {                                                            \
+        cudaError_t e_ = (call);                                    \
+        if (e_ != cudaSuccess) return cuda_fail(e_, where, detail); \
+    } while (0)
+
+__global__ void copy_i32(int64_t n, const int32_t *a, int32_t *b) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        b[i] = a[i];
+}
+
+recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool host) {
+    int32_t *detail = nullptr;
+    if (!pb) return RECON_ERR_ARGUMENT;
+    const recon_grid_batch *b = &pb->grid;
+    if (!b->occ || !b->path_src || !b->path_dst || !b->path_count || !b->total_displacement || !b->status ||
+        !pb->move_batch || !pb->batch_count)
+        return RECON_ERR_ARGUMENT;
+    if (b->count <= 0) return RECON_OK;
+    Ctx *c = resolve(ctx);
+    if (!c) return RECON_ERR_CUDA;
+    CK(cudaSetDevice(c->device), "cudaSetDevice");
+    // 1. solve on device (host variant stages through the context)
+    recon_grid_batch g = *b;
+    const size_t n = (size_t)b->count, S = (size_t)b->width * b->h_prime, WH = (size_t)b->width * b->height;
+    const int wpc = (b->height + 63) / 64;
+    std::vector<int32_t> h_status;
+    if (host) {
+        g.occ = c->dev<uint64_t>(S_OCC, n * b->width * wpc);
+        g.path_src = c->dev<int32_t>(S_PSRC, n * S);
+        g.path_dst = c->dev<int32_t>(S_PDST, n * S);
+        g.path_event = b->path_event ? c->dev<int32_t>(S_PEV, n * S) : nullptr;
+        g.path_count = c->dev<int32_t>(S_PCNT, n);
+        g.total_displacement = c->dev<int64_t>(S_TDISP, n);
+        g.status = c->dev<int32_t>(S_STATUS, n);
+        g.detail = c->dev<int32_t>(S_DETAIL, n);
+        g.events = nullptr;
+        if (!g.occ || !g.path_src || !g.path_dst || !g.path_count || !g.total_displacement || !g.status || !g.detail)
+            return cuda_fail(cudaErrorMemoryAllocation, "pipeline workspace", detail);
+        CK(cudaMemcpyAsync((void *)g.occ, b->occ, n * b->width * wpc * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+    }
+    recon_status st = pb->solver == 1 ? recon_bird_solve_batch(ctx, &g) : recon_redrec_solve_batch(ctx, &g);
+    if (st != RECON_OK) return st;
+    // 2. DAG + batching scratch
+    PipelineArgs a{};
+    a.count = b->count;
+    a.W = b->width;
+    a.H = b->height;
+    a.k = b->h_prime;
+    a.preset = pb->preset;
+    a.path_src = g.path_src;
+    a.path_dst = g.path_dst;
+    a.path_count = g.path_count;
+    a.solve_status = g.status;
+    a.move_stride = pb->move_stride;
+    a.grid_occ = g.occ;
+    const size_t nwb = (WH + 31) / 32;
+    int32_t *i32 = c->dev<int32_t>(S_BM_AUX0, n * WH * 2 + n * S * 10 + n * 2 + 8);
+    int64_t *i64 = c->dev<int64_t>(S_BM_AUX1, (n * S + 1) * 2 + 4);
+    uint32_t *bits = c->dev<uint32_t>(S_BM_AUX2, n * nwb * 2 + 4);
+    uint8_t *done = c->dev<uint8_t>(S_BM_AUX3, n * S + 16);
+    int32_t *mb = host ? c->dev<int32_t>(S_BM_OUT, n * (size_t)pb->move_stride) : pb->move_batch;
+    int32_t *bc = host ? c->dev<int32_t>(S_BM_AUX4, n * 3) : pb->batch_count;
+    int32_t *bst = host ? bc + n : g.status;  // batching status (device variant reuses solve status)
+    int32_t *bdet = host ? bc + 2 * n : g.detail;
+    if (!i32 || !i64 || !bits || !done || !mb || !bc) return cuda_fail(cudaErrorMemoryAllocation, "pipeline", detail);
+    if (host) CK(cudaMemsetAsync(mb, 0xff, n * (size_t)pb->move_stride * 4, c->stream), "memset");
+    a.source_of = i32;
+    a.target_of = i32 + n * WH;
+    int32_t *q = i32 + 2 * n * WH;
+    a.outdeg = q;
+    a.indeg = q + n * S;
+    a.fill = q + 2 * n * S;
+    a.next = q + 3 * n * S;
+    a.ready = q + 4 * n * S;
+    a.ready2 = q + 5 * n * S;
+    a.newly = q + 6 * n * S;
+    a.mem = q + 7 * n * S;
+    a.mfr = q + 8 * n * S;
+    a.mto = q + 9 * n * S;
+    a.counter = q + 10 * n * S;
+    a.soff = i64;
+    a.mbase = i64 + n * S + 1;
+    a.occ = bits;
+    a.inb = bits + n * nwb;
+    a.done = done;
+    a.move_batch = mb;
+    a.batch_count = bc;
+    a.status = bst;
+    a.detail = bdet;
+    a.temp_bytes = pipeline_temp_bytes((int64_t)(n * S + 1));
+    a.temp = c->get(S_TEMP, a.temp_bytes);
+    if (!a.temp) return cuda_fail(cudaErrorMemoryAllocation, "pipeline temp", detail);
+    int64_t edges = 0;
+    CK(pipeline_dag_count(a, c->stream, &edges), "pipeline dag");
+    c->launches += 5;
+    a.succ = c->dev<int32_t>(S_BM_AUX5, (size_t)edges + 1);
+    a.edge_capacity = edges;
+    if (!a.succ) return cuda_fail(cudaErrorMemoryAllocation, "pipeline succ", detail);
+    CK(pipeline_run_batching(a, c->sms, c->stream), "pipeline batching");
+    c->launches += 3;
+    if (!host) return RECON_OK;
+    CK(cudaMemcpyAsync(b->path_src, g.path_src, n * S * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    CK(cudaMemcpyAsync(b->path_dst, g.path_dst, n * S * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    if (b->path_event)
+        CK(cudaMemcpyAsync(b->path_event, g.path_event, n * S * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    CK(cudaMemcpyAsync(b->path_count, g.path_count, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    CK(cudaMemcpyAsync(b->total_displacement, g.total_displacement, n * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    CK(cudaMemcpyAsync(b->status, bst, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    if (b->detail) CK(cudaMemcpyAsync(b->detail, bdet, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    CK(cudaMemcpyAsync(pb->batch_count, bc, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    CK(cudaMemcpyAsync(pb->move_batch, mb, n * (size_t)pb->move_stride * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    CK(cudaStreamSynchronize(c->stream), "pipeline");
+    return RECON_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+recon_status recon_batch_moves(recon_ctx *ctx, int32_t width, int32_t height, const uint64_t *occ, int32_t P,
+                               const int64_t *off, const int32_t *verts, int64_t E, const int32_t *es,
+                               const int32_t *ed, int32_t preset, int32_t edge_level, int32_t *move_batch,
+                               int64_t *batch_count, int32_t *detail) {
+    if (detail) *detail = 0;
+    if (!batch_count || (P > 0 && (!off || !verts || !occ)) || (E > 0 && (!es || !ed))) return RECON_ERR_ARGUMENT;
+    if (width <= 0 || height <= 0) {
+        if (detail) *detail = RECON_D_GRID_DIMENSIONS;
+        return RECON_ERR_INPUT;
+    }
+    *batch_count = 0;
+    Ctx *c = resolve(ctx);
+    if (!c) return RECON_ERR_CUDA;
+    CK(cudaSetDevice(c->device), "cudaSetDevice");
+    cudaStream_t st = c->stream;
+    const int64_t WH = (int64_t)width * height, nwb = (WH + 31) / 32;
+    const int64_t nverts = P > 0 ? off[P] : 0, moves = nverts - P;
+    const int wpc = (height + 63) / 64;
+    // device buffers
+    int64_t *d_off = c->dev<int64_t>(S_BM_OFF, (size_t)P + 2);
+    int32_t *d_verts = c->dev<int32_t>(S_BM_VERT, (size_t)nverts + 1);
+    int32_t *d_es = c->dev<int32_t>(S_BM_ES, (size_t)E + 1), *d_ed = c->dev<int32_t>(S_BM_ED, (size_t)E + 1);
+    int32_t *d_out = c->dev<int32_t>(S_BM_OUT, (size_t)moves + 1);
+    uint64_t *d_occ = c->dev<uint64_t>(S_OCC, (size_t)width * wpc);
+    // i32: outdeg[P+1] indeg[P+1] fill[P+1] fill2[P+1] succ[E] in_src[E] misc[16] ar[12P]
+    const size_t n32 = 4 * ((size_t)P + 1) + 2 * (size_t)E + 16 + 12 * (size_t)P + 16;
+    int32_t *i32 = c->dev<int32_t>(S_BM_AUX0, n32);
+    int64_t *i64 = c->dev<int64_t>(S_BM_AUX1, 2 * ((size_t)P + 2) + 2 * ((size_t)E + 1) + 4);
+    uint32_t *bits = c->dev<uint32_t>(S_BM_AUX2, 2 * (size_t)nwb + 2);
+    uint8_t *done = c->dev<uint8_t>(S_BM_AUX3, (size_t)P + 16);
+    if (!d_off || !d_verts || !d_es || !d_ed || !d_out || !d_occ || !i32 || !i64 || !bits || !done)
+        return cuda_fail(cudaErrorMemoryAllocation, "batch_moves workspace", detail);
+    int32_t *outdeg = i32, *indeg = outdeg + (P + 1), *fill = indeg + (P + 1), *fill2 = fill + (P + 1);
+    int32_t *succ = fill2 + (P + 1), *in_src = succ + E, *misc = in_src + E, *ar = misc + 16;
+    int32_t *bad = misc, *processed = misc + 1, *counter = misc + 2, *res = misc + 4;
+    int64_t *soff = i64, *in_off = soff + (P + 2), *need = in_off + (P + 2), *need_sorted = need + (E + 1);
+    CK(cudaMemsetAsync(i32, 0, n32 * 4, st), "memset");
+    if (P > 0) {
+        CK(cudaMemcpyAsync(d_off, off, ((size_t)P + 1) * 8, cudaMemcpyHostToDevice, st), "H2D");
+        CK(cudaMemcpyAsync(d_verts, verts, (size_t)nverts * 4, cudaMemcpyHostToDevice, st), "H2D");
+    }
+    if (E > 0) {
+        CK(cudaMemcpyAsync(d_es, es, (size_t)E * 4, cudaMemcpyHostToDevice, st), "H2D");
+        CK(cudaMemcpyAsync(d_ed, ed, (size_t)E * 4, cudaMemcpyHostToDevice, st), "H2D");
+    }
+    CK(cudaMemcpyAsync(d_occ, occ, (size_t)width * wpc * 8, cudaMemcpyHostToDevice, st), "H2D");
+    const int blocks = 148 * 4;
+    // MoveDag::is_acyclic (batching.cpp:34): endpoint range + Kahn
+    edges_check_kernel<<<blocks, 256, 0, st>>>(P, E, d_es, d_ed, bad, outdeg, indeg);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, (const int32_t *)nullptr, (int64_t *)nullptr, P + 1);
+    void *temp = c->get(S_TEMP, tb);
+    if (!temp) return cuda_fail(cudaErrorMemoryAllocation, "temp", detail);
+    // soff = exclusive scan of outdeg (widened)
+    {
+        std::vector<int32_t> h_bad(1);
+        CK(cudaMemcpyAsync(h_bad.data(), bad, 4, cudaMemcpyDeviceToHost, st), "D2H");
+        CK(cudaStreamSynchronize(st), "check");
+        if (h_bad[0]) {
+            if (detail) *detail = RECON_D_BATCH_CYCLIC;
+            return RECON_ERR_INPUT;
+        }
+    }
+    auto widen_scan = [&](const int32_t *deg, int64_t *out) -> cudaError_t {
+        size_t t2 = tb;
+        return cub::DeviceScan::ExclusiveSum(temp, t2, deg, out, P + 1, st);
+    };
+    CK(cudaMemsetAsync(outdeg + P, 0, 4, st), "memset");
+    CK(widen_scan(outdeg, soff), "scan");
+    csr_fill_kernel<<<blocks, 256, 0, st>>>(E, d_es, d_ed, soff, fill, succ, nullptr, nullptr);
+    // Kahn on a copy of the in-degrees
+    int32_t *indeg_copy = ar + 10 * P;  // ar[10P, 11P)
+    copy_i32<<<blocks, 256, 0, st>>>(P, indeg, indeg_copy);
+    kahn_kernel<<<1, 1024, 0, st>>>(P, soff, succ, indeg_copy, ar, ar + P, processed);
+    c->launches += 5;
+    int32_t h_proc = 0;
+    CK(cudaMemcpyAsync(&h_proc, processed, 4, cudaMemcpyDeviceToHost, st), "D2H");
+    CK(cudaStreamSynchronize(st), "kahn");
+    if (h_proc != P) {
+        if (detail) *detail = RECON_D_BATCH_CYCLIC;
+        return RECON_ERR_INPUT;
+    }
+    BatchJob J{};
+    J.P = P;
+    J.W = width;
+    J.H = height;
+    J.preset = preset;
+    J.edge_level = edge_level ? 1 : 0;
+    J.soff = soff;
+    J.succ = succ;
+    if (edge_level) {
+        // incoming CSR with release thresholds (batching.cpp:38-59)
+        need_kernel<<<blocks, 256, 0, st>>>(E, d_es, d_ed, d_off, d_verts, need);
+        CK(cudaMemsetAsync(indeg + P, 0, 4, st), "memset");
+        size_t t2 = tb;
+        CK(cub::DeviceScan::ExclusiveSum(temp, t2, indeg, in_off, P + 1, st), "scan");
+        csr_fill_kernel<<<blocks, 256, 0, st>>>(E, d_ed, d_es, in_off, fill2, in_src, need, need_sorted);
+        J.in_off = in_off;
+        J.in_src = in_src;
+        J.in_need = need_sorted;
+        c->launches += 2;
+    }
+    J.s.occ = bits;
+    J.s.inb = bits + nwb;
+    occ_to_vertex_bits<<<blocks, 256, 0, st>>>(1, width, height, d_occ, bits);
+    CK(cudaMemsetAsync(bits + nwb, 0, (size_t)nwb * 4, st), "memset");
+    J.s.next = ar;
+    J.s.blockers = indeg;
+    J.s.done = done;
+    J.s.ready = ar + P;
+    J.s.ready2 = ar + 2 * P;
+    J.s.newly = ar + 3 * P;
+    J.s.mem = ar + 4 * P;
+    J.s.mfr = ar + 5 * P;
+    J.s.mto = ar + 6 * P;
+    J.s.counter = counter;
+    J.move_batch = d_out;
+    J.batch_count = res;
+    J.status = res + 1;
+    J.detail = res + 2;
+    CK(launch_batch_explicit(J, d_off, d_verts, st), "batch launch");
+    c->launches += 2;
+    int32_t h_res[3];
+    CK(cudaMemcpyAsync(h_res, res, 12, cudaMemcpyDeviceToHost, st), "D2H");
+    CK(cudaStreamSynchronize(st), "batching");
+    if (h_res[1] != RECON_OK) {
+        if (detail) *detail = h_res[2];
+        return (recon_status)h_res[1];
+    }
+    *batch_count = h_res[0];
+    if (moves > 0) {
+        CK(cudaMemcpyAsync(move_batch, d_out, (size_t)moves * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        CK(cudaStreamSynchronize(st), "D2H");
+    }
+    return RECON_OK;
+}
+
+recon_status recon_pipeline_batch_run(recon_ctx *ctx, const recon_pipeline_batch *pb) {
+    return pipeline_impl(ctx, pb, false);
+}
+
+recon_status recon_pipeline_batch_run_host(recon_ctx *ctx, const recon_pipeline_batch *pb) {
+    return pipeline_impl(ctx, pb, true);
+}
+
+}  // extern "C"

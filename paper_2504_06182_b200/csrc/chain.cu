@@ -1,0 +1,362 @@
+// Exact 1D chain solve (solve_1d / assign_1d) on sm_100a.
+//
+// Reference: /root/reference/proj/src/exact1d.cpp:219-372 (candidate and
+// certified blocks, per-block window DP), :430-562 (paths, nesting, order).
+//
+// Band mode (targets = one contiguous run [tl, th], the batched C2 workload):
+// one WARP per chain.
+//   * candidate cuts (exact1d.cpp:219-247) are a prefix-max scan: with
+//     D(v) = #S<v - #T<v and E = |S|-|T|, an empty vertex v is a cut iff
+//     D(v) <= E and D(v) >= max(0, D(u)) over earlier eligible empty u;
+//   * the target block is the one holding [tl, th] (no cut can fall inside);
+//     source-only blocks cost 0 and never merge with each other (0 < 0 is
+//     false), so the certification sweep (exact1d.cpp:255-297) only ever tests
+//     joins with the target block; it is simulated literally (same i / --i
+//     walk) on the block-boundary list;
+//   * block costs and the final assignment use the split rule: residents
+//     (sources inside [tl, th]) are always used (leaving one unused is strictly
+//     worse), a = sources taken from the left, cost(a) convex, and the
+//     reference's tie rule (lex-min use vector read from the last source,
+//     exact1d.cpp:155-207) is the LARGEST minimiser;
+//   * pairs are order preserving, so resolve_nesting (exact1d.cpp:454-492) is
+//     the identity and path i = (i-th used source, tl + i); the used sources
+//     are a contiguous run of the sorted sources.
+
+#include <climits>
+
+#include "chain.cuh"
+#include "common.cuh"
+
+namespace rb {
+
+struct ChainCtx {
+    int tl, th, k;
+    int ns, idxL, idxR, R;  // sources; #S < tl; #S <= th; residents
+    const int16_t *S;       // sorted sources
+};
+
+// #(residents with e < a), e_r = S[idxL+r] - tl - r (non-decreasing)
+__device__ __forceinline__ int cnt_e_lt(const ChainCtx &c, int a) {
+    int lo = 0, hi = c.R;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (c.S[c.idxL + mid] - c.tl - mid < a) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Delta(a) = cost(a) - cost(a-1)
+__device__ __forceinline__ long long chain_delta(const ChainCtx &c, int a) {
+    const int b = (c.k - c.R) - a;
+    return (long long)(c.tl + a - 1) - c.S[c.idxL - a] + 2LL * cnt_e_lt(c, a) - c.R - c.S[c.idxR + b] + c.th - b;
+}
+
+// largest a in [amin, amax] with Delta(a) <= 0 for all amin < a' <= a (32-ary search)
+__device__ int chain_best_a(const ChainCtx &c, int amin, int amax) {
+    const int lane = lane_id();
+    int lo = amin, hi = amax;
+    while (hi > lo) {
+        const int step = (hi - lo + 31) / 32;
+        const int a = lo + 1 + lane * step;
+        const bool ok = a <= hi && chain_delta(c, a) <= 0;
+        const unsigned m = __ballot_sync(FULL, ok);
+        if (!m) break;
+        const int a_last = lo + 1 + (31 - __clz(m)) * step;
+        if (step == 1) {
+            lo = a_last;
+            break;
+        }
+        lo = a_last;
+        hi = min(hi, a_last + step - 1);
+    }
+    return lo;
+}
+
+// split-rule cost at a (warp-cooperative range sums)
+__device__ long long chain_cost(const ChainCtx &c, int a) {
+    const int b = (c.k - c.R) - a;
+    const int m = cnt_e_lt(c, a);
+    long long top = 0, resm = 0, resR = 0, bot = 0;
+    for (int i = c.idxL - a + lane_id(); i < c.idxR + b; i += 32) {
+        const long long v = c.S[i];
+        if (i < c.idxL) top += v;
+        else if (i < c.idxR) {
+            resR += v;
+            if (i < c.idxL + m) resm += v;
+        } else bot += v;
+    }
+    top = warp_sum64(top);
+    resm = warp_sum64(resm);
+    resR = warp_sum64(resR);
+    bot = warp_sum64(bot);
+    const long long Em = resm - (long long)m * c.tl - (long long)m * (m - 1) / 2;
+    const long long ER = resR - (long long)c.R * c.tl - (long long)c.R * (c.R - 1) / 2;
+    long long cost = (long long)a * c.tl + (long long)a * (a - 1) / 2 - top;
+    cost += (long long)a * m - Em + (ER - Em) - (long long)a * (c.R - m);
+    cost += bot - ((long long)b * c.th - (long long)b * (b - 1) / 2);
+    return cost;
+}
+
+// optimum over sources S[s0, s1) (holding every resident); *best_a = -1 if infeasible
+__device__ long long block_opt(const ChainCtx &c, int s0, int s1, int *best_a) {
+    const int holes = c.k - c.R;
+    const int amin = max(0, holes - (s1 - c.idxR)), amax = min(c.idxL - s0, holes);
+    if (amin > amax) {
+        *best_a = -1;
+        return LLONG_MAX / 4;
+    }
+    const int a = chain_best_a(c, amin, amax);
+    *best_a = a;
+    return chain_cost(c, a);
+}
+
+__global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = lane_id(), warp = warp_id(), nw = blockDim.x >> 5;
+    const int n = p.n, tl = p.t_lo, th = p.t_hi, k = th - tl + 1;
+    const int words64 = (n + 63) / 64;
+    const int per32 = (n + 1023) / 1024;  // u32 words per lane (<= 4)
+    int16_t *S = (int16_t *)(smem + (size_t)warp * p.warp_smem);
+    int16_t *B = (int16_t *)(smem + (size_t)warp * p.warp_smem + p.b_off);   // block boundaries
+    int16_t *BE = (int16_t *)(smem + (size_t)warp * p.warp_smem + p.be_off);  // kept block ends
+    for (int ch = blockIdx.x * nw + warp; ch < p.count; ch += gridDim.x * nw) {
+        const uint32_t *bits = (const uint32_t *)(p.occ + (size_t)ch * words64);
+        uint32_t w[4] = {0u, 0u, 0u, 0u};
+        int cnt = 0;
+        for (int q = 0; q < per32; ++q) {
+            const int wi = lane * per32 + q;
+            if (wi * 32 < n) {
+                w[q] = bits[wi];
+                if (n - wi * 32 < 32) w[q] &= (1u << (n - wi * 32)) - 1u;
+            }
+            cnt += __popc(w[q]);
+        }
+        int ns;
+        const int base_ps = warp_excl_scan(cnt, &ns);
+        {
+            int e = base_ps;
+            for (int q = 0; q < per32; ++q)
+                for (uint32_t x = w[q]; x; x &= x - 1) S[e++] = (int16_t)((lane * per32 + q) * 32 + __ffs(x) - 1);
+        }
+        __syncwarp();
+        ChainCtx c;
+        c.tl = tl;
+        c.th = th;
+        c.k = k;
+        c.ns = ns;
+        c.S = S;
+        {
+            int l = 0, r = 0;
+            for (int q = 0; q < per32; ++q) {
+                const int v0 = (lane * per32 + q) * 32;
+                l += __popc(w[q] & chunk_range(v0, 32, 0, tl));
+                r += __popc(w[q] & chunk_range(v0, 32, 0, th + 1));
+            }
+            c.idxL = warp_sum(l);
+            c.idxR = warp_sum(r);
+        }
+        c.R = c.idxR - c.idxL;
+        int status = RECON_OK, detail = 0, a = -1;
+        int s0 = 0, s1 = ns;
+        if (ns < k) {  // validate_chain_instance (exact1d.cpp:311)
+            status = RECON_ERR_INFEASIBLE;
+            detail = RECON_D_FEWER_SOURCES;
+        } else {
+            // ---- candidate cuts (exact1d.cpp:219-247) as a prefix-max scan
+            const int E = ns - k;
+            int lmax = INT_MIN, ncut = 0;
+            {
+                int ps = base_ps;
+                for (int q = 0; q < per32; ++q)
+                    for (int bb = 0; bb < 32; ++bb) {
+                        const int v = (lane * per32 + q) * 32 + bb;
+                        if (v >= n) break;
+                        const bool s = (w[q] >> bb) & 1u;
+                        const int D = ps - min(max(v - tl, 0), k);
+                        if (!s && (v < tl || v > th) && D <= E) lmax = max(lmax, D);
+                        ps += s;
+                    }
+            }
+            int incl = lmax;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl = max(incl, y);
+            }
+            int run0 = __shfl_up_sync(FULL, incl, 1);
+            if (lane == 0) run0 = 0;
+            run0 = max(run0, 0);
+            for (int pass = 0; pass < 2; ++pass) {
+                int run = run0, ps = base_ps, slot = 0;
+                if (pass == 1) {
+                    int tot;
+                    slot = 1 + warp_excl_scan(ncut, &tot);
+                    if (lane == 0) {
+                        B[0] = 0;
+                        B[tot + 1] = (int16_t)ns;
+                    }
+                    ncut = tot;
+                }
+                int mine = 0;
+                for (int q = 0; q < per32; ++q)
+                    for (int bb = 0; bb < 32; ++bb) {
+                        const int v = (lane * per32 + q) * 32 + bb;
+                        if (v >= n) break;
+                        const bool s = (w[q] >> bb) & 1u;
+                        const int D = ps - min(max(v - tl, 0), k);
+                        if (!s && (v < tl || v > th) && D <= E && D >= run) {
+                            run = D;
+                            if (pass == 0) ++mine;
+                            else B[slot++] = (int16_t)ps;
+                        }
+                        ps += s;
+                    }
+                if (pass == 0) ncut = mine;
+            }
+            __syncwarp();
+            // boundaries B[0..ncut+1]; cut j is left of tl iff B[j] <= idxL and
+            // it was found before tl: count left cuts = cuts with vertex < tl.
+            // A cut at vertex v < tl has ps <= idxL; a cut at v > th has ps >= idxR.
+            // (idxL == idxR only if there are no residents; disambiguate via the
+            // number of left cuts computed from vertex positions.)
+            int nleft = 0;
+            {
+                int run = run0, ps = base_ps;
+                for (int q = 0; q < per32; ++q)
+                    for (int bb = 0; bb < 32; ++bb) {
+                        const int v = (lane * per32 + q) * 32 + bb;
+                        if (v >= n || v >= tl) break;
+                        const bool s = (w[q] >> bb) & 1u;
+                        const int D = ps - min(max(v - tl, 0), k);
+                        if (!s && D <= E && D >= run) {
+                            run = D;
+                            ++nleft;
+                        }
+                        ps += s;
+                    }
+                nleft = warp_sum(nleft);
+            }
+            // non-empty blocks: [B[q], B[q+1]) for q in [0, ncut]; the target is
+            // q == nleft (it holds the targets even without sources)
+            int nb = 0, t = 0;
+            for (int q0 = 0; q0 <= ncut; q0 += 32) {
+                const int q = q0 + lane;
+                const bool keep = q <= ncut && (B[q + 1] > B[q] || q == nleft);
+                const int st = q <= ncut ? B[q] : 0, en = q <= ncut ? B[q + 1] : 0;
+                const unsigned m = __ballot_sync(FULL, keep);
+                __syncwarp();
+                const int j = nb + __popc(m & lanemask_lt());
+                if (keep) {
+                    B[j] = (int16_t)st;  // in-place compaction (j <= q)
+                    BE[j] = (int16_t)en;
+                    if (q == nleft) t = j;
+                }
+                nb += __popc(m);
+                __syncwarp();
+            }
+            t = warp_max(t);
+            s0 = B[t];
+            s1 = BE[t];
+            if (nb > 1) {
+                int ba;
+                const long long global = block_opt(c, 0, ns, &ba);
+                long long wt = block_opt(c, s0, s1, &ba);
+                if (wt != global) {
+                    // literal sweep (exact1d.cpp:269-289): blocks tL..tR form the
+                    // target; list index i maps to the current merged list
+                    int tL = t, tR = t, i = tL >= 1 ? tL - 1 : 0;
+                    const int nb0 = nb;
+                    for (;;) {
+                        const int ncur = nb0 - (tR - tL);
+                        if (i + 1 >= ncur) break;
+                        if (i + 1 < tL) {  // two source-only blocks: 0 < 0 is false
+                            i = tL - 1;
+                            continue;
+                        }
+                        if (i > tL) break;  // only source-only pairs remain
+                        int tmp;
+                        if (i + 1 == tL) {  // (left neighbour, target)
+                            const long long wj = block_opt(c, B[tL - 1], BE[tR], &tmp);
+                            if (wj < wt) {
+                                --tL;
+                                wt = wj;
+                                if (i > 0) --i;
+                            } else {
+                                ++i;
+                            }
+                        } else {  // i == tL: (target, right neighbour)
+                            const long long wj = block_opt(c, B[tL], BE[tR + 1], &tmp);
+                            if (wj < wt) {
+                                ++tR;
+                                wt = wj;
+                                if (i > 0) --i;
+                            } else {
+                                ++i;
+                            }
+                        }
+                    }
+                    s0 = B[tL];
+                    s1 = BE[tR];
+                    if (wt != global) {  // whole chain (exact1d.cpp:293-296)
+                        s0 = 0;
+                        s1 = ns;
+                    }
+                }
+            }
+            block_opt(c, s0, s1, &a);
+            if (a < 0) {
+                status = RECON_ERR_INFEASIBLE;
+                detail = RECON_D_GEN_NO_ASSIGNMENT;
+            }
+        }
+        // ---- paths: used sources are S[idxL - a, idxL - a + k)
+        long long disp = 0;
+        int displaced = 0;
+        if (status == RECON_OK) {
+            const int first = c.idxL - a;
+            int32_t *ps_out = p.path_src + (size_t)ch * k;
+            int32_t *pd_out = p.path_dst + (size_t)ch * k;
+            for (int i = lane; i < k; i += 32) {
+                const int src = S[first + i];
+                const int dst = tl + i;
+                ps_out[i] = src;
+                pd_out[i] = dst;
+                disp += src > dst ? src - dst : dst - src;
+                displaced += src != dst;
+            }
+            disp = warp_sum64(disp);
+            displaced = warp_sum(displaced);
+        }
+        if (lane == 0) {
+            p.total_displacement[ch] = status == RECON_OK ? disp : 0;
+            p.displaced[ch] = status == RECON_OK ? displaced : 0;
+            p.status[ch] = status;
+            if (p.detail) p.detail[ch] = detail;
+            if (p.use_first) p.use_first[ch] = status == RECON_OK ? c.idxL - a : -1;
+        }
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_chain_band(const ChainBandParams &p0, int sms, cudaStream_t st) {
+    ChainBandParams p = p0;
+    const int n = p.n;
+    if (n <= 0 || n > 4096) return cudaErrorInvalidValue;
+    p.b_off = (int)(((size_t)n * 2 + 15) / 16 * 16);
+    p.be_off = p.b_off + (int)(((size_t)(n + 2) * 2 + 15) / 16 * 16);
+    p.warp_smem = p.be_off + (int)(((size_t)(n + 2) * 2 + 15) / 16 * 16);
+    const int warps = 8;
+    const size_t smem = (size_t)warps * p.warp_smem;
+    cudaError_t e = cudaFuncSetAttribute(chain_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chain_band_kernel, warps * 32, smem);
+    const long long want = ((long long)p.count + warps - 1) / warps;
+    const long long cap = (long long)(per_sm > 0 ? per_sm : 1) * sms;
+    const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
+    chain_band_kernel<<<grid, warps * 32, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace rb
