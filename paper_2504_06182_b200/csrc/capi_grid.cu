@@ -40,6 +40,13 @@ int grid_blocks(Ctx *c, int solver, const GridShape &s, int count) {
     return std::max(1, std::min(count, occ * c->sms));
 }
 
+// launches with the per-CTA snapshot scratch the red-rec kernel needs
+cudaError_t launch(Ctx *c, int solver, GridParams &p, int grid) {
+    p.snap = c->dev<uint64_t>(S_SNAP, (size_t)grid * grid_snap_words(p.shape));
+    if (!p.snap) return cudaErrorMemoryAllocation;
+    return launch_grid_solver(solver, p, grid, c->stream);
+}
+
 // runs the DAG over `P` device-resident paths; copies edges to host arrays
 recon_status run_dag(Ctx *c, int W, int H, const int32_t *d_src, const int32_t *d_dst, int64_t P,
                      int32_t *h_a, int32_t *h_b, int64_t cap, int64_t *count, int32_t *detail) {
@@ -110,7 +117,7 @@ recon_status grid_single(int solver, recon_ctx *ctx, const uint64_t *occ, int W,
         !p.status || !p.detail || !p.events)
         return cuda_fail(cudaErrorMemoryAllocation, "grid workspace", detail);
     CK(cudaMemcpyAsync(d_occ, occ, words * 8, cudaMemcpyHostToDevice, c->stream), "occ H2D");
-    CK(launch_grid_solver(solver, p, 1, c->stream), "grid kernel launch");
+    CK(launch(c, solver, p, 1), "grid kernel launch");
     c->launches += 1;
     int32_t h_cnt = 0, h_st = 0, h_det = 0;
     int64_t h_td = 0;
@@ -176,7 +183,7 @@ recon_status grid_batch(int solver, recon_ctx *ctx, const recon_grid_batch *b, b
         p.status = b->status;
         p.detail = b->detail;
         p.events = b->events;
-        CK(launch_grid_solver(solver, p, grid_blocks(c, solver, s, b->count), c->stream), "grid kernel launch");
+        CK(launch(c, solver, p, grid_blocks(c, solver, s, b->count)), "grid kernel launch");
         c->launches += 1;
         return RECON_OK;
     }
@@ -194,7 +201,7 @@ recon_status grid_batch(int solver, recon_ctx *ctx, const recon_grid_batch *b, b
         !p.total_displacement || !p.status || !p.detail || (b->events && !p.events))
         return cuda_fail(cudaErrorMemoryAllocation, "grid batch workspace", detail);
     CK(cudaMemcpyAsync(d_occ, b->occ, n * words * 8, cudaMemcpyHostToDevice, c->stream), "occ H2D");
-    CK(launch_grid_solver(solver, p, grid_blocks(c, solver, s, b->count), c->stream), "grid kernel launch");
+    CK(launch(c, solver, p, grid_blocks(c, solver, s, b->count)), "grid kernel launch");
     c->launches += 1;
     CK(cudaMemcpyAsync(b->path_src, p.path_src, n * stride * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
     CK(cudaMemcpyAsync(b->path_dst, p.path_dst, n * stride * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
@@ -252,3 +259,33 @@ recon_status recon_occupancy_dag(recon_ctx *ctx, int32_t width, int32_t height, 
 }
 
 }  // extern "C"
+
+// Profiling hook (not part of the public ABI): solves one instance and
+// returns clock64 stamps at the kernel's phase boundaries (plan, phase 1 +
+// pairing loop, phase 3) plus the phase-1 / loop event counts.
+extern "C" recon_status recon_debug_grid_phases(int32_t solver, const uint64_t *occ, int32_t W, int32_t H,
+                                                int32_t hp, long long *out6) {
+    int32_t *detail = nullptr;
+    Ctx *c = resolve(nullptr);
+    if (!c) return RECON_ERR_CUDA;
+    GridShape s;
+    if (!grid_shape(W, H, hp, kWarps, s)) return RECON_ERR_ARGUMENT;
+    const size_t words = (size_t)W * s.wpd, stride = (size_t)W * hp;
+    GridParams p{};
+    p.shape = s;
+    p.count = 1;
+    uint64_t *d_occ = c->dev<uint64_t>(S_OCC, words);
+    p.occ = d_occ;
+    p.path_src = c->dev<int32_t>(S_PSRC, stride);
+    p.path_dst = c->dev<int32_t>(S_PDST, stride);
+    p.path_count = c->dev<int32_t>(S_PCNT, 1);
+    p.total_displacement = c->dev<int64_t>(S_TDISP, 1);
+    p.status = c->dev<int32_t>(S_STATUS, 1);
+    p.detail = c->dev<int32_t>(S_DETAIL, 1);
+    p.phase_clock = c->dev<long long>(S_KEYS, 8);
+    CK(cudaMemcpyAsync(d_occ, occ, words * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+    CK(launch(c, solver, p, 1), "launch");
+    CK(cudaMemcpyAsync(out6, p.phase_clock, 6 * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    CK(cudaStreamSynchronize(c->stream), "sync");
+    return RECON_OK;
+}

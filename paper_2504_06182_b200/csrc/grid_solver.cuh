@@ -19,8 +19,8 @@ struct GridShape {
 };
 
 struct GridSmem {
-    int64_t dep, keys, bal, sigma, ev_count, ev_off, lvl_t, lvl_b, scal, lists, plists, mark_dest, ev_col,
-        ev_aux, ev_a, ev_type, solved, total;
+    int64_t dep, keys, bal, sigma, ev_count, ev_off, wave_off, lvl_t, lvl_b, scal, lists, plists, mark_dest,
+        ev_col, ev_aux, ev_a, ev_level, wave_list, lastc, lastm, ev_type, solved, total;
 };
 
 struct GridParams {
@@ -31,10 +31,13 @@ struct GridParams {
     int32_t *path_count;
     int64_t *total_displacement;
     int32_t *status, *detail, *events;
+    uint64_t *snap;          // red-rec: per-CTA event snapshots, 2*W*wpd words per CTA (grid-sized)
+    long long *phase_clock;  // optional: clock64 at phase boundaries of instance 0 (profiling)
 };
 
 bool grid_shape(int W, int H, int k, int nwarps, GridShape &s);
 cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaStream_t stream);
 int grid_occupancy(int solver, const GridShape &s);
+size_t grid_snap_words(const GridShape &s);
 
 }  // namespace rb

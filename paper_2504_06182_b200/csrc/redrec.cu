@@ -1,0 +1,623 @@
+// red-rec on sm_100a: one CTA per instance.
+//
+// Reference: /root/reference/proj/src/redrec.cpp:15-232.
+//
+// 1. Plan (warp 0).  red-rec's control flow depends only on the surplus
+//    vector (the pairing loop reads sigma and `solved`, redrec.cpp:43-86,
+//    205-232), so the whole event sequence is replayed first from sigma.
+//    Per lane, a block of <= 32 columns is held as register bitmasks
+//    (receivers, donors; unsolved = non-transit), so the nearest
+//    non-transit column on either side of a receiver (scan_for_donor,
+//    redrec.cpp:43-51) is a bit-scan plus a warp max/min scan instead of a
+//    walk through shared memory.  The plan also assigns each pairing-loop
+//    event a dependency level: 1 + the last level touching any column it
+//    reads/writes or the mark set of its receiver.
+// 2. Waves.  Loop events of one level touch disjoint state and run
+//    concurrently, one warp per event; each records its split `a`, its path
+//    count, and a snapshot of the masks it read (global scratch).
+// 3. Phase-3 compactions are solved in parallel on the final state.
+// 4. One scan over all W events in canonical order gives every event's
+//    output offset; every event is re-materialised from its snapshot and
+//    emitted in parallel.
+// Marks (parked tokens of a donating compaction, redrec.cpp:155-160) stay in
+// the marker's column plane and are never cleared: only their receiver's
+// transfer reads them, in both passes.
+
+#include "grid_common.cuh"
+
+namespace rb {
+
+// --------------------------------------------------------------------------
+// warp-level transfer event (Runner::flush + build_redistribution_instance,
+// redrec.cpp:92-116, 169-191): receiver r's own tokens and the marks parked
+// for it are mandatory, donor d's reservoir is the optional pool
+// --------------------------------------------------------------------------
+
+struct FlushSolve {
+    int a, b, R, holes, m_top, m_bot, n_ot, n_ob, n_right, n_left, dd;
+};
+
+__device__ bool flush_solve(const Geo &g, const uint64_t *mr, const uint64_t *md, int r, int d, const uint64_t *dep,
+                            const int16_t *mark_dest, int16_t *L, int forced_a, FlushSolve &f) {
+    int16_t *otop = L, *obot = L + g.LK, *hole = L + 2 * g.LK, *res = L + 3 * g.LK;
+    const int lane = lane_id(), B = g.B, base = lane * B;
+    const int dd = d > r ? d - r : r - d;
+    const uint32_t rtop = chunk_range(base, B, 0, g.lo), rband = chunk_range(base, B, g.lo, g.hi + 1),
+                   rbot = chunk_range(base, B, g.hi + 1, g.H);
+    const uint32_t chr = lane_chunk(mr, g.wpd, lane, B);
+    const uint32_t resm = chr & rband, holem = ~chr & rband;
+    int R, nh;
+    int er = warp_excl_scan(__popc(resm), &R);
+    int eh = warp_excl_scan(__popc(holem), &nh);
+    const int holes = nh;
+    for (uint32_t x = holem; x; x &= x - 1, ++eh) hole[eh + 1] = (int16_t)(base + __ffs(x) - 1);
+    for (uint32_t x = resm; x; x &= x - 1, ++er) res[er] = (int16_t)(base + __ffs(x) - 1);
+    int m_top = __popc(chr & rtop), m_bot = __popc(chr & rbot);
+    for (int x0 = 0; x0 < g.W; x0 += 32) {
+        unsigned mk = __ballot_sync(FULL, x0 + lane < g.W && mark_dest[x0 + lane] == r);
+        while (mk) {
+            const int x = x0 + __ffs(mk) - 1;
+            mk &= mk - 1;
+            const uint32_t chx = lane_chunk(dep + (size_t)x * g.wpd, g.wpd, lane, B);
+            m_top += __popc(chx & rtop);
+            m_bot += __popc(chx & rbot);
+        }
+    }
+    m_top = warp_sum(m_top);
+    m_bot = warp_sum(m_bot);
+    const uint32_t chd = lane_chunk(md, g.wpd, lane, B);
+    const uint32_t dtop = chd & rtop, dbot = chd & rbot;
+    int n_ot, n_ob;
+    int et = warp_excl_scan(__popc(dtop), &n_ot);
+    int eb = warp_excl_scan(__popc(dbot), &n_ob);
+    for (uint32_t x = dtop; x; x &= x - 1, ++et) {
+        const int desc = n_ot - 1 - et;
+        if (desc < holes) otop[desc + 1] = (int16_t)(base + __ffs(x) - 1 - dd);
+    }
+    for (uint32_t x = dbot; x; x &= x - 1, ++eb)
+        if (eb < holes) obot[eb + 1] = (int16_t)(base + __ffs(x) - 1 + dd);
+    if (lane == 0) {
+        hole[0] = (int16_t)(g.lo - 1);
+        hole[holes + 1] = (int16_t)(g.hi + 1);
+    }
+    __syncwarp();
+    const int amin = max(m_top, holes - m_bot - n_ob), amax = min(m_top + n_ot, holes - m_bot);
+    if (amin > amax) return false;
+    int a = forced_a;
+    if (a < 0) {
+        int cnt = 0;
+        for (int a0 = amin + 1; a0 <= amax; a0 += 32) {
+            const int aa = a0 + lane;
+            bool le = false;
+            if (aa <= amax) {
+                const int delta = (g.lo + aa - 1) - otop[aa - m_top] + 2 * (hole[aa] - g.lo - aa + 1) - R -
+                                  obot[holes - aa + 1 - m_bot] + g.hi - (holes - aa);
+                le = delta <= 0;
+            }
+            cnt += __popc(__ballot_sync(FULL, le));
+        }
+        a = amin + cnt;
+    }
+    f.a = a;
+    f.b = holes - a;
+    f.R = R;
+    f.holes = holes;
+    f.m_top = m_top;
+    f.m_bot = m_bot;
+    f.n_ot = n_ot;
+    f.n_ob = n_ob;
+    f.dd = dd;
+    const int cntE = hole[a] - g.lo - a + 1;
+    const int nstat = hole[a + 1] - hole[a] - 1;
+    f.n_right = a + cntE;
+    f.n_left = (R - cntE - nstat) + f.b;
+    return true;
+}
+
+__device__ long long flush_emit(const Geo &g, const FlushSolve &f, const uint64_t *mr, const uint64_t *md, int r,
+                                int d, const uint64_t *dep, const int16_t *mark_dest, const int16_t *L,
+                                uint32_t *keys, PathOut o, int off, int evid) {
+    const int16_t *res = L + 3 * g.LK;
+    const int lane = lane_id(), B = g.B, base = lane * B;
+    const uint32_t rtop = chunk_range(base, B, 0, g.lo), rbot = chunk_range(base, B, g.hi + 1, g.H);
+    const int a = f.a, b = f.b, R = f.R, dd = f.dd;
+    const int xa = a - f.m_top, xb = b - f.m_bot;
+    uint32_t *ktop = keys, *kbot = keys + g.LK;
+    {
+        const uint32_t chr = lane_chunk(mr, g.wpd, lane, B);
+        int tot;
+        int e = warp_excl_scan(__popc(chr & rtop), &tot);
+        for (uint32_t x = chr & rtop; x; x &= x - 1) ktop[e++] = tok_key(base + __ffs(x) - 1, 0, r);
+        int pos_t = tot;
+        e = warp_excl_scan(__popc(chr & rbot), &tot);
+        for (uint32_t x = chr & rbot; x; x &= x - 1) kbot[e++] = tok_key(base + __ffs(x) - 1, 0, r);
+        int pos_b = tot;
+        for (int x0 = 0; x0 < g.W; x0 += 32) {
+            unsigned mk = __ballot_sync(FULL, x0 + lane < g.W && mark_dest[x0 + lane] == r);
+            while (mk) {
+                const int x = x0 + __ffs(mk) - 1;
+                mk &= mk - 1;
+                const int dx = x > r ? x - r : r - x;
+                const uint32_t chx = lane_chunk(dep + (size_t)x * g.wpd, g.wpd, lane, B);
+                e = warp_excl_scan(__popc(chx & rtop), &tot);
+                for (uint32_t y = chx & rtop; y; y &= y - 1) ktop[pos_t + e++] = tok_key(base + __ffs(y) - 1 - dx, dx, x);
+                pos_t += tot;
+                e = warp_excl_scan(__popc(chx & rbot), &tot);
+                for (uint32_t y = chx & rbot; y; y &= y - 1) kbot[pos_b + e++] = tok_key(base + __ffs(y) - 1 + dx, dx, x);
+                pos_b += tot;
+            }
+        }
+        // donor: innermost xa top (largest depth), innermost xb bottom
+        const uint32_t chd = lane_chunk(md, g.wpd, lane, B);
+        const uint32_t dtop = chd & rtop, dbot = chd & rbot;
+        e = warp_excl_scan(__popc(dtop), &tot);
+        for (uint32_t x = dtop; x; x &= x - 1, ++e) {
+            const int desc = f.n_ot - 1 - e;
+            if (desc < xa) ktop[pos_t + desc] = tok_key(base + __ffs(x) - 1 - dd, dd, d);
+        }
+        e = warp_excl_scan(__popc(dbot), &tot);
+        for (uint32_t x = dbot; x; x &= x - 1, ++e)
+            if (e < xb) kbot[pos_b + e] = tok_key(base + __ffs(x) - 1 + dd, dd, d);
+    }
+    __syncwarp();
+    long long disp = 0;
+    for (int i = lane; i < a; i += 32) {
+        const uint32_t key = ktop[i];
+        int rank = 0;
+        for (int q = 0; q < a; ++q) rank += ktop[q] < key;
+        const int v = (int)(key >> 20) - 2048, dist = (key >> 10) & 1023, col = key & 1023;
+        const int depth = v + dist, j = rank, t = g.lo + j;
+        const int p = off + emit_slot(g, j, f.n_right, f.n_left);
+        o.src[p] = col * g.H + (g.H - 1 - depth);
+        o.dst[p] = r * g.H + (g.H - 1 - t);
+        if (o.ev) o.ev[p] = evid;
+        disp += t - v;
+    }
+    for (int i = lane; i < b; i += 32) {
+        const uint32_t key = kbot[i];
+        int rank = 0;
+        for (int q = 0; q < b; ++q) rank += kbot[q] < key;
+        const int v = (int)(key >> 20) - 2048, dist = (key >> 10) & 1023, col = key & 1023;
+        const int depth = v - dist, j = a + R + rank, t = g.lo + j;
+        const int p = off + emit_slot(g, j, f.n_right, f.n_left);
+        o.src[p] = col * g.H + (g.H - 1 - depth);
+        o.dst[p] = r * g.H + (g.H - 1 - t);
+        if (o.ev) o.ev[p] = evid;
+        disp += v - t;
+    }
+    for (int i = lane; i < R; i += 32) {
+        const int depth = res[i], j = a + i, t = g.lo + j;
+        if (t == depth) continue;
+        const int p = off + emit_slot(g, j, f.n_right, f.n_left);
+        o.src[p] = r * g.H + (g.H - 1 - depth);
+        o.dst[p] = r * g.H + (g.H - 1 - t);
+        if (o.ev) o.ev[p] = evid;
+        disp += t > depth ? t - depth : depth - t;
+    }
+    __syncwarp();
+    return warp_sum64(disp);
+}
+
+// donor loses its drawn innermost reservoir tokens; receiver keeps band cells
+__device__ void flush_update(const Geo &g, uint64_t *dep, int r, int d, const FlushSolve &f, const int16_t *L) {
+    const int16_t *otop = L, *obot = L + g.LK;
+    const int xa = f.a - f.m_top, xb = f.b - f.m_bot;
+    const int thr_t = xa >= 1 ? otop[xa] + f.dd : g.lo;  // clear donor top depth >= thr_t
+    const int thr_b = xb >= 1 ? obot[xb] - f.dd : g.hi;  // clear donor bottom depth <= thr_b
+    __syncwarp();
+    uint64_t *md = dep + (size_t)d * g.wpd;
+    for (int w = lane_id(); w < g.wpd; w += 32) {
+        md[w] &= ~(word_range(64 * w, thr_t, g.lo) | word_range(64 * w, g.hi + 1, thr_b + 1));
+        dep[(size_t)r * g.wpd + w] = word_range(64 * w, g.lo, g.hi + 1);
+    }
+    __syncwarp();
+}
+
+// --------------------------------------------------------------------------
+// plan: surplus-only replay of redrec.cpp:205-232 with dependency levels
+// --------------------------------------------------------------------------
+
+// key of receiver q: best of its nearest unsolved neighbours that are donors,
+// ranked (-exchange, |d-r|, deficit-exchange, r, d) (select_best_pair,
+// redrec.cpp:55-86); ~0 when neither side has an admissible donor
+__device__ __forceinline__ unsigned long long receiver_key(int q, int W, const int *sig, const uint8_t *solved,
+                                                           const int16_t *NL, const int16_t *NR) {
+    unsigned long long best = ~0ull;
+    const int deficit = -sig[q];
+    const int cand[2] = {NL[q], NR[q]};
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+        const int d = cand[side];
+        if (d < 0 || d >= W || solved[d] || sig[d] <= 0) continue;
+        const int ex = min(sig[d], deficit);
+        const unsigned long long key = ((unsigned long long)(4095 - ex) << 42) |
+                                       ((unsigned long long)(d > q ? d - q : q - d) << 32) |
+                                       ((unsigned long long)(deficit - ex) << 20) | ((unsigned long long)q << 10) |
+                                       (unsigned long long)d;
+        best = key < best ? key : best;
+    }
+    return best;
+}
+
+// Surplus-only replay of the pairing loop with incremental candidate keys.
+// Columns are "unsolved" (non-transit) or solved with zero surplus (transit,
+// scan_for_donor redrec.cpp:43-51); NL/NR link every column to its nearest
+// unsolved neighbour on each side.  An iteration changes only the donor d and
+// the receiver r, so only r and the receivers adjacent to d and r (their
+// nearest unsolved neighbours) need new keys; a column turning transit is
+// unlinked with two range updates.
+__device__ int redrec_plan(const Geo &g, Block &b, int *n1o, int *n2o, int *nlevo) {
+    const int lane = lane_id(), W = g.W;
+    const int per = (W + 31) / 32, c0 = lane * per, c1 = min(W, c0 + per);
+    int *sig = b.ev_count;                           // scratch: plan-time surplus
+    int16_t *NL = b.wave_list, *NR = b.ev_a;         // scratch until the plan ends
+    unsigned long long *rkey = (unsigned long long *)b.keys;
+    uint8_t *solved = b.solved;
+    uint32_t recvm = 0;
+    for (int c = c0; c < c1; ++c) {
+        const int s = b.sigma[c];
+        sig[c] = s;
+        solved[c] = s == 0;  // phase 1 solves every sigma == 0 column (redrec.cpp:211-212)
+        if (s < 0) recvm |= 1u << (c - c0);
+        b.lastc[c] = 0;
+        b.lastm[c] = 0;
+    }
+    int nev = 0;
+    for (int x0 = 0; x0 < W; x0 += 32) {
+        const int c = x0 + lane;
+        const bool z = c < W && b.sigma[c] == 0;
+        const unsigned bz = __ballot_sync(FULL, z);
+        if (z) {
+            const int slot = nev + __popc(bz & lanemask_lt());
+            b.ev_type[slot] = EV_OWN;
+            b.ev_col[slot] = (int16_t)c;
+            b.ev_aux[slot] = -1;
+        }
+        nev += __popc(bz);
+    }
+    const int n1 = nev;
+    // initial links: nearest unsolved (sigma != 0) column on each side
+    {
+        uint32_t ntm = 0;
+        for (int c = c0; c < c1; ++c)
+            if (b.sigma[c] != 0) ntm |= 1u << (c - c0);
+        int exL = ntm ? c0 + 31 - __clz(ntm) : -1;
+        int exR = ntm ? c0 + __ffs(ntm) - 1 : W;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, exL, o);
+            if (lane >= o) exL = max(exL, y);
+            const int z = __shfl_down_sync(FULL, exR, o);
+            if (lane + o < 32) exR = min(exR, z);
+        }
+        int left = __shfl_up_sync(FULL, exL, 1);
+        int right = __shfl_down_sync(FULL, exR, 1);
+        if (lane == 0) left = -1;
+        if (lane == 31) right = W;
+        for (int c = c0; c < c1; ++c) {
+            NL[c] = (int16_t)left;
+            if (b.sigma[c] != 0) left = c;
+        }
+        for (int c = c1 - 1; c >= c0; --c) {
+            NR[c] = (int16_t)right;
+            if (b.sigma[c] != 0) right = c;
+        }
+    }
+    __syncwarp();
+    for (uint32_t m = recvm; m; m &= m - 1) {
+        const int q = c0 + __ffs(m) - 1;
+        rkey[q] = receiver_key(q, W, sig, solved, NL, NR);
+    }
+    __syncwarp();
+    int nlev = 0;
+    for (;;) {
+        if (!__any_sync(FULL, recvm)) break;
+        unsigned long long best = ~0ull;
+        for (uint32_t m = recvm; m; m &= m - 1) {
+            const unsigned long long k = rkey[c0 + __ffs(m) - 1];
+            best = k < best ? k : best;
+        }
+        best = warp_min_u64(best);
+        if (best == ~0ull) return RECON_D_NO_DONOR;
+        const int d = (int)(best & 1023), r = (int)((best >> 10) & 1023);
+        const int ds = sig[d], def = -sig[r];
+        __syncwarp();
+        const bool own_r = r >= c0 && r < c1;
+        int tr0 = -1, tr1 = -1;  // columns turning transit
+        if (ds < def) {
+            tr0 = d;  // OWN(d, r): d donates by marking
+            if (lane == 0) {
+                const int lv = 1 + max((int)b.lastc[d], (int)b.lastm[r]);
+                b.lastc[d] = b.lastm[r] = (int16_t)lv;
+                nlev = max(nlev, lv);
+                b.ev_type[nev] = EV_OWN;
+                b.ev_col[nev] = (int16_t)d;
+                b.ev_aux[nev] = (int16_t)r;
+                b.ev_level[nev] = (int16_t)lv;
+                sig[r] += ds;
+                sig[d] = 0;
+                solved[d] = 1;
+            }
+            nev += 1;
+        } else {
+            // FLUSH(r, d), then OWN(d, -1) if the donor is exhausted exactly
+            tr0 = r;
+            if (ds == def) tr1 = d;
+            if (own_r) recvm &= ~(1u << (r - c0));
+            if (lane == 0) {
+                int lv = 1 + max(max((int)b.lastc[r], (int)b.lastc[d]), (int)b.lastm[r]);
+                b.lastc[r] = b.lastc[d] = b.lastm[r] = (int16_t)lv;
+                b.ev_type[nev] = EV_FLUSH;
+                b.ev_col[nev] = (int16_t)r;
+                b.ev_aux[nev] = (int16_t)d;
+                b.ev_level[nev] = (int16_t)lv;
+                nlev = max(nlev, lv);
+                sig[d] -= def;
+                sig[r] = 0;
+                solved[r] = 1;
+                if (ds == def) {
+                    lv += 1;
+                    b.lastc[d] = (int16_t)lv;
+                    b.ev_type[nev + 1] = EV_OWN;
+                    b.ev_col[nev + 1] = (int16_t)d;
+                    b.ev_aux[nev + 1] = -1;
+                    b.ev_level[nev + 1] = (int16_t)lv;
+                    nlev = max(nlev, lv);
+                    solved[d] = 1;
+                }
+            }
+            nev += ds == def ? 2 : 1;
+        }
+        __syncwarp();
+        // unlink columns that turned transit: [L, x) -> NR = R, (x, R] -> NL = L
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int x = t == 0 ? tr0 : tr1;
+            if (x < 0) continue;
+            const int L = NL[x], R = NR[x];
+            for (int c = max(L, 0) + lane; c < x; c += 32) NR[c] = (int16_t)R;
+            for (int c = x + 1 + lane; c <= min(R, W - 1); c += 32) NL[c] = (int16_t)L;
+            __syncwarp();
+        }
+        // refresh the keys of r and of the receivers adjacent to d and r
+        {
+            int q = -1;
+            if (lane == 0) q = r;
+            else if (lane == 1) q = NL[d];
+            else if (lane == 2) q = NR[d];
+            else if (lane == 3) q = NL[r];
+            else if (lane == 4) q = NR[r];
+            else if (lane == 5) q = d;
+            if (q >= 0 && q < W && !solved[q] && sig[q] < 0) rkey[q] = receiver_key(q, W, sig, solved, NL, NR);
+        }
+        __syncwarp();
+    }
+    const int n2 = nev - n1;
+    // phase 3: remaining columns ascending (redrec.cpp:228-229)
+    for (int x0 = 0; x0 < W; x0 += 32) {
+        const int c = x0 + lane;
+        const bool u = c < W && !solved[c];
+        const unsigned bu = __ballot_sync(FULL, u);
+        if (u) {
+            const int slot = nev + __popc(bu & lanemask_lt());
+            b.ev_type[slot] = EV_OWN;
+            b.ev_col[slot] = (int16_t)c;
+            b.ev_aux[slot] = -1;
+        }
+        nev += __popc(bu);
+    }
+    // waves: counting sort of the loop events by level -> wave_list / wave_off
+    nlev = __shfl_sync(FULL, nlev, 0);
+    for (int i = lane; i <= nlev + 1; i += 32) b.wave_off[i] = 0;
+    __syncwarp();
+    for (int e = n1 + lane; e < n1 + n2; e += 32) atomicAdd(&b.wave_off[b.ev_level[e]], 1);
+    __syncwarp();
+    if (lane == 0) {
+        int run = 0;
+        for (int lv = 0; lv <= nlev + 1; ++lv) {
+            const int c = b.wave_off[lv];
+            b.wave_off[lv] = run;
+            run += c;
+        }
+        for (int e = n1; e < n1 + n2; ++e) {
+            const int lv = b.ev_level[e];
+            b.wave_list[b.wave_off[lv]++] = (int16_t)e;
+        }
+        for (int lv = nlev + 1; lv >= 1; --lv) b.wave_off[lv] = b.wave_off[lv - 1];
+        b.wave_off[0] = 0;
+    }
+    __syncwarp();
+    *n1o = n1;
+    *n2o = n2;
+    *nlevo = nlev;
+    return 0;
+}
+
+// --------------------------------------------------------------------------
+// kernel
+// --------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) redrec_kernel(GridParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Geo g = make_geo(p.shape);
+    Block b = carve(p.shape, smem);
+    const int warp = warp_id(), lane = lane_id(), nw = blockDim.x >> 5;
+    int16_t *L = b.lists + (size_t)warp * 4 * g.LK;
+    uint32_t *keys = b.keys + (size_t)warp * 2 * g.LK;
+    uint64_t *snap = p.snap + (size_t)blockIdx.x * 2 * g.W * g.wpd;
+    __shared__ long long s_tokens;
+    __shared__ unsigned long long s_disp;
+    __shared__ int s_status, s_detail, s_n1, s_n2, s_nlev, s_total, s_fail;
+    for (int inst = blockIdx.x; inst < p.count; inst += gridDim.x) {
+        const size_t pbase = (size_t)inst * g.W * g.k;
+        PathOut o{p.path_src + pbase, p.path_dst + pbase, p.path_event ? p.path_event + pbase : nullptr};
+        if (threadIdx.x == 0) {
+            s_tokens = 0;
+            s_disp = 0;
+            s_status = RECON_OK;
+            s_detail = 0;
+            s_fail = 0;
+        }
+        __syncthreads();
+        load_instance(g, p.occ + (size_t)inst * g.W * g.wpd, b, &s_tokens);
+        __syncthreads();
+        if (threadIdx.x == 0 && s_tokens < (long long)g.W * g.k) {
+            s_status = RECON_ERR_INFEASIBLE;  // Problem::check (problem.hpp:113-116)
+            s_detail = RECON_D_FEWER_SOURCES;
+        }
+        __syncthreads();
+        if (p.phase_clock && inst == 0 && threadIdx.x == 0) p.phase_clock[0] = clock64();
+        if (s_status == RECON_OK && warp == 0) {
+            int n1 = 0, n2 = 0, nlev = 0;
+            const int rc = redrec_plan(g, b, &n1, &n2, &nlev);
+            if (lane == 0) {
+                s_n1 = n1;
+                s_n2 = n2;
+                s_nlev = nlev;
+                if (rc) {
+                    s_status = RECON_ERR_LOGIC;
+                    s_detail = rc;
+                }
+            }
+        }
+        __syncthreads();
+        if (s_status == RECON_OK) {
+            const int n1 = s_n1, n2 = s_n2, nlev = s_nlev, W = g.W;
+            if (p.phase_clock && inst == 0 && threadIdx.x == 0) p.phase_clock[1] = clock64();
+            // phase 1 (sigma == 0 compactions): solve + count
+            for (int e = warp; e < n1; e += nw) {
+                OwnSolve s;
+                const int c = b.ev_col[e];
+                if (!own_solve(g, b.dep + (size_t)c * g.wpd, L, -1, s)) {
+                    if (lane == 0) s_fail = 1;
+                    continue;
+                }
+                if (lane == 0) {
+                    b.ev_a[e] = (int16_t)s.a;
+                    b.ev_count[e] = s.n_right + s.n_left;
+                }
+                __syncwarp();
+            }
+            // pairing-loop events in dependency waves
+            for (int lv = 1; lv <= nlev; ++lv) {
+                for (int q = b.wave_off[lv] + warp; q < b.wave_off[lv + 1]; q += nw) {
+                    const int e = b.wave_list[q];
+                    const int col = b.ev_col[e], aux = b.ev_aux[e];
+                    uint64_t *mc = b.dep + (size_t)col * g.wpd;
+                    if (b.ev_type[e] == EV_OWN) {
+                        for (int w = lane; w < g.wpd; w += 32) snap[(size_t)(2 * col) * g.wpd + w] = mc[w];
+                        OwnSolve s;
+                        if (!own_solve(g, mc, L, -1, s)) {
+                            if (lane == 0) s_fail = 1;
+                            continue;
+                        }
+                        own_update(g, mc, s, L);
+                        if (lane == 0) {
+                            b.ev_a[e] = (int16_t)s.a;
+                            b.ev_count[e] = s.n_right + s.n_left;
+                            if (aux >= 0) b.mark_dest[col] = (int16_t)aux;  // parked -> marks for aux
+                        }
+                    } else {
+                        uint64_t *md = b.dep + (size_t)aux * g.wpd;
+                        for (int w = lane; w < g.wpd; w += 32) {
+                            snap[(size_t)(2 * col) * g.wpd + w] = mc[w];
+                            snap[(size_t)(2 * col + 1) * g.wpd + w] = md[w];
+                        }
+                        FlushSolve f;
+                        if (!flush_solve(g, mc, md, col, aux, b.dep, b.mark_dest, L, -1, f)) {
+                            if (lane == 0) s_fail = 1;
+                            continue;
+                        }
+                        flush_update(g, b.dep, col, aux, f, L);
+                        if (lane == 0) {
+                            b.ev_a[e] = (int16_t)f.a;
+                            b.ev_count[e] = f.n_right + f.n_left;
+                        }
+                    }
+                    __syncwarp();
+                }
+                __syncthreads();
+            }
+            if (p.phase_clock && inst == 0 && threadIdx.x == 0) p.phase_clock[2] = clock64();
+            // phase 3: remaining compactions on the final state
+            for (int e = n1 + n2 + warp; e < W; e += nw) {
+                OwnSolve s;
+                const int c = b.ev_col[e];
+                if (!own_solve(g, b.dep + (size_t)c * g.wpd, L, -1, s)) {
+                    if (lane == 0) s_fail = 1;
+                    continue;
+                }
+                if (lane == 0) {
+                    b.ev_a[e] = (int16_t)s.a;
+                    b.ev_count[e] = s.n_right + s.n_left;
+                }
+                __syncwarp();
+            }
+            __syncthreads();
+            // canonical offsets (event order), then parallel emission
+            if (warp == 0) {
+                int run = 0;
+                for (int i0 = 0; i0 < W; i0 += 32) {
+                    const int i = i0 + lane;
+                    const int v = i < W ? b.ev_count[i] : 0;
+                    int tot;
+                    const int ex = warp_excl_scan(v, &tot);
+                    if (i < W) b.ev_off[i] = run + ex;
+                    run += tot;
+                }
+                if (lane == 0) s_total = run;
+            }
+            __syncthreads();
+            if (!s_fail) {
+                long long disp = 0;
+                for (int e = warp; e < W; e += nw) {
+                    const int col = b.ev_col[e], aux = b.ev_aux[e];
+                    const bool loop = e >= n1 && e < n1 + n2;
+                    if (b.ev_type[e] == EV_OWN) {
+                        const uint64_t *m = loop ? snap + (size_t)(2 * col) * g.wpd : b.dep + (size_t)col * g.wpd;
+                        OwnSolve s;
+                        own_solve(g, m, L, b.ev_a[e], s);
+                        disp += own_emit(g, col, s, L, o, b.ev_off[e], e);
+                    } else {
+                        const uint64_t *mr = snap + (size_t)(2 * col) * g.wpd, *md = snap + (size_t)(2 * col + 1) * g.wpd;
+                        FlushSolve f;
+                        flush_solve(g, mr, md, col, aux, b.dep, b.mark_dest, L, b.ev_a[e], f);
+                        disp += flush_emit(g, f, mr, md, col, aux, b.dep, b.mark_dest, L, keys, o, b.ev_off[e], e);
+                    }
+                    __syncwarp();
+                }
+                if (lane == 0 && disp) atomicAdd(&s_disp, (unsigned long long)disp);
+            }
+            __syncthreads();
+            if (p.phase_clock && inst == 0 && threadIdx.x == 0) {
+                p.phase_clock[3] = clock64();
+                p.phase_clock[4] = n1;
+                p.phase_clock[5] = n2 * 1000 + nlev;
+            }
+            if (s_fail && threadIdx.x == 0) {
+                s_status = RECON_ERR_INFEASIBLE;
+                s_detail = RECON_D_GEN_NO_ASSIGNMENT;
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            const bool ok = s_status == RECON_OK;
+            p.path_count[inst] = ok ? s_total : 0;
+            p.total_displacement[inst] = ok ? (long long)s_disp : 0;
+            p.status[inst] = s_status;
+            if (p.detail) p.detail[inst] = s_detail;
+        }
+        if (p.events && s_status == RECON_OK) {
+            for (int e = threadIdx.x; e < g.W; e += blockDim.x) {
+                int32_t *ev = p.events + ((size_t)inst * g.W + e) * 4;
+                ev[0] = e;
+                ev[1] = b.ev_col[e];
+                ev[2] = b.ev_type[e] == EV_FLUSH ? b.ev_aux[e] : -1;
+                ev[3] = b.ev_type[e] == EV_OWN ? b.ev_aux[e] : -1;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace rb

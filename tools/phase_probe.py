@@ -1,0 +1,22 @@
+"""clock64 phase split of one red-rec solve (plan / phase-1 + pairing loop / phase 3)."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2504_06182_b200 import LIB_PATH  # noqa: E402
+from paper_2504_06182_b200.inputs import sample_grids  # noqa: E402
+
+lib = C.CDLL(LIB_PATH)
+for (W, H, hp, k, seed) in [(256, 256, 128, 39322, 256), (256, 256, 153, 39322, 257), (32, 32, 16, 614, 1),
+                            (512, 512, 307, 157286, 0x51200000)]:
+    occ = sample_grids(seed, 1, W, H, k)
+    out = np.zeros(6, np.int64)
+    for rep in range(2):
+        st = lib.recon_debug_grid_phases(0, occ.ctypes.data_as(C.c_void_p), W, H, hp, out.ctypes.data_as(C.c_void_p))
+    c = out
+    print(f"{W}x{H} h'={hp}: plan {(c[1]-c[0])/1965:.1f} us, phase1+loop {(c[2]-c[1])/1965:.1f} us, "
+          f"phase3 {(c[3]-c[2])/1965:.1f} us (n1={c[4]}, loop events={c[5]//1000}, levels={c[5]%1000}) st={st}")
