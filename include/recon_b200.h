@@ -204,9 +204,22 @@ recon_status recon_bird_solve_batch(recon_ctx *ctx, const recon_grid_batch *batc
 recon_status recon_redrec_solve_batch_host(recon_ctx *ctx, const recon_grid_batch *batch);
 recon_status recon_bird_solve_batch_host(recon_ctx *ctx, const recon_grid_batch *batch);
 
+/* occupancy_dag over explicit vertex lists (paths of any shape, CSR
+ * off[P+1] into verts); edges sorted by (src, dst), deduplicated. */
+recon_status recon_occupancy_dag_paths(recon_ctx *ctx, int32_t width, int32_t height, int32_t path_count,
+                                       const int64_t *path_offsets, const int32_t *path_vertices,
+                                       int32_t *dag_src, int32_t *dag_dst, int64_t dag_capacity,
+                                       int64_t *dag_count, int32_t *detail);
+
 /* ------------------------------------------------------------------------- */
 /* Exact 1D                                                                   */
 /* ------------------------------------------------------------------------- */
+
+/* min_assignment_cost_1d (exact1d.hpp:48-49): exact optimum of assigning the
+ * (unsorted, possibly repeated) sources onto the targets; virtual (negative)
+ * positions allowed. */
+recon_status recon_min_cost_1d(recon_ctx *ctx, int32_t ns, const int64_t *sources, int32_t nt,
+                               const int64_t *targets, int64_t *cost, int32_t *detail);
 
 /*
  * assign_1d: S and T need not be sorted (the reference sorts them,

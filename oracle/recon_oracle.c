@@ -1473,3 +1473,86 @@ recon_status recon_pipeline_batch_run(recon_ctx *ctx, const recon_pipeline_batch
 recon_status recon_pipeline_batch_run_host(recon_ctx *ctx, const recon_pipeline_batch *pb) {
     return recon_pipeline_batch_run(ctx, pb);
 }
+
+static int cmp_i64(const void *a, const void *b) {
+    int64_t x = *(const int64_t *)a, y = *(const int64_t *)b;
+    return x < y ? -1 : (x > y);
+}
+
+/* min_assignment_cost_1d (exact1d.cpp:320-326): window DP over grouped sources */
+recon_status recon_min_cost_1d(recon_ctx *ctx, int32_t ns, const int64_t *sources, int32_t nt, const int64_t *targets,
+                               int64_t *cost, int32_t *detail) {
+    (void)ctx;
+    if (detail) *detail = 0;
+    *cost = 0;
+    if (nt == 0) return RECON_OK;
+    if (ns < nt) {
+        if (detail) *detail = RECON_D_INFEASIBLE_SUPPLY;
+        return RECON_ERR_INFEASIBLE;
+    }
+    int64_t *s = xcalloc((size_t)ns, 8), *t = xcalloc((size_t)nt, 8), *pos = xcalloc((size_t)ns, 8);
+    int32_t *lo = xcalloc((size_t)ns, 4), *hi = xcalloc((size_t)ns, 4), *use = xcalloc((size_t)ns, 4);
+    memcpy(s, sources, (size_t)ns * 8);
+    memcpy(t, targets, (size_t)nt * 8);
+    qsort(s, (size_t)ns, 8, cmp_i64);
+    qsort(t, (size_t)nt, 8, cmp_i64);
+    int np = 0;
+    for (int i = 0; i < ns; ++i) {
+        if (np && pos[np - 1] == s[i]) ++hi[np - 1];
+        else {
+            pos[np] = s[i];
+            hi[np] = 1;
+            ++np;
+        }
+    }
+    window_dp(np, pos, lo, hi, nt, t, use, cost);
+    free(s);
+    free(t);
+    free(pos);
+    free(lo);
+    free(hi);
+    free(use);
+    return RECON_OK;
+}
+
+recon_status recon_occupancy_dag_paths(recon_ctx *ctx, int32_t width, int32_t height, int32_t P, const int64_t *off,
+                                       const int32_t *verts, int32_t *dag_src, int32_t *dag_dst, int64_t dag_capacity,
+                                       int64_t *dag_count, int32_t *detail) {
+    (void)ctx;
+    if (detail) *detail = 0;
+    int64_t N = (int64_t)width * height;
+    int32_t *so = xcalloc((size_t)N, 4), *to = xcalloc((size_t)N, 4);
+    for (int64_t v = 0; v < N; ++v) so[v] = to[v] = -1;
+    for (int i = 0; i < P; ++i) {
+        so[verts[off[i]]] = i;
+        to[verts[off[i + 1] - 1]] = i;
+    }
+    int64_t cap = 64, ne = 0;
+    edge_t *e = xcalloc((size_t)cap, sizeof(edge_t));
+    for (int i = 0; i < P; ++i)
+        for (int64_t q = off[i]; q < off[i + 1]; ++q) {
+            int32_t v = verts[q];
+            if (ne + 2 > cap) {
+                cap *= 2;
+                e = realloc(e, (size_t)cap * sizeof(edge_t));
+            }
+            if (so[v] >= 0 && so[v] != i) e[ne++] = (edge_t){so[v], i};
+            if (to[v] >= 0 && to[v] != i) e[ne++] = (edge_t){i, to[v]};
+        }
+    qsort(e, (size_t)ne, sizeof(edge_t), cmp_edge);
+    int64_t u = 0;
+    for (int64_t i = 0; i < ne; ++i)
+        if (u == 0 || e[i].a != e[u - 1].a || e[i].b != e[u - 1].b) e[u++] = e[i];
+    *dag_count = u;
+    recon_status st = RECON_OK;
+    if (u > dag_capacity) st = RECON_ERR_CAPACITY;
+    else
+        for (int64_t i = 0; i < u; ++i) {
+            dag_src[i] = e[i].a;
+            dag_dst[i] = e[i].b;
+        }
+    free(so);
+    free(to);
+    free(e);
+    return st;
+}

@@ -523,3 +523,27 @@ extern "C" void recon_ref_sample(uint64_t seed, int32_t n, int32_t k, int32_t *o
 extern "C" recon_status recon_pipeline_batch_run_host(recon_ctx *c, const recon_pipeline_batch *pb) {
     return recon_pipeline_batch_run(c, pb);
 }
+
+extern "C" recon_status recon_min_cost_1d(recon_ctx *, int32_t ns, const int64_t *sources, int32_t nt,
+                                          const int64_t *targets, int64_t *cost, int32_t *detail) {
+    return guarded(detail, [&] {
+        *cost = min_assignment_cost_1d(std::vector<long long>(sources, sources + ns),
+                                       std::vector<long long>(targets, targets + nt));
+    });
+}
+
+extern "C" recon_status recon_occupancy_dag_paths(recon_ctx *, int32_t, int32_t, int32_t P, const int64_t *off,
+                                                  const int32_t *verts, int32_t *dag_src, int32_t *dag_dst,
+                                                  int64_t dag_capacity, int64_t *dag_count, int32_t *detail) {
+    return guarded(detail, [&] {
+        std::vector<Path> paths(static_cast<size_t>(P));
+        for (int32_t i = 0; i < P; ++i) paths[static_cast<size_t>(i)].vertices.assign(verts + off[i], verts + off[i + 1]);
+        const MoveDag dag = occupancy_dag(paths);
+        *dag_count = static_cast<int64_t>(dag.edges.size());
+        if (*dag_count > dag_capacity) throw Failure{RECON_ERR_CAPACITY, RECON_D_NONE};
+        for (size_t i = 0; i < dag.edges.size(); ++i) {
+            dag_src[i] = dag.edges[i].first;
+            dag_dst[i] = dag.edges[i].second;
+        }
+    });
+}

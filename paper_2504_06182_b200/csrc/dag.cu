@@ -118,3 +118,66 @@ cudaError_t dag_emit(const DagArgs &d, int64_t n_edges, cudaStream_t st, int32_t
 }
 
 }  // namespace rb
+
+// --------------------------------------------------------------------------
+// occupancy_dag over explicit vertex lists (any path shape, e.g. aro's):
+// every candidate pair is emitted, then sorted and deduplicated
+// (virtual_line.cpp:261-262).
+// --------------------------------------------------------------------------
+
+namespace rb {
+
+__global__ void dagx_mark_kernel(int P, const int64_t *off, const int32_t *verts, int32_t *source_of,
+                                 int32_t *target_of) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
+        source_of[verts[off[i]]] = i;
+        target_of[verts[off[i + 1] - 1]] = i;
+    }
+}
+
+template <bool WRITE>
+__global__ void dagx_walk_kernel(int P, const int64_t *off, const int32_t *verts, const int32_t *source_of,
+                                 const int32_t *target_of, int32_t *cnt, const int64_t *eoff,
+                                 unsigned long long *keys) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
+        int n = 0;
+        int64_t o = WRITE ? eoff[i] : 0;
+        for (int64_t q = off[i]; q < off[i + 1]; ++q) {
+            const int32_t v = verts[q];
+            const int32_t a = source_of[v];
+            if (a >= 0 && a != i) {
+                if (WRITE) keys[o++] = ((unsigned long long)(uint32_t)a << 32) | (uint32_t)i;
+                ++n;
+            }
+            const int32_t b = target_of[v];
+            if (b >= 0 && b != i) {
+                if (WRITE) keys[o++] = ((unsigned long long)(uint32_t)i << 32) | (uint32_t)b;
+                ++n;
+            }
+        }
+        if (!WRITE) cnt[i] = n;
+    }
+}
+
+__global__ void unique_flags_kernel(int64_t n, const unsigned long long *k, int32_t *flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = (i == 0 || k[i] != k[i - 1]) ? 1 : 0;
+}
+
+__global__ void unique_scatter_kernel(int64_t n, const unsigned long long *k, const int32_t *flag,
+                                      const int64_t *pos, int32_t *a, int32_t *b) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (flag[i]) {
+            a[pos[i]] = (int32_t)(k[i] >> 32);
+            b[pos[i]] = (int32_t)(k[i] & 0xffffffffull);
+        }
+}
+
+}  // namespace rb
+
+namespace rb {
+template __global__ void dagx_walk_kernel<false>(int, const int64_t *, const int32_t *, const int32_t *,
+                                                 const int32_t *, int32_t *, const int64_t *, unsigned long long *);
+template __global__ void dagx_walk_kernel<true>(int, const int64_t *, const int32_t *, const int32_t *,
+                                                const int32_t *, int32_t *, const int64_t *, unsigned long long *);
+}  // namespace rb
