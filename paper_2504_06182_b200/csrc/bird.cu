@@ -74,7 +74,20 @@ __device__ int scan_counts(Block &b, int e0, int e1) {
 }
 
 // --------------------------------------------------------------------------
-// CTA-level pooled event (bird row pass)
+// CTA-level pooled event (bird row pass, bird.cpp:35-46, 64-100)
+//
+// The optional pool of column c is every reservoir token of every column; a
+// token of column x at depth d sits at virtual level d - |x-c| (top side) or
+// d + |x-c| (bottom side), virtual_line.cpp:65-68.  Levels are scanned in
+// 64-level windows outward from the band.  Inside a window the 2*dist+1
+// columns that can reach it are "slots" in group order (own column, then
+// dist 1 left, dist 1 right, ...; virtual_line.cpp:112-118); 32 slots x 64
+// levels form a bit block that one warp transposes with shuffles, giving per
+// level the ballot of slots holding a token (-> per-level counts and each
+// token's rank inside its level).  Top and bottom windows are scanned by two
+// warp groups at once, and scanning stops as soon as the split a is pinned
+// down (Delta(a) is known on a contiguous range that brackets the
+// minimiser), instead of collecting `holes` tokens per side.
 // --------------------------------------------------------------------------
 
 __device__ __forceinline__ int slot_col(int c, int gslot, int W) {
@@ -85,25 +98,30 @@ __device__ __forceinline__ int slot_col(int c, int gslot, int W) {
 }
 
 struct PooledScratch {
-    int16_t *otop, *obot;      // [LK]
-    int *lvl_t, *lvl_b;        // [LT], [LB]: count << 16 | cum_before (cum < 65536)
-    uint32_t *bal;             // [nchunk][64]
-    int *scal;                 // scalars
+    int16_t *otop, *obot;  // [LK] virtual levels of the k-th nearest optional token per side (1-based)
+    int *lvl_t, *lvl_b;    // [LT], [LB]: count << 16 | tokens at nearer levels (saturating)
+    uint32_t *bal;         // [2][nchunk][64] transposed slot words of the current window per side
+    int *scal;             // scalars
 };
 
-// 64 ballots per warp: per-level token counts of the slots this warp holds
-__device__ __forceinline__ void ballot_counts(uint64_t word, uint32_t *bal_row, int *cnt_lo, int *cnt_hi) {
+// 32 slots x 64 levels: lane L receives the slot masks of levels L and L+32
+__device__ __forceinline__ void transpose64(uint64_t word, uint32_t &t_lo, uint32_t &t_hi) {
+    uint32_t a = (uint32_t)word, b = (uint32_t)(word >> 32);
     const int lane = lane_id();
-#pragma unroll 8
-    for (int i = 0; i < 64; ++i) {
-        const uint32_t b = __ballot_sync(FULL, (word >> i) & 1ull);
-        if (bal_row && lane == 0) bal_row[i] = b;
-        if (i < 32) {
-            if (lane == i) *cnt_lo = __popc(b);
+#pragma unroll
+    for (int j = 16; j >= 1; j >>= 1) {
+        const uint32_t m = j == 16 ? 0x0000FFFFu : (j == 8 ? 0x00FF00FFu : (j == 4 ? 0x0F0F0F0Fu : (j == 2 ? 0x33333333u : 0x55555555u)));
+        const uint32_t ya = __shfl_xor_sync(FULL, a, j), yb = __shfl_xor_sync(FULL, b, j);
+        if (lane & j) {
+            a = (a & ~m) | ((ya & ~m) >> j);
+            b = (b & ~m) | ((yb & ~m) >> j);
         } else {
-            if (lane == i - 32) *cnt_hi = __popc(b);
+            a = (a & m) | ((ya & m) << j);
+            b = (b & m) | ((yb & m) << j);
         }
     }
+    t_lo = a;
+    t_hi = b;
 }
 
 // token word of a slot: bit i = a reservoir token at virtual level V0 + i
@@ -118,153 +136,152 @@ __device__ __forceinline__ uint64_t slot_word(const Geo &g, const uint64_t *dep,
     *col_out = x;
     *dist_out = dist;
     const uint64_t *m = dep + (size_t)x * g.wpd;
-    if (top) {
-        // depth = v + dist < lo
+    if (top) {  // depth = v + dist < lo
         const int start = V0 + dist;
         const uint64_t w = extract64(m, g.wpd, start);
-        const int nvalid = g.lo - start;  // bits i < nvalid have depth < lo
+        const int nvalid = g.lo - start;
         if (nvalid <= 0) return 0ull;
         return nvalid >= 64 ? w : (w & ((1ull << nvalid) - 1ull));
-    } else {
-        // depth = v - dist > hi
-        const int start = V0 - dist;
-        const uint64_t w = extract64(m, g.wpd, start);
-        const int skip = g.hi + 1 - start;  // bits i < skip have depth <= hi
-        if (skip >= 64) return 0ull;
-        return skip <= 0 ? w : (w & ~((1ull << skip) - 1ull));
     }
+    const int start = V0 - dist;  // depth = v - dist > hi
+    const uint64_t w = extract64(m, g.wpd, start);
+    const int skip = g.hi + 1 - start;
+    if (skip >= 64) return 0ull;
+    return skip <= 0 ? w : (w & ~((1ull << skip) - 1ull));
 }
 
-// Scans 64-level windows outward from the band until `need` tokens are found
-// or no token can exist further out.  Fills lvl[] (count << 16 | cum_before).
-// Returns total found (scalars: found, nlevels) — CTA-uniform.
-__device__ void pooled_scan(const Geo &g, const uint64_t *dep, int c, bool top, int need, int *lvl,
-                            int *scal_found, int *scal_nlev) {
-    const int lane = lane_id(), warp = warp_id(), nw = blockDim.x >> 5;
-    const int maxlev = top ? (g.lo + g.W - 1) : ((g.H - 1 - g.hi) + g.W - 1);  // levels available
-    int found = 0, nlev = 0;
-    for (int w = 0; nlev < maxlev && found < need; ++w) {
-        const int V0 = top ? g.lo - 64 * (w + 1) : g.hi + 1 + 64 * w;
-        const int maxd = min(g.W - 1, 64 * (w + 1));
-        const int nslots = 2 * maxd + 1;
-        const int base_li = 64 * w;  // level index of the level nearest the band in this window
-        for (int i = threadIdx.x; i < 64; i += blockDim.x) lvl[base_li + i] = 0;
-        __syncthreads();
-        for (int chn = warp; chn * 32 < nslots; chn += nw) {
-            int col, dist;
-            const uint64_t word = slot_word(g, dep, c, chn * 32 + lane, nslots, V0, top, &col, &dist);
-            if (!__any_sync(FULL, word != 0ull)) continue;
-            int clo = 0, chi = 0;
-            ballot_counts(word, nullptr, &clo, &chi);
-            // window bit i <-> level index: top li = 63 - i + base_li; bottom li = i + base_li
-            if (clo) atomicAdd(&lvl[base_li + (top ? 63 - lane : lane)], clo);
-            if (chi) atomicAdd(&lvl[base_li + (top ? 31 - lane : lane + 32)], chi);
-        }
-        __syncthreads();
-        // cumulative (warp 0): li ascending = outward from the band
-        if (warp == 0) {
-            int run = found;
-            for (int i0 = 0; i0 < 64; i0 += 32) {
-                const int li = base_li + i0 + lane;
-                const int cnt = lvl[li];
-                int tot;
-                const int ex = warp_excl_scan(cnt, &tot);
-                lvl[li] = (cnt << 16) | min(run + ex, 65535);
-                run += tot;
-            }
-            if (lane == 0) *scal_found = run;
-        }
-        __syncthreads();
-        found = *scal_found;
-        nlev = 64 * (w + 1);
-        __syncthreads();
+__device__ __forceinline__ int win_V0(const Geo &g, bool top, int w) {
+    return top ? g.lo - 64 * (w + 1) : g.hi + 1 + 64 * w;
+}
+__device__ __forceinline__ int win_nslots(const Geo &g, int w) { return 2 * min(g.W - 1, 64 * (w + 1)) + 1; }
+// window bit i -> level index (0 = nearest the band)
+__device__ __forceinline__ int bit_li(bool top, int w, int i) { return top ? 64 * w + 63 - i : 64 * w + i; }
+
+// counts one window of one side with the warps [g0, g0 + gn) of the CTA
+__device__ void count_window(const Geo &g, const uint64_t *dep, int c, bool top, int w, int *lvl, int g0, int gn) {
+    const int warp = warp_id(), lane = lane_id();
+    if (warp < g0 || warp >= g0 + gn) return;
+    const int V0 = win_V0(g, top, w), nslots = win_nslots(g, w), nch = (nslots + 31) / 32;
+    int acc_lo = 0, acc_hi = 0;
+    for (int ch = warp - g0; ch < nch; ch += gn) {
+        int col, dist;
+        const uint64_t word = slot_word(g, dep, c, ch * 32 + lane, nslots, V0, top, &col, &dist);
+        if (!__any_sync(FULL, word != 0ull)) continue;
+        uint32_t t_lo, t_hi;
+        transpose64(word, t_lo, t_hi);
+        acc_lo += __popc(t_lo);
+        acc_hi += __popc(t_hi);
     }
-    if (threadIdx.x == 0) {
-        *scal_found = found;
-        *scal_nlev = nlev;
-    }
-    __syncthreads();
+    if (acc_lo) atomicAdd(&lvl[bit_li(top, w, lane)], acc_lo);
+    if (acc_hi) atomicAdd(&lvl[bit_li(top, w, lane + 32)], acc_hi);
 }
 
-// Emits the used reservoir tokens of one side and clears them from their
-// columns (drawn externals leave their reservoirs, bird.cpp:79-88).
-__device__ long long pooled_emit_side(const Geo &g, uint64_t *dep, int *sigma, int c, bool top, int used,
-                                      int a, int R, int n_right, int n_left, const int *lvl, uint32_t *bal,
-                                      int vstar_li, int r_star, PathOut o, int off, int evid) {
-    const int lane = lane_id(), warp = warp_id(), nw = blockDim.x >> 5;
+// (one warp) cumulative over a freshly counted window; materializes the
+// 1-based token stream list[] (levels, nearest first) up to `cap` entries.
+// Returns the running total.
+__device__ int finish_window(const Geo &g, bool top, int w, int *lvl, int found, int16_t *list, int cap) {
+    const int lane = lane_id();
+    int run = found;
+    for (int i0 = 0; i0 < 64; i0 += 32) {
+        const int li = 64 * w + i0 + lane;
+        const int cnt = lvl[li];
+        int tot;
+        const int ex = warp_excl_scan(cnt, &tot);
+        const int cb = run + ex;
+        lvl[li] = (cnt << 16) | min(cb, 65535);
+        const int v = top ? g.lo - 1 - li : g.hi + 1 + li;
+        for (int q = cb + 1; q <= min(cb + cnt, cap); ++q) list[q] = (int16_t)v;
+        run += tot;
+    }
+    return run;
+}
+
+// Emits (and clears from their columns) the used tokens of one side in one
+// window; T = this side's transposed words of the window (all chunks).
+__device__ long long emit_window(const Geo &g, uint64_t *dep, int *sigma, int c, bool top, int w, int used, int a,
+                                 int R, int n_right, int n_left, const int *lvl, const uint32_t *T, int vstar_li,
+                                 int r_star, PathOut o, int off, int evid, int g0, int gn) {
+    const int warp = warp_id(), lane = lane_id();
     long long disp = 0;
-    if (used <= 0) return 0;
-    const int last_w = vstar_li / 64;
-    for (int w = 0; w <= last_w; ++w) {
-        const int V0 = top ? g.lo - 64 * (w + 1) : g.hi + 1 + 64 * w;
-        const int maxd = min(g.W - 1, 64 * (w + 1));
-        const int nslots = 2 * maxd + 1;
-        const int nch = (nslots + 31) / 32;
-        // pass 1: ballots per chunk (group-order prefix within a level)
-        for (int chn = warp; chn < nch; chn += nw) {
-            int col, dist;
-            const uint64_t word = slot_word(g, dep, c, chn * 32 + lane, nslots, V0, top, &col, &dist);
-            int clo, chi;
-            ballot_counts(word, bal + chn * 64, &clo, &chi);
-        }
-        __syncthreads();
-        // pass 2: emit
-        for (int chn = warp; chn < nch; chn += nw) {
-            int col, dist;
-            const int gslot = chn * 32 + lane;
-            uint64_t word = slot_word(g, dep, c, gslot, nslots, V0, top, &col, &dist);
-            uint64_t cleared = 0ull;
-            for (uint64_t x = word; x; x &= x - 1) {
-                const int i = __ffsll((long long)x) - 1;
-                const int li = top ? 64 * w + 63 - i : 64 * w + i;
-                if (li > vstar_li) continue;  // beyond the last used level
-                int rank_lt = __popc(bal[chn * 64 + i] & lanemask_lt());
-                for (int q = 0; q < chn; ++q) rank_lt += __popc(bal[q * 64 + i]);
-                int jside;
-                if (li == vstar_li) {
-                    if (rank_lt >= r_star) continue;
-                    jside = top ? rank_lt : (used - 1 - (r_star - 1 - rank_lt));
-                } else {
-                    const int cb = lvl[li] & 0xffff, cnt = lvl[li] >> 16;
-                    // top: ascending (pos, g) index = used - (#at levels nearer + this level) + rank
-                    // bottom: ascending index = levels nearer + rank
-                    jside = top ? used - (cb + cnt) + rank_lt : cb + rank_lt;
-                }
-                const int v = V0 + i;
-                const int depth = top ? v + dist : v - dist;
-                const int j = top ? jside : a + R + jside;
-                const int t = g.lo + j;
-                const int p = off + emit_slot(g, j, n_right, n_left);
-                o.src[p] = col * g.H + (g.H - 1 - depth);
-                o.dst[p] = c * g.H + (g.H - 1 - t);
-                if (o.ev) o.ev[p] = evid;
-                disp += top ? t - v : v - t;
-                cleared |= 1ull << i;
+    if (warp < g0 || warp >= g0 + gn) return 0;
+    const int V0 = win_V0(g, top, w), nslots = win_nslots(g, w), nch = (nslots + 31) / 32;
+    for (int ch = warp - g0; ch < nch; ch += gn) {
+        int col, dist;
+        const uint64_t word = slot_word(g, dep, c, ch * 32 + lane, nslots, V0, top, &col, &dist);
+        uint64_t cleared = 0ull;
+        for (uint64_t x = word; x; x &= x - 1) {
+            const int i = __ffsll((long long)x) - 1;
+            const int li = bit_li(top, w, i);
+            if (li > vstar_li) continue;
+            int rank_lt = __popc(T[ch * 64 + i] & lanemask_lt());
+            for (int q = 0; q < ch; ++q) rank_lt += __popc(T[q * 64 + i]);
+            int jside;
+            if (li == vstar_li) {
+                if (rank_lt >= r_star) continue;
+                jside = top ? rank_lt : used - r_star + rank_lt;
+            } else {
+                const int cb = lvl[li] & 0xffff, cnt = lvl[li] >> 16;
+                jside = top ? used - (cb + cnt) + rank_lt : cb + rank_lt;
             }
-            if (cleared) {
-                uint64_t *m = dep + (size_t)col * g.wpd;
-                const int start = top ? V0 + dist : V0 - dist;
-                // clear bits depth = start + i
-                for (uint64_t x = cleared; x; x &= x - 1) {
-                    const int dpt = start + __ffsll((long long)x) - 1;
-                    m[dpt >> 6] &= ~(1ull << (dpt & 63));
-                }
-                if (col != c) sigma[col] -= __popcll(cleared);
-            }
+            const int v = V0 + i;
+            const int depth = top ? v + dist : v - dist;
+            const int j = top ? jside : a + R + jside;
+            const int t = g.lo + j;
+            const int p = off + emit_slot(g, j, n_right, n_left);
+            o.src[p] = col * g.H + (g.H - 1 - depth);
+            o.dst[p] = c * g.H + (g.H - 1 - t);
+            if (o.ev) o.ev[p] = evid;
+            disp += top ? t - v : v - t;
+            cleared |= 1ull << i;
         }
-        __syncthreads();
+        if (cleared) {
+            uint64_t *m = dep + (size_t)col * g.wpd;
+            const int start = top ? V0 + dist : V0 - dist;
+            // top and bottom windows run concurrently and may share a word / a column
+            for (uint64_t x = cleared; x; x &= x - 1) {
+                const int dpt = start + __ffsll((long long)x) - 1;
+                atomicAnd((unsigned long long *)&m[dpt >> 6], ~(1ull << (dpt & 63)));
+            }
+            if (col != c) atomicSub(&sigma[col], __popcll(cleared));
+        }
     }
     return disp;
+}
+
+// stores the transposed words of one window (all chunks) into T
+__device__ void transpose_window(const Geo &g, const uint64_t *dep, int c, bool top, int w, uint32_t *T, int g0,
+                                 int gn) {
+    const int warp = warp_id(), lane = lane_id();
+    if (warp < g0 || warp >= g0 + gn) return;
+    const int V0 = win_V0(g, top, w), nslots = win_nslots(g, w), nch = (nslots + 31) / 32;
+    for (int ch = warp - g0; ch < nch; ch += gn) {
+        int col, dist;
+        const uint64_t word = slot_word(g, dep, c, ch * 32 + lane, nslots, V0, top, &col, &dist);
+        uint32_t t_lo, t_hi;
+        transpose64(word, t_lo, t_hi);
+        T[ch * 64 + lane] = t_lo;
+        T[ch * 64 + 32 + lane] = t_hi;
+    }
+}
+
+// Delta(a) = cost(a) - cost(a-1) (split rule, no mandatory reservoir tokens)
+__device__ __forceinline__ int pooled_delta(const Geo &g, int a, int holes, int R, const int16_t *otop,
+                                            const int16_t *obot, const int16_t *hole) {
+    return (g.lo + a - 1) - otop[a] + 2 * (hole[a] - g.lo - a + 1) - R - obot[holes - a + 1] + g.hi - (holes - a);
 }
 
 // One bird row-pass event for column c (BirdRunner::solve_column(c, true)).
 // Returns the path count (CTA-uniform) or -1 when infeasible.
 __device__ int pooled_event(const Geo &g, uint64_t *dep, int *sigma, int c, int16_t *L0, PooledScratch ps,
-                            PathOut o, int off, int evid, unsigned long long *disp_acc) {
-    const int lane = lane_id(), warp = warp_id();
+                            PathOut o, int off, int evid, unsigned long long *disp_acc, long long *dbg) {
+    const int lane = lane_id(), warp = warp_id(), nw = blockDim.x >> 5;
     int16_t *hole = L0 + 2 * g.LK, *res = L0 + 3 * g.LK;
     int *S = ps.scal;
-    // A: own residents and holes (warp 0)
+    enum { sR, sHoles, sFoundT, sFoundB, sWT, sWB, sWantT, sWantB, sDone, sA, sFail };
+    const int maxlev_t = g.lo + g.W - 1, maxlev_b = (g.H - 1 - g.hi) + g.W - 1;
+    // A: own residents and holes (warp 0); level tables cleared
+    for (int i = threadIdx.x; i < g.LT; i += blockDim.x) ps.lvl_t[i] = 0;
+    for (int i = threadIdx.x; i < g.LB; i += blockDim.x) ps.lvl_b[i] = 0;
     if (warp == 0) {
         const int B = g.B, base = lane * B;
         const uint32_t ch = lane_chunk(dep + (size_t)c * g.wpd, g.wpd, lane, B);
@@ -278,51 +295,111 @@ __device__ int pooled_event(const Geo &g, uint64_t *dep, int *sigma, int c, int1
         if (lane == 0) {
             hole[0] = (int16_t)(g.lo - 1);
             hole[nh + 1] = (int16_t)(g.hi + 1);
-            S[0] = R;
-            S[1] = nh;
+            S[sR] = R;
+            S[sHoles] = nh;
+            S[sFoundT] = S[sFoundB] = 0;
+            S[sWT] = S[sWB] = 0;
+            S[sWantT] = S[sWantB] = nh > 0;
+            S[sDone] = nh == 0;
+            S[sA] = 0;
+            S[sFail] = 0;
         }
     }
     __syncthreads();
-    const int R = S[0], holes = S[1];
-    // B/C: optional streams per side
-    pooled_scan(g, dep, c, true, holes, ps.lvl_t, &S[2], &S[3]);
-    pooled_scan(g, dep, c, false, holes, ps.lvl_b, &S[4], &S[5]);
-    const int found_t = S[2], nlev_t = S[3], found_b = S[4], nlev_b = S[5];
-    // D: materialize otop/obot (1-based, innermost first)
-    for (int li = threadIdx.x; li < nlev_t; li += blockDim.x) {
-        const int cnt = ps.lvl_t[li] >> 16, cb = ps.lvl_t[li] & 0xffff;
-        for (int q = cb + 1; q <= min(cb + cnt, holes); ++q) ps.otop[q] = (int16_t)(g.lo - 1 - li);
-    }
-    for (int li = threadIdx.x; li < nlev_b; li += blockDim.x) {
-        const int cnt = ps.lvl_b[li] >> 16, cb = ps.lvl_b[li] & 0xffff;
-        for (int q = cb + 1; q <= min(cb + cnt, holes); ++q) ps.obot[q] = (int16_t)(g.hi + 1 + li);
-    }
-    if (threadIdx.x == 0) S[6] = 0;
-    __syncthreads();
-    const int n_ot = found_t, n_ob = found_b;  // exact when < holes, else >= holes
-    const int amin = max(0, holes - n_ob), amax = min(n_ot, holes);
-    if (amin > amax) return -1;
-    // E: a = amin + #{Delta(a) <= 0}
-    {
-        int cnt = 0;
-        for (int a0 = amin + 1 + warp * 32; a0 <= amax; a0 += blockDim.x) {
-            const int aa = a0 + lane;
-            bool le = false;
-            if (aa <= amax) {
-                const int delta = (g.lo + aa - 1) - ps.otop[aa] + 2 * (hole[aa] - g.lo - aa + 1) - R -
-                                  ps.obot[holes - aa + 1] + g.hi - (holes - aa);
-                le = delta <= 0;
+    const int R = S[sR], holes = S[sHoles];
+    // B: progressive two-sided scan until the split a is pinned down
+    while (!S[sDone]) {
+        const bool wt = S[sWantT], wb = S[sWantB];
+        const int wtop = S[sWT], wbot = S[sWB];
+        const int half = nw / 2;
+        if (wt) count_window(g, dep, c, true, wtop, ps.lvl_t, 0, wb ? half : nw);
+        if (wb) count_window(g, dep, c, false, wbot, ps.lvl_b, wt ? half : 0, wt ? nw - half : nw);
+        __syncthreads();
+        if (warp == 0 && wt) {
+            const int f = finish_window(g, true, wtop, ps.lvl_t, S[sFoundT], ps.otop, holes);
+            if (lane == 0) {
+                S[sFoundT] = f;
+                S[sWT] = wtop + 1;
             }
-            cnt += __popc(__ballot_sync(FULL, le));
         }
-        if (lane == 0 && cnt) atomicAdd(&S[6], cnt);
+        if (warp == (nw > 1 ? 1 : 0) && wb) {
+            __syncwarp();
+            const int f = finish_window(g, false, wbot, ps.lvl_b, S[sFoundB], ps.obot, holes);
+            if (lane == 0) {
+                S[sFoundB] = f;
+                S[sWB] = wbot + 1;
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int ft = S[sFoundT], fb = S[sFoundB];
+            const bool exh_t = 64 * S[sWT] >= maxlev_t, exh_b = 64 * S[sWB] >= maxlev_b;
+            const int BIG = 1 << 28;
+            const int n_ot = exh_t ? ft : BIG, n_ob = exh_b ? fb : BIG;
+            const int amin = max(0, holes - n_ob), amax = min(n_ot, holes);
+            bool need_t = false, need_b = false, done = false, fail = false;
+            int astar = 0;
+            if (amin > amax) {
+                fail = true;
+            } else {
+                // Delta(a) is computable for a in [A_lo, A_hi]
+                const int A_lo = max(amin + 1, holes + 1 - min(fb, holes)), A_hi = min(amax, min(ft, holes));
+                if (amin == amax) {
+                    astar = amin;
+                    done = true;
+                } else if (A_lo > A_hi) {
+                    need_t = ft < holes && !exh_t;
+                    need_b = fb < holes && !exh_b;
+                } else {
+                    const int d_lo = pooled_delta(g, A_lo, holes, R, ps.otop, ps.obot, hole);
+                    const int d_hi = pooled_delta(g, A_hi, holes, R, ps.otop, ps.obot, hole);
+                    need_b = d_lo > 0 && A_lo > amin + 1;
+                    need_t = d_hi <= 0 && A_hi < amax;
+                    if (!need_b && !need_t) {
+                        int cnt = 0;
+                        if (d_lo <= 0) {
+                            for (int a0 = A_lo; a0 <= A_hi; a0 += 32) {
+                                const int aa = a0 + lane;
+                                const bool le = aa <= A_hi && pooled_delta(g, aa, holes, R, ps.otop, ps.obot, hole) <= 0;
+                                cnt += __popc(__ballot_sync(FULL, le));
+                            }
+                            cnt += A_lo - (amin + 1);
+                        }
+                        astar = amin + cnt;
+                        done = true;
+                    }
+                }
+            }
+            if (done) {
+                // the emission needs the used tokens' levels on both sides
+                if (ft < astar && !exh_t) need_t = true, done = false;
+                if (fb < holes - astar && !exh_b) need_b = true, done = false;
+            }
+            if (lane == 0) {
+                S[sWantT] = need_t;
+                S[sWantB] = need_b;
+                S[sDone] = done || fail;
+                S[sFail] = fail;
+                S[sA] = astar;
+            }
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    const int a = amin + S[6], b = holes - a;
+    if (S[sFail]) return -1;
+    const int a = S[sA], b = holes - a;
+    if (dbg && threadIdx.x == 0) {
+        dbg[0] = holes;
+        dbg[1] = 64 * S[sWT];
+        dbg[2] = 64 * S[sWB];
+        dbg[3] = S[sFoundT];
+        dbg[4] = S[sFoundB];
+        dbg[5] = a;
+        dbg[6] = b;
+    }
     const int cntE = hole[a] - g.lo - a + 1;
     const int nstat = hole[a + 1] - hole[a] - 1;
     const int n_right = a + cntE, n_left = (R - cntE - nstat) + b;
-    // F: last used level and how many of its members (group order) are used
+    // C: last used level per side and how many of its members (group order) are used
     int vt_li = -1, rt = 0, vb_li = -1, rb = 0;
     if (a >= 1) {
         vt_li = g.lo - 1 - ps.otop[a];
@@ -332,14 +409,25 @@ __device__ int pooled_event(const Geo &g, uint64_t *dep, int *sigma, int c, int1
         vb_li = ps.obot[b] - (g.hi + 1);
         rb = b - (ps.lvl_b[vb_li] & 0xffff);
     }
-    __syncthreads();
-    // G/H: emit + clear drawn tokens
+    // D: emission, top and bottom windows side by side
     long long disp = 0;
-    disp += pooled_emit_side(g, dep, sigma, c, true, a, a, R, n_right, n_left, ps.lvl_t, ps.bal, vt_li, rt, o, off,
-                             evid);
-    disp += pooled_emit_side(g, dep, sigma, c, false, b, a, R, n_right, n_left, ps.lvl_b, ps.bal, vb_li, rb, o,
-                             off, evid);
-    // I: residents
+    const int last_t = vt_li >= 0 ? vt_li / 64 : -1, last_b = vb_li >= 0 ? vb_li / 64 : -1;
+    uint32_t *Tt = ps.bal, *Tb = ps.bal + (size_t)g.nchunk * 64;
+    for (int w = 0; w <= max(last_t, last_b); ++w) {
+        const bool dt = w <= last_t, db = w <= last_b;
+        const int half = nw / 2;
+        if (dt) transpose_window(g, dep, c, true, w, Tt, 0, db ? half : nw);
+        if (db) transpose_window(g, dep, c, false, w, Tb, dt ? half : 0, dt ? nw - half : nw);
+        __syncthreads();
+        if (dt)
+            disp += emit_window(g, dep, sigma, c, true, w, a, a, R, n_right, n_left, ps.lvl_t, Tt, vt_li, rt, o, off,
+                                evid, 0, db ? half : nw);
+        if (db)
+            disp += emit_window(g, dep, sigma, c, false, w, b, a, R, n_right, n_left, ps.lvl_b, Tb, vb_li, rb, o, off,
+                                evid, dt ? half : 0, dt ? nw - half : nw);
+        __syncthreads();
+    }
+    // E: residents
     if (warp == 0) {
         for (int i = lane; i < R; i += 32) {
             const int depth = res[i], j = a + i, t = g.lo + j;
@@ -354,7 +442,7 @@ __device__ int pooled_event(const Geo &g, uint64_t *dep, int *sigma, int c, int1
     disp = warp_sum64(disp);
     if (lane == 0 && disp) atomicAdd(disp_acc, (unsigned long long)disp);
     __syncthreads();
-    // J: own column = band + unused own reservoir (bird.cpp:90-99)
+    // F: own column = band + unused own reservoir (bird.cpp:90-99)
     if (warp == 0) {
         int left = 0;
         for (int w = lane; w < g.wpd; w += 32) {
@@ -370,7 +458,7 @@ __device__ int pooled_event(const Geo &g, uint64_t *dep, int *sigma, int c, int1
     return n_right + n_left;
 }
 
-__global__ void __launch_bounds__(256) bird_kernel(GridParams p) {
+__global__ void __launch_bounds__(256, 3) bird_kernel(GridParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geo g = make_geo(p.shape);
     Block b = carve(p.shape, smem);
@@ -430,7 +518,8 @@ __global__ void __launch_bounds__(256) bird_kernel(GridParams p) {
             // row pass: pooled events, strictly sequential
             for (int e = n1; e < g.W; ++e) {
                 const int c = b.ev_col[e];
-                const int cnt = pooled_event(g, b.dep, b.sigma, c, b.lists, ps, o, s_off, e, &s_disp);
+                long long *dbg = (p.phase_clock && inst == 0) ? p.phase_clock + 8 + 8 * (e - n1) : nullptr;
+                const int cnt = pooled_event(g, b.dep, b.sigma, c, b.lists, ps, o, s_off, e, &s_disp, dbg);
                 if (cnt < 0) {
                     if (threadIdx.x == 0) s_fail = 1;
                     __syncthreads();

@@ -264,7 +264,7 @@ recon_status recon_occupancy_dag(recon_ctx *ctx, int32_t width, int32_t height, 
 // returns clock64 stamps at the kernel's phase boundaries (plan, phase 1 +
 // pairing loop, phase 3) plus the phase-1 / loop event counts.
 extern "C" recon_status recon_debug_grid_phases(int32_t solver, const uint64_t *occ, int32_t W, int32_t H,
-                                                int32_t hp, long long *out6) {
+                                                int32_t hp, long long *out6, int32_t nout) {
     int32_t *detail = nullptr;
     Ctx *c = resolve(nullptr);
     if (!c) return RECON_ERR_CUDA;
@@ -282,10 +282,11 @@ extern "C" recon_status recon_debug_grid_phases(int32_t solver, const uint64_t *
     p.total_displacement = c->dev<int64_t>(S_TDISP, 1);
     p.status = c->dev<int32_t>(S_STATUS, 1);
     p.detail = c->dev<int32_t>(S_DETAIL, 1);
-    p.phase_clock = c->dev<long long>(S_KEYS, 8);
+    p.phase_clock = c->dev<long long>(S_KEYS, (size_t)(nout > 8 ? nout : 8));
+    CK(cudaMemsetAsync(p.phase_clock, 0, (size_t)(nout > 8 ? nout : 8) * 8, c->stream), "memset");
     CK(cudaMemcpyAsync(d_occ, occ, words * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
     CK(launch(c, solver, p, 1), "launch");
-    CK(cudaMemcpyAsync(out6, p.phase_clock, 6 * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    CK(cudaMemcpyAsync(out6, p.phase_clock, (size_t)(nout > 6 ? nout : 6) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
     CK(cudaStreamSynchronize(c->stream), "sync");
     return RECON_OK;
 }

@@ -38,7 +38,7 @@ __host__ __device__ inline void grid_smem_layout(const GridShape &s, GridSmem &o
     o.dep = take((int64_t)s.W * s.wpd * 8, 16);
     const int64_t keys_a = (int64_t)s.nwarps * 2 * s.LK * 4, keys_b = (int64_t)s.W * 8;
     o.keys = take(keys_a > keys_b ? keys_a : keys_b, 16);
-    o.bal = take((int64_t)s.nchunk * 64 * 4, 16);
+    o.bal = take((int64_t)2 * s.nchunk * 64 * 4, 16);
     o.sigma = take((int64_t)s.W * 4, 16);
     o.ev_count = take((int64_t)s.W * 4, 16);
     o.ev_off = take((int64_t)(s.W + 1) * 4, 16);

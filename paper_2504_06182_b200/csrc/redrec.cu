@@ -437,7 +437,7 @@ __device__ int redrec_plan(const Geo &g, Block &b, int *n1o, int *n2o, int *nlev
 // kernel
 // --------------------------------------------------------------------------
 
-__global__ void __launch_bounds__(256) redrec_kernel(GridParams p) {
+__global__ void __launch_bounds__(256, 4) redrec_kernel(GridParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geo g = make_geo(p.shape);
     Block b = carve(p.shape, smem);
