@@ -21,6 +21,7 @@
 // The batch index of every move is written at its path-major slot.
 
 #include <algorithm>
+#include <climits>
 #include <cub/device/device_scan.cuh>
 
 #include "batching.cuh"
@@ -80,7 +81,39 @@ __device__ __forceinline__ bool compatible(int preset, int H, int32_t af, int32_
     return af % H == bf % H;
 }
 
-template <class Paths>
+// sorts up to 32 ints held one per lane (INT_MAX = empty), ascending
+__device__ __forceinline__ int warp_sort32(int v) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const int o = __shfl_xor_sync(FULL, v, j);
+            const bool up = (lane & k) == 0;
+            const bool lower = (lane & j) == 0;
+            const int mn = min(v, o), mx = max(v, o);
+            v = (lower == up) ? mn : mx;
+        }
+    }
+    return v;
+}
+
+// #elements < x in a sorted array
+__device__ __forceinline__ int lower_bound_i32(const int32_t *a, int n, int x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if (a[m] < x) lo = m + 1;
+        else hi = m;
+    }
+    return lo;
+}
+
+// FAST: paths are solver output (every source occupied, distinct tokens), so
+// the only possible vertex conflict inside a batch is a shared destination;
+// the minimum id wins (and, under column_direction, the class of the first
+// accepted move).  The general entry point keeps the literal pairwise checks.
+template <class Paths, bool FAST>
 __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
     const int lane = lane_id();
     const int P = J.P, H = J.H;
@@ -148,19 +181,42 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
                 cand = !bit_get(s.occ, to) && !bit_get(s.inb, fr) && !bit_get(s.inb, to);
                 if (cand && f_from >= 0) cand = compatible(J.preset, H, fr, to, f_from, f_to);
             }
-            // conflicts with earlier lanes of this step
-            unsigned cm = 0;
-            for (int i = 0; i < 32; ++i) {
-                const int32_t ofr = __shfl_sync(FULL, fr, i), oto = __shfl_sync(FULL, to, i);
-                if (i < lane && valid && ofr >= 0) {
-                    const bool share = ofr == fr || ofr == to || oto == fr || oto == to;
-                    if (share || !compatible(J.preset, H, fr, to, ofr, oto)) cm |= 1u << i;
-                }
-            }
+            const unsigned cm_all = __ballot_sync(FULL, cand);
+            if (!cm_all) continue;
             unsigned acc = 0;
-            for (int i = 0; i < 32; ++i) {
-                const bool a = __shfl_sync(FULL, cand && !(cm & acc), i);
-                if (a) acc |= 1u << i;
+            if (FAST) {
+                bool a;
+                if (J.preset != 0) {
+                    // column_direction: every candidate in the class (direction + column/row)
+                    // of the batch's first move; a shared destination needs two directions,
+                    // so it cannot occur inside one class
+                    const int first = __ffs(cm_all) - 1;
+                    const int32_t ff = f_from >= 0 ? f_from : __shfl_sync(FULL, fr, first);
+                    const int32_t ft = f_from >= 0 ? f_to : __shfl_sync(FULL, to, first);
+                    a = cand && compatible(J.preset, H, fr, to, ff, ft);
+                } else {
+                    // shared destination: the lowest lane (= lowest id) of each group wins
+                    const unsigned same = __match_any_sync(FULL, cand ? to : -2 - lane);
+                    a = cand && (same & lanemask_lt()) == 0;
+                }
+                acc = __ballot_sync(FULL, a);
+            } else {
+                // literal batching.cpp:107-125 greedy: pairwise vertex-disjointness
+                // and the constraint predicate against earlier accepted lanes
+                unsigned cm = 0;
+                for (unsigned m = cm_all; m; m &= m - 1) {
+                    const int i = __ffs(m) - 1;
+                    const int32_t ofr = __shfl_sync(FULL, fr, i), oto = __shfl_sync(FULL, to, i);
+                    if (i < lane && cand) {
+                        const bool share = ofr == fr || ofr == to || oto == fr || oto == to;
+                        if (share || !compatible(J.preset, H, fr, to, ofr, oto)) cm |= 1u << i;
+                    }
+                }
+                for (unsigned m = cm_all; m; m &= m - 1) {
+                    const int i = __ffs(m) - 1;
+                    const bool a = __shfl_sync(FULL, cand && !(cm & acc), i);
+                    if (a) acc |= 1u << i;
+                }
             }
             if ((acc >> lane) & 1u) {
                 bit_set(s.inb, fr);
@@ -197,68 +253,85 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
             const int i = i0 + lane;
             bool fin = false;
             int p = -1;
+            int64_t q0 = 0, q1 = 0;
             if (i < nacc) {
                 p = s.mem[i];
                 const int k = s.next[p];
                 J.move_batch[paths.move_base(p) + k] = nb;
                 s.next[p] = k + 1;
                 fin = k + 1 == paths.len(p);
-                if (fin) s.done[p] = 1;
-            }
-            const unsigned fm = __ballot_sync(FULL, fin);
-            nfin += __popc(fm);
-            // release successors of finished members
-            if (fin)
-                for (int64_t q = J.soff[p]; q < J.soff[p + 1]; ++q) {
-                    const int sc = J.succ[q];
-                    if (atomicSub(&s.blockers[sc], 1) == 1) {
-                        const int slot = atomicAdd(&s.counter[0], 1);
-                        s.newly[slot] = sc;
-                    }
+                if (fin) {
+                    s.done[p] = 1;
+                    q0 = J.soff[p];
+                    q1 = J.soff[p + 1];
                 }
+            }
+            nfin += __popc(__ballot_sync(FULL, fin));
+            // successors of the finished members, flattened across the warp
+            int tot;
+            const int base = warp_excl_scan((int)(q1 - q0), &tot);
+            for (int t0 = 0; t0 < tot; t0 += 32) {
+                const int t = t0 + lane;
+                int owner = 0;  // largest lane with base <= t
+#pragma unroll
+                for (int st = 16; st > 0; st >>= 1) {
+                    const int cand_l = owner + st;
+                    const int b = __shfl_sync(FULL, base, cand_l);
+                    if (b <= t) owner = cand_l;
+                }
+                const int64_t oq0 = __shfl_sync(FULL, q0, owner);
+                const int ob = __shfl_sync(FULL, base, owner);
+                bool released = false;
+                int sc = -1;
+                if (t < tot) {
+                    sc = J.succ[oq0 + (t - ob)];
+                    released = atomicSub(&s.blockers[sc], 1) == 1;
+                }
+                const unsigned rm = __ballot_sync(FULL, released);
+                if (released) s.newly[nnew + __popc(rm & lanemask_lt())] = sc;
+                nnew += __popc(rm);
+            }
             __syncwarp();
         }
         left -= nacc;
         __syncwarp();
-        nnew = s.counter[0];
-        __syncwarp();
-        if (lane == 0) s.counter[0] = 0;
         if (!J.edge_level && (nfin > 0 || nnew > 0)) {
-            // ready' = (ready - finished) U newly, sorted: merge by rank
+            // ready' = (ready - finished) U newly, sorted
             int nkeep = 0;
             for (int c0 = 0; c0 < nready; c0 += 32) {
                 const int idx = c0 + lane;
-                const bool keep = idx < nready && !s.done[ready[idx]];
+                const int x = idx < nready ? ready[idx] : 0;
+                const bool keep = idx < nready && !s.done[x];
                 const unsigned m = __ballot_sync(FULL, keep);
-                if (keep) {
-                    const int x = ready[idx];
-                    int lt = 0;
-                    for (int q = 0; q < nnew; ++q) lt += s.newly[q] < x;
-                    ready2[nkeep + __popc(m & lanemask_lt()) + lt] = x;
-                }
+                if (keep) ready2[nkeep + __popc(m & lanemask_lt())] = x;
                 nkeep += __popc(m);
             }
-            __syncwarp();
-            for (int q = lane; q < nnew; q += 32) {
-                const int x = s.newly[q];
-                int lt = 0;
-                for (int r = 0; r < nnew; ++r) lt += s.newly[r] < x;
-                // kept ready ids below x: binary search is not possible on ready2
-                // (interleaved), count in the pre-merge list instead
-                int a = 0, b = nready, kept_lt = 0;
-                (void)a;
-                (void)b;
-                for (int r = 0; r < nready; ++r) {
-                    const int y = ready[r];
-                    if (y >= x) break;
-                    kept_lt += !s.done[y];
+            // sorted newly (in place)
+            if (nnew <= 32) {
+                int v = lane < nnew ? s.newly[lane] : INT_MAX;
+                v = warp_sort32(v);
+                if (lane < nnew) s.newly[lane] = v;
+            } else {
+                for (int q = lane; q < nnew; q += 32) {
+                    const int x = s.newly[q];
+                    int lt = 0;
+                    for (int r2 = 0; r2 < nnew; ++r2) lt += s.newly[r2] < x;
+                    s.mem[lt] = x;  // mem is free at this point
                 }
-                ready2[kept_lt + lt] = x;
+                __syncwarp();
+                for (int q = lane; q < nnew; q += 32) s.newly[q] = s.mem[q];
             }
             __syncwarp();
-            int32_t *t = ready;
-            ready = ready2;
-            ready2 = t;
+            // merge by rank: kept x -> i + #newly<x ; newly y -> j + #kept<y
+            for (int i = lane; i < nkeep; i += 32) {
+                const int x = ready2[i];
+                ready[i + lower_bound_i32(s.newly, nnew, x)] = x;
+            }
+            for (int j = lane; j < nnew; j += 32) {
+                const int y = s.newly[j];
+                ready[j + lower_bound_i32(ready2, nkeep, y)] = y;
+            }
+            __syncwarp();
             nready = nkeep + nnew;
         }
         ++nb;
@@ -271,7 +344,7 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
 }
 
 __global__ void batch_explicit_kernel(BatchJob J, ExplicitPaths paths) {
-    if (threadIdx.x < 32) batch_warp(J, paths);
+    if (threadIdx.x < 32) batch_warp<ExplicitPaths, false>(J, paths);
 }
 
 cudaError_t launch_batch_explicit(const BatchJob &J, const int64_t *off, const int32_t *verts, cudaStream_t st) {
@@ -529,7 +602,7 @@ __global__ void batch_pipeline_kernel(PipelineArgs a) {
         J.status = a.status + inst;
         J.detail = a.detail ? a.detail + inst : nullptr;
         ImplicitPaths ip{a.path_src + o, a.path_dst + o, a.mbase + o, a.mbase[o], a.H};
-        batch_warp(J, ip);
+        batch_warp<ImplicitPaths, true>(J, ip);
     }
 }
 
