@@ -44,6 +44,12 @@ int grid_blocks(Ctx *c, int solver, const GridShape &s, int count) {
 cudaError_t launch(Ctx *c, int solver, GridParams &p, int grid) {
     p.snap = c->dev<uint64_t>(S_SNAP, (size_t)grid * grid_snap_words(p.shape));
     if (!p.snap) return cudaErrorMemoryAllocation;
+    if (solver == 0) {
+        void *pl = c->get(S_PLAN, (size_t)p.count * redrec_plan_bytes(p.shape.W) + 1024);
+        if (!pl) return cudaErrorMemoryAllocation;
+        p.plans = redrec_plans_carve(pl, p.shape.W, p.count);
+    }
+    c->launches += solver == 0 ? 2 : 1;
     return launch_grid_solver(solver, p, grid, c->stream);
 }
 
@@ -118,7 +124,6 @@ recon_status grid_single(int solver, recon_ctx *ctx, const uint64_t *occ, int W,
         return cuda_fail(cudaErrorMemoryAllocation, "grid workspace", detail);
     CK(cudaMemcpyAsync(d_occ, occ, words * 8, cudaMemcpyHostToDevice, c->stream), "occ H2D");
     CK(launch(c, solver, p, 1), "grid kernel launch");
-    c->launches += 1;
     int32_t h_cnt = 0, h_st = 0, h_det = 0;
     int64_t h_td = 0;
     CK(cudaMemcpyAsync(&h_cnt, p.path_count, 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
@@ -184,7 +189,6 @@ recon_status grid_batch(int solver, recon_ctx *ctx, const recon_grid_batch *b, b
         p.detail = b->detail;
         p.events = b->events;
         CK(launch(c, solver, p, grid_blocks(c, solver, s, b->count)), "grid kernel launch");
-        c->launches += 1;
         return RECON_OK;
     }
     uint64_t *d_occ = c->dev<uint64_t>(S_OCC, n * words);
@@ -202,7 +206,6 @@ recon_status grid_batch(int solver, recon_ctx *ctx, const recon_grid_batch *b, b
         return cuda_fail(cudaErrorMemoryAllocation, "grid batch workspace", detail);
     CK(cudaMemcpyAsync(d_occ, b->occ, n * words * 8, cudaMemcpyHostToDevice, c->stream), "occ H2D");
     CK(launch(c, solver, p, grid_blocks(c, solver, s, b->count)), "grid kernel launch");
-    c->launches += 1;
     CK(cudaMemcpyAsync(b->path_src, p.path_src, n * stride * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
     CK(cudaMemcpyAsync(b->path_dst, p.path_dst, n * stride * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
     if (b->path_event)

@@ -8,6 +8,8 @@
 namespace rb {
 
 __global__ void redrec_kernel(GridParams p);
+__global__ void redrec_plan_kernel(GridParams p);
+int64_t redrec_plan_smem(int W);
 __global__ void bird_kernel(GridParams p);
 
 bool grid_shape(int W, int H, int k, int nwarps, GridShape &s) {
@@ -33,10 +35,47 @@ bool grid_shape(int W, int H, int k, int nwarps, GridShape &s) {
 
 size_t grid_snap_words(const GridShape &s) { return (size_t)2 * s.W * s.wpd; }
 
+size_t redrec_plan_bytes(int W) {
+    return (size_t)align_up(W, 16) + 3 * (size_t)align_up(2 * W, 16) + (size_t)align_up(4 * (W + 2), 16) + 32;
+}
+
+RedrecPlans redrec_plans_carve(void *base, int W, int count) {
+    unsigned char *b = (unsigned char *)base;
+    RedrecPlans pl;
+    const size_t n = (size_t)count;
+    pl.ev_type = (uint8_t *)b;
+    b += align_up(n * W, 16);
+    pl.ev_col = (int16_t *)b;
+    b += align_up(n * W * 2, 16);
+    pl.ev_aux = (int16_t *)b;
+    b += align_up(n * W * 2, 16);
+    pl.wave_list = (int16_t *)b;
+    b += align_up(n * W * 2, 16);
+    pl.wave_off = (int32_t *)b;
+    b += align_up(n * (W + 2) * 4, 16);
+    pl.meta = (int32_t *)b;
+    return pl;
+}
+
 cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaStream_t stream) {
     const int threads = 32 * p.shape.nwarps;
     void (*kern)(GridParams) = solver == 0 ? redrec_kernel : bird_kernel;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.shape.smem_bytes);
+    cudaError_t e;
+    if (solver == 0) {
+        // plans first: one warp per instance, all instances in parallel
+        const int pw = 4;
+        const int64_t psmem = pw * redrec_plan_smem(p.shape.W);
+        e = cudaFuncSetAttribute(redrec_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+        if (e != cudaSuccess) return e;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, redrec_plan_kernel, 32 * pw, psmem);
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int pgrid = std::max(1, std::min((p.count + pw - 1) / pw, std::max(1, per_sm) * sms));
+        redrec_plan_kernel<<<pgrid, 32 * pw, psmem, stream>>>(p);
+    }
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.shape.smem_bytes);
     if (e != cudaSuccess) return e;
     kern<<<grid, threads, p.shape.smem_bytes, stream>>>(p);
     return cudaGetLastError();

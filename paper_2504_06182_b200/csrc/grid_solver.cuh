@@ -23,6 +23,15 @@ struct GridSmem {
         ev_col, ev_aux, ev_a, ev_level, wave_list, lastc, lastm, ev_type, solved, total;
 };
 
+// red-rec plans in global memory (redrec_plan_kernel -> redrec_kernel), per
+// instance: W event types / columns / aux columns / wave list, W+2 wave
+// offsets, 8 meta ints (n1, n2, nlev, status, detail)
+struct RedrecPlans {
+    uint8_t *ev_type;
+    int16_t *ev_col, *ev_aux, *wave_list;
+    int32_t *wave_off, *meta;
+};
+
 struct GridParams {
     GridShape shape;
     const uint64_t *occ;
@@ -32,6 +41,7 @@ struct GridParams {
     int64_t *total_displacement;
     int32_t *status, *detail, *events;
     uint64_t *snap;          // red-rec: per-CTA event snapshots, 2*W*wpd words per CTA (grid-sized)
+    RedrecPlans plans;       // red-rec: [count] plans
     long long *phase_clock;  // optional: clock64 at phase boundaries of instance 0 (profiling)
 };
 
@@ -39,5 +49,7 @@ bool grid_shape(int W, int H, int k, int nwarps, GridShape &s);
 cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaStream_t stream);
 int grid_occupancy(int solver, const GridShape &s);
 size_t grid_snap_words(const GridShape &s);
+size_t redrec_plan_bytes(int W);  // global plan bytes per instance
+RedrecPlans redrec_plans_carve(void *base, int W, int count);
 
 }  // namespace rb

@@ -246,7 +246,8 @@ __device__ __forceinline__ unsigned long long receiver_key(int q, int W, const i
 // the receiver r, so only r and the receivers adjacent to d and r (their
 // nearest unsolved neighbours) need new keys; a column turning transit is
 // unlinked with two range updates.
-__device__ int redrec_plan(const Geo &g, Block &b, int *n1o, int *n2o, int *nlevo) {
+template <class B>
+__device__ int redrec_plan(const Geo &g, B &b, int *n1o, int *n2o, int *nlevo) {
     const int lane = lane_id(), W = g.W;
     const int per = (W + 31) / 32, c0 = lane * per, c1 = min(W, c0 + per);
     int *sig = b.ev_count;                           // scratch: plan-time surplus
@@ -437,6 +438,101 @@ __device__ int redrec_plan(const Geo &g, Block &b, int *n1o, int *n2o, int *nlev
 // kernel
 // --------------------------------------------------------------------------
 
+// --------------------------------------------------------------------------
+// planner kernel: one warp per instance, plans written to global memory
+// --------------------------------------------------------------------------
+
+// the planner warp's shared-memory view (same field names as Block)
+struct PlanView {
+    int *sigma, *ev_count, *wave_off;
+    uint32_t *keys;
+    uint8_t *ev_type, *solved;
+    int16_t *ev_col, *ev_aux, *ev_level, *wave_list, *ev_a, *lastc, *lastm;
+};
+
+__host__ __device__ inline int64_t plan_warp_bytes(int W) {
+    return align_up((int64_t)W * 8, 16) + align_up((int64_t)W * 4, 16) * 2 + align_up((int64_t)(W + 2) * 4, 16) +
+           align_up(W, 16) * 2 + align_up((int64_t)W * 2, 16) * 7;
+}
+
+__device__ PlanView carve_plan(unsigned char *base, int W) {
+    PlanView v;
+    int64_t off = 0;
+    auto take = [&](int64_t bytes) {
+        unsigned char *at = base + off;
+        off += align_up(bytes, 16);
+        return at;
+    };
+    v.keys = (uint32_t *)take((int64_t)W * 8);
+    v.sigma = (int *)take((int64_t)W * 4);
+    v.ev_count = (int *)take((int64_t)W * 4);
+    v.wave_off = (int *)take((int64_t)(W + 2) * 4);
+    v.ev_type = (uint8_t *)take(W);
+    v.solved = (uint8_t *)take(W);
+    v.ev_col = (int16_t *)take((int64_t)W * 2);
+    v.ev_aux = (int16_t *)take((int64_t)W * 2);
+    v.ev_level = (int16_t *)take((int64_t)W * 2);
+    v.wave_list = (int16_t *)take((int64_t)W * 2);
+    v.ev_a = (int16_t *)take((int64_t)W * 2);
+    v.lastc = (int16_t *)take((int64_t)W * 2);
+    v.lastm = (int16_t *)take((int64_t)W * 2);
+    return v;
+}
+
+int64_t redrec_plan_smem(int W) { return plan_warp_bytes(W); }
+
+__global__ void __launch_bounds__(128) redrec_plan_kernel(GridParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Geo g = make_geo(p.shape);
+    const int warp = warp_id(), lane = lane_id(), wpb = blockDim.x >> 5;
+    PlanView v = carve_plan(smem + (size_t)warp * plan_warp_bytes(g.W), g.W);
+    const RedrecPlans pg = p.plans;
+    const uint64_t last_mask = (g.H & 63) ? ((1ull << (g.H & 63)) - 1ull) : ~0ull;
+    for (int inst = blockIdx.x * wpb + warp; inst < p.count; inst += gridDim.x * wpb) {
+        const uint64_t *occ = p.occ + (size_t)inst * g.W * g.wpd;
+        long long tot = 0;
+        for (int x = lane; x < g.W; x += 32) {
+            int cnt = 0;
+            for (int j = 0; j < g.wpd; ++j) cnt += __popcll(occ[(size_t)x * g.wpd + j] & (j == g.wpd - 1 ? last_mask : ~0ull));
+            v.sigma[x] = cnt - g.k;
+            tot += cnt;
+        }
+        tot = warp_sum64(tot);
+        __syncwarp();
+        int n1 = 0, n2 = 0, nlev = 0, st = RECON_OK, det = 0;
+        if (tot < (long long)g.W * g.k) {  // Problem::check (problem.hpp:113-116)
+            st = RECON_ERR_INFEASIBLE;
+            det = RECON_D_FEWER_SOURCES;
+        } else {
+            const int rc = redrec_plan(g, v, &n1, &n2, &nlev);
+            if (rc) {
+                st = RECON_ERR_LOGIC;
+                det = rc;
+            }
+        }
+        __syncwarp();
+        int *meta = pg.meta + (size_t)inst * 8;
+        if (lane == 0) {
+            meta[0] = n1;
+            meta[1] = n2;
+            meta[2] = nlev;
+            meta[3] = st;
+            meta[4] = det;
+        }
+        if (st == RECON_OK) {
+            const size_t W = g.W;
+            for (int e = lane; e < g.W; e += 32) {
+                pg.ev_type[inst * W + e] = v.ev_type[e];
+                pg.ev_col[inst * W + e] = v.ev_col[e];
+                pg.ev_aux[inst * W + e] = v.ev_aux[e];
+                pg.wave_list[inst * W + e] = v.wave_list[e];
+            }
+            for (int i = lane; i <= nlev + 1; i += 32) pg.wave_off[inst * (W + 2) + i] = v.wave_off[i];
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void __launch_bounds__(256, 4) redrec_kernel(GridParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geo g = make_geo(p.shape);
@@ -467,17 +563,28 @@ __global__ void __launch_bounds__(256, 4) redrec_kernel(GridParams p) {
         }
         __syncthreads();
         if (p.phase_clock && inst == 0 && threadIdx.x == 0) p.phase_clock[0] = clock64();
-        if (s_status == RECON_OK && warp == 0) {
-            int n1 = 0, n2 = 0, nlev = 0;
-            const int rc = redrec_plan(g, b, &n1, &n2, &nlev);
-            if (lane == 0) {
-                s_n1 = n1;
-                s_n2 = n2;
-                s_nlev = nlev;
-                if (rc) {
-                    s_status = RECON_ERR_LOGIC;
-                    s_detail = rc;
+        // the instance's plan (redrec_plan_kernel) -> shared memory
+        {
+            const RedrecPlans pg = p.plans;
+            const int *meta = pg.meta + (size_t)inst * 8;
+            const size_t W = g.W;
+            if (threadIdx.x == 0) {
+                s_n1 = meta[0];
+                s_n2 = meta[1];
+                s_nlev = meta[2];
+                if (s_status == RECON_OK && meta[3] != RECON_OK) {
+                    s_status = meta[3];
+                    s_detail = meta[4];
                 }
+            }
+            if (meta[3] == RECON_OK) {
+                for (int e = threadIdx.x; e < g.W; e += blockDim.x) {
+                    b.ev_type[e] = pg.ev_type[inst * W + e];
+                    b.ev_col[e] = pg.ev_col[inst * W + e];
+                    b.ev_aux[e] = pg.ev_aux[inst * W + e];
+                    b.wave_list[e] = pg.wave_list[inst * W + e];
+                }
+                for (int i = threadIdx.x; i <= meta[2] + 1; i += blockDim.x) b.wave_off[i] = pg.wave_off[inst * (W + 2) + i];
             }
         }
         __syncthreads();
