@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <type_traits>
 #include <cub/device/device_scan.cuh>
 
 #include "batching.cuh"
@@ -58,6 +59,32 @@ struct ImplicitPaths {
     }
     __device__ __forceinline__ int64_t move_base(int p) const { return base[p] - base0; }
 };
+
+// one ready path cached in a lane's registers (register-resident frontier)
+struct LanePath {
+    int p, k, len, xs, ys, xt, yt;
+    int64_t base;
+    __device__ __forceinline__ int32_t v(int H, int kk) const {
+        const int dx = abs(xt - xs);
+        if (kk <= dx) return (xs + (xt > xs ? kk : -kk)) * H + ys;
+        const int m = kk - dx;
+        return xt * H + ys + (yt > ys ? m : -m);
+    }
+};
+
+__device__ __forceinline__ LanePath load_lane_path(const ImplicitPaths &ip, const int32_t *next, int p) {
+    LanePath r;
+    r.p = p;
+    r.k = next[p];
+    const int s = ip.src[p], t = ip.dst[p];
+    r.xs = s / ip.H;
+    r.ys = s - r.xs * ip.H;
+    r.xt = t / ip.H;
+    r.yt = t - r.xt * ip.H;
+    r.len = abs(r.xt - r.xs) + abs(r.yt - r.ys);
+    r.base = ip.move_base(p);
+    return r;
+}
 
 __device__ __forceinline__ bool bit_get(const uint32_t *bm, int v) { return (bm[v >> 5] >> (v & 31)) & 1u; }
 __device__ __forceinline__ void bit_set(uint32_t *bm, int v) { atomicOr(&bm[v >> 5], 1u << (v & 31)); }
@@ -145,7 +172,166 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
     __syncwarp();
     int32_t *ready = s.ready, *ready2 = s.ready2;
     int nb = 0, status = RECON_OK;
+    // Register-resident frontier (FAST path, <= 32 ready paths): lane i keeps
+    // ready path i (ascending id) with its step and endpoints in registers, so
+    // a batch costs one occupancy probe plus fire-and-forget atomics.
+    constexpr bool REG = FAST && std::is_same<Paths, ImplicitPaths>::value;
+    bool regmode = false;
+    LanePath lp;
+    lp.p = INT_MAX;
+    auto enter_regmode = [&]() {
+        lp.p = INT_MAX;
+        if (lane < nready) lp = load_lane_path(reinterpret_cast<const ImplicitPaths &>(paths), s.next, ready[lane]);
+        regmode = true;
+        __syncwarp();
+    };
+    if (REG && nready <= 32) enter_regmode();
     while (left > 0) {
+        if (REG && regmode) {
+            const bool valid = lp.p != INT_MAX;
+            int32_t fr = -1, to = -1;
+            if (valid) {
+                fr = lp.v(H, lp.k);
+                to = lp.v(H, lp.k + 1);
+            }
+            const bool cand = valid && !bit_get(s.occ, to);
+            const unsigned cm = __ballot_sync(FULL, cand);
+            if (!cm) {
+                status = RECON_ERR_INPUT;  // batching.cpp:127-128
+                break;
+            }
+            bool a;
+            if (J.preset != 0) {
+                const int first = __ffs(cm) - 1;
+                const int32_t ff = __shfl_sync(FULL, fr, first), ft = __shfl_sync(FULL, to, first);
+                a = cand && compatible(J.preset, H, fr, to, ff, ft);
+            } else {
+                const unsigned same = __match_any_sync(FULL, cand ? to : -2 - lane);
+                a = cand && (same & lanemask_lt()) == 0;
+            }
+            const unsigned acc = __ballot_sync(FULL, a);
+            if (a) bit_clr(s.occ, fr);
+            __syncwarp();
+            if (a) bit_set(s.occ, to);
+            bool fin = false;
+            if (a) {
+                J.move_batch[lp.base + lp.k] = nb;
+                ++lp.k;
+                fin = lp.k == lp.len;
+            }
+            left -= __popc(acc);
+            const unsigned fm = __ballot_sync(FULL, fin);
+            if (fm) {
+                int64_t q0 = 0, q1 = 0;
+                if (fin) {
+                    s.done[lp.p] = 1;
+                    q0 = J.soff[lp.p];
+                    q1 = J.soff[lp.p + 1];
+                }
+                int nnew = 0, tot;
+                const int basei = warp_excl_scan((int)(q1 - q0), &tot);
+                for (int t0 = 0; t0 < tot; t0 += 32) {
+                    const int t = t0 + lane;
+                    int owner = 0;
+#pragma unroll
+                    for (int st = 16; st > 0; st >>= 1) {
+                        const int cl = owner + st;
+                        if (__shfl_sync(FULL, basei, cl) <= t) owner = cl;
+                    }
+                    const int64_t oq0 = __shfl_sync(FULL, q0, owner);
+                    const int ob = __shfl_sync(FULL, basei, owner);
+                    bool released = false;
+                    int sc = -1;
+                    if (t < tot) {
+                        sc = J.succ[oq0 + (t - ob)];
+                        released = atomicSub(&s.blockers[sc], 1) == 1;
+                    }
+                    const unsigned rm = __ballot_sync(FULL, released);
+                    if (released) s.newly[nnew + __popc(rm & lanemask_lt())] = sc;
+                    nnew += __popc(rm);
+                }
+                if (fin) lp.p = INT_MAX;
+                __syncwarp();
+                const unsigned live = __ballot_sync(FULL, lp.p != INT_MAX);
+                const int nlive = __popc(live);
+                if (nlive + nnew > 32) {
+                    // spill to the shared-list path: live lanes are ascending
+                    if (lp.p != INT_MAX) {
+                        s.next[lp.p] = lp.k;
+                        ready2[__popc(live & lanemask_lt())] = lp.p;
+                    }
+                    __syncwarp();
+                    if (nnew <= 32) {
+                        int v = lane < nnew ? s.newly[lane] : INT_MAX;
+                        v = warp_sort32(v);
+                        if (lane < nnew) s.newly[lane] = v;
+                    } else {
+                        for (int q = lane; q < nnew; q += 32) {
+                            const int x = s.newly[q];
+                            int lt = 0;
+                            for (int r2 = 0; r2 < nnew; ++r2) lt += s.newly[r2] < x;
+                            s.mem[lt] = x;
+                        }
+                        __syncwarp();
+                        for (int q = lane; q < nnew; q += 32) s.newly[q] = s.mem[q];
+                    }
+                    __syncwarp();
+                    for (int i = lane; i < nlive; i += 32) {
+                        const int x = ready2[i];
+                        ready[i + lower_bound_i32(s.newly, nnew, x)] = x;
+                    }
+                    for (int j = lane; j < nnew; j += 32) {
+                        const int y = s.newly[j];
+                        ready[j + lower_bound_i32(ready2, nlive, y)] = y;
+                    }
+                    __syncwarp();
+                    nready = nlive + nnew;
+                    regmode = false;
+                } else if (nnew > 0) {
+                    // newly released paths take the empty lanes, then sort lanes by id
+                    const unsigned empty = ~live;
+                    const int erank = __popc(empty & lanemask_lt());
+                    if (lp.p == INT_MAX && erank < nnew)
+                        lp = load_lane_path(reinterpret_cast<const ImplicitPaths &>(paths), s.next, s.newly[erank]);
+                    int key = lp.p == INT_MAX ? INT_MAX : (lp.p << 5) | lane;
+                    key = warp_sort32(key);
+                    const int src = key == INT_MAX ? lane : (key & 31);
+                    LanePath q;
+                    q.p = __shfl_sync(FULL, lp.p, src);
+                    q.k = __shfl_sync(FULL, lp.k, src);
+                    q.len = __shfl_sync(FULL, lp.len, src);
+                    q.xs = __shfl_sync(FULL, lp.xs, src);
+                    q.ys = __shfl_sync(FULL, lp.ys, src);
+                    q.xt = __shfl_sync(FULL, lp.xt, src);
+                    q.yt = __shfl_sync(FULL, lp.yt, src);
+                    q.base = __shfl_sync(FULL, lp.base, src);
+                    lp = key == INT_MAX ? LanePath{INT_MAX, 0, 0, 0, 0, 0, 0, 0} : q;
+                } else {
+                    // finished lanes leave gaps: compact live lanes (order kept)
+                    const int dst_rank = __popc(live & lanemask_lt());
+                    int src = lane;
+                    // lane L takes the L-th live lane
+                    for (int st = 0; st < 32; ++st) {
+                        const bool hit = ((live >> st) & 1u) && __popc(live & ((1u << st) - 1u)) == lane;
+                        if (hit) src = st;
+                    }
+                    (void)dst_rank;
+                    LanePath q;
+                    q.p = __shfl_sync(FULL, lp.p, src);
+                    q.k = __shfl_sync(FULL, lp.k, src);
+                    q.len = __shfl_sync(FULL, lp.len, src);
+                    q.xs = __shfl_sync(FULL, lp.xs, src);
+                    q.ys = __shfl_sync(FULL, lp.ys, src);
+                    q.xt = __shfl_sync(FULL, lp.xt, src);
+                    q.yt = __shfl_sync(FULL, lp.yt, src);
+                    q.base = __shfl_sync(FULL, lp.base, src);
+                    lp = lane < nlive ? q : LanePath{INT_MAX, 0, 0, 0, 0, 0, 0, 0};
+                }
+            }
+            __syncwarp();
+            ++nb;
+            continue;
+        }
         // ---- 1. candidate scan (ascending id), greedy acceptance
         int nacc = 0;
         int32_t f_from = -1, f_to = -1;  // first accepted move of the batch
@@ -335,6 +521,7 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
             nready = nkeep + nnew;
         }
         ++nb;
+        if (REG && nready <= 32) enter_regmode();
     }
     if (lane == 0) {
         *J.batch_count = status == RECON_OK ? nb : 0;
@@ -557,7 +744,8 @@ cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *
     return cudaGetLastError();
 }
 
-__global__ void batch_pipeline_kernel(PipelineArgs a) {
+__global__ void batch_pipeline_kernel(PipelineArgs a, int occ_in_smem) {
+    extern __shared__ __align__(16) uint32_t bsmem[];
     const int64_t S = (int64_t)a.W * a.k, nwb = ((int64_t)a.W * a.H + 31) / 32;
     const int nw = blockDim.x >> 5;
     for (int inst = blockIdx.x * nw + warp_id(); inst < a.count; inst += gridDim.x * nw) {
@@ -586,6 +774,12 @@ __global__ void batch_pipeline_kernel(PipelineArgs a) {
         J.soff = a.soff + o;
         J.succ = a.succ;
         J.s.occ = a.occ + inst * nwb;
+        if (occ_in_smem) {  // the instance's occupancy bitmap lives in this warp's shared memory
+            uint32_t *mine = bsmem + (size_t)warp_id() * nwb;
+            for (int64_t w = lane_id(); w < nwb; w += 32) mine[w] = J.s.occ[w];
+            __syncwarp();
+            J.s.occ = mine;
+        }
         J.s.inb = a.inb + inst * nwb;
         J.s.next = a.next + o;
         J.s.blockers = a.indeg + o;
@@ -614,9 +808,18 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
     cudaMemsetAsync(a.inb, 0, (size_t)a.count * nwb * 4, st);
     cudaMemsetAsync(a.counter, 0, (size_t)a.count * 4, st);
     (void)N;
-    const int warps = 4;
-    const int grid = (int)std::min<int64_t>(((int64_t)a.count + warps - 1) / warps, (int64_t)sms * 16);
-    batch_pipeline_kernel<<<grid, warps * 32, 0, st>>>(a);
+    // occupancy bitmap in shared memory when a few warps' worth fits
+    const int64_t bm_bytes = nwb * 4;
+    int warps = 4, occ_smem = 0;
+    size_t smem = 0;
+    if (bm_bytes <= 48 * 1024) {
+        warps = (int)std::max<int64_t>(1, std::min<int64_t>(8, (96 * 1024) / bm_bytes));
+        occ_smem = 1;
+        smem = (size_t)warps * bm_bytes;
+        cudaFuncSetAttribute(batch_pipeline_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    const int grid = (int)std::min<int64_t>(((int64_t)a.count + warps - 1) / warps, (int64_t)sms * 32);
+    batch_pipeline_kernel<<<grid, warps * 32, smem, st>>>(a, occ_smem);
     return cudaGetLastError();
 }
 

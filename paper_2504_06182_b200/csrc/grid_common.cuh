@@ -52,6 +52,8 @@ __host__ __device__ inline void grid_smem_layout(const GridShape &s, GridSmem &o
     o.ev_col = take((int64_t)s.W * 2, 16);
     o.ev_aux = take((int64_t)s.W * 2, 16);
     o.ev_a = take((int64_t)s.W * 2, 16);
+    o.ev_nr = take((int64_t)s.W * 2, 16);
+    o.ev_nl = take((int64_t)s.W * 2, 16);
     o.ev_level = take((int64_t)s.W * 2, 16);
     o.wave_list = take((int64_t)s.W * 2, 16);
     o.lastc = take((int64_t)s.W * 2, 16);
@@ -186,6 +188,45 @@ __device__ __forceinline__ long long own_emit(const Geo &g, int col, const OwnSo
     return warp_sum64(disp);
 }
 
+// Emission of a solved OWN event straight from the column plane: every
+// lane ranks its own chunk's tokens with three warp scans (top tokens by
+// depth descending, residents, bottom tokens) and writes the paths of the
+// used ones; the split a and the right/left counts come from the solve pass.
+__device__ __forceinline__ long long own_emit_direct(const Geo &g, int col, const uint64_t *m, int a, int n_right,
+                                                     int n_left, PathOut o, int off, int evid) {
+    const int lane = lane_id(), B = g.B, base = lane * B;
+    const uint32_t ch = lane_chunk(m, g.wpd, lane, B);
+    const uint32_t topm = ch & chunk_range(base, B, 0, g.lo);
+    const uint32_t resm = ch & chunk_range(base, B, g.lo, g.hi + 1);
+    const uint32_t botm = ch & chunk_range(base, B, g.hi + 1, g.H);
+    int nt, R, nb;
+    int et = warp_excl_scan(__popc(topm), &nt);
+    int er = warp_excl_scan(__popc(resm), &R);
+    int eb = warp_excl_scan(__popc(botm), &nb);
+    (void)nb;
+    const int b = g.k - R - a;
+    long long disp = 0;
+    auto put = [&](int j, int depth) {
+        const int t = g.lo + j;
+        const int p = off + emit_slot(g, j, n_right, n_left);
+        o.src[p] = col * g.H + (g.H - 1 - depth);
+        o.dst[p] = col * g.H + (g.H - 1 - t);
+        if (o.ev) o.ev[p] = evid;
+        disp += t > depth ? t - depth : depth - t;
+    };
+    for (uint32_t x = topm; x; x &= x - 1, ++et) {
+        const int desc = nt - 1 - et;  // 0 = innermost
+        if (desc < a) put(a - 1 - desc, base + __ffs(x) - 1);
+    }
+    for (uint32_t x = resm; x; x &= x - 1, ++er) {
+        const int depth = base + __ffs(x) - 1, j = a + er;
+        if (g.lo + j != depth) put(j, depth);
+    }
+    for (uint32_t x = botm; x; x &= x - 1, ++eb)
+        if (eb < b) put(a + R + eb, base + __ffs(x) - 1);
+    return warp_sum64(disp);
+}
+
 // Column after its OWN event: band full, used reservoir tokens gone, parked
 // (unused) reservoir tokens stay (redrec.cpp:150-164, bird.cpp:90-99).
 // Returns the parked count.
@@ -210,7 +251,7 @@ struct Block {
     uint64_t *dep;
     uint32_t *keys, *bal;
     int *sigma, *ev_count, *ev_off, *wave_off, *lvl_t, *lvl_b, *scal;
-    int16_t *lists, *plists, *mark_dest, *ev_col, *ev_aux, *ev_a, *ev_level, *wave_list, *lastc, *lastm;
+    int16_t *lists, *plists, *mark_dest, *ev_col, *ev_aux, *ev_a, *ev_nr, *ev_nl, *ev_level, *wave_list, *lastc, *lastm;
     uint8_t *ev_type, *solved;
 };
 
@@ -234,6 +275,8 @@ __device__ __forceinline__ Block carve(const GridShape &s, unsigned char *smem) 
     b.ev_col = (int16_t *)(smem + o.ev_col);
     b.ev_aux = (int16_t *)(smem + o.ev_aux);
     b.ev_a = (int16_t *)(smem + o.ev_a);
+    b.ev_nr = (int16_t *)(smem + o.ev_nr);
+    b.ev_nl = (int16_t *)(smem + o.ev_nl);
     b.ev_level = (int16_t *)(smem + o.ev_level);
     b.wave_list = (int16_t *)(smem + o.wave_list);
     b.lastc = (int16_t *)(smem + o.lastc);

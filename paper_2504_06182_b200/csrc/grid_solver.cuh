@@ -20,7 +20,7 @@ struct GridShape {
 
 struct GridSmem {
     int64_t dep, keys, bal, sigma, ev_count, ev_off, wave_off, lvl_t, lvl_b, scal, lists, plists, mark_dest,
-        ev_col, ev_aux, ev_a, ev_level, wave_list, lastc, lastm, ev_type, solved, total;
+        ev_col, ev_aux, ev_a, ev_nr, ev_nl, ev_level, wave_list, lastc, lastm, ev_type, solved, total;
 };
 
 // red-rec plans in global memory (redrec_plan_kernel -> redrec_kernel), per

@@ -601,6 +601,8 @@ __global__ void __launch_bounds__(256, 4) redrec_kernel(GridParams p) {
                 }
                 if (lane == 0) {
                     b.ev_a[e] = (int16_t)s.a;
+                    b.ev_nr[e] = (int16_t)s.n_right;
+                    b.ev_nl[e] = (int16_t)s.n_left;
                     b.ev_count[e] = s.n_right + s.n_left;
                 }
                 __syncwarp();
@@ -621,6 +623,8 @@ __global__ void __launch_bounds__(256, 4) redrec_kernel(GridParams p) {
                         own_update(g, mc, s, L);
                         if (lane == 0) {
                             b.ev_a[e] = (int16_t)s.a;
+                            b.ev_nr[e] = (int16_t)s.n_right;
+                            b.ev_nl[e] = (int16_t)s.n_left;
                             b.ev_count[e] = s.n_right + s.n_left;
                             if (aux >= 0) b.mark_dest[col] = (int16_t)aux;  // parked -> marks for aux
                         }
@@ -656,6 +660,8 @@ __global__ void __launch_bounds__(256, 4) redrec_kernel(GridParams p) {
                 }
                 if (lane == 0) {
                     b.ev_a[e] = (int16_t)s.a;
+                    b.ev_nr[e] = (int16_t)s.n_right;
+                    b.ev_nl[e] = (int16_t)s.n_left;
                     b.ev_count[e] = s.n_right + s.n_left;
                 }
                 __syncwarp();
@@ -682,9 +688,7 @@ __global__ void __launch_bounds__(256, 4) redrec_kernel(GridParams p) {
                     const bool loop = e >= n1 && e < n1 + n2;
                     if (b.ev_type[e] == EV_OWN) {
                         const uint64_t *m = loop ? snap + (size_t)(2 * col) * g.wpd : b.dep + (size_t)col * g.wpd;
-                        OwnSolve s;
-                        own_solve(g, m, L, b.ev_a[e], s);
-                        disp += own_emit(g, col, s, L, o, b.ev_off[e], e);
+                        disp += own_emit_direct(g, col, m, b.ev_a[e], b.ev_nr[e], b.ev_nl[e], o, b.ev_off[e], e);
                     } else {
                         const uint64_t *mr = snap + (size_t)(2 * col) * g.wpd, *md = snap + (size_t)(2 * col + 1) * g.wpd;
                         FlushSolve f;

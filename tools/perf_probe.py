@@ -56,7 +56,7 @@ def grid(solver, W, H, hp, k, seed, count):
             "paths_per_grid": P / count, "GBps_alg": (count * W * H / 8 + 8 * P + 32 * count) / mn / 1e6}
 
 
-def pipeline(solver, W, H, hp, k, seed, count, preset):
+def pipeline(solver, W, H, hp, k, seed, count, preset, ms_=None):
     occ = torch.from_numpy(sample_grids(seed, count, W, H, k).view(np.int64)).to(dev)
     S = W * hp
     src = torch.empty(count * S, dtype=torch.int32, device=dev)
@@ -65,7 +65,7 @@ def pipeline(solver, W, H, hp, k, seed, count, preset):
     td = torch.empty(count, dtype=torch.int64, device=dev)
     st = torch.empty(count, dtype=torch.int32, device=dev)
     de = torch.empty(count, dtype=torch.int32, device=dev)
-    ms_ = W * H * 12
+    ms_ = ms_ or W * H * 12
     mb = torch.empty(count * ms_, dtype=torch.int32, device=dev)
     bc = torch.empty(count, dtype=torch.int32, device=dev)
     g = GridBatch(occ.data_ptr(), count, W, H, hp, src.data_ptr(), dst.data_ptr(), None, pc.data_ptr(),
@@ -106,6 +106,8 @@ CASES = {
     "c3_bird_solve": lambda: grid("bird", 64, 64, 40, 2662, 0x64000000, 4096),
     "c3_pipeline_none": lambda: pipeline("bird", 64, 64, 40, 2662, 0x64000000, 4096, 0),
     "c3_pipeline_coldir": lambda: pipeline("bird", 64, 64, 40, 2662, 0x64000000, 1024, 1),
+    "c5_pipeline_4": lambda: pipeline("bird", 512, 512, 307, 157286, 0x51200000, 4, 0, 12_000_000),
+    "c4_pipeline_redrec_64": lambda: pipeline("redrec", 256, 256, 153, 39322, 257, 64, 0, 1_500_000),
     "c5_bird_solve_64": lambda: grid("bird", 512, 512, 307, 157286, 0x51200000, 64),
     "c5_bird_solve_1": lambda: grid("bird", 512, 512, 307, 157286, 0x51200000, 1),
     "c2_chains_1m": lambda: chains(1024, 563, 256, 767, 0x1D000000, 1 << 20),
