@@ -33,18 +33,13 @@ struct ChainCtx {
     int tl, th, k;
     int ns, idxL, idxR, R;  // sources; #S < tl; #S <= th; residents
     const int16_t *S;       // sorted sources
+    const int32_t *PS;      // PS[i] = S[0] + ... + S[i-1]
+    const int16_t *hole;    // hole[q] = q-th empty band cell (1-based), hole[0] = tl-1
 };
 
-// #(residents with e < a), e_r = S[idxL+r] - tl - r (non-decreasing)
-__device__ __forceinline__ int cnt_e_lt(const ChainCtx &c, int a) {
-    int lo = 0, hi = c.R;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (c.S[c.idxL + mid] - c.tl - mid < a) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
+// #(residents with e < a), e_r = S[idxL+r] - tl - r: the residents before the
+// a-th empty band cell
+__device__ __forceinline__ int cnt_e_lt(const ChainCtx &c, int a) { return c.hole[a] - c.tl - a + 1; }
 
 // Delta(a) = cost(a) - cost(a-1)
 __device__ __forceinline__ long long chain_delta(const ChainCtx &c, int a) {
@@ -77,19 +72,10 @@ __device__ int chain_best_a(const ChainCtx &c, int amin, int amax) {
 __device__ long long chain_cost(const ChainCtx &c, int a) {
     const int b = (c.k - c.R) - a;
     const int m = cnt_e_lt(c, a);
-    long long top = 0, resm = 0, resR = 0, bot = 0;
-    for (int i = c.idxL - a + lane_id(); i < c.idxR + b; i += 32) {
-        const long long v = c.S[i];
-        if (i < c.idxL) top += v;
-        else if (i < c.idxR) {
-            resR += v;
-            if (i < c.idxL + m) resm += v;
-        } else bot += v;
-    }
-    top = warp_sum64(top);
-    resm = warp_sum64(resm);
-    resR = warp_sum64(resR);
-    bot = warp_sum64(bot);
+    const long long top = (long long)c.PS[c.idxL] - c.PS[c.idxL - a];
+    const long long resm = (long long)c.PS[c.idxL + m] - c.PS[c.idxL];
+    const long long resR = (long long)c.PS[c.idxR] - c.PS[c.idxL];
+    const long long bot = (long long)c.PS[c.idxR + b] - c.PS[c.idxR];
     const long long Em = resm - (long long)m * c.tl - (long long)m * (m - 1) / 2;
     const long long ER = resR - (long long)c.R * c.tl - (long long)c.R * (c.R - 1) / 2;
     long long cost = (long long)a * c.tl + (long long)a * (a - 1) / 2 - top;
@@ -120,6 +106,8 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
     int16_t *S = (int16_t *)(smem + (size_t)warp * p.warp_smem);
     int16_t *B = (int16_t *)(smem + (size_t)warp * p.warp_smem + p.b_off);   // block boundaries
     int16_t *BE = (int16_t *)(smem + (size_t)warp * p.warp_smem + p.be_off);  // kept block ends
+    int32_t *PS = (int32_t *)(smem + (size_t)warp * p.warp_smem + p.ps_off);  // prefix sums of S
+    int16_t *HL = (int16_t *)(smem + (size_t)warp * p.warp_smem + p.hole_off); // empty band cells
     for (int ch = blockIdx.x * nw + warp; ch < p.count; ch += gridDim.x * nw) {
         const uint32_t *bits = (const uint32_t *)(p.occ + (size_t)ch * words64);
         uint32_t w[4] = {0u, 0u, 0u, 0u};
@@ -140,12 +128,45 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
                 for (uint32_t x = w[q]; x; x &= x - 1) S[e++] = (int16_t)((lane * per32 + q) * 32 + __ffs(x) - 1);
         }
         __syncwarp();
+        // prefix sums of the sorted sources and the empty band cells
+        {
+            int carry = 0;
+            for (int i0 = 0; i0 <= ns; i0 += 32) {
+                const int i = i0 + lane;
+                int x = (i > 0 && i <= ns) ? S[i - 1] : 0;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(FULL, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (i <= ns) PS[i] = carry + x;
+                carry += __shfl_sync(FULL, x, 31);
+            }
+            int hcnt = 0;
+            uint32_t hm[4];
+            for (int q = 0; q < per32; ++q) {
+                const int v0 = (lane * per32 + q) * 32;
+                hm[q] = ~w[q] & chunk_range(v0, 32, tl, th + 1);
+                hcnt += __popc(hm[q]);
+            }
+            int htot;
+            int he = warp_excl_scan(hcnt, &htot);
+            for (int q = 0; q < per32; ++q)
+                for (uint32_t x = hm[q]; x; x &= x - 1) HL[1 + he++] = (int16_t)((lane * per32 + q) * 32 + __ffs(x) - 1);
+            if (lane == 0) {
+                HL[0] = (int16_t)(tl - 1);
+                HL[htot + 1] = (int16_t)(th + 1);
+            }
+        }
+        __syncwarp();
         ChainCtx c;
         c.tl = tl;
         c.th = th;
         c.k = k;
         c.ns = ns;
         c.S = S;
+        c.PS = PS;
+        c.hole = HL;
         {
             int l = 0, r = 0;
             for (int q = 0; q < per32; ++q) {
@@ -165,7 +186,7 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
         } else {
             // ---- candidate cuts (exact1d.cpp:219-247) as a prefix-max scan
             const int E = ns - k;
-            int lmax = INT_MIN, ncut = 0;
+            int lmax = INT_MIN, ncut = 0, nleft = 0;
             {
                 int ps = base_ps;
                 for (int q = 0; q < per32; ++q)
@@ -207,8 +228,11 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
                         const int D = ps - min(max(v - tl, 0), k);
                         if (!s && (v < tl || v > th) && D <= E && D >= run) {
                             run = D;
-                            if (pass == 0) ++mine;
-                            else B[slot++] = (int16_t)ps;
+                            if (pass == 1) B[slot++] = (int16_t)ps;
+                            else {
+                                ++mine;
+                                nleft += v < tl;  // cuts left of the targets
+                            }
                         }
                         ps += s;
                     }
@@ -220,23 +244,7 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
             // A cut at vertex v < tl has ps <= idxL; a cut at v > th has ps >= idxR.
             // (idxL == idxR only if there are no residents; disambiguate via the
             // number of left cuts computed from vertex positions.)
-            int nleft = 0;
-            {
-                int run = run0, ps = base_ps;
-                for (int q = 0; q < per32; ++q)
-                    for (int bb = 0; bb < 32; ++bb) {
-                        const int v = (lane * per32 + q) * 32 + bb;
-                        if (v >= n || v >= tl) break;
-                        const bool s = (w[q] >> bb) & 1u;
-                        const int D = ps - min(max(v - tl, 0), k);
-                        if (!s && D <= E && D >= run) {
-                            run = D;
-                            ++nleft;
-                        }
-                        ps += s;
-                    }
-                nleft = warp_sum(nleft);
-            }
+            nleft = warp_sum(nleft);
             // non-empty blocks: [B[q], B[q+1]) for q in [0, ncut]; the target is
             // q == nleft (it holds the targets even without sources)
             int nb = 0, t = 0;
@@ -259,9 +267,9 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
             s0 = B[t];
             s1 = BE[t];
             if (nb > 1) {
-                int ba;
-                const long long global = block_opt(c, 0, ns, &ba);
-                long long wt = block_opt(c, s0, s1, &ba);
+                int ga;
+                const long long global = block_opt(c, 0, ns, &ga);
+                long long wt = block_opt(c, s0, s1, &a);
                 if (wt != global) {
                     // literal sweep (exact1d.cpp:269-289): blocks tL..tR form the
                     // target; list index i maps to the current merged list
@@ -281,6 +289,7 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
                             if (wj < wt) {
                                 --tL;
                                 wt = wj;
+                                a = tmp;
                                 if (i > 0) --i;
                             } else {
                                 ++i;
@@ -290,6 +299,7 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
                             if (wj < wt) {
                                 ++tR;
                                 wt = wj;
+                                a = tmp;
                                 if (i > 0) --i;
                             } else {
                                 ++i;
@@ -301,10 +311,11 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
                     if (wt != global) {  // whole chain (exact1d.cpp:293-296)
                         s0 = 0;
                         s1 = ns;
+                        a = ga;
                     }
                 }
             }
-            block_opt(c, s0, s1, &a);
+            if (nb <= 1) block_opt(c, s0, s1, &a);
             if (a < 0) {
                 status = RECON_ERR_INFEASIBLE;
                 detail = RECON_D_GEN_NO_ASSIGNMENT;
@@ -343,9 +354,13 @@ cudaError_t launch_chain_band(const ChainBandParams &p0, int sms, cudaStream_t s
     ChainBandParams p = p0;
     const int n = p.n;
     if (n <= 0 || n > 4096) return cudaErrorInvalidValue;
-    p.b_off = (int)(((size_t)n * 2 + 15) / 16 * 16);
-    p.be_off = p.b_off + (int)(((size_t)(n + 2) * 2 + 15) / 16 * 16);
-    p.warp_smem = p.be_off + (int)(((size_t)(n + 2) * 2 + 15) / 16 * 16);
+    const int k = p.t_hi - p.t_lo + 1;
+    auto al = [](size_t x) { return (int)((x + 15) / 16 * 16); };
+    p.b_off = al((size_t)n * 2);
+    p.be_off = p.b_off + al((size_t)(n + 2) * 2);
+    p.ps_off = p.be_off + al((size_t)(n + 2) * 2);
+    p.hole_off = p.ps_off + al((size_t)(n + 1) * 4);
+    p.warp_smem = p.hole_off + al((size_t)(k + 2) * 2);
     const int warps = 8;
     const size_t smem = (size_t)warps * p.warp_smem;
     cudaError_t e = cudaFuncSetAttribute(chain_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
