@@ -5,6 +5,7 @@
 // occupancy_dag (virtual_line.hpp:104).
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "capi_internal.cuh"
@@ -35,16 +36,28 @@ recon_status validate_grid(int W, int H, int hp, int32_t *detail) {
     return RECON_OK;
 }
 
+// warps per CTA: 8 for throughput; a red-rec batch with no more instances
+// than SMs runs one CTA per SM anyway, so it takes up to 32 warps (RECON_GRID_WARPS
+// overrides) to shorten phase 1/3 and the waves
+bool shape_for(Ctx *c, int solver, int W, int H, int hp, int count, GridShape &s) {
+    int w = kWarps;
+    if (solver == 0 && count <= c->sms) w = 32;
+    if (const char *e = getenv("RECON_GRID_WARPS")) w = std::max(1, std::min(32, atoi(e)));
+    for (; w >= kWarps; w /= 2)
+        if (grid_shape(W, H, hp, w, s)) return true;
+    return grid_shape(W, H, hp, kWarps, s);
+}
+
 int grid_blocks(Ctx *c, int solver, const GridShape &s, int count) {
     const int occ = std::max(1, grid_occupancy(solver, s));
     return std::max(1, std::min(count, occ * c->sms));
 }
 
-// launches with the per-CTA snapshot scratch the red-rec kernel needs
+// launches with the per-CTA staging scratch and the plans the red-rec kernels need
 cudaError_t launch(Ctx *c, int solver, GridParams &p, int grid) {
-    p.snap = c->dev<uint64_t>(S_SNAP, (size_t)grid * grid_snap_words(p.shape));
-    if (!p.snap) return cudaErrorMemoryAllocation;
     if (solver == 0) {
+        p.stage = c->dev<int32_t>(S_STAGE, (size_t)grid * grid_stage_ints(p.shape));
+        if (!p.stage) return cudaErrorMemoryAllocation;
         void *pl = c->get(S_PLAN, (size_t)p.count * redrec_plan_bytes(p.shape.W) + 1024);
         if (!pl) return cudaErrorMemoryAllocation;
         p.plans = redrec_plans_carve(pl, p.shape.W, p.count);
@@ -104,7 +117,7 @@ recon_status grid_single(int solver, recon_ctx *ctx, const uint64_t *occ, int W,
     }
     CK(cudaSetDevice(c->device), "cudaSetDevice");
     GridShape s;
-    if (!grid_shape(W, H, hp, kWarps, s)) return RECON_ERR_ARGUMENT;
+    if (!shape_for(c, solver, W, H, hp, 1, s)) return RECON_ERR_ARGUMENT;
     const size_t words = (size_t)W * s.wpd, stride = (size_t)W * hp;
     GridParams p{};
     p.shape = s;
@@ -172,7 +185,7 @@ recon_status grid_batch(int solver, recon_ctx *ctx, const recon_grid_batch *b, b
     if (!c) return RECON_ERR_CUDA;
     CK(cudaSetDevice(c->device), "cudaSetDevice");
     GridShape s;
-    if (!grid_shape(b->width, b->height, b->h_prime, kWarps, s)) return RECON_ERR_ARGUMENT;
+    if (!shape_for(c, solver, b->width, b->height, b->h_prime, b->count, s)) return RECON_ERR_ARGUMENT;
     const size_t n = (size_t)b->count, words = (size_t)b->width * s.wpd, stride = (size_t)b->width * b->h_prime;
     const int per = solver == 0 ? 4 : 1;
     GridParams p{};
@@ -272,7 +285,7 @@ extern "C" recon_status recon_debug_grid_phases(int32_t solver, const uint64_t *
     Ctx *c = resolve(nullptr);
     if (!c) return RECON_ERR_CUDA;
     GridShape s;
-    if (!grid_shape(W, H, hp, kWarps, s)) return RECON_ERR_ARGUMENT;
+    if (!shape_for(c, solver, W, H, hp, 1, s)) return RECON_ERR_ARGUMENT;
     const size_t words = (size_t)W * s.wpd, stride = (size_t)W * hp;
     GridParams p{};
     p.shape = s;

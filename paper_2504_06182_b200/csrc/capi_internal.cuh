@@ -23,7 +23,7 @@ enum Slot {
     S_SRCOF, S_TGTOF, S_DCNT, S_DOFF, S_KEYS, S_KEYS2, S_TEMP, S_EA, S_EB,
     S_CHAIN_A, S_CHAIN_B, S_CHAIN_C, S_CHAIN_D, S_CHAIN_E,
     S_BM_OFF, S_BM_VERT, S_BM_ES, S_BM_ED, S_BM_OUT, S_BM_AUX0, S_BM_AUX1, S_BM_AUX2, S_BM_AUX3,
-    S_BM_AUX4, S_BM_AUX5, S_BM_AUX6, S_SNAP, S_PLAN,
+    S_BM_AUX4, S_BM_AUX5, S_BM_AUX6, S_STAGE, S_PLAN,
     S_NSLOTS
 };
 

@@ -40,7 +40,7 @@ struct GridParams {
     int32_t *path_count;
     int64_t *total_displacement;
     int32_t *status, *detail, *events;
-    uint64_t *snap;          // red-rec: per-CTA event snapshots, 2*W*wpd words per CTA (grid-sized)
+    int32_t *stage;          // red-rec: per-CTA event staging, 2*W*k ints per CTA (grid-sized)
     RedrecPlans plans;       // red-rec: [count] plans
     long long *phase_clock;  // optional: clock64 at phase boundaries of instance 0 (profiling)
 };
@@ -48,7 +48,7 @@ struct GridParams {
 bool grid_shape(int W, int H, int k, int nwarps, GridShape &s);
 cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaStream_t stream);
 int grid_occupancy(int solver, const GridShape &s);
-size_t grid_snap_words(const GridShape &s);
+size_t grid_stage_ints(const GridShape &s);
 size_t redrec_plan_bytes(int W);  // global plan bytes per instance
 RedrecPlans redrec_plans_carve(void *base, int W, int count);
 

@@ -13,15 +13,16 @@
 //    event a dependency level: 1 + the last level touching any column it
 //    reads/writes or the mark set of its receiver.
 // 2. Waves.  Loop events of one level touch disjoint state and run
-//    concurrently, one warp per event; each records its split `a`, its path
-//    count, and a snapshot of the masks it read (global scratch).
+//    concurrently, one warp per event.  Every event (phase 1, loop, phase 3)
+//    writes its paths, in emission order, to its own k-slot region of a
+//    per-CTA staging buffer (global, L2-resident in practice) right after
+//    its solve, and records its path count.
 // 3. Phase-3 compactions are solved in parallel on the final state.
 // 4. One scan over all W events in canonical order gives every event's
-//    output offset; every event is re-materialised from its snapshot and
-//    emitted in parallel.
+//    output offset; the staged paths move there with coalesced copies.
 // Marks (parked tokens of a donating compaction, redrec.cpp:155-160) stay in
 // the marker's column plane and are never cleared: only their receiver's
-// transfer reads them, in both passes.
+// transfer reads them.
 
 #include "grid_common.cuh"
 
@@ -533,20 +534,21 @@ __global__ void __launch_bounds__(128) redrec_plan_kernel(GridParams p) {
     }
 }
 
-__global__ void __launch_bounds__(256, 4) redrec_kernel(GridParams p) {
+// 64 registers (the cap of 4 x 256-thread CTAs per SM); 8 warps per CTA for
+// batches, up to 32 for a lone instance (latency)
+__global__ void __launch_bounds__(1024, 1) redrec_kernel(GridParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geo g = make_geo(p.shape);
     Block b = carve(p.shape, smem);
     const int warp = warp_id(), lane = lane_id(), nw = blockDim.x >> 5;
     int16_t *L = b.lists + (size_t)warp * 4 * g.LK;
     uint32_t *keys = b.keys + (size_t)warp * 2 * g.LK;
-    uint64_t *snap = p.snap + (size_t)blockIdx.x * 2 * g.W * g.wpd;
+    // event e's paths are staged at stage + 2ke (sources) / + k (targets)
+    int32_t *const stage = p.stage + (size_t)blockIdx.x * 2 * g.W * g.k;
     __shared__ long long s_tokens;
     __shared__ unsigned long long s_disp;
     __shared__ int s_status, s_detail, s_n1, s_n2, s_nlev, s_total, s_fail;
     for (int inst = blockIdx.x; inst < p.count; inst += gridDim.x) {
-        const size_t pbase = (size_t)inst * g.W * g.k;
-        PathOut o{p.path_src + pbase, p.path_dst + pbase, p.path_event ? p.path_event + pbase : nullptr};
         if (threadIdx.x == 0) {
             s_tokens = 0;
             s_disp = 0;
@@ -590,8 +592,9 @@ __global__ void __launch_bounds__(256, 4) redrec_kernel(GridParams p) {
         __syncthreads();
         if (s_status == RECON_OK) {
             const int n1 = s_n1, n2 = s_n2, nlev = s_nlev, W = g.W;
+            long long disp = 0;
             if (p.phase_clock && inst == 0 && threadIdx.x == 0) p.phase_clock[1] = clock64();
-            // phase 1 (sigma == 0 compactions): solve + count
+            // phase 1 (sigma == 0 compactions): solve + stage
             for (int e = warp; e < n1; e += nw) {
                 OwnSolve s;
                 const int c = b.ev_col[e];
@@ -599,51 +602,41 @@ __global__ void __launch_bounds__(256, 4) redrec_kernel(GridParams p) {
                     if (lane == 0) s_fail = 1;
                     continue;
                 }
-                if (lane == 0) {
-                    b.ev_a[e] = (int16_t)s.a;
-                    b.ev_nr[e] = (int16_t)s.n_right;
-                    b.ev_nl[e] = (int16_t)s.n_left;
-                    b.ev_count[e] = s.n_right + s.n_left;
-                }
+                int32_t *st = stage + (size_t)e * 2 * g.k;
+                disp += own_emit(g, c, s, L, PathOut{st, st + g.k, nullptr}, 0, e);
+                if (lane == 0) b.ev_count[e] = s.n_right + s.n_left;
                 __syncwarp();
             }
-            // pairing-loop events in dependency waves
+            // pairing-loop events in dependency waves: solve, stage, update
             for (int lv = 1; lv <= nlev; ++lv) {
                 for (int q = b.wave_off[lv] + warp; q < b.wave_off[lv + 1]; q += nw) {
                     const int e = b.wave_list[q];
                     const int col = b.ev_col[e], aux = b.ev_aux[e];
                     uint64_t *mc = b.dep + (size_t)col * g.wpd;
+                    int32_t *st = stage + (size_t)e * 2 * g.k;
                     if (b.ev_type[e] == EV_OWN) {
-                        for (int w = lane; w < g.wpd; w += 32) snap[(size_t)(2 * col) * g.wpd + w] = mc[w];
                         OwnSolve s;
                         if (!own_solve(g, mc, L, -1, s)) {
                             if (lane == 0) s_fail = 1;
                             continue;
                         }
+                        disp += own_emit(g, col, s, L, PathOut{st, st + g.k, nullptr}, 0, e);
                         own_update(g, mc, s, L);
                         if (lane == 0) {
-                            b.ev_a[e] = (int16_t)s.a;
-                            b.ev_nr[e] = (int16_t)s.n_right;
-                            b.ev_nl[e] = (int16_t)s.n_left;
                             b.ev_count[e] = s.n_right + s.n_left;
                             if (aux >= 0) b.mark_dest[col] = (int16_t)aux;  // parked -> marks for aux
                         }
                     } else {
                         uint64_t *md = b.dep + (size_t)aux * g.wpd;
-                        for (int w = lane; w < g.wpd; w += 32) {
-                            snap[(size_t)(2 * col) * g.wpd + w] = mc[w];
-                            snap[(size_t)(2 * col + 1) * g.wpd + w] = md[w];
-                        }
                         FlushSolve f;
                         if (!flush_solve(g, mc, md, col, aux, b.dep, b.mark_dest, L, -1, f)) {
                             if (lane == 0) s_fail = 1;
                             continue;
                         }
+                        disp += flush_emit(g, f, mc, md, col, aux, b.dep, b.mark_dest, L, keys,
+                                           PathOut{st, st + g.k, nullptr}, 0, e);
                         flush_update(g, b.dep, col, aux, f, L);
-                        if (lane == 0) {
-                            b.ev_a[e] = (int16_t)f.a;
-                            b.ev_count[e] = f.n_right + f.n_left;
-                        }
+                        if (lane == 0) b.ev_count[e] = f.n_right + f.n_left;
                     }
                     __syncwarp();
                 }
@@ -658,16 +651,15 @@ __global__ void __launch_bounds__(256, 4) redrec_kernel(GridParams p) {
                     if (lane == 0) s_fail = 1;
                     continue;
                 }
-                if (lane == 0) {
-                    b.ev_a[e] = (int16_t)s.a;
-                    b.ev_nr[e] = (int16_t)s.n_right;
-                    b.ev_nl[e] = (int16_t)s.n_left;
-                    b.ev_count[e] = s.n_right + s.n_left;
-                }
+                int32_t *st = stage + (size_t)e * 2 * g.k;
+                disp += own_emit(g, c, s, L, PathOut{st, st + g.k, nullptr}, 0, e);
+                if (lane == 0) b.ev_count[e] = s.n_right + s.n_left;
                 __syncwarp();
             }
+            if (lane == 0 && disp) atomicAdd(&s_disp, (unsigned long long)disp);
             __syncthreads();
-            // canonical offsets (event order), then parallel emission
+            // canonical offsets (event order), then the staged paths move to
+            // their offsets with coalesced copies
             if (warp == 0) {
                 int run = 0;
                 for (int i0 = 0; i0 < W; i0 += 32) {
@@ -682,22 +674,18 @@ __global__ void __launch_bounds__(256, 4) redrec_kernel(GridParams p) {
             }
             __syncthreads();
             if (!s_fail) {
-                long long disp = 0;
+                const size_t pbase = (size_t)inst * g.W * g.k;
+                int32_t *const osrc = p.path_src + pbase, *const odst = p.path_dst + pbase;
+                int32_t *const oev = p.path_event ? p.path_event + pbase : nullptr;
                 for (int e = warp; e < W; e += nw) {
-                    const int col = b.ev_col[e], aux = b.ev_aux[e];
-                    const bool loop = e >= n1 && e < n1 + n2;
-                    if (b.ev_type[e] == EV_OWN) {
-                        const uint64_t *m = loop ? snap + (size_t)(2 * col) * g.wpd : b.dep + (size_t)col * g.wpd;
-                        disp += own_emit_direct(g, col, m, b.ev_a[e], b.ev_nr[e], b.ev_nl[e], o, b.ev_off[e], e);
-                    } else {
-                        const uint64_t *mr = snap + (size_t)(2 * col) * g.wpd, *md = snap + (size_t)(2 * col + 1) * g.wpd;
-                        FlushSolve f;
-                        flush_solve(g, mr, md, col, aux, b.dep, b.mark_dest, L, b.ev_a[e], f);
-                        disp += flush_emit(g, f, mr, md, col, aux, b.dep, b.mark_dest, L, keys, o, b.ev_off[e], e);
+                    const int n = b.ev_count[e], off = b.ev_off[e];
+                    const int32_t *st = stage + (size_t)e * 2 * g.k;
+                    for (int i = lane; i < n; i += 32) {
+                        osrc[off + i] = st[i];
+                        odst[off + i] = st[g.k + i];
+                        if (oev) oev[off + i] = e;
                     }
-                    __syncwarp();
                 }
-                if (lane == 0 && disp) atomicAdd(&s_disp, (unsigned long long)disp);
             }
             __syncthreads();
             if (p.phase_clock && inst == 0 && threadIdx.x == 0) {

@@ -101,6 +101,8 @@ CASES = {
     "c4_redrec_h128_1": lambda: grid("redrec", 256, 256, 128, 39322, 256, 1),
     "c4_redrec_h153_1": lambda: grid("redrec", 256, 256, 153, 39322, 257, 1),
     "c4_bird_h153_1": lambda: grid("bird", 256, 256, 153, 39322, 257, 1),
+    "c4_redrec_2048": lambda: grid("redrec", 256, 256, 153, 39322, 0x25600000, 2048),
+    "c4_bird_2048": lambda: grid("bird", 256, 256, 153, 39322, 0x25600000, 2048),
     "r256_redrec_b2048": lambda: grid("redrec", 256, 256, 153, 39322, 0x25600000, 2048),
     "r256_bird_b2048": lambda: grid("bird", 256, 256, 153, 39322, 0x25600000, 2048),
     "c3_bird_solve": lambda: grid("bird", 64, 64, 40, 2662, 0x64000000, 4096),
