@@ -13,7 +13,7 @@ from .abi import (CollisionError, InfeasibleError, InputError, LogicError, Recon
                   words_per_column)
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "lib", "librecon_b200.so")
+LIB_PATH = os.environ.get("RECON_B200_LIB") or os.path.join(PKG_DIR, "lib", "librecon_b200.so")
 
 _native: ReconLib | None = None
 

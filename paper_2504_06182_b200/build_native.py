@@ -21,6 +21,7 @@ LIB = os.path.join(LIB_DIR, "librecon_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+EXTRA = os.environ.get("RECON_NVCC_EXTRA", "").split()  # experiments only
 
 
 def _needs(out: str, deps: list[str]) -> bool:
@@ -36,7 +37,7 @@ def _compile(src: str, headers: list[str], verbose: bool) -> str:
     if not _needs(out, [src] + headers):
         return out
     if src.endswith(".cu"):
-        cmd = [NVCC, *ARCH, "-lineinfo", "-Xptxas", "-v" if verbose else "-O3", *COMMON, "-c", src, "-o", out]
+        cmd = [NVCC, *ARCH, "-lineinfo", "-Xptxas", "-v" if verbose else "-O3", *COMMON, *EXTRA, "-c", src, "-o", out]
     else:
         cmd = [NVCC, *COMMON, "-c", src, "-o", out]
     r = subprocess.run(cmd, capture_output=True, text=True)

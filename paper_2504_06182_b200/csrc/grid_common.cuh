@@ -48,7 +48,8 @@ __host__ __device__ inline void grid_smem_layout(const GridShape &s, GridSmem &o
     o.scal = take(32 * 8, 16);
     o.lists = take((int64_t)s.nwarps * 4 * s.LK * 2, 16);
     o.plists = take((int64_t)2 * s.LK * 2, 16);
-    o.mark_dest = take((int64_t)s.W * 2, 16);
+    o.mark_next = take((int64_t)s.W * 2, 16);
+    o.mark_head = take((int64_t)s.W * 2, 16);
     o.ev_col = take((int64_t)s.W * 2, 16);
     o.ev_aux = take((int64_t)s.W * 2, 16);
     o.ev_a = take((int64_t)s.W * 2, 16);
@@ -73,9 +74,8 @@ __device__ __forceinline__ Geo make_geo(const GridShape &s) {
     g.H = s.H;
     g.k = s.k;
     // centered band rows y in [(H-h')/2, +h'-1] (problem.hpp:78-79) -> depths
-    const int ylo = (s.H - s.k) / 2, yhi = ylo + s.k - 1;
-    g.lo = s.H - 1 - yhi;
-    g.hi = s.H - 1 - ylo;
+    g.lo = s.lo;
+    g.hi = s.hi;
     g.wpd = s.wpd;
     g.B = s.B;
     g.LK = s.LK;
@@ -251,7 +251,7 @@ struct Block {
     uint64_t *dep;
     uint32_t *keys, *bal;
     int *sigma, *ev_count, *ev_off, *wave_off, *lvl_t, *lvl_b, *scal;
-    int16_t *lists, *plists, *mark_dest, *ev_col, *ev_aux, *ev_a, *ev_nr, *ev_nl, *ev_level, *wave_list, *lastc, *lastm;
+    int16_t *lists, *plists, *mark_next, *mark_head, *ev_col, *ev_aux, *ev_a, *ev_nr, *ev_nl, *ev_level, *wave_list, *lastc, *lastm;
     uint8_t *ev_type, *solved;
 };
 
@@ -271,7 +271,8 @@ __device__ __forceinline__ Block carve(const GridShape &s, unsigned char *smem) 
     b.scal = (int *)(smem + o.scal);
     b.lists = (int16_t *)(smem + o.lists);
     b.plists = (int16_t *)(smem + o.plists);
-    b.mark_dest = (int16_t *)(smem + o.mark_dest);
+    b.mark_next = (int16_t *)(smem + o.mark_next);
+    b.mark_head = (int16_t *)(smem + o.mark_head);
     b.ev_col = (int16_t *)(smem + o.ev_col);
     b.ev_aux = (int16_t *)(smem + o.ev_aux);
     b.ev_a = (int16_t *)(smem + o.ev_a);
@@ -307,7 +308,7 @@ __device__ __forceinline__ void load_instance(const Geo &g, const uint64_t *occ,
         }
         b.sigma[x] = cnt - g.k;
         b.solved[x] = 0;
-        b.mark_dest[x] = -1;
+        b.mark_head[x] = -1;
         tot += cnt;
     }
     tot = warp_sum64(tot);

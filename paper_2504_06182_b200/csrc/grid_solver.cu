@@ -2,12 +2,25 @@
 // redrec_kernel (redrec.cu) and bird_kernel (bird.cu).
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "grid_common.cuh"
 
 namespace rb {
 
+template <int MINB>
 __global__ void redrec_kernel(GridParams p);
+
+// executor variant: 32-warp CTAs for lone instances, else 8-warp CTAs with
+// MINB per SM (RECON_REDREC_MINB = 3 trades occupancy for 85 registers)
+static void (*redrec_exec(const GridShape &s))(GridParams) {
+    if (s.nwarps > 8) return redrec_kernel<1>;
+    static const int minb = [] {
+        const char *e = getenv("RECON_REDREC_MINB");
+        return e ? atoi(e) : 4;
+    }();
+    return minb == 3 ? redrec_kernel<3> : redrec_kernel<4>;
+}
 __global__ void redrec_plan_kernel(GridParams p);
 int64_t redrec_plan_smem(int W);
 __global__ void bird_kernel(GridParams p);
@@ -27,6 +40,8 @@ bool grid_shape(int W, int H, int k, int nwarps, GridShape &s) {
     s.LB = (int)align_up((H - 1 - hi) + W - 1 + 64, 64);
     s.nchunk = (2 * W - 1 + 31) / 32;
     s.nwarps = nwarps;
+    s.lo = lo;
+    s.hi = hi;
     GridSmem o;
     grid_smem_layout(s, o);
     s.smem_bytes = o.total;
@@ -59,7 +74,7 @@ RedrecPlans redrec_plans_carve(void *base, int W, int count) {
 
 cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaStream_t stream) {
     const int threads = 32 * p.shape.nwarps;
-    void (*kern)(GridParams) = solver == 0 ? redrec_kernel : bird_kernel;
+    void (*kern)(GridParams) = solver == 0 ? redrec_exec(p.shape) : bird_kernel;
     cudaError_t e;
     if (solver == 0) {
         // plans first: one warp per instance, all instances in parallel
@@ -83,7 +98,7 @@ cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaSt
 
 int grid_occupancy(int solver, const GridShape &s) {
     int nb = 0;
-    void (*kern)(GridParams) = solver == 0 ? redrec_kernel : bird_kernel;
+    void (*kern)(GridParams) = solver == 0 ? redrec_exec(s) : bird_kernel;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s.smem_bytes);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32 * s.nwarps, s.smem_bytes);
     return nb;

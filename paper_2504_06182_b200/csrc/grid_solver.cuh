@@ -15,11 +15,12 @@ struct GridShape {
     int LT, LB;       // level-table sizes (top / bottom), multiples of 64
     int nchunk;       // 32-slot chunks covering 2W-1 group-order slots
     int nwarps;
+    int lo, hi;       // band depths (rows from the top)
     int64_t smem_bytes;
 };
 
 struct GridSmem {
-    int64_t dep, keys, bal, sigma, ev_count, ev_off, wave_off, lvl_t, lvl_b, scal, lists, plists, mark_dest,
+    int64_t dep, keys, bal, sigma, ev_count, ev_off, wave_off, lvl_t, lvl_b, scal, lists, plists, mark_next, mark_head,
         ev_col, ev_aux, ev_a, ev_nr, ev_nl, ev_level, wave_list, lastc, lastm, ev_type, solved, total;
 };
 

@@ -38,8 +38,10 @@ struct FlushSolve {
     int a, b, R, holes, m_top, m_bot, n_ot, n_ob, n_right, n_left, dd;
 };
 
+// Marks parked for receiver r form a list through the marker columns:
+// mark_head[r], then mark_next[x] (-1 ends it); order is irrelevant.
 __device__ bool flush_solve(const Geo &g, const uint64_t *mr, const uint64_t *md, int r, int d, const uint64_t *dep,
-                            const int16_t *mark_dest, int16_t *L, int forced_a, FlushSolve &f) {
+                            int mark_first, const int16_t *mark_next, int16_t *L, int forced_a, FlushSolve &f) {
     int16_t *otop = L, *obot = L + g.LK, *hole = L + 2 * g.LK, *res = L + 3 * g.LK;
     const int lane = lane_id(), B = g.B, base = lane * B;
     const int dd = d > r ? d - r : r - d;
@@ -54,15 +56,10 @@ __device__ bool flush_solve(const Geo &g, const uint64_t *mr, const uint64_t *md
     for (uint32_t x = holem; x; x &= x - 1, ++eh) hole[eh + 1] = (int16_t)(base + __ffs(x) - 1);
     for (uint32_t x = resm; x; x &= x - 1, ++er) res[er] = (int16_t)(base + __ffs(x) - 1);
     int m_top = __popc(chr & rtop), m_bot = __popc(chr & rbot);
-    for (int x0 = 0; x0 < g.W; x0 += 32) {
-        unsigned mk = __ballot_sync(FULL, x0 + lane < g.W && mark_dest[x0 + lane] == r);
-        while (mk) {
-            const int x = x0 + __ffs(mk) - 1;
-            mk &= mk - 1;
-            const uint32_t chx = lane_chunk(dep + (size_t)x * g.wpd, g.wpd, lane, B);
-            m_top += __popc(chx & rtop);
-            m_bot += __popc(chx & rbot);
-        }
+    for (int x = mark_first; x >= 0; x = mark_next[x]) {
+        const uint32_t chx = lane_chunk(dep + (size_t)x * g.wpd, g.wpd, lane, B);
+        m_top += __popc(chx & rtop);
+        m_bot += __popc(chx & rbot);
     }
     m_top = warp_sum(m_top);
     m_bot = warp_sum(m_bot);
@@ -116,14 +113,15 @@ __device__ bool flush_solve(const Geo &g, const uint64_t *mr, const uint64_t *md
 }
 
 __device__ long long flush_emit(const Geo &g, const FlushSolve &f, const uint64_t *mr, const uint64_t *md, int r,
-                                int d, const uint64_t *dep, const int16_t *mark_dest, const int16_t *L,
-                                uint32_t *keys, PathOut o, int off, int evid) {
+                                int d, const uint64_t *dep, int mark_first, const int16_t *mark_next,
+                                const int16_t *L, uint32_t *keys, PathOut o, int off, int evid) {
     const int16_t *res = L + 3 * g.LK;
     const int lane = lane_id(), B = g.B, base = lane * B;
     const uint32_t rtop = chunk_range(base, B, 0, g.lo), rbot = chunk_range(base, B, g.hi + 1, g.H);
     const int a = f.a, b = f.b, R = f.R, dd = f.dd;
     const int xa = a - f.m_top, xb = b - f.m_bot;
     uint32_t *ktop = keys, *kbot = keys + g.LK;
+    // keys of the used tokens: own, each marker column's, the donor's
     {
         const uint32_t chr = lane_chunk(mr, g.wpd, lane, B);
         int tot;
@@ -133,22 +131,17 @@ __device__ long long flush_emit(const Geo &g, const FlushSolve &f, const uint64_
         e = warp_excl_scan(__popc(chr & rbot), &tot);
         for (uint32_t x = chr & rbot; x; x &= x - 1) kbot[e++] = tok_key(base + __ffs(x) - 1, 0, r);
         int pos_b = tot;
-        for (int x0 = 0; x0 < g.W; x0 += 32) {
-            unsigned mk = __ballot_sync(FULL, x0 + lane < g.W && mark_dest[x0 + lane] == r);
-            while (mk) {
-                const int x = x0 + __ffs(mk) - 1;
-                mk &= mk - 1;
-                const int dx = x > r ? x - r : r - x;
-                const uint32_t chx = lane_chunk(dep + (size_t)x * g.wpd, g.wpd, lane, B);
-                e = warp_excl_scan(__popc(chx & rtop), &tot);
-                for (uint32_t y = chx & rtop; y; y &= y - 1) ktop[pos_t + e++] = tok_key(base + __ffs(y) - 1 - dx, dx, x);
-                pos_t += tot;
-                e = warp_excl_scan(__popc(chx & rbot), &tot);
-                for (uint32_t y = chx & rbot; y; y &= y - 1) kbot[pos_b + e++] = tok_key(base + __ffs(y) - 1 + dx, dx, x);
-                pos_b += tot;
-            }
+        for (int x = mark_first; x >= 0; x = mark_next[x]) {
+            const int dx = x > r ? x - r : r - x;
+            const uint32_t chx = lane_chunk(dep + (size_t)x * g.wpd, g.wpd, lane, B);
+            e = warp_excl_scan(__popc(chx & rtop), &tot);
+            for (uint32_t y = chx & rtop; y; y &= y - 1) ktop[pos_t + e++] = tok_key(base + __ffs(y) - 1 - dx, dx, x);
+            pos_t += tot;
+            e = warp_excl_scan(__popc(chx & rbot), &tot);
+            for (uint32_t y = chx & rbot; y; y &= y - 1) kbot[pos_b + e++] = tok_key(base + __ffs(y) - 1 + dx, dx, x);
+            pos_b += tot;
         }
-        // donor: innermost xa top (largest depth), innermost xb bottom
+        // donor: innermost xa top, innermost xb bottom
         const uint32_t chd = lane_chunk(md, g.wpd, lane, B);
         const uint32_t dtop = chd & rtop, dbot = chd & rbot;
         e = warp_excl_scan(__popc(dtop), &tot);
@@ -161,6 +154,7 @@ __device__ long long flush_emit(const Geo &g, const FlushSolve &f, const uint64_
             if (e < xb) kbot[pos_b + e] = tok_key(base + __ffs(x) - 1 + dd, dd, d);
     }
     __syncwarp();
+    // a token's target index is its rank among the used keys (all distinct)
     long long disp = 0;
     for (int i = lane; i < a; i += 32) {
         const uint32_t key = ktop[i];
@@ -218,56 +212,62 @@ __device__ void flush_update(const Geo &g, uint64_t *dep, int r, int d, const Fl
 // plan: surplus-only replay of redrec.cpp:205-232 with dependency levels
 // --------------------------------------------------------------------------
 
+// link word of column c: NL (nearest unsolved column on the left, -1 if none)
+// in the low half, NR (on the right, W if none) in the high half
+__device__ __forceinline__ int link_l(int v) { return (int)(int16_t)(v & 0xffff); }
+__device__ __forceinline__ int link_r(int v) { return v >> 16; }
+__device__ __forceinline__ int make_link(int l, int r) { return (r << 16) | (l & 0xffff); }
+
 // key of receiver q: best of its nearest unsolved neighbours that are donors,
 // ranked (-exchange, |d-r|, deficit-exchange, r, d) (select_best_pair,
-// redrec.cpp:55-86); ~0 when neither side has an admissible donor
-__device__ __forceinline__ unsigned long long receiver_key(int q, int W, const int *sig, const uint8_t *solved,
-                                                           const int16_t *NL, const int16_t *NR) {
-    unsigned long long best = ~0ull;
-    const int deficit = -sig[q];
-    const int cand[2] = {NL[q], NR[q]};
-#pragma unroll
-    for (int side = 0; side < 2; ++side) {
-        const int d = cand[side];
-        if (d < 0 || d >= W || solved[d] || sig[d] <= 0) continue;
-        const int ex = min(sig[d], deficit);
-        const unsigned long long key = ((unsigned long long)(4095 - ex) << 42) |
-                                       ((unsigned long long)(d > q ? d - q : q - d) << 32) |
-                                       ((unsigned long long)(deficit - ex) << 20) | ((unsigned long long)q << 10) |
-                                       (unsigned long long)d;
-        best = key < best ? key : best;
-    }
-    return best;
+// redrec.cpp:55-86), packed as hi = (2047-ex)<<21 | dist<<11 | (deficit-ex)
+// (|sigma| <= H <= 1024, so every field fits) and lo = q<<10 | d; ~0 when
+// neither side has an admissible donor.  Transit columns have sigma 0, so
+// `sig[d] > 0` alone admits a donor.
+__device__ __forceinline__ unsigned long long receiver_key(int q, int W, int sq, int lk, const int *sig) {
+    const int deficit = -sq;
+    const int dl = link_l(lk), dr = link_r(lk);
+    const int sl = dl >= 0 ? sig[dl] : 0, sr = dr < W ? sig[dr] : 0;
+    auto key = [&](int d, int sd) {
+        const int ex = min(sd, deficit);
+        const unsigned hi = ((unsigned)(2047 - ex) << 21) | ((unsigned)(d > q ? d - q : q - d) << 11) |
+                            (unsigned)(deficit - ex);
+        return sd > 0 ? ((unsigned long long)hi << 32) | ((unsigned)q << 10) | (unsigned)d : ~0ull;
+    };
+    const unsigned long long kl = key(dl, sl), kr = key(dr, sr);
+    return kl < kr ? kl : kr;
 }
 
 // Surplus-only replay of the pairing loop with incremental candidate keys.
-// Columns are "unsolved" (non-transit) or solved with zero surplus (transit,
-// scan_for_donor redrec.cpp:43-51); NL/NR link every column to its nearest
-// unsolved neighbour on each side.  An iteration changes only the donor d and
-// the receiver r, so only r and the receivers adjacent to d and r (their
-// nearest unsolved neighbours) need new keys; a column turning transit is
-// unlinked with two range updates.
+// Columns are "unsolved" (non-transit, sigma != 0) or solved with zero
+// surplus (transit, scan_for_donor redrec.cpp:43-51).  The unsolved columns
+// form a doubly linked list, so a column turning transit is unlinked in O(1);
+// links are only read at columns that were unsolved when the iteration began,
+// and a neighbour unlinked in the same iteration is skipped with one more hop.
+// An iteration changes only the donor d and the receiver r, so only r and the
+// receivers adjacent to d and r need new keys.  Keys live in shared memory
+// (lane L owns columns [L*per, L*per+per)); the global minimum is two
+// redux.sync reductions over the lanes' minima.
 template <class B>
-__device__ int redrec_plan(const Geo &g, B &b, int *n1o, int *n2o, int *nlevo) {
+__device__ int redrec_plan(const Geo &g, B &b, int *n1o, int *n2o, int *nlevo, long long *prof = nullptr) {
     const int lane = lane_id(), W = g.W;
     const int per = (W + 31) / 32, c0 = lane * per, c1 = min(W, c0 + per);
-    int *sig = b.ev_count;                           // scratch: plan-time surplus
-    int16_t *NL = b.wave_list, *NR = b.ev_a;         // scratch until the plan ends
-    unsigned long long *rkey = (unsigned long long *)b.keys;
-    uint8_t *solved = b.solved;
-    uint32_t recvm = 0;
+    int *sig = b.ev_count;                                    // scratch: plan-time surplus
+    int *lnk = b.links;                                       // NL / NR pairs
+    unsigned long long *rkey = (unsigned long long *)b.keys;  // 32*per + 8 entries
+    int nrecv = 0;
     for (int c = c0; c < c1; ++c) {
         const int s = b.sigma[c];
         sig[c] = s;
-        solved[c] = s == 0;  // phase 1 solves every sigma == 0 column (redrec.cpp:211-212)
-        if (s < 0) recvm |= 1u << (c - c0);
+        nrecv += s < 0;
         b.lastc[c] = 0;
         b.lastm[c] = 0;
     }
+    nrecv = warp_sum(nrecv);
     int nev = 0;
     for (int x0 = 0; x0 < W; x0 += 32) {
         const int c = x0 + lane;
-        const bool z = c < W && b.sigma[c] == 0;
+        const bool z = c < W && b.sigma[c] == 0;  // phase 1 (redrec.cpp:211-212)
         const unsigned bz = __ballot_sync(FULL, z);
         if (z) {
             const int slot = nev + __popc(bz & lanemask_lt());
@@ -297,37 +297,50 @@ __device__ int redrec_plan(const Geo &g, B &b, int *n1o, int *n2o, int *nlevo) {
         if (lane == 0) left = -1;
         if (lane == 31) right = W;
         for (int c = c0; c < c1; ++c) {
-            NL[c] = (int16_t)left;
+            lnk[c] = left & 0xffff;
             if (b.sigma[c] != 0) left = c;
         }
         for (int c = c1 - 1; c >= c0; --c) {
-            NR[c] = (int16_t)right;
+            lnk[c] |= right << 16;
             if (b.sigma[c] != 0) right = c;
         }
     }
     __syncwarp();
-    for (uint32_t m = recvm; m; m &= m - 1) {
-        const int q = c0 + __ffs(m) - 1;
-        rkey[q] = receiver_key(q, W, sig, solved, NL, NR);
+    for (int i = lane; i < 32 * per + 8; i += 32) {
+        const int sq = i < W ? sig[i] : 0;
+        rkey[i] = sq < 0 ? receiver_key(i, W, sq, lnk[i], sig) : ~0ull;
     }
     __syncwarp();
     int nlev = 0;
-    for (;;) {
-        if (!__any_sync(FULL, recvm)) break;
-        unsigned long long best = ~0ull;
-        for (uint32_t m = recvm; m; m &= m - 1) {
-            const unsigned long long k = rkey[c0 + __ffs(m) - 1];
-            best = k < best ? k : best;
+    long long pt[3] = {0, 0, 0}, t0 = prof ? clock64() : 0;
+    auto tick = [&](int i) {
+        if (prof) {
+            const long long t = clock64();
+            pt[i] += t - t0;
+            t0 = t;
         }
-        best = warp_min_u64(best);
-        if (best == ~0ull) return RECON_D_NO_DONOR;
-        const int d = (int)(best & 1023), r = (int)((best >> 10) & 1023);
-        const int ds = sig[d], def = -sig[r];
-        __syncwarp();
-        const bool own_r = r >= c0 && r < c1;
-        int tr0 = -1, tr1 = -1;  // columns turning transit
-        if (ds < def) {
-            tr0 = d;  // OWN(d, r): d donates by marking
+    };
+    while (nrecv > 0) {
+        // lane minimum over 8 keys at a time (the tail past the lane's own
+        // columns reads its neighbour's keys, which cannot change the minimum)
+        unsigned long long best = ~0ull;
+        for (int i0 = 0; i0 < per; i0 += 8) {
+            unsigned long long k[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) k[i] = rkey[c0 + i0 + i];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) best = k[i] < best ? k[i] : best;
+        }
+        const unsigned hi = __reduce_min_sync(FULL, (unsigned)(best >> 32));
+        const unsigned lo = __reduce_min_sync(FULL, (unsigned)(best >> 32) == hi ? (unsigned)best : ~0u);
+        if (hi == ~0u) return RECON_D_NO_DONOR;
+        const int d = (int)(lo & 1023), r = (int)((lo >> 10) & 1023);
+        // exchange and deficit straight from the key: ex < deficit <=> OWN(d, r)
+        const int ex = 2047 - (int)(hi >> 21), def = ex + (int)(hi & 2047);
+        tick(0);
+        int tr0, tr1 = -1;  // columns turning transit
+        if (ex < def) {
+            tr0 = d;  // OWN(d, r): d donates by marking (ds = ex)
             if (lane == 0) {
                 const int lv = 1 + max((int)b.lastc[d], (int)b.lastm[r]);
                 b.lastc[d] = b.lastm[r] = (int16_t)lv;
@@ -336,16 +349,16 @@ __device__ int redrec_plan(const Geo &g, B &b, int *n1o, int *n2o, int *nlevo) {
                 b.ev_col[nev] = (int16_t)d;
                 b.ev_aux[nev] = (int16_t)r;
                 b.ev_level[nev] = (int16_t)lv;
-                sig[r] += ds;
+                sig[r] = ex - def;
                 sig[d] = 0;
-                solved[d] = 1;
             }
             nev += 1;
         } else {
             // FLUSH(r, d), then OWN(d, -1) if the donor is exhausted exactly
+            const int ds = sig[d];
             tr0 = r;
             if (ds == def) tr1 = d;
-            if (own_r) recvm &= ~(1u << (r - c0));
+            nrecv -= 1;
             if (lane == 0) {
                 int lv = 1 + max(max((int)b.lastc[r], (int)b.lastc[d]), (int)b.lastm[r]);
                 b.lastc[r] = b.lastc[d] = b.lastm[r] = (int16_t)lv;
@@ -354,9 +367,9 @@ __device__ int redrec_plan(const Geo &g, B &b, int *n1o, int *n2o, int *nlevo) {
                 b.ev_aux[nev] = (int16_t)d;
                 b.ev_level[nev] = (int16_t)lv;
                 nlev = max(nlev, lv);
-                sig[d] -= def;
+                sig[d] = ds - def;
                 sig[r] = 0;
-                solved[r] = 1;
+                rkey[r] = ~0ull;
                 if (ds == def) {
                     lv += 1;
                     b.lastc[d] = (int16_t)lv;
@@ -365,40 +378,53 @@ __device__ int redrec_plan(const Geo &g, B &b, int *n1o, int *n2o, int *nlevo) {
                     b.ev_aux[nev + 1] = -1;
                     b.ev_level[nev + 1] = (int16_t)lv;
                     nlev = max(nlev, lv);
-                    solved[d] = 1;
                 }
             }
             nev += ds == def ? 2 : 1;
         }
-        __syncwarp();
-        // unlink columns that turned transit: [L, x) -> NR = R, (x, R] -> NL = L
+        // unlink the columns that turned transit (in order)
+        if (lane == 0) {
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            const int x = t == 0 ? tr0 : tr1;
-            if (x < 0) continue;
-            const int L = NL[x], R = NR[x];
-            for (int c = max(L, 0) + lane; c < x; c += 32) NR[c] = (int16_t)R;
-            for (int c = x + 1 + lane; c <= min(R, W - 1); c += 32) NL[c] = (int16_t)L;
-            __syncwarp();
-        }
-        // refresh the keys of r and of the receivers adjacent to d and r
-        {
-            int q = -1;
-            if (lane == 0) q = r;
-            else if (lane == 1) q = NL[d];
-            else if (lane == 2) q = NR[d];
-            else if (lane == 3) q = NL[r];
-            else if (lane == 4) q = NR[r];
-            else if (lane == 5) q = d;
-            if (q >= 0 && q < W && !solved[q] && sig[q] < 0) rkey[q] = receiver_key(q, W, sig, solved, NL, NR);
+            for (int t = 0; t < 2; ++t) {
+                const int x = t == 0 ? tr0 : tr1;
+                if (x < 0) continue;
+                const int v = lnk[x], L = link_l(v), R = link_r(v);
+                if (L >= 0) lnk[L] = make_link(link_l(lnk[L]), R);
+                if (R < W) lnk[R] = make_link(L, link_r(lnk[R]));
+            }
         }
         __syncwarp();
+        tick(1);
+        // refresh r (lane 0) and the nearest unsolved receivers on both sides
+        // of d (lanes 1, 2) and r (lanes 3, 4)
+        if (lane < 5) {
+            const int x = lane == 0 ? r : (lane <= 2 ? d : r);
+            const bool left = (lane & 1) != 0;
+            int q = x;
+            if (lane > 0) {
+                const int v = lnk[x];
+                q = left ? link_l(v) : link_r(v);
+            }
+            const bool in = q >= 0 && q < W;
+            int lq = in ? lnk[q] : 0, sq = in ? sig[q] : 1;
+            if (lane > 0 && in && sq == 0) {  // unlinked this iteration: one more hop
+                q = left ? link_l(lq) : link_r(lq);
+                const bool in2 = q >= 0 && q < W;
+                lq = in2 ? lnk[q] : 0;
+                sq = in2 ? sig[q] : 1;
+            }
+            if (sq < 0) rkey[q] = receiver_key(q, W, sq, lq, sig);
+        }
+        __syncwarp();
+        tick(2);
     }
+    if (prof && lane == 0)
+        for (int i = 0; i < 3; ++i) prof[i] = pt[i];
     const int n2 = nev - n1;
     // phase 3: remaining columns ascending (redrec.cpp:228-229)
     for (int x0 = 0; x0 < W; x0 += 32) {
         const int c = x0 + lane;
-        const bool u = c < W && !solved[c];
+        const bool u = c < W && sig[c] != 0;
         const unsigned bu = __ballot_sync(FULL, u);
         if (u) {
             const int slot = nev + __popc(bu & lanemask_lt());
@@ -447,12 +473,13 @@ __device__ int redrec_plan(const Geo &g, B &b, int *n1o, int *n2o, int *nlevo) {
 struct PlanView {
     int *sigma, *ev_count, *wave_off;
     uint32_t *keys;
-    uint8_t *ev_type, *solved;
+    uint8_t *ev_type;
+    int *links;
     int16_t *ev_col, *ev_aux, *ev_level, *wave_list, *ev_a, *lastc, *lastm;
 };
 
 __host__ __device__ inline int64_t plan_warp_bytes(int W) {
-    return align_up((int64_t)W * 8, 16) + align_up((int64_t)W * 4, 16) * 2 + align_up((int64_t)(W + 2) * 4, 16) +
+    return align_up((align_up(W, 32) + 8) * 8, 16) + align_up((int64_t)W * 4, 16) * 3 + align_up((int64_t)(W + 2) * 4, 16) +
            align_up(W, 16) * 2 + align_up((int64_t)W * 2, 16) * 7;
 }
 
@@ -464,12 +491,12 @@ __device__ PlanView carve_plan(unsigned char *base, int W) {
         off += align_up(bytes, 16);
         return at;
     };
-    v.keys = (uint32_t *)take((int64_t)W * 8);
+    v.keys = (uint32_t *)take(((int64_t)align_up(W, 32) + 8) * 8);
+    v.links = (int *)take((int64_t)W * 4);
     v.sigma = (int *)take((int64_t)W * 4);
     v.ev_count = (int *)take((int64_t)W * 4);
     v.wave_off = (int *)take((int64_t)(W + 2) * 4);
     v.ev_type = (uint8_t *)take(W);
-    v.solved = (uint8_t *)take(W);
     v.ev_col = (int16_t *)take((int64_t)W * 2);
     v.ev_aux = (int16_t *)take((int64_t)W * 2);
     v.ev_level = (int16_t *)take((int64_t)W * 2);
@@ -505,7 +532,7 @@ __global__ void __launch_bounds__(128) redrec_plan_kernel(GridParams p) {
             st = RECON_ERR_INFEASIBLE;
             det = RECON_D_FEWER_SOURCES;
         } else {
-            const int rc = redrec_plan(g, v, &n1, &n2, &nlev);
+            const int rc = redrec_plan(g, v, &n1, &n2, &nlev, (p.phase_clock && inst == 0) ? p.phase_clock + 8 : nullptr);
             if (rc) {
                 st = RECON_ERR_LOGIC;
                 det = rc;
@@ -534,9 +561,10 @@ __global__ void __launch_bounds__(128) redrec_plan_kernel(GridParams p) {
     }
 }
 
-// 64 registers (the cap of 4 x 256-thread CTAs per SM); 8 warps per CTA for
-// batches, up to 32 for a lone instance (latency)
-__global__ void __launch_bounds__(1024, 1) redrec_kernel(GridParams p) {
+// MINB = 1: up to 32 warps for a lone instance (latency), 64 registers;
+// otherwise 8-warp CTAs, MINB per SM (batches)
+template <int MINB>
+__global__ void __launch_bounds__(MINB == 1 ? 1024 : 256, MINB) redrec_kernel(GridParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geo g = make_geo(p.shape);
     Block b = carve(p.shape, smem);
@@ -624,16 +652,20 @@ __global__ void __launch_bounds__(1024, 1) redrec_kernel(GridParams p) {
                         own_update(g, mc, s, L);
                         if (lane == 0) {
                             b.ev_count[e] = s.n_right + s.n_left;
-                            if (aux >= 0) b.mark_dest[col] = (int16_t)aux;  // parked -> marks for aux
+                            if (aux >= 0) {  // parked -> marks for aux
+                                b.mark_next[col] = b.mark_head[aux];
+                                b.mark_head[aux] = (int16_t)col;
+                            }
                         }
                     } else {
                         uint64_t *md = b.dep + (size_t)aux * g.wpd;
                         FlushSolve f;
-                        if (!flush_solve(g, mc, md, col, aux, b.dep, b.mark_dest, L, -1, f)) {
+                        const int mfirst = b.mark_head[col];
+                        if (!flush_solve(g, mc, md, col, aux, b.dep, mfirst, b.mark_next, L, -1, f)) {
                             if (lane == 0) s_fail = 1;
                             continue;
                         }
-                        disp += flush_emit(g, f, mc, md, col, aux, b.dep, b.mark_dest, L, keys,
+                        disp += flush_emit(g, f, mc, md, col, aux, b.dep, mfirst, b.mark_next, L, keys,
                                            PathOut{st, st + g.k, nullptr}, 0, e);
                         flush_update(g, b.dep, col, aux, f, L);
                         if (lane == 0) b.ev_count[e] = f.n_right + f.n_left;
@@ -680,10 +712,23 @@ __global__ void __launch_bounds__(1024, 1) redrec_kernel(GridParams p) {
                 for (int e = warp; e < W; e += nw) {
                     const int n = b.ev_count[e], off = b.ev_off[e];
                     const int32_t *st = stage + (size_t)e * 2 * g.k;
-                    for (int i = lane; i < n; i += 32) {
-                        osrc[off + i] = st[i];
-                        odst[off + i] = st[g.k + i];
-                        if (oev) oev[off + i] = e;
+                    for (int i0 = 0; i0 < n; i0 += 128) {  // 8 loads in flight per lane
+                        int32_t vs[4], vd[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int i = i0 + 32 * u + lane;
+                            vs[u] = i < n ? st[i] : 0;
+                            vd[u] = i < n ? st[g.k + i] : 0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int i = i0 + 32 * u + lane;
+                            if (i < n) {
+                                osrc[off + i] = vs[u];
+                                odst[off + i] = vd[u];
+                                if (oev) oev[off + i] = e;
+                            }
+                        }
                     }
                 }
             }
@@ -718,5 +763,9 @@ __global__ void __launch_bounds__(1024, 1) redrec_kernel(GridParams p) {
         __syncthreads();
     }
 }
+
+template __global__ void redrec_kernel<1>(GridParams);
+template __global__ void redrec_kernel<3>(GridParams);
+template __global__ void redrec_kernel<4>(GridParams);
 
 }  // namespace rb

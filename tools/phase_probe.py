@@ -31,3 +31,11 @@ for (W, H, hp, k, seed) in [(256, 256, 153, 39322, 257), (512, 512, 307, 157286,
     print(f"bird {W}x{H} h'={hp}: pooled events {len(ev)}; holes mean {ev[:,0].mean():.1f} max {ev[:,0].max()}; "
           f"levels top mean {ev[:,1].mean():.1f} max {ev[:,1].max()}; bottom mean {ev[:,2].mean():.1f} max {ev[:,2].max()}; "
           f"a mean {ev[:,5].mean():.1f}, b mean {ev[:,6].mean():.1f}")
+
+# plan-loop sections (cycles): select (scan + warp min), record, unlink, refresh
+for (W, H, hp, k, seed) in [(256, 256, 153, 39322, 257), (512, 512, 307, 157286, 0x51200000)]:
+    occ = sample_grids(seed, 1, W, H, k)
+    out = np.zeros(16, np.int64)
+    lib.recon_debug_grid_phases(0, occ.ctypes.data_as(C.c_void_p), W, H, hp, out.ctypes.data_as(C.c_void_p), 16)
+    print(f"plan {W}x{H}: select {out[8]/1965:.1f} us, record {out[9]/1965:.1f} us, unlink {out[10]/1965:.1f} us, "
+          f"refresh {out[11]/1965:.1f} us")
