@@ -73,7 +73,7 @@ class Clocks:
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -160,7 +160,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=2048, help="grids per GPU per step")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -212,8 +212,11 @@ def main():
         if st != 0:
             raise RuntimeError(f"solve failed {st}: {lib.last_cuda_error()}")
 
-    def timed(fn, steps, warmup):
+    ktimes = []  # (planner ms, executor ms) per timed step, CUDA events on the context stream
+
+    def timed(fn, steps, warmup, kernels=False):
         times = []
+        lib.set_kernel_timing(kernels)
         for i in range(warmup + steps):
             with torch.cuda.stream(stream):
                 flush.fill_(i)
@@ -225,6 +228,9 @@ def main():
             e1.synchronize()
             if i >= warmup:
                 times.append(e0.elapsed_time(e1))
+                if kernels:
+                    ktimes.append(lib.kernel_times())
+        lib.set_kernel_timing(False)
         return times
 
     # warm-up + correctness status
@@ -237,7 +243,7 @@ def main():
     torch.cuda.synchronize()
     launches0 = lib.launch_count()
     with Clocks(local) as clk:
-        times = timed(lib.lib.recon_redrec_solve_batch, args.steps, args.warmup)
+        times = timed(lib.lib.recon_redrec_solve_batch, args.steps, args.warmup, kernels=True)
     launches = lib.launch_count() - launches0
     torch.cuda.synchronize()
     ms = sum(times) / len(times)
@@ -248,7 +254,16 @@ def main():
     counts = pcount.cpu().numpy()
     alg_bytes = algorithmic_bytes(counts)
     hbm_peak, peak_kind = peaks()
-    achieved_gbs = alg_bytes / (ms * 1e-3) / 1e9
+    plan_ms = sum(k[0] for k in ktimes) / len(ktimes)
+    exec_ms = sum(k[1] for k in ktimes) / len(ktimes)
+    achieved_gbs = alg_bytes / (exec_ms * 1e-3) / 1e9  # dominant kernel: the executor
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tr = json.load(f).get("redrec_kernel", {})
+        if tr.get("batch") == B and tr.get("workload_seed") == hex(SEED_BASE):
+            traffic = tr.get("dram_bytes")
     value = ws * B / (ms * 1e-3)
 
     # bird on the same grids (secondary)
@@ -317,8 +332,10 @@ def main():
             "us_per_grid": ms * 1000.0 / B,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved_gbs / hbm_peak, "traffic": None, "peak_kind": peak_kind,
-                         "algorithmic_bytes_per_step": alg_bytes},
+                         "frac": achieved_gbs / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "rb::redrec_kernel (executor)", "kernel_ms": exec_ms,
+                         "algorithmic_bytes_per_launch": alg_bytes,
+                         "planner_kernel_ms": plan_ms},
             "e2e": {"value": ws * B / e2e_s, "unit": "grids/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "bird": {"grids_per_s": ws * B / (bird_ms * 1e-3), "ms_per_step": bird_ms},

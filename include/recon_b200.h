@@ -117,6 +117,12 @@ void recon_ctx_destroy(recon_ctx *ctx);
 void *recon_ctx_stream(recon_ctx *ctx);
 /* Number of kernel launches this context has issued (for bench accounting). */
 int64_t recon_ctx_launch_count(recon_ctx *ctx);
+/* Profiling (no reference counterpart): with timing enabled, the grid
+   solvers record CUDA events on the context stream around their kernels;
+   recon_ctx_kernel_times waits for the last solve and writes ms[0] = red-rec
+   planner, ms[1] = red-rec executor or bird kernel (0 when not launched). */
+recon_status recon_ctx_set_kernel_timing(recon_ctx *ctx, int32_t enable);
+recon_status recon_ctx_kernel_times(recon_ctx *ctx, float *ms, int32_t n);
 
 /* ------------------------------------------------------------------------- */
 /* Grid solvers (red-rec, bird): single instance, host buffers                */

@@ -603,6 +603,16 @@ int64_t recon_ctx_launch_count(recon_ctx *ctx) {
     (void)ctx;
     return 0;
 }
+recon_status recon_ctx_set_kernel_timing(recon_ctx *ctx, int32_t enable) {
+    (void)ctx;
+    (void)enable;
+    return RECON_OK;
+}
+recon_status recon_ctx_kernel_times(recon_ctx *ctx, float *ms, int32_t n) {
+    (void)ctx;
+    for (int32_t i = 0; i < n; ++i) ms[i] = 0.0f;
+    return RECON_OK;
+}
 
 static recon_status grid_solve(int pooled, const uint64_t *occ, int W, int H, int hp,
                                recon_grid_solution *out, int32_t *detail) {

@@ -289,6 +289,11 @@ recon_status recon_ctx_create(int32_t device, recon_ctx **out) {
 void recon_ctx_destroy(recon_ctx *ctx) { delete ctx; }
 void *recon_ctx_stream(recon_ctx *) { return nullptr; }
 int64_t recon_ctx_launch_count(recon_ctx *) { return 0; }
+recon_status recon_ctx_set_kernel_timing(recon_ctx *, int32_t) { return RECON_OK; }
+recon_status recon_ctx_kernel_times(recon_ctx *, float *ms, int32_t n) {
+    for (int32_t i = 0; i < n; ++i) ms[i] = 0.0f;
+    return RECON_OK;
+}
 
 recon_status recon_redrec_solve(recon_ctx *, const uint64_t *occ, int32_t width, int32_t height,
                                 int32_t h_prime, recon_grid_solution *out, int32_t *detail) {

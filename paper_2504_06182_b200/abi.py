@@ -154,6 +154,7 @@ class PipelineBatch(C.Structure):
 EXPORTED_SYMBOLS = [
     "recon_detail_message", "recon_last_cuda_error", "recon_abi_version",
     "recon_ctx_create", "recon_ctx_destroy", "recon_ctx_stream", "recon_ctx_launch_count",
+    "recon_ctx_set_kernel_timing", "recon_ctx_kernel_times",
     "recon_redrec_solve", "recon_bird_solve", "recon_occupancy_dag",
     "recon_redrec_solve_batch", "recon_bird_solve_batch",
     "recon_redrec_solve_batch_host", "recon_bird_solve_batch_host",
@@ -212,6 +213,8 @@ class ReconLib:
         L.recon_ctx_stream.restype = C.c_void_p
         L.recon_ctx_launch_count.argtypes = [C.c_void_p]
         L.recon_ctx_launch_count.restype = C.c_int64
+        L.recon_ctx_set_kernel_timing.argtypes = [C.c_void_p, C.c_int32]
+        L.recon_ctx_kernel_times.argtypes = [C.c_void_p, C.c_void_p, C.c_int32]
         L.recon_last_cuda_error.restype = C.c_char_p
         L.recon_abi_version.restype = C.c_int32
         for fn in ("recon_redrec_solve", "recon_bird_solve"):
@@ -265,6 +268,15 @@ class ReconLib:
 
     def launch_count(self) -> int:
         return int(self.lib.recon_ctx_launch_count(self.ctx()))
+
+    def set_kernel_timing(self, enable: bool) -> None:
+        self.lib.recon_ctx_set_kernel_timing(self.ctx(), 1 if enable else 0)
+
+    def kernel_times(self) -> tuple:
+        """(planner ms, executor ms) of the last grid solve (timing enabled)."""
+        ms = (C.c_float * 2)()
+        self.lib.recon_ctx_kernel_times(self.ctx(), ms, 2)
+        return float(ms[0]), float(ms[1])
 
     def close(self):
         if self._ctx is not None:

@@ -55,6 +55,8 @@ Ctx::~Ctx() {
         if (b.p) cudaFree(b.p);
     for (auto &b : hbuf)
         if (b.p) cudaFreeHost(b.p);
+    for (auto &e : tev)
+        if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -152,6 +154,33 @@ void *recon_ctx_stream(recon_ctx *ctx) {
 int64_t recon_ctx_launch_count(recon_ctx *ctx) {
     Ctx *c = resolve(ctx);
     return c ? c->launches : 0;
+}
+
+recon_status recon_ctx_set_kernel_timing(recon_ctx *ctx, int32_t enable) {
+    Ctx *c = resolve(ctx);
+    if (!c) return RECON_ERR_CUDA;
+    if (enable && !c->tev[0]) {
+        for (auto &e : c->tev) {
+            cudaError_t err = cudaEventCreate(&e);
+            if (err != cudaSuccess) return cuda_fail(err, "cudaEventCreate", nullptr);
+        }
+    }
+    c->timing = enable != 0;
+    return RECON_OK;
+}
+
+recon_status recon_ctx_kernel_times(recon_ctx *ctx, float *ms, int32_t n) {
+    Ctx *c = resolve(ctx);
+    if (!c || !ms) return RECON_ERR_ARGUMENT;
+    for (int32_t i = 0; i < n; ++i) ms[i] = 0.0f;
+    if (!c->tev[0]) return RECON_OK;
+    cudaError_t e = cudaEventSynchronize(c->tev[2]);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize", nullptr);
+    float t[2] = {0.0f, 0.0f};
+    if (c->timed_plan) cudaEventElapsedTime(&t[0], c->tev[0], c->tev[1]);
+    cudaEventElapsedTime(&t[1], c->tev[1], c->tev[2]);
+    for (int32_t i = 0; i < n && i < 2; ++i) ms[i] = t[i];
+    return RECON_OK;
 }
 
 }  // extern "C"

@@ -56,14 +56,15 @@ int grid_blocks(Ctx *c, int solver, const GridShape &s, int count) {
 // launches with the per-CTA staging scratch and the plans the red-rec kernels need
 cudaError_t launch(Ctx *c, int solver, GridParams &p, int grid) {
     if (solver == 0) {
-        p.stage = c->dev<int32_t>(S_STAGE, (size_t)grid * grid_stage_ints(p.shape));
+        p.stage = c->dev<uint32_t>(S_STAGE, (size_t)grid * grid_stage_ints(p.shape));
         if (!p.stage) return cudaErrorMemoryAllocation;
         void *pl = c->get(S_PLAN, (size_t)p.count * redrec_plan_bytes(p.shape.W) + 1024);
         if (!pl) return cudaErrorMemoryAllocation;
         p.plans = redrec_plans_carve(pl, p.shape.W, p.count);
     }
     c->launches += solver == 0 ? 2 : 1;
-    return launch_grid_solver(solver, p, grid, c->stream);
+    c->timed_plan = solver == 0;
+    return launch_grid_solver(solver, p, grid, c->stream, c->timing ? c->tev : nullptr);
 }
 
 // runs the DAG over `P` device-resident paths; copies edges to host arrays

@@ -32,6 +32,9 @@ struct Ctx {
     int sms = 148;
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
+    bool timing = false;          // recon_ctx_set_kernel_timing
+    bool timed_plan = false;      // the last timed solve launched the planner
+    cudaEvent_t tev[3] = {};      // before planner, before executor, after executor
     DevBuf buf[S_NSLOTS];
     HostBuf hbuf[8];
     void *get(int slot, size_t bytes);

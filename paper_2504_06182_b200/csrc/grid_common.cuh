@@ -168,10 +168,24 @@ __device__ __forceinline__ bool own_solve(const Geo &g, const uint64_t *m, int16
     return true;
 }
 
+// Path sinks: PathOut writes vertex ids (src/dst/event arrays); a packed
+// stage (redrec) keeps one word per path, source column << 20 | source depth
+// << 10 | target depth, the target column being the event's.
+__device__ __forceinline__ void emit_put(const PathOut &o, const Geo &g, int p, int scol, int sdepth, int dcol, int t,
+                                         int evid) {
+    o.src[p] = scol * g.H + (g.H - 1 - sdepth);
+    o.dst[p] = dcol * g.H + (g.H - 1 - t);
+    if (o.ev) o.ev[p] = evid;
+}
+__device__ __forceinline__ void emit_put(uint32_t *st, const Geo &, int p, int scol, int sdepth, int, int t, int) {
+    st[p] = ((uint32_t)scol << 20) | ((uint32_t)sdepth << 10) | (uint32_t)t;
+}
+
 // Emits a solved OWN event at [off, off + count); returns its displacement
 // (warp-uniform).
-__device__ __forceinline__ long long own_emit(const Geo &g, int col, const OwnSolve &s, const int16_t *L,
-                                              PathOut o, int off, int evid) {
+template <class Out>
+__device__ __forceinline__ long long own_emit(const Geo &g, int col, const OwnSolve &s, const int16_t *L, Out o,
+                                              int off, int evid) {
     const int16_t *otop = L, *obot = L + g.LK, *res = L + 3 * g.LK;
     long long disp = 0;
     for (int j = lane_id(); j < g.k; j += 32) {
@@ -179,51 +193,9 @@ __device__ __forceinline__ long long own_emit(const Geo &g, int col, const OwnSo
         if (!right && !left) continue;
         const int depth = j < s.a ? otop[s.a - j] : (j < s.a + s.R ? res[j - s.a] : obot[j - s.a - s.R + 1]);
         const int t = g.lo + j;
-        const int p = off + emit_slot(g, j, s.n_right, s.n_left);
-        o.src[p] = col * g.H + (g.H - 1 - depth);
-        o.dst[p] = col * g.H + (g.H - 1 - t);
-        if (o.ev) o.ev[p] = evid;
+        emit_put(o, g, off + emit_slot(g, j, s.n_right, s.n_left), col, depth, col, t, evid);
         disp += t > depth ? t - depth : depth - t;
     }
-    return warp_sum64(disp);
-}
-
-// Emission of a solved OWN event straight from the column plane: every
-// lane ranks its own chunk's tokens with three warp scans (top tokens by
-// depth descending, residents, bottom tokens) and writes the paths of the
-// used ones; the split a and the right/left counts come from the solve pass.
-__device__ __forceinline__ long long own_emit_direct(const Geo &g, int col, const uint64_t *m, int a, int n_right,
-                                                     int n_left, PathOut o, int off, int evid) {
-    const int lane = lane_id(), B = g.B, base = lane * B;
-    const uint32_t ch = lane_chunk(m, g.wpd, lane, B);
-    const uint32_t topm = ch & chunk_range(base, B, 0, g.lo);
-    const uint32_t resm = ch & chunk_range(base, B, g.lo, g.hi + 1);
-    const uint32_t botm = ch & chunk_range(base, B, g.hi + 1, g.H);
-    int nt, R, nb;
-    int et = warp_excl_scan(__popc(topm), &nt);
-    int er = warp_excl_scan(__popc(resm), &R);
-    int eb = warp_excl_scan(__popc(botm), &nb);
-    (void)nb;
-    const int b = g.k - R - a;
-    long long disp = 0;
-    auto put = [&](int j, int depth) {
-        const int t = g.lo + j;
-        const int p = off + emit_slot(g, j, n_right, n_left);
-        o.src[p] = col * g.H + (g.H - 1 - depth);
-        o.dst[p] = col * g.H + (g.H - 1 - t);
-        if (o.ev) o.ev[p] = evid;
-        disp += t > depth ? t - depth : depth - t;
-    };
-    for (uint32_t x = topm; x; x &= x - 1, ++et) {
-        const int desc = nt - 1 - et;  // 0 = innermost
-        if (desc < a) put(a - 1 - desc, base + __ffs(x) - 1);
-    }
-    for (uint32_t x = resm; x; x &= x - 1, ++er) {
-        const int depth = base + __ffs(x) - 1, j = a + er;
-        if (g.lo + j != depth) put(j, depth);
-    }
-    for (uint32_t x = botm; x; x &= x - 1, ++eb)
-        if (eb < b) put(a + R + eb, base + __ffs(x) - 1);
     return warp_sum64(disp);
 }
 

@@ -48,7 +48,7 @@ bool grid_shape(int W, int H, int k, int nwarps, GridShape &s) {
     return s.smem_bytes <= 227 * 1024;
 }
 
-size_t grid_stage_ints(const GridShape &s) { return (size_t)2 * s.W * s.k; }
+size_t grid_stage_ints(const GridShape &s) { return (size_t)s.W * s.k; }
 
 size_t redrec_plan_bytes(int W) {
     return (size_t)align_up(W, 16) + 3 * (size_t)align_up(2 * W, 16) + (size_t)align_up(4 * (W + 2), 16) + 32;
@@ -72,7 +72,7 @@ RedrecPlans redrec_plans_carve(void *base, int W, int count) {
     return pl;
 }
 
-cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaStream_t stream) {
+cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaStream_t stream, cudaEvent_t *ev) {
     const int threads = 32 * p.shape.nwarps;
     void (*kern)(GridParams) = solver == 0 ? redrec_exec(p.shape) : bird_kernel;
     cudaError_t e;
@@ -88,11 +88,14 @@ cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaSt
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int pgrid = std::max(1, std::min((p.count + pw - 1) / pw, std::max(1, per_sm) * sms));
+        if (ev) cudaEventRecord(ev[0], stream);
         redrec_plan_kernel<<<pgrid, 32 * pw, psmem, stream>>>(p);
     }
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.shape.smem_bytes);
     if (e != cudaSuccess) return e;
+    if (ev) cudaEventRecord(ev[1], stream);
     kern<<<grid, threads, p.shape.smem_bytes, stream>>>(p);
+    if (ev) cudaEventRecord(ev[2], stream);
     return cudaGetLastError();
 }
 

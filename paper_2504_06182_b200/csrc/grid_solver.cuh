@@ -41,13 +41,16 @@ struct GridParams {
     int32_t *path_count;
     int64_t *total_displacement;
     int32_t *status, *detail, *events;
-    int32_t *stage;          // red-rec: per-CTA event staging, 2*W*k ints per CTA (grid-sized)
+    uint32_t *stage;         // red-rec: per-CTA packed path staging, W*k words per CTA (grid-sized)
     RedrecPlans plans;       // red-rec: [count] plans
     long long *phase_clock;  // optional: clock64 at phase boundaries of instance 0 (profiling)
 };
 
 bool grid_shape(int W, int H, int k, int nwarps, GridShape &s);
-cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaStream_t stream);
+// ev (optional): events recorded before the planner, before and after the
+// executor (bird: the last two)
+cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaStream_t stream,
+                               cudaEvent_t *ev = nullptr);
 int grid_occupancy(int solver, const GridShape &s);
 size_t grid_stage_ints(const GridShape &s);
 size_t redrec_plan_bytes(int W);  // global plan bytes per instance

@@ -114,7 +114,7 @@ __device__ bool flush_solve(const Geo &g, const uint64_t *mr, const uint64_t *md
 
 __device__ long long flush_emit(const Geo &g, const FlushSolve &f, const uint64_t *mr, const uint64_t *md, int r,
                                 int d, const uint64_t *dep, int mark_first, const int16_t *mark_next,
-                                const int16_t *L, uint32_t *keys, PathOut o, int off, int evid) {
+                                const int16_t *L, uint32_t *keys, uint32_t *st) {
     const int16_t *res = L + 3 * g.LK;
     const int lane = lane_id(), B = g.B, base = lane * B;
     const uint32_t rtop = chunk_range(base, B, 0, g.lo), rbot = chunk_range(base, B, g.hi + 1, g.H);
@@ -162,10 +162,7 @@ __device__ long long flush_emit(const Geo &g, const FlushSolve &f, const uint64_
         for (int q = 0; q < a; ++q) rank += ktop[q] < key;
         const int v = (int)(key >> 20) - 2048, dist = (key >> 10) & 1023, col = key & 1023;
         const int depth = v + dist, j = rank, t = g.lo + j;
-        const int p = off + emit_slot(g, j, f.n_right, f.n_left);
-        o.src[p] = col * g.H + (g.H - 1 - depth);
-        o.dst[p] = r * g.H + (g.H - 1 - t);
-        if (o.ev) o.ev[p] = evid;
+        emit_put(st, g, emit_slot(g, j, f.n_right, f.n_left), col, depth, r, t, 0);
         disp += t - v;
     }
     for (int i = lane; i < b; i += 32) {
@@ -174,19 +171,13 @@ __device__ long long flush_emit(const Geo &g, const FlushSolve &f, const uint64_
         for (int q = 0; q < b; ++q) rank += kbot[q] < key;
         const int v = (int)(key >> 20) - 2048, dist = (key >> 10) & 1023, col = key & 1023;
         const int depth = v - dist, j = a + R + rank, t = g.lo + j;
-        const int p = off + emit_slot(g, j, f.n_right, f.n_left);
-        o.src[p] = col * g.H + (g.H - 1 - depth);
-        o.dst[p] = r * g.H + (g.H - 1 - t);
-        if (o.ev) o.ev[p] = evid;
+        emit_put(st, g, emit_slot(g, j, f.n_right, f.n_left), col, depth, r, t, 0);
         disp += v - t;
     }
     for (int i = lane; i < R; i += 32) {
         const int depth = res[i], j = a + i, t = g.lo + j;
         if (t == depth) continue;
-        const int p = off + emit_slot(g, j, f.n_right, f.n_left);
-        o.src[p] = r * g.H + (g.H - 1 - depth);
-        o.dst[p] = r * g.H + (g.H - 1 - t);
-        if (o.ev) o.ev[p] = evid;
+        emit_put(st, g, emit_slot(g, j, f.n_right, f.n_left), r, depth, r, t, 0);
         disp += t > depth ? t - depth : depth - t;
     }
     __syncwarp();
@@ -571,8 +562,8 @@ __global__ void __launch_bounds__(MINB == 1 ? 1024 : 256, MINB) redrec_kernel(Gr
     const int warp = warp_id(), lane = lane_id(), nw = blockDim.x >> 5;
     int16_t *L = b.lists + (size_t)warp * 4 * g.LK;
     uint32_t *keys = b.keys + (size_t)warp * 2 * g.LK;
-    // event e's paths are staged at stage + 2ke (sources) / + k (targets)
-    int32_t *const stage = p.stage + (size_t)blockIdx.x * 2 * g.W * g.k;
+    // event e's paths are staged (packed, emission order) at stage + k*e
+    uint32_t *const stage = p.stage + (size_t)blockIdx.x * g.W * g.k;
     __shared__ long long s_tokens;
     __shared__ unsigned long long s_disp;
     __shared__ int s_status, s_detail, s_n1, s_n2, s_nlev, s_total, s_fail;
@@ -630,8 +621,7 @@ __global__ void __launch_bounds__(MINB == 1 ? 1024 : 256, MINB) redrec_kernel(Gr
                     if (lane == 0) s_fail = 1;
                     continue;
                 }
-                int32_t *st = stage + (size_t)e * 2 * g.k;
-                disp += own_emit(g, c, s, L, PathOut{st, st + g.k, nullptr}, 0, e);
+                disp += own_emit(g, c, s, L, stage + (size_t)e * g.k, 0, e);
                 if (lane == 0) b.ev_count[e] = s.n_right + s.n_left;
                 __syncwarp();
             }
@@ -641,14 +631,14 @@ __global__ void __launch_bounds__(MINB == 1 ? 1024 : 256, MINB) redrec_kernel(Gr
                     const int e = b.wave_list[q];
                     const int col = b.ev_col[e], aux = b.ev_aux[e];
                     uint64_t *mc = b.dep + (size_t)col * g.wpd;
-                    int32_t *st = stage + (size_t)e * 2 * g.k;
+                    uint32_t *st = stage + (size_t)e * g.k;
                     if (b.ev_type[e] == EV_OWN) {
                         OwnSolve s;
                         if (!own_solve(g, mc, L, -1, s)) {
                             if (lane == 0) s_fail = 1;
                             continue;
                         }
-                        disp += own_emit(g, col, s, L, PathOut{st, st + g.k, nullptr}, 0, e);
+                        disp += own_emit(g, col, s, L, st, 0, e);
                         own_update(g, mc, s, L);
                         if (lane == 0) {
                             b.ev_count[e] = s.n_right + s.n_left;
@@ -665,8 +655,7 @@ __global__ void __launch_bounds__(MINB == 1 ? 1024 : 256, MINB) redrec_kernel(Gr
                             if (lane == 0) s_fail = 1;
                             continue;
                         }
-                        disp += flush_emit(g, f, mc, md, col, aux, b.dep, mfirst, b.mark_next, L, keys,
-                                           PathOut{st, st + g.k, nullptr}, 0, e);
+                        disp += flush_emit(g, f, mc, md, col, aux, b.dep, mfirst, b.mark_next, L, keys, st);
                         flush_update(g, b.dep, col, aux, f, L);
                         if (lane == 0) b.ev_count[e] = f.n_right + f.n_left;
                     }
@@ -683,8 +672,7 @@ __global__ void __launch_bounds__(MINB == 1 ? 1024 : 256, MINB) redrec_kernel(Gr
                     if (lane == 0) s_fail = 1;
                     continue;
                 }
-                int32_t *st = stage + (size_t)e * 2 * g.k;
-                disp += own_emit(g, c, s, L, PathOut{st, st + g.k, nullptr}, 0, e);
+                disp += own_emit(g, c, s, L, stage + (size_t)e * g.k, 0, e);
                 if (lane == 0) b.ev_count[e] = s.n_right + s.n_left;
                 __syncwarp();
             }
@@ -711,21 +699,21 @@ __global__ void __launch_bounds__(MINB == 1 ? 1024 : 256, MINB) redrec_kernel(Gr
                 int32_t *const oev = p.path_event ? p.path_event + pbase : nullptr;
                 for (int e = warp; e < W; e += nw) {
                     const int n = b.ev_count[e], off = b.ev_off[e];
-                    const int32_t *st = stage + (size_t)e * 2 * g.k;
-                    for (int i0 = 0; i0 < n; i0 += 128) {  // 8 loads in flight per lane
-                        int32_t vs[4], vd[4];
+                    const int dbase = b.ev_col[e] * g.H + g.H - 1;
+                    const uint32_t *st = stage + (size_t)e * g.k;
+                    for (int i0 = 0; i0 < n; i0 += 128) {  // 4 loads in flight per lane
+                        uint32_t v[4];
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const int i = i0 + 32 * u + lane;
-                            vs[u] = i < n ? st[i] : 0;
-                            vd[u] = i < n ? st[g.k + i] : 0;
+                            v[u] = i < n ? st[i] : 0u;
                         }
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const int i = i0 + 32 * u + lane;
                             if (i < n) {
-                                osrc[off + i] = vs[u];
-                                odst[off + i] = vd[u];
+                                osrc[off + i] = (int)(v[u] >> 20) * g.H + g.H - 1 - (int)((v[u] >> 10) & 1023);
+                                odst[off + i] = dbase - (int)(v[u] & 1023);
                                 if (oev) oev[off + i] = e;
                             }
                         }
