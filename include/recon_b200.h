@@ -329,6 +329,76 @@ recon_status recon_pipeline_batch_run(recon_ctx *ctx, const recon_pipeline_batch
 recon_status recon_pipeline_batch_run_host(recon_ctx *ctx, const recon_pipeline_batch *batch);
 
 /* ------------------------------------------------------------------------- */
+/* Validators (device)                                                        */
+/* ------------------------------------------------------------------------- */
+
+/*
+ * Batched, on-device restatement of the reference's solution checks for grid
+ * solutions in this ABI's path format (one-bend paths from (src, dst), the
+ * identity schedule = paths in order, each path's moves in order):
+ *   validate_solution        executor.hpp:38, executor.cpp:142-183
+ *   check_one_move_per_token executor.hpp:43, executor.cpp:185-219
+ *   validate_batches         batching.hpp:64-65, batching.cpp:161-252
+ * Each report keeps the reference's check order and early returns; the
+ * verdict is a bit set of the failure categories the reference would report
+ * (0 = every check passes).  Batch checks run when move_batch != NULL.  A
+ * path endpoint off the grid yields exactly RECON_V_PATH_BOUNDS (the path
+ * cannot be drawn, so nothing else is evaluated).
+ */
+typedef enum recon_verdict {
+    RECON_V_PATH_BOUNDS = 1u << 0,          /* "path i leaves the grid" */
+    RECON_V_SHARED_SOURCE = 1u << 1,        /* "two paths share source vertex v" */
+    RECON_V_SHARED_TARGET = 1u << 2,        /* "two paths share target vertex v" */
+    RECON_V_DAG_CYCLE = 1u << 3,            /* "dependency dag has a cycle" */
+    RECON_V_STATS_DISPLACEMENT = 1u << 4,   /* stats.total_displacement != weight */
+    RECON_V_STATS_DISPLACED = 1u << 5,      /* stats.displaced_tokens != displaced count */
+    RECON_V_EXECUTION = 1u << 6,            /* "execution failed: ..." (collision) */
+    RECON_V_TARGETS = 1u << 7,              /* final configuration misses a target */
+    RECON_V_DAG_ORDER = 1u << 8,            /* "schedule violates dag edge i->j" */
+    RECON_V_TOKEN_EMPTY = 1u << 9,          /* one-move check: move from an empty vertex */
+    RECON_V_TOKEN_SECOND_PATH = 1u << 10,   /* one-move check: token begins a second path */
+    RECON_V_BATCH_CONSERVATION = 1u << 11,  /* batched moves != path-system edge multiset */
+    RECON_V_BATCH_BOUND = 1u << 12,         /* more batches than elementary moves */
+    RECON_V_BATCH_EMPTY = 1u << 13,         /* "batch b is empty" */
+    RECON_V_BATCH_DISJOINT = 1u << 14,      /* "batch b is not vertex-disjoint" */
+    RECON_V_BATCH_CONSTRAINT = 1u << 15,    /* "batch b violates the constraint set" */
+    RECON_V_BATCH_COLLISION = 1u << 16,     /* batch moves from an empty / into an occupied vertex */
+    RECON_V_BATCH_TARGETS = 1u << 17,       /* batched execution misses a target */
+    RECON_V_BATCH_DAG = 1u << 18,           /* "batch order violates dag edge i->j" */
+    RECON_V_BATCH_ORDER = 1u << 19,         /* a path's move precedes its earlier move (match_schedule fails) */
+    RECON_V_TOKEN_MATCH = 1u << 20          /* one-move check: match_schedule attributes the moves to
+                                               other paths and then fails (colliding schedules only) */
+} recon_verdict;
+
+typedef enum recon_dag_mode {
+    RECON_DAG_NONE = 0,       /* solution without dependency edges */
+    RECON_DAG_EXPLICIT = 1,   /* edges (dag_a[e], dag_b[e]) for e in [dag_offset[i], dag_offset[i+1]) */
+    RECON_DAG_OCCUPANCY = 2   /* occupancy_dag of the paths (virtual_line.cpp:241-268), derived on the device */
+} recon_dag_mode;
+
+typedef struct recon_validate_batch {
+    const uint64_t *occ;                 /* initial configurations, count * width * wpc words */
+    int32_t count, width, height, h_prime;
+    const int32_t *path_src, *path_dst;  /* instance i at i * path_stride */
+    int64_t path_stride;
+    const int32_t *path_count;           /* [count] */
+    const int64_t *total_displacement;   /* claimed stats [count], NULL = not checked */
+    const int32_t *displaced;            /* claimed displaced_tokens [count], NULL = not checked */
+    int32_t dag_mode;                    /* recon_dag_mode */
+    const int32_t *dag_a, *dag_b;        /* RECON_DAG_EXPLICIT: edge lists (global edge index) */
+    const int64_t *dag_offset;           /* [count + 1] */
+    const int32_t *move_batch;           /* batch per move, path-major, instance i at i * move_stride; NULL = no batch checks */
+    int64_t move_stride;
+    const int32_t *batch_count;          /* [count] */
+    int32_t preset;                      /* recon_preset of the batch schedule */
+    uint32_t *verdict;                   /* [count] recon_verdict bits */
+} recon_validate_batch;
+
+recon_status recon_validate_batch_run(recon_ctx *ctx, const recon_validate_batch *batch);
+/* Same with every pointer in `batch` in host memory. */
+recon_status recon_validate_batch_run_host(recon_ctx *ctx, const recon_validate_batch *batch);
+
+/* ------------------------------------------------------------------------- */
 /* Synthetic inputs (host)                                                    */
 /* ------------------------------------------------------------------------- */
 

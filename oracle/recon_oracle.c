@@ -1566,3 +1566,336 @@ recon_status recon_occupancy_dag_paths(recon_ctx *ctx, int32_t width, int32_t he
     free(e);
     return st;
 }
+
+/* ======================================================================== */
+/* Validators: sequential restatement of validate_solution                  */
+/* (executor.cpp:142-183), check_one_move_per_token (executor.cpp:185-219)  */
+/* and validate_batches (batching.cpp:161-252) for one-bend grid solutions  */
+/* with the identity schedule.                                               */
+/* ======================================================================== */
+
+/* Kahn's algorithm (MoveDag::topo_order, path_system.cpp) */
+static int edges_acyclic(int64_t np, const edge_t *e, int64_t ne) {
+    int32_t *indeg = xcalloc((size_t)np, 4), *q = xcalloc((size_t)np, 4);
+    int64_t *off = xcalloc((size_t)np + 1, 8);
+    int32_t *adj = xcalloc((size_t)ne, 4);
+    for (int64_t i = 0; i < ne; ++i) {
+        off[e[i].a + 1]++;
+        indeg[e[i].b]++;
+    }
+    for (int64_t i = 0; i < np; ++i) off[i + 1] += off[i];
+    int64_t *cur = xcalloc((size_t)np + 1, 8);
+    memcpy(cur, off, (size_t)(np + 1) * 8);
+    for (int64_t i = 0; i < ne; ++i) adj[cur[e[i].a]++] = e[i].b;
+    int64_t h = 0, t = 0;
+    for (int64_t i = 0; i < np; ++i)
+        if (!indeg[i]) q[t++] = (int32_t)i;
+    while (h < t) {
+        const int32_t u = q[h++];
+        for (int64_t k = off[u]; k < off[u + 1]; ++k)
+            if (--indeg[adj[k]] == 0) q[t++] = adj[k];
+    }
+    free(indeg);
+    free(q);
+    free(off);
+    free(adj);
+    free(cur);
+    return t == np;
+}
+
+static uint32_t validate_one(int W, int H, int hp, const uint64_t *occ, const int32_t *ps, const int32_t *pt,
+                             int64_t np, const int64_t *tdisp, const int32_t *displaced, int dag_mode,
+                             const int32_t *ea, const int32_t *eb, int64_t ne_in, const int32_t *mb, int64_t nb,
+                             int preset) {
+    const int64_t V = (int64_t)W * H;
+    const int wpc = wpc_of(H), ylo = (H - hp) / 2;
+    uint32_t v = 0;
+    char *seen_s = xcalloc((size_t)V, 1), *seen_t = xcalloc((size_t)V, 1), *ok = xcalloc((size_t)np, 1);
+    int64_t *len = xcalloc((size_t)np, 8), *off = xcalloc((size_t)np + 1, 8);
+    int64_t weight = 0, moved = 0;
+    /* check_paths (executor.cpp:38-80) */
+    for (int64_t i = 0; i < np; ++i) {
+        if (ps[i] < 0 || ps[i] >= V || pt[i] < 0 || pt[i] >= V) {
+            v |= RECON_V_PATH_BOUNDS;
+            continue;
+        }
+        ok[i] = 1;
+        const int dx = ps[i] / H - pt[i] / H, dy = ps[i] % H - pt[i] % H;
+        len[i] = (dx < 0 ? -dx : dx) + (dy < 0 ? -dy : dy);
+        if (seen_s[ps[i]]) v |= RECON_V_SHARED_SOURCE;
+        if (seen_t[pt[i]]) v |= RECON_V_SHARED_TARGET;
+        seen_s[ps[i]] = seen_t[pt[i]] = 1;
+    }
+    if (v & RECON_V_PATH_BOUNDS) { /* endpoints off the grid: nothing else is evaluated */
+        free(seen_s);
+        free(seen_t);
+        free(ok);
+        free(len);
+        free(off);
+        return RECON_V_PATH_BOUNDS;
+    }
+    for (int64_t i = 0; i < np; ++i) {
+        off[i + 1] = off[i] + len[i];
+        weight += len[i];
+        moved += len[i] > 0;
+    }
+    /* the dag */
+    edge_t *e = NULL;
+    int64_t ne = 0;
+    if (dag_mode == RECON_DAG_EXPLICIT) {
+        e = xcalloc((size_t)ne_in, sizeof(edge_t));
+        for (int64_t i = 0; i < ne_in; ++i) e[i] = (edge_t){ea[i], eb[i]};
+        ne = ne_in;
+    } else if (dag_mode == RECON_DAG_OCCUPANCY && !(v & RECON_V_PATH_BOUNDS)) {
+        ne = dag_edges(W, H, ps, pt, np, &e);
+    }
+    if (ne && !edges_acyclic(np, e, ne)) v |= RECON_V_DAG_CYCLE;
+    if (tdisp && *tdisp != weight) v |= RECON_V_STATS_DISPLACEMENT;
+    if (displaced && *displaced != moved) v |= RECON_V_STATS_DISPLACED;
+    int32_t *verts = xcalloc((size_t)(W + H + 2), 4);
+    char *cfg = xcalloc((size_t)V, 1);
+    if (!v) {
+        for (int64_t x = 0; x < V; ++x) cfg[x] = getbit(occ + (x / H) * wpc, (int)(x % H));
+        int fail = 0;
+        for (int64_t i = 0; i < np && !fail; ++i) { /* execute_schedule (executor.cpp:10-26) */
+            const int64_t nv = walk_path(H, ps[i], pt[i], verts);
+            for (int64_t k = 0; k + 1 < nv && !fail; ++k) {
+                if (!cfg[verts[k]] || cfg[verts[k + 1]]) fail = 1;
+                cfg[verts[k]] = 0;
+                cfg[verts[k + 1]] = 1;
+            }
+        }
+        if (fail) {
+            v |= RECON_V_EXECUTION;
+        } else {
+            for (int x = 0; x < W; ++x)
+                for (int y = ylo; y < ylo + hp; ++y)
+                    if (!cfg[(int64_t)x * H + y]) v |= RECON_V_TARGETS;
+            for (int64_t k = 0; k < ne; ++k) { /* linear extension, identity schedule */
+                const int32_t i = e[k].a, j = e[k].b;
+                if (len[i] > 0 && len[j] > 0 && off[i] + len[i] - 1 > off[j]) {
+                    v |= RECON_V_DAG_ORDER;
+                    break;
+                }
+            }
+        }
+    }
+    /* check_one_move_per_token (executor.cpp:185-219): match_schedule
+       (executor.cpp:82-140, pending path fronts per vertex, first pending
+       path whose next vertex fits) attributes each move to a path; then
+       token identities are followed */
+    {
+        int32_t *head = xcalloc((size_t)V, 4), *tail = xcalloc((size_t)V, 4);
+        int32_t *nx = xcalloc((size_t)np + 1, 4), *pv = xcalloc((size_t)np + 1, 4);
+        int64_t *nextk = xcalloc((size_t)np + 1, 8);
+        char *starts = xcalloc((size_t)weight + 1, 1);
+        for (int64_t x = 0; x < V; ++x) head[x] = tail[x] = -1;
+#define PUSH(vv, pid)                                   \
+    do {                                                \
+        nx[pid] = -1;                                   \
+        pv[pid] = tail[vv];                             \
+        if (tail[vv] >= 0) nx[tail[vv]] = (int32_t)(pid); \
+        else head[vv] = (int32_t)(pid);                  \
+        tail[vv] = (int32_t)(pid);                       \
+    } while (0)
+        for (int64_t i = 0; i < np; ++i)
+            if (len[i] > 0) PUSH(ps[i], i);
+        int matched_all = 1;
+        int64_t mi = 0;
+        int32_t *pv2 = xcalloc((size_t)(W + H + 2), 4);
+        for (int64_t i = 0; i < np && matched_all; ++i) {
+            const int64_t nv = walk_path(H, ps[i], pt[i], verts);
+            for (int64_t k = 0; k + 1 < nv; ++k, ++mi) {
+                const int32_t from = verts[k], to = verts[k + 1];
+                int32_t m = -1;
+                for (int32_t q = head[from]; q >= 0; q = nx[q]) {
+                    walk_path(H, ps[q], pt[q], pv2);
+                    if (pv2[nextk[q] + 1] == to) {
+                        m = q;
+                        break;
+                    }
+                }
+                if (m < 0) {
+                    matched_all = 0;
+                    break;
+                }
+                if (pv[m] >= 0) nx[pv[m]] = nx[m];
+                else head[from] = nx[m];
+                if (nx[m] >= 0) pv[nx[m]] = pv[m];
+                else tail[from] = pv[m];
+                starts[mi] = nextk[m] == 0;
+                const int64_t kk = ++nextk[m];
+                if (kk < len[m]) {
+                    walk_path(H, ps[m], pt[m], pv2);
+                    PUSH(pv2[kk], m);
+                }
+            }
+        }
+#undef PUSH
+        if (!matched_all) {
+            v |= RECON_V_TOKEN_MATCH;
+        } else {
+            int32_t *tok = xcalloc((size_t)V, 4);
+            for (int64_t x = 0; x < V; ++x) tok[x] = getbit(occ + (x / H) * wpc, (int)(x % H)) ? (int32_t)x : -1;
+            char *began = xcalloc((size_t)V, 1);
+            int stop = 0;
+            mi = 0;
+            for (int64_t i = 0; i < np && !stop; ++i) {
+                const int64_t nv = walk_path(H, ps[i], pt[i], verts);
+                for (int64_t k = 0; k + 1 < nv; ++k, ++mi) {
+                    const int32_t t = tok[verts[k]];
+                    if (t < 0) {
+                        v |= RECON_V_TOKEN_EMPTY;
+                        stop = 1;
+                        break;
+                    }
+                    if (starts[mi]) {
+                        if (began[t]) {
+                            v |= RECON_V_TOKEN_SECOND_PATH;
+                            stop = 1;
+                            break;
+                        }
+                        began[t] = 1;
+                    }
+                    tok[verts[k]] = -1;
+                    tok[verts[k + 1]] = t;
+                }
+            }
+            free(tok);
+            free(began);
+        }
+        free(head);
+        free(tail);
+        free(nx);
+        free(pv);
+        free(nextk);
+        free(starts);
+        free(pv2);
+    }
+    /* validate_batches (batching.cpp:161-252) */
+    if (mb) {
+        uint32_t bv = 0;
+        int64_t *bcnt = xcalloc((size_t)nb + 1, 8), *bstart = xcalloc((size_t)nb + 2, 8);
+        for (int64_t i = 0; i < np; ++i)
+            for (int64_t k = 0; k < len[i]; ++k) {
+                const int32_t b = mb[off[i] + k];
+                if (b < 0 || b >= nb) bv |= RECON_V_BATCH_CONSERVATION;
+                else bcnt[b]++;
+            }
+        if (nb > weight) bv |= RECON_V_BATCH_BOUND;
+        for (int64_t b = 0; b < nb; ++b) bstart[b + 1] = bstart[b] + bcnt[b];
+        int32_t *mf = xcalloc((size_t)bstart[nb] + 1, 4), *mt = xcalloc((size_t)bstart[nb] + 1, 4);
+        int64_t *fill = xcalloc((size_t)nb + 1, 8);
+        for (int64_t i = 0; i < np; ++i) { /* batch b = its moves in ascending path id */
+            if (!ok[i]) continue;
+            const int64_t nv = walk_path(H, ps[i], pt[i], verts);
+            for (int64_t k = 0; k + 1 < nv; ++k) {
+                const int32_t b = mb[off[i] + k];
+                if (b < 0 || b >= nb) continue;
+                const int64_t at = bstart[b] + fill[b]++;
+                mf[at] = verts[k];
+                mt[at] = verts[k + 1];
+            }
+        }
+        for (int64_t x = 0; x < V; ++x) cfg[x] = getbit(occ + (x / H) * wpc, (int)(x % H));
+        char *used = xcalloc((size_t)V, 1);
+        int ret = 0;
+        for (int64_t b = 0; b < nb && !ret; ++b) {
+            const int64_t s = bstart[b], n = bcnt[b];
+            if (!n) {
+                bv |= RECON_V_BATCH_EMPTY;
+                continue;
+            }
+            for (int64_t m = s; m < s + n; ++m) {
+                if (used[mf[m]] || used[mt[m]]) {
+                    bv |= RECON_V_BATCH_DISJOINT;
+                    ret = 1;
+                    break;
+                }
+                used[mf[m]] = used[mt[m]] = 1;
+            }
+            for (int64_t m = s; m < s + n; ++m) used[mf[m]] = used[mt[m]] = 0;
+            if (ret) break;
+            if (preset == RECON_PRESET_COLUMN_DIRECTION) { /* ConstraintSet::compatible (batching.cpp:17-24) */
+                int bad = 0;
+                for (int64_t m = s + 1; m < s + n && !bad; ++m) {
+                    const int fx0 = mf[s] / H, fy0 = mf[s] % H, tx0 = mt[s] / H, ty0 = mt[s] % H;
+                    const int fx = mf[m] / H, fy = mf[m] % H, tx = mt[m] / H, ty = mt[m] % H;
+                    const int d0 = ty0 > fy0 ? 0 : ty0 < fy0 ? 1 : tx0 < fx0 ? 2 : 3;
+                    const int d = ty > fy ? 0 : ty < fy ? 1 : tx < fx ? 2 : 3;
+                    if (d != d0 || (d < 2 ? fx != fx0 : fy != fy0)) bad = 1;
+                }
+                if (bad) bv |= RECON_V_BATCH_CONSTRAINT;
+            }
+            for (int64_t m = s; m < s + n; ++m)
+                if (!cfg[mf[m]] || cfg[mt[m]]) {
+                    bv |= RECON_V_BATCH_COLLISION;
+                    ret = 1;
+                    break;
+                }
+            if (ret) break;
+            for (int64_t m = s; m < s + n; ++m) cfg[mf[m]] = 0;
+            for (int64_t m = s; m < s + n; ++m) cfg[mt[m]] = 1;
+        }
+        if (!ret) {
+            for (int x = 0; x < W; ++x)
+                for (int y = ylo; y < ylo + hp; ++y)
+                    if (!cfg[(int64_t)x * H + y]) bv |= RECON_V_BATCH_TARGETS;
+            if (!bv) {
+                /* match_schedule on the batch-ordered move list: a path's moves
+                   must appear in batch order; then dag order by first moves */
+                for (int64_t i = 0; i < np && !bv; ++i)
+                    for (int64_t k = 1; k < len[i]; ++k)
+                        if (mb[off[i] + k] < mb[off[i] + k - 1]) {
+                            bv |= RECON_V_BATCH_ORDER;
+                            break;
+                        }
+                for (int64_t k = 0; k < ne && !bv; ++k) {
+                    const int32_t i = e[k].a, j = e[k].b;
+                    if (len[i] > 0 && len[j] > 0 && mb[off[j]] < mb[off[i]]) bv |= RECON_V_BATCH_DAG;
+                }
+            }
+        }
+        v |= bv;
+        free(bcnt);
+        free(bstart);
+        free(mf);
+        free(mt);
+        free(fill);
+        free(used);
+    }
+    free(seen_s);
+    free(seen_t);
+    free(ok);
+    free(len);
+    free(off);
+    free(e);
+    free(verts);
+    free(cfg);
+    return v;
+}
+
+static recon_status validate_run(const recon_validate_batch *b) {
+    if (!b || !b->occ || !b->path_src || !b->path_dst || !b->path_count || !b->verdict) return RECON_ERR_ARGUMENT;
+    const int wpc = wpc_of(b->height);
+    for (int32_t i = 0; i < b->count; ++i) {
+        const int64_t e0 = b->dag_mode == RECON_DAG_EXPLICIT ? b->dag_offset[i] : 0;
+        const int64_t e1 = b->dag_mode == RECON_DAG_EXPLICIT ? b->dag_offset[i + 1] : 0;
+        b->verdict[i] = validate_one(
+            b->width, b->height, b->h_prime, b->occ + (size_t)i * b->width * wpc, b->path_src + i * b->path_stride,
+            b->path_dst + i * b->path_stride, b->path_count[i], b->total_displacement ? b->total_displacement + i : NULL,
+            b->displaced ? b->displaced + i : NULL, b->dag_mode, b->dag_a ? b->dag_a + e0 : NULL,
+            b->dag_b ? b->dag_b + e0 : NULL, e1 - e0, b->move_batch ? b->move_batch + i * b->move_stride : NULL,
+            b->batch_count ? b->batch_count[i] : 0, b->preset);
+    }
+    return RECON_OK;
+}
+
+recon_status recon_validate_batch_run(recon_ctx *c, const recon_validate_batch *b) {
+    (void)c;
+    return validate_run(b);
+}
+recon_status recon_validate_batch_run_host(recon_ctx *c, const recon_validate_batch *b) {
+    (void)c;
+    return validate_run(b);
+}

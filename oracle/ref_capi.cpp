@@ -552,3 +552,130 @@ extern "C" recon_status recon_occupancy_dag_paths(recon_ctx *, int32_t, int32_t,
         }
     });
 }
+
+// Validators: the reference's validate_solution / check_one_move_per_token /
+// validate_batches on the decoded solution; failures map to recon_verdict
+// bits by message (executor.cpp:38-219, batching.cpp:161-252).
+namespace {
+
+uint32_t bits_of(const ValidationReport &r, bool batch) {
+    static const std::pair<const char *, uint32_t> sol[] = {
+        {"leaves the grid", RECON_V_PATH_BOUNDS},
+        {"two paths share source vertex", RECON_V_SHARED_SOURCE},
+        {"two paths share target vertex", RECON_V_SHARED_TARGET},
+        {"dependency dag has a cycle", RECON_V_DAG_CYCLE},
+        {"stats.total_displacement does not equal", RECON_V_STATS_DISPLACEMENT},
+        {"stats.displaced_tokens does not equal", RECON_V_STATS_DISPLACED},
+        {"execution failed", RECON_V_EXECUTION},
+        {"final configuration does not cover", RECON_V_TARGETS},
+        {"schedule violates dag edge", RECON_V_DAG_ORDER},
+        {"from an empty vertex", RECON_V_TOKEN_EMPTY},
+        {"begins a second path", RECON_V_TOKEN_SECOND_PATH},
+        {"matches no pending path edge", RECON_V_TOKEN_MATCH},
+        {"edges missing from the schedule", RECON_V_TOKEN_MATCH},
+    };
+    static const std::pair<const char *, uint32_t> bat[] = {
+        {"batched moves do not conserve", RECON_V_BATCH_CONSERVATION},
+        {"more batches than elementary moves", RECON_V_BATCH_BOUND},
+        {"is empty", RECON_V_BATCH_EMPTY},
+        {"is not vertex-disjoint", RECON_V_BATCH_DISJOINT},
+        {"violates the constraint set", RECON_V_BATCH_CONSTRAINT},
+        {"moves a token from an empty vertex", RECON_V_BATCH_COLLISION},
+        {"moves into a vertex occupied", RECON_V_BATCH_COLLISION},
+        {"batched execution does not cover", RECON_V_BATCH_TARGETS},
+        {"matches no pending path edge", RECON_V_BATCH_ORDER},
+        {"edges missing from the schedule", RECON_V_BATCH_ORDER},
+        {"batch order violates dag edge", RECON_V_BATCH_DAG},
+    };
+    uint32_t v = 0;
+    for (const std::string &f : r.failures) {
+        uint32_t b = 1u << 31;  // unmapped message
+        if (batch) {
+            for (const auto &[m, bit] : bat)
+                if (f.find(m) != std::string::npos) {
+                    b = bit;
+                    break;
+                }
+        } else {
+            for (const auto &[m, bit] : sol)
+                if (f.find(m) != std::string::npos) {
+                    b = bit;
+                    break;
+                }
+        }
+        v |= b;
+    }
+    return v;
+}
+
+uint32_t validate_ref(const recon_validate_batch *b, int i) {
+    const int wpc = words_per_column(b->height);
+    const Problem p = grid_problem(b->occ + static_cast<size_t>(i) * b->width * wpc, b->width, b->height, b->h_prime);
+    const Geometry &g = p.geometry;
+    const int np = b->path_count[i];
+    const int32_t *ps = b->path_src + i * b->path_stride, *pt = b->path_dst + i * b->path_stride;
+    PathSystem sys;
+    bool oob = false;
+    for (int k = 0; k < np; ++k) {
+        if (!g.in_bounds(ps[k]) || !g.in_bounds(pt[k])) {
+            Path q;
+            q.vertices = {ps[k], pt[k]};
+            sys.paths.push_back(q);
+            oob = true;
+        } else {
+            sys.paths.push_back(one_bend_path(g, ps[k], pt[k]));
+        }
+    }
+    MoveDag dag;
+    dag.node_count = np;
+    if (b->dag_mode == RECON_DAG_EXPLICIT) {
+        for (int64_t e = b->dag_offset[i]; e < b->dag_offset[i + 1]; ++e) dag.add_edge(b->dag_a[e], b->dag_b[e]);
+    } else if (b->dag_mode == RECON_DAG_OCCUPANCY && !oob) {
+        dag = occupancy_dag(sys.paths);
+    }
+    std::vector<int> order(static_cast<size_t>(np));
+    for (int k = 0; k < np; ++k) order[static_cast<size_t>(k)] = k;
+    Solution sol;
+    if (oob) {  // make_solution would walk out-of-grid vertices
+        sol.path_system = sys;
+        sol.dag = dag;
+        sol.stats.displaced_tokens = np;
+        sol.stats.total_displacement = 0;
+    } else {
+        sol = make_solution(sys, dag, order);
+    }
+    if (b->total_displacement) sol.stats.total_displacement = b->total_displacement[i];
+    if (b->displaced) sol.stats.displaced_tokens = b->displaced[i];
+    if (oob) return RECON_V_PATH_BOUNDS;  // a one-bend path needs in-grid endpoints; nothing else is evaluated
+    uint32_t v = bits_of(validate_solution(p, sol), false);
+    v |= bits_of(check_one_move_per_token(p, sol), false);
+    if (b->move_batch) {
+        const int32_t *mb = b->move_batch + i * b->move_stride;
+        const int nb = b->batch_count[i];
+        BatchSchedule bs;
+        bs.batches.resize(static_cast<size_t>(std::max(nb, 0)));
+        int64_t m = 0;
+        for (const Path &q : sol.path_system.paths)
+            for (size_t k = 0; k + 1 < q.vertices.size(); ++k, ++m) {
+                const int32_t bi = mb[m];
+                if (bi >= 0 && bi < nb) bs.batches[static_cast<size_t>(bi)].moves.push_back({q.vertices[k], q.vertices[k + 1]});
+            }
+        BatchOptions opt;
+        opt.constraints.preset = b->preset == RECON_PRESET_COLUMN_DIRECTION ? ConstraintPreset::column_direction
+                                                                            : ConstraintPreset::none;
+        v |= bits_of(validate_batches(p, sol, bs, opt), true);
+    }
+    return v;
+}
+
+}  // namespace
+
+extern "C" recon_status recon_validate_batch_run(recon_ctx *, const recon_validate_batch *b) {
+    if (!b || !b->occ || !b->path_src || !b->path_dst || !b->path_count || !b->verdict) return RECON_ERR_ARGUMENT;
+    parallel_for(b->count, [&](int i) { b->verdict[i] = validate_ref(b, i); });
+    return RECON_OK;
+}
+
+extern "C" recon_status recon_validate_batch_run_host(recon_ctx *c, const recon_validate_batch *b) {
+    return recon_validate_batch_run(c, b);
+}

@@ -151,6 +151,33 @@ class PipelineBatch(C.Structure):
     ]
 
 
+class ValidateBatch(C.Structure):
+    _fields_ = [
+        ("occ", C.c_void_p), ("count", C.c_int32), ("width", C.c_int32), ("height", C.c_int32),
+        ("h_prime", C.c_int32), ("path_src", C.c_void_p), ("path_dst", C.c_void_p), ("path_stride", C.c_int64),
+        ("path_count", C.c_void_p), ("total_displacement", C.c_void_p), ("displaced", C.c_void_p),
+        ("dag_mode", C.c_int32), ("dag_a", C.c_void_p), ("dag_b", C.c_void_p), ("dag_offset", C.c_void_p),
+        ("move_batch", C.c_void_p), ("move_stride", C.c_int64), ("batch_count", C.c_void_p),
+        ("preset", C.c_int32), ("verdict", C.c_void_p),
+    ]
+
+
+# recon_verdict bits (include/recon_b200.h)
+VERDICT_BITS = {
+    "PATH_BOUNDS": 1 << 0, "SHARED_SOURCE": 1 << 1, "SHARED_TARGET": 1 << 2, "DAG_CYCLE": 1 << 3,
+    "STATS_DISPLACEMENT": 1 << 4, "STATS_DISPLACED": 1 << 5, "EXECUTION": 1 << 6, "TARGETS": 1 << 7,
+    "DAG_ORDER": 1 << 8, "TOKEN_EMPTY": 1 << 9, "TOKEN_SECOND_PATH": 1 << 10, "BATCH_CONSERVATION": 1 << 11,
+    "BATCH_BOUND": 1 << 12, "BATCH_EMPTY": 1 << 13, "BATCH_DISJOINT": 1 << 14, "BATCH_CONSTRAINT": 1 << 15,
+    "BATCH_COLLISION": 1 << 16, "BATCH_TARGETS": 1 << 17, "BATCH_DAG": 1 << 18, "BATCH_ORDER": 1 << 19,
+    "TOKEN_MATCH": 1 << 20,
+}
+DAG_NONE, DAG_EXPLICIT, DAG_OCCUPANCY = 0, 1, 2
+
+
+def verdict_names(v: int) -> list:
+    return [k for k, b in VERDICT_BITS.items() if v & b] + (["UNMAPPED"] if v & (1 << 31) else [])
+
+
 EXPORTED_SYMBOLS = [
     "recon_detail_message", "recon_last_cuda_error", "recon_abi_version",
     "recon_ctx_create", "recon_ctx_destroy", "recon_ctx_stream", "recon_ctx_launch_count",
@@ -161,6 +188,7 @@ EXPORTED_SYMBOLS = [
     "recon_assign_1d", "recon_assign_1d_generalized", "recon_solve_1d",
     "recon_solve_1d_batch", "recon_solve_1d_batch_host",
     "recon_batch_moves", "recon_pipeline_batch_run", "recon_pipeline_batch_run_host",
+    "recon_validate_batch_run", "recon_validate_batch_run_host",
 ]
 
 
@@ -250,6 +278,10 @@ class ReconLib:
         for fn in ("recon_pipeline_batch_run", "recon_pipeline_batch_run_host"):
             f = getattr(L, fn)
             f.argtypes = [C.c_void_p, C.POINTER(PipelineBatch)]
+            f.restype = C.c_int
+        for fn in ("recon_validate_batch_run", "recon_validate_batch_run_host"):
+            f = getattr(L, fn)
+            f.argtypes = [C.c_void_p, C.POINTER(ValidateBatch)]
             f.restype = C.c_int
         self._ctx = None
 
@@ -475,6 +507,32 @@ class ReconLib:
                                         C.byref(det))
         self._check(st, det)
         return mb[:moves].copy(), int(nb.value)
+
+    def validate(self, occ, count, width, height, h_prime, path_src, path_dst, path_stride, path_count,
+                 total_displacement=None, displaced=None, dag_mode=DAG_NONE, dag_a=None, dag_b=None,
+                 dag_offset=None, move_batch=None, move_stride=0, batch_count=None, preset=0):
+        """recon_validate_batch_run_host: one recon_verdict bit set per instance."""
+        arrs = {
+            "occ": np.ascontiguousarray(occ, np.uint64),
+            "src": np.ascontiguousarray(path_src, np.int32), "dst": np.ascontiguousarray(path_dst, np.int32),
+            "pc": np.ascontiguousarray(path_count, np.int32),
+            "td": None if total_displacement is None else np.ascontiguousarray(total_displacement, np.int64),
+            "dp": None if displaced is None else np.ascontiguousarray(displaced, np.int32),
+            "ea": None if dag_a is None else np.ascontiguousarray(dag_a, np.int32),
+            "eb": None if dag_b is None else np.ascontiguousarray(dag_b, np.int32),
+            "eo": None if dag_offset is None else np.ascontiguousarray(dag_offset, np.int64),
+            "mb": None if move_batch is None else np.ascontiguousarray(move_batch, np.int32),
+            "nb": None if batch_count is None else np.ascontiguousarray(batch_count, np.int32),
+        }
+        verdict = np.zeros(count, np.uint32)
+        vb = ValidateBatch(_vp(arrs["occ"]).value, count, width, height, h_prime, _vp(arrs["src"]).value,
+                           _vp(arrs["dst"]).value, path_stride, _vp(arrs["pc"]).value, _vp(arrs["td"]).value,
+                           _vp(arrs["dp"]).value, dag_mode, _vp(arrs["ea"]).value, _vp(arrs["eb"]).value,
+                           _vp(arrs["eo"]).value, _vp(arrs["mb"]).value, move_stride, _vp(arrs["nb"]).value,
+                           preset, _vp(verdict).value)
+        st = self.lib.recon_validate_batch_run_host(self.ctx(), C.byref(vb))
+        self._check(st, 0)
+        return verdict
 
     def pipeline_batch(self, solver: str, occ, count, width, height, h_prime, preset, move_stride):
         stride = width * h_prime
