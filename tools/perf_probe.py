@@ -14,7 +14,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2504_06182_b200 import load_native  # noqa: E402
-from paper_2504_06182_b200.abi import ChainBatch, GridBatch, PipelineBatch  # noqa: E402
+from paper_2504_06182_b200.abi import ChainBatch, GridBatch, PipelineBatch, ValidateBatch  # noqa: E402
 from paper_2504_06182_b200.inputs import sample_chains, sample_grids  # noqa: E402
 
 lib = load_native()
@@ -56,7 +56,7 @@ def grid(solver, W, H, hp, k, seed, count):
             "paths_per_grid": P / count, "GBps_alg": (count * W * H / 8 + 8 * P + 32 * count) / mn / 1e6}
 
 
-def pipeline(solver, W, H, hp, k, seed, count, preset, ms_=None):
+def pipeline(solver, W, H, hp, k, seed, count, preset, ms_=None, validate=False):
     occ = torch.from_numpy(sample_grids(seed, count, W, H, k).view(np.int64)).to(dev)
     S = W * hp
     src = torch.empty(count * S, dtype=torch.int32, device=dev)
@@ -74,8 +74,19 @@ def pipeline(solver, W, H, hp, k, seed, count, preset, ms_=None):
     t0 = time.perf_counter()
     mn, avg = timeit(lambda: lib.lib.recon_pipeline_batch_run(lib.ctx(), C.byref(pb)), reps=2)
     D = int(td.sum())
-    return {"ms": mn, "grids_per_s": count / mn * 1e3, "moves_per_grid": D / count,
-            "batches_per_grid": float(bc.float().mean()), "status_nonzero": int((st != 0).sum())}
+    res = {"ms": mn, "grids_per_s": count / mn * 1e3, "moves_per_grid": D / count,
+           "batches_per_grid": float(bc.float().mean()), "status_nonzero": int((st != 0).sum())}
+    if validate:  # on-device validators over the whole batch (failed solves report path_count 0)
+        verdict = torch.empty(count, dtype=torch.int32, device=dev)
+        vb = ValidateBatch(occ.data_ptr(), count, W, H, hp, src.data_ptr(), dst.data_ptr(), S, pc.data_ptr(),
+                           td.data_ptr(), pc.data_ptr(), 2, None, None, None, mb.data_ptr(), ms_, bc.data_ptr(),
+                           preset, verdict.data_ptr())
+        vmn, _ = timeit(lambda: lib.lib.recon_validate_batch_run(lib.ctx(), C.byref(vb)), reps=1)
+        ok = st == 0
+        res["validate_ms"] = vmn
+        res["validate_pass"] = int(((verdict == 0) & ok).sum())
+        res["validate_checked"] = int(ok.sum())
+    return res
 
 
 def chains(n, k, tl, th, seed, count):
@@ -109,6 +120,9 @@ CASES = {
     "c3_pipeline_none": lambda: pipeline("bird", 64, 64, 40, 2662, 0x64000000, 4096, 0),
     "c3_pipeline_coldir": lambda: pipeline("bird", 64, 64, 40, 2662, 0x64000000, 1024, 1),
     "c5_pipeline_4": lambda: pipeline("bird", 512, 512, 307, 157286, 0x51200000, 4, 0, 12_000_000),
+    "c5_pipeline_4_validate": lambda: pipeline("bird", 512, 512, 307, 157286, 0x51200000, 4, 0, 12_000_000, True),
+    "c3_pipeline_validate": lambda: pipeline("bird", 64, 64, 40, 2662, 0x64000000, 4096, 0, None, True),
+    "c4_pipeline_redrec_64_validate": lambda: pipeline("redrec", 256, 256, 153, 39322, 257, 64, 0, 1_500_000, True),
     "c4_pipeline_redrec_64": lambda: pipeline("redrec", 256, 256, 153, 39322, 257, 64, 0, 1_500_000),
     "c5_bird_solve_64": lambda: grid("bird", 512, 512, 307, 157286, 0x51200000, 64),
     "c5_bird_solve_1": lambda: grid("bird", 512, 512, 307, 157286, 0x51200000, 1),
