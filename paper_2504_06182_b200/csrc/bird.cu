@@ -126,7 +126,7 @@ __device__ __forceinline__ void transpose64(uint64_t word, uint32_t &t_lo, uint3
 
 // token word of a slot: bit i = a reservoir token at virtual level V0 + i
 __device__ __forceinline__ uint64_t slot_word(const Geo &g, const uint64_t *dep, int c, int gslot, int nslots,
-                                              int V0, bool top, int *col_out, int *dist_out) {
+                                              int V0, bool top, int *col_out, int *dist_out, uint64_t wmask) {
     *col_out = -1;
     *dist_out = 0;
     if (gslot >= nslots) return 0ull;
@@ -141,38 +141,58 @@ __device__ __forceinline__ uint64_t slot_word(const Geo &g, const uint64_t *dep,
         const uint64_t w = extract64(m, g.wpd, start);
         const int nvalid = g.lo - start;
         if (nvalid <= 0) return 0ull;
-        return nvalid >= 64 ? w : (w & ((1ull << nvalid) - 1ull));
+        return (nvalid >= 64 ? w : (w & ((1ull << nvalid) - 1ull))) & wmask;
     }
     const int start = V0 - dist;  // depth = v - dist > hi
     const uint64_t w = extract64(m, g.wpd, start);
     const int skip = g.hi + 1 - start;
     if (skip >= 64) return 0ull;
-    return skip <= 0 ? w : (w & ~((1ull << skip) - 1ull));
+    return (skip <= 0 ? w : (w & ~((1ull << skip) - 1ull))) & wmask;
 }
 
+
+// Windows cover level indices [win_lo(w), win_hi(w)): the first BIRD_W0
+// levels, then 64 at a time.
+#ifndef BIRD_W0
+#define BIRD_W0 64
+#endif
+__device__ __forceinline__ int win_hi(int w) { return BIRD_W0 + 64 * w; }
+__device__ __forceinline__ int win_lo(int w) { return w == 0 ? 0 : win_hi(w - 1); }
+__device__ __forceinline__ int win_of(int li) { return li < BIRD_W0 ? 0 : (li - BIRD_W0) / 64 + 1; }
 __device__ __forceinline__ int win_V0(const Geo &g, bool top, int w) {
-    return top ? g.lo - 64 * (w + 1) : g.hi + 1 + 64 * w;
+    return top ? g.lo - win_hi(w) : g.hi + 1 + win_lo(w);
 }
-__device__ __forceinline__ int win_nslots(const Geo &g, int w) { return 2 * min(g.W - 1, 64 * (w + 1)) + 1; }
+// slots (columns in group order) that reach levels < lim: distance <= level
+__device__ __forceinline__ int win_nslots(const Geo &g, int lim) { return 2 * min(g.W - 1, lim - 1) + 1; }
 // window bit i -> level index (0 = nearest the band)
-__device__ __forceinline__ int bit_li(bool top, int w, int i) { return top ? 64 * w + 63 - i : 64 * w + i; }
+__device__ __forceinline__ int bit_li(bool top, int w, int i) { return top ? win_hi(w) - 1 - i : win_lo(w) + i; }
+
+// bits of window w holding levels <= lim (all of them: lim >= win_hi - 1)
+__device__ __forceinline__ uint64_t win_mask(bool top, int w, int lim) {
+    const int lo = win_lo(w), n = min(win_hi(w), lim + 1) - lo;  // levels [lo, lo + n)
+    if (n <= 0) return 0ull;
+    const uint64_t low = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
+    const int size = win_hi(w) - lo;
+    return top ? low << (size - n) : low;  // top: bit i <-> level win_hi - 1 - i
+}
 
 // counts one window of one side with the warps [g0, g0 + gn) of the CTA
 __device__ void count_window(const Geo &g, const uint64_t *dep, int c, bool top, int w, int *lvl, int g0, int gn) {
     const int warp = warp_id(), lane = lane_id();
     if (warp < g0 || warp >= g0 + gn) return;
-    const int V0 = win_V0(g, top, w), nslots = win_nslots(g, w), nch = (nslots + 31) / 32;
+    const int V0 = win_V0(g, top, w), nslots = win_nslots(g, win_hi(w)), nch = (nslots + 31) / 32;
+    const uint64_t wmask = win_mask(top, w, win_hi(w));
     int acc_lo = 0, acc_hi = 0;
     for (int ch = warp - g0; ch < nch; ch += gn) {
         int col, dist;
-        const uint64_t word = slot_word(g, dep, c, ch * 32 + lane, nslots, V0, top, &col, &dist);
+        const uint64_t word = slot_word(g, dep, c, ch * 32 + lane, nslots, V0, top, &col, &dist, wmask);
         if (!__any_sync(FULL, word != 0ull)) continue;
         uint32_t t_lo, t_hi;
         transpose64(word, t_lo, t_hi);
         acc_lo += __popc(t_lo);
         acc_hi += __popc(t_hi);
     }
-    if (acc_lo) atomicAdd(&lvl[bit_li(top, w, lane)], acc_lo);
+    if (acc_lo) atomicAdd(&lvl[bit_li(top, w, lane)], acc_lo);  // bits past the window are 0
     if (acc_hi) atomicAdd(&lvl[bit_li(top, w, lane + 32)], acc_hi);
 }
 
@@ -182,13 +202,13 @@ __device__ void count_window(const Geo &g, const uint64_t *dep, int c, bool top,
 __device__ int finish_window(const Geo &g, bool top, int w, int *lvl, int found, int16_t *list, int cap) {
     const int lane = lane_id();
     int run = found;
-    for (int i0 = 0; i0 < 64; i0 += 32) {
-        const int li = 64 * w + i0 + lane;
-        const int cnt = lvl[li];
+    for (int i0 = win_lo(w); i0 < win_hi(w); i0 += 32) {
+        const int li = i0 + lane;
+        const int cnt = li < win_hi(w) ? lvl[li] : 0;
         int tot;
         const int ex = warp_excl_scan(cnt, &tot);
         const int cb = run + ex;
-        lvl[li] = (cnt << 16) | min(cb, 65535);
+        if (li < win_hi(w)) lvl[li] = (cnt << 16) | min(cb, 65535);
         const int v = top ? g.lo - 1 - li : g.hi + 1 + li;
         for (int q = cb + 1; q <= min(cb + cnt, cap); ++q) list[q] = (int16_t)v;
         run += tot;
@@ -204,15 +224,17 @@ __device__ long long emit_window(const Geo &g, uint64_t *dep, int *sigma, int c,
     const int warp = warp_id(), lane = lane_id();
     long long disp = 0;
     if (warp < g0 || warp >= g0 + gn) return 0;
-    const int V0 = win_V0(g, top, w), nslots = win_nslots(g, w), nch = (nslots + 31) / 32;
+    // only levels <= vstar are used; they reach no column farther than vstar
+    const int lim = min(win_hi(w), vstar_li + 1);
+    const int V0 = win_V0(g, top, w), nslots = win_nslots(g, lim), nch = (nslots + 31) / 32;
+    const uint64_t wmask = win_mask(top, w, vstar_li);
     for (int ch = warp - g0; ch < nch; ch += gn) {
         int col, dist;
-        const uint64_t word = slot_word(g, dep, c, ch * 32 + lane, nslots, V0, top, &col, &dist);
+        const uint64_t word = slot_word(g, dep, c, ch * 32 + lane, nslots, V0, top, &col, &dist, wmask);
         uint64_t cleared = 0ull;
         for (uint64_t x = word; x; x &= x - 1) {
             const int i = __ffsll((long long)x) - 1;
             const int li = bit_li(top, w, i);
-            if (li > vstar_li) continue;
             int rank_lt = __popc(T[ch * 64 + i] & lanemask_lt());
             for (int q = 0; q < ch; ++q) rank_lt += __popc(T[q * 64 + i]);
             int jside;
@@ -249,14 +271,16 @@ __device__ long long emit_window(const Geo &g, uint64_t *dep, int *sigma, int c,
 }
 
 // stores the transposed words of one window (all chunks) into T
-__device__ void transpose_window(const Geo &g, const uint64_t *dep, int c, bool top, int w, uint32_t *T, int g0,
-                                 int gn) {
+__device__ void transpose_window(const Geo &g, const uint64_t *dep, int c, bool top, int w, int vstar_li, uint32_t *T,
+                                 int g0, int gn) {
     const int warp = warp_id(), lane = lane_id();
     if (warp < g0 || warp >= g0 + gn) return;
-    const int V0 = win_V0(g, top, w), nslots = win_nslots(g, w), nch = (nslots + 31) / 32;
+    const int lim = min(win_hi(w), vstar_li + 1);
+    const int V0 = win_V0(g, top, w), nslots = win_nslots(g, lim), nch = (nslots + 31) / 32;
+    const uint64_t wmask = win_mask(top, w, vstar_li);
     for (int ch = warp - g0; ch < nch; ch += gn) {
         int col, dist;
-        const uint64_t word = slot_word(g, dep, c, ch * 32 + lane, nslots, V0, top, &col, &dist);
+        const uint64_t word = slot_word(g, dep, c, ch * 32 + lane, nslots, V0, top, &col, &dist, wmask);
         uint32_t t_lo, t_hi;
         transpose64(word, t_lo, t_hi);
         T[ch * 64 + lane] = t_lo;
@@ -333,7 +357,8 @@ __device__ int pooled_event(const Geo &g, uint64_t *dep, int *sigma, int c, int1
         __syncthreads();
         if (warp == 0) {
             const int ft = S[sFoundT], fb = S[sFoundB];
-            const bool exh_t = 64 * S[sWT] >= maxlev_t, exh_b = 64 * S[sWB] >= maxlev_b;
+            const bool exh_t = (S[sWT] ? win_hi(S[sWT] - 1) : 0) >= maxlev_t;
+            const bool exh_b = (S[sWB] ? win_hi(S[sWB] - 1) : 0) >= maxlev_b;
             const int BIG = 1 << 28;
             const int n_ot = exh_t ? ft : BIG, n_ob = exh_b ? fb : BIG;
             const int amin = max(0, holes - n_ob), amax = min(n_ot, holes);
@@ -389,8 +414,8 @@ __device__ int pooled_event(const Geo &g, uint64_t *dep, int *sigma, int c, int1
     const int a = S[sA], b = holes - a;
     if (dbg && threadIdx.x == 0) {
         dbg[0] = holes;
-        dbg[1] = 64 * S[sWT];
-        dbg[2] = 64 * S[sWB];
+        dbg[1] = S[sWT] ? win_hi(S[sWT] - 1) : 0;
+        dbg[2] = S[sWB] ? win_hi(S[sWB] - 1) : 0;
         dbg[3] = S[sFoundT];
         dbg[4] = S[sFoundB];
         dbg[5] = a;
@@ -411,13 +436,13 @@ __device__ int pooled_event(const Geo &g, uint64_t *dep, int *sigma, int c, int1
     }
     // D: emission, top and bottom windows side by side
     long long disp = 0;
-    const int last_t = vt_li >= 0 ? vt_li / 64 : -1, last_b = vb_li >= 0 ? vb_li / 64 : -1;
+    const int last_t = vt_li >= 0 ? win_of(vt_li) : -1, last_b = vb_li >= 0 ? win_of(vb_li) : -1;
     uint32_t *Tt = ps.bal, *Tb = ps.bal + (size_t)g.nchunk * 64;
     for (int w = 0; w <= max(last_t, last_b); ++w) {
         const bool dt = w <= last_t, db = w <= last_b;
         const int half = nw / 2;
-        if (dt) transpose_window(g, dep, c, true, w, Tt, 0, db ? half : nw);
-        if (db) transpose_window(g, dep, c, false, w, Tb, dt ? half : 0, dt ? nw - half : nw);
+        if (dt) transpose_window(g, dep, c, true, w, vt_li, Tt, 0, db ? half : nw);
+        if (db) transpose_window(g, dep, c, false, w, vb_li, Tb, dt ? half : 0, dt ? nw - half : nw);
         __syncthreads();
         if (dt)
             disp += emit_window(g, dep, sigma, c, true, w, a, a, R, n_right, n_left, ps.lvl_t, Tt, vt_li, rt, o, off,
