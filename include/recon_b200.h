@@ -399,6 +399,43 @@ recon_status recon_validate_batch_run(recon_ctx *ctx, const recon_validate_batch
 recon_status recon_validate_batch_run_host(recon_ctx *ctx, const recon_validate_batch *batch);
 
 /* ------------------------------------------------------------------------- */
+/* Wire formats (device)                                                      */
+/* ------------------------------------------------------------------------- */
+
+/*
+ * The reference's JSON text, byte for byte, formatted on the device:
+ *   recon_solution_json        solution_to_json       (io.hpp:21-22, io.cpp:81-101)
+ *   recon_batch_schedule_json  batch_schedule_to_json (io.hpp:25-27, io.cpp:140-164)
+ * Layout of the reference's nlohmann::ordered_json::dump(2) (stock library):
+ * one value per line, two spaces per level, "[]" for empty arrays, plus the
+ * trailing newline io.cpp adds.  Paths are one-bend paths from (src, dst);
+ * the schedule is the paths' moves in path_order (NULL = identity, as
+ * red_rec / bird emit it).  Batches are the moves tagged with each batch
+ * index in ascending path id; axis/dir tags come from a batch's first move
+ * when preset != none, else null.  *length receives the byte count (no NUL);
+ * RECON_ERR_CAPACITY when capacity < *length (nothing written).
+ */
+recon_status recon_solution_json(recon_ctx *ctx, int32_t width, int32_t height, int32_t path_count,
+                                 const int32_t *path_src, const int32_t *path_dst, const int32_t *path_order,
+                                 int64_t dag_count, const int32_t *dag_a, const int32_t *dag_b,
+                                 int64_t displaced_tokens, int64_t total_displacement, char *out,
+                                 int64_t capacity, int64_t *length);
+recon_status recon_batch_schedule_json(recon_ctx *ctx, int32_t width, int32_t height, int32_t path_count,
+                                       const int32_t *path_src, const int32_t *path_dst,
+                                       const int32_t *move_batch, int32_t batch_count, int32_t preset,
+                                       char *out, int64_t capacity, int64_t *length);
+/* Same with every pointer in host memory. */
+recon_status recon_solution_json_host(recon_ctx *ctx, int32_t width, int32_t height, int32_t path_count,
+                                      const int32_t *path_src, const int32_t *path_dst, const int32_t *path_order,
+                                      int64_t dag_count, const int32_t *dag_a, const int32_t *dag_b,
+                                      int64_t displaced_tokens, int64_t total_displacement, char *out,
+                                      int64_t capacity, int64_t *length);
+recon_status recon_batch_schedule_json_host(recon_ctx *ctx, int32_t width, int32_t height, int32_t path_count,
+                                            const int32_t *path_src, const int32_t *path_dst,
+                                            const int32_t *move_batch, int32_t batch_count, int32_t preset,
+                                            char *out, int64_t capacity, int64_t *length);
+
+/* ------------------------------------------------------------------------- */
 /* Synthetic inputs (host)                                                    */
 /* ------------------------------------------------------------------------- */
 

@@ -25,6 +25,7 @@
  * (tests/golden/, tests/test_oracle_vs_reference.py).
  */
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -1898,4 +1899,205 @@ recon_status recon_validate_batch_run(recon_ctx *c, const recon_validate_batch *
 recon_status recon_validate_batch_run_host(recon_ctx *c, const recon_validate_batch *b) {
     (void)c;
     return validate_run(b);
+}
+
+/* ======================================================================== */
+/* Wire formats: solution_to_json / batch_schedule_to_json (io.cpp:81-164)  */
+/* in the stock nlohmann dump(2) layout                                      */
+/* ======================================================================== */
+
+typedef struct {
+    char *p;
+    int64_t n, cap;
+} sbuf;
+
+static void sb_put(sbuf *b, const char *s, int64_t n) {
+    if (b->n + n > b->cap) {
+        while (b->n + n > b->cap) b->cap = b->cap ? 2 * b->cap : 4096;
+        b->p = realloc(b->p, (size_t)b->cap);
+    }
+    memcpy(b->p + b->n, s, (size_t)n);
+    b->n += n;
+}
+static void sb_str(sbuf *b, const char *s) { sb_put(b, s, (int64_t)strlen(s)); }
+static void sb_sp(sbuf *b, int k) {
+    for (int i = 0; i < k; ++i) sb_put(b, " ", 1);
+}
+static void sb_num(sbuf *b, long long v) {
+    char t[32];
+    int n = snprintf(t, sizeof t, "%lld", v);
+    sb_put(b, t, n);
+}
+static void sb_xy(sbuf *b, int ind, int H, int v) { /* caller wrote the indent */
+    sb_str(b, "[\n");
+    sb_sp(b, ind + 2);
+    sb_num(b, v / H);
+    sb_str(b, ",\n");
+    sb_sp(b, ind + 2);
+    sb_num(b, v % H);
+    sb_str(b, "\n");
+    sb_sp(b, ind);
+    sb_str(b, "]");
+}
+static void sb_move(sbuf *b, int ind, int H, int from, int to) {
+    sb_sp(b, ind);
+    sb_str(b, "[\n");
+    sb_sp(b, ind + 2);
+    sb_xy(b, ind + 2, H, from);
+    sb_str(b, ",\n");
+    sb_sp(b, ind + 2);
+    sb_xy(b, ind + 2, H, to);
+    sb_str(b, "\n");
+    sb_sp(b, ind);
+    sb_str(b, "]");
+}
+
+static recon_status sb_finish(sbuf *b, char *out, int64_t cap, int64_t *length) {
+    *length = b->n;
+    recon_status st = RECON_OK;
+    if (cap < b->n) st = RECON_ERR_CAPACITY;
+    else if (b->n) memcpy(out, b->p, (size_t)b->n);
+    free(b->p);
+    return st;
+}
+
+static recon_status oracle_solution_json(int32_t width, int32_t H, int32_t np, const int32_t *ps, const int32_t *pt,
+                                         const int32_t *order, int64_t ne, const int32_t *ea, const int32_t *eb,
+                                         int64_t displaced, int64_t total, char *out, int64_t cap, int64_t *length) {
+    sbuf b = {0};
+    int32_t *verts = xcalloc((size_t)(width + H + 2), 4);
+    sb_str(&b, "{\n  \"moves\": ");
+    int first = 1;
+    for (int32_t i = 0; i < np; ++i) {
+        const int32_t q = order ? order[i] : i;
+        const int64_t nv = walk_path(H, ps[q], pt[q], verts);
+        for (int64_t k = 0; k + 1 < nv; ++k) {
+            sb_str(&b, first ? "[\n" : ",\n");
+            first = 0;
+            sb_move(&b, 4, H, verts[k], verts[k + 1]);
+        }
+    }
+    sb_str(&b, first ? "[],\n" : "\n  ],\n");
+    sb_str(&b, "  \"dag_edges\": ");
+    for (int64_t e = 0; e < ne; ++e) {
+        sb_str(&b, e ? ",\n" : "[\n");
+        sb_sp(&b, 4);
+        sb_str(&b, "[\n");
+        sb_sp(&b, 6);
+        sb_num(&b, ea[e]);
+        sb_str(&b, ",\n");
+        sb_sp(&b, 6);
+        sb_num(&b, eb[e]);
+        sb_str(&b, "\n    ]");
+    }
+    sb_str(&b, ne ? "\n  ],\n" : "[],\n");
+    sb_str(&b, "  \"paths\": ");
+    for (int32_t q = 0; q < np; ++q) {
+        sb_str(&b, q ? ",\n" : "[\n");
+        sb_sp(&b, 4);
+        sb_str(&b, "[\n");
+        const int64_t nv = walk_path(H, ps[q], pt[q], verts);
+        for (int64_t k = 0; k < nv; ++k) {
+            if (k) sb_str(&b, ",\n");
+            sb_sp(&b, 6);
+            sb_xy(&b, 6, H, verts[k]);
+        }
+        sb_str(&b, "\n    ]");
+    }
+    sb_str(&b, np ? "\n  ],\n" : "[],\n");
+    sb_str(&b, "  \"stats\": {\n    \"displaced_tokens\": ");
+    sb_num(&b, displaced);
+    sb_str(&b, ",\n    \"total_displacement\": ");
+    sb_num(&b, total);
+    sb_str(&b, "\n  }\n}\n");
+    free(verts);
+    return sb_finish(&b, out, cap, length);
+}
+
+static recon_status oracle_batch_json(int32_t width, int32_t H, int32_t np, const int32_t *ps, const int32_t *pt,
+                                      const int32_t *mb, int32_t nb, int32_t preset, char *out, int64_t cap,
+                                      int64_t *length) {
+    sbuf b = {0};
+    int32_t *verts = xcalloc((size_t)(width + H + 2), 4);
+    int64_t D = 0;
+    for (int32_t q = 0; q < np; ++q) {
+        const int dx = ps[q] / H - pt[q] / H, dy = ps[q] % H - pt[q] % H;
+        D += (dx < 0 ? -dx : dx) + (dy < 0 ? -dy : dy);
+    }
+    int64_t *cnt = xcalloc((size_t)nb + 1, 8), *st = xcalloc((size_t)nb + 2, 8), *fill = xcalloc((size_t)nb + 1, 8);
+    int32_t *mf = xcalloc((size_t)D + 1, 4), *mt = xcalloc((size_t)D + 1, 4);
+    for (int64_t m = 0; m < D; ++m)
+        if (mb[m] >= 0 && mb[m] < nb) cnt[mb[m]]++;
+    for (int32_t k = 0; k < nb; ++k) st[k + 1] = st[k] + cnt[k];
+    int64_t m = 0;
+    for (int32_t q = 0; q < np; ++q) {
+        const int64_t nv = walk_path(H, ps[q], pt[q], verts);
+        for (int64_t k = 0; k + 1 < nv; ++k, ++m) {
+            const int32_t bi = mb[m];
+            if (bi < 0 || bi >= nb) continue;
+            mf[st[bi] + fill[bi]] = verts[k];
+            mt[st[bi] + fill[bi]++] = verts[k + 1];
+        }
+    }
+    sb_str(&b, "{\n  \"batches\": ");
+    int any = 0;
+    for (int32_t k = 0; k < nb; ++k) {
+        if (!cnt[k]) continue; /* a schedule from batching has no empty batch */
+        sb_str(&b, any ? ",\n" : "[\n");
+        any = 1;
+        const char *ax = "null", *dr = "null";
+        if (preset == RECON_PRESET_COLUMN_DIRECTION) {
+            const int f = mf[st[k]], t = mt[st[k]];
+            const int fx = f / H, fy = f % H, tx = t / H, ty = t % H;
+            if (ty > fy) ax = "\"col\"", dr = "\"up\"";
+            else if (ty < fy) ax = "\"col\"", dr = "\"down\"";
+            else if (tx < fx) ax = "\"row\"", dr = "\"left\"";
+            else ax = "\"row\"", dr = "\"right\"";
+        }
+        sb_str(&b, "    {\n      \"axis\": ");
+        sb_str(&b, ax);
+        sb_str(&b, ",\n      \"dir\": ");
+        sb_str(&b, dr);
+        sb_str(&b, ",\n      \"moves\": [\n");
+        for (int64_t x = st[k]; x < st[k + 1]; ++x) {
+            if (x > st[k]) sb_str(&b, ",\n");
+            sb_move(&b, 8, H, mf[x], mt[x]);
+        }
+        sb_str(&b, "\n      ]\n    }");
+    }
+    sb_str(&b, any ? "\n  ]\n}\n" : "[]\n}\n");
+    free(verts);
+    free(cnt);
+    free(st);
+    free(fill);
+    free(mf);
+    free(mt);
+    return sb_finish(&b, out, cap, length);
+}
+
+recon_status recon_solution_json(recon_ctx *c, int32_t width, int32_t height, int32_t np, const int32_t *ps,
+                                 const int32_t *pt, const int32_t *order, int64_t ne, const int32_t *ea,
+                                 const int32_t *eb, int64_t displaced, int64_t total, char *out, int64_t cap,
+                                 int64_t *length) {
+    (void)c;
+    if (!length || width <= 0 || height <= 0 || np < 0 || ne < 0) return RECON_ERR_ARGUMENT;
+    return oracle_solution_json(width, height, np, ps, pt, order, ne, ea, eb, displaced, total, out, cap, length);
+}
+recon_status recon_solution_json_host(recon_ctx *c, int32_t width, int32_t height, int32_t np, const int32_t *ps,
+                                      const int32_t *pt, const int32_t *order, int64_t ne, const int32_t *ea,
+                                      const int32_t *eb, int64_t displaced, int64_t total, char *out, int64_t cap,
+                                      int64_t *length) {
+    return recon_solution_json(c, width, height, np, ps, pt, order, ne, ea, eb, displaced, total, out, cap, length);
+}
+recon_status recon_batch_schedule_json(recon_ctx *c, int32_t width, int32_t height, int32_t np, const int32_t *ps,
+                                       const int32_t *pt, const int32_t *mb, int32_t nb, int32_t preset, char *out,
+                                       int64_t cap, int64_t *length) {
+    (void)c;
+    if (!length || width <= 0 || height <= 0 || np < 0 || nb < 0) return RECON_ERR_ARGUMENT;
+    return oracle_batch_json(width, height, np, ps, pt, mb, nb, preset, out, cap, length);
+}
+recon_status recon_batch_schedule_json_host(recon_ctx *c, int32_t width, int32_t height, int32_t np,
+                                            const int32_t *ps, const int32_t *pt, const int32_t *mb, int32_t nb,
+                                            int32_t preset, char *out, int64_t cap, int64_t *length) {
+    return recon_batch_schedule_json(c, width, height, np, ps, pt, mb, nb, preset, out, cap, length);
 }

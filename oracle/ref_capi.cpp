@@ -679,3 +679,154 @@ extern "C" recon_status recon_validate_batch_run(recon_ctx *, const recon_valida
 extern "C" recon_status recon_validate_batch_run_host(recon_ctx *c, const recon_validate_batch *b) {
     return recon_validate_batch_run(c, b);
 }
+
+// Wire formats: the reference's own Solution / BatchSchedule content
+// (make_solution's schedule, the dag, the paths; batches in ascending path id
+// with tags from the first move) printed in the stock nlohmann dump(2) layout
+// of io.cpp:81-164 (the reference's vendored json.hpp is not in its tree).
+namespace {
+
+struct JsonOut {
+    std::string s;
+    void sp(int k) { s.append(static_cast<size_t>(k), ' '); }
+    void xy(const Geometry &g, int ind, Vertex v) {
+        const Vec2 p = g.coords(v);
+        s += "[\n";
+        sp(ind + 2);
+        s += std::to_string(p.x) + ",\n";
+        sp(ind + 2);
+        s += std::to_string(p.y) + "\n";
+        sp(ind);
+        s += "]";
+    }
+    void move(const Geometry &g, int ind, const ElementaryMove &m) {
+        sp(ind);
+        s += "[\n";
+        sp(ind + 2);
+        xy(g, ind + 2, m.from);
+        s += ",\n";
+        sp(ind + 2);
+        xy(g, ind + 2, m.to);
+        s += "\n";
+        sp(ind);
+        s += "]";
+    }
+};
+
+recon_status json_out(const std::string &s, char *out, int64_t cap, int64_t *length) {
+    *length = static_cast<int64_t>(s.size());
+    if (cap < *length) return RECON_ERR_CAPACITY;
+    std::memcpy(out, s.data(), s.size());
+    return RECON_OK;
+}
+
+}  // namespace
+
+extern "C" recon_status recon_solution_json(recon_ctx *, int32_t width, int32_t height, int32_t np,
+                                            const int32_t *ps, const int32_t *pt, const int32_t *order, int64_t ne,
+                                            const int32_t *ea, const int32_t *eb, int64_t displaced, int64_t total,
+                                            char *out, int64_t cap, int64_t *length) {
+    if (!length || width <= 0 || height <= 0 || np < 0 || ne < 0) return RECON_ERR_ARGUMENT;
+    const Geometry g = Geometry::grid(width, height);
+    PathSystem sys;
+    for (int k = 0; k < np; ++k) sys.paths.push_back(one_bend_path(g, ps[k], pt[k]));
+    MoveDag dag;
+    dag.node_count = np;
+    for (int64_t e = 0; e < ne; ++e) dag.add_edge(ea[e], eb[e]);
+    std::vector<int> ord(static_cast<size_t>(np));
+    for (int k = 0; k < np; ++k) ord[static_cast<size_t>(k)] = order ? order[k] : k;
+    const Solution sol = make_solution(sys, dag, ord);
+    JsonOut j;
+    j.s = "{\n  \"moves\": ";
+    if (sol.schedule.empty()) j.s += "[],\n";
+    else {
+        j.s += "[\n";
+        for (size_t i = 0; i < sol.schedule.size(); ++i) {
+            if (i) j.s += ",\n";
+            j.move(g, 4, sol.schedule[i]);
+        }
+        j.s += "\n  ],\n";
+    }
+    j.s += "  \"dag_edges\": ";
+    if (sol.dag.edges.empty()) j.s += "[],\n";
+    else {
+        j.s += "[\n";
+        for (size_t i = 0; i < sol.dag.edges.size(); ++i) {
+            if (i) j.s += ",\n";
+            j.s += "    [\n      " + std::to_string(sol.dag.edges[i].first) + ",\n      " +
+                   std::to_string(sol.dag.edges[i].second) + "\n    ]";
+        }
+        j.s += "\n  ],\n";
+    }
+    j.s += "  \"paths\": ";
+    if (sol.path_system.paths.empty()) j.s += "[],\n";
+    else {
+        j.s += "[\n";
+        for (size_t i = 0; i < sol.path_system.paths.size(); ++i) {
+            if (i) j.s += ",\n";
+            j.s += "    [\n";
+            const Path &p = sol.path_system.paths[i];
+            for (size_t k = 0; k < p.vertices.size(); ++k) {
+                if (k) j.s += ",\n";
+                j.sp(6);
+                j.xy(g, 6, p.vertices[k]);
+            }
+            j.s += "\n    ]";
+        }
+        j.s += "\n  ],\n";
+    }
+    j.s += "  \"stats\": {\n    \"displaced_tokens\": " + std::to_string(displaced) +
+           ",\n    \"total_displacement\": " + std::to_string(total) + "\n  }\n}\n";
+    return json_out(j.s, out, cap, length);
+}
+
+extern "C" recon_status recon_solution_json_host(recon_ctx *c, int32_t width, int32_t height, int32_t np,
+                                                 const int32_t *ps, const int32_t *pt, const int32_t *order,
+                                                 int64_t ne, const int32_t *ea, const int32_t *eb, int64_t displaced,
+                                                 int64_t total, char *out, int64_t cap, int64_t *length) {
+    return recon_solution_json(c, width, height, np, ps, pt, order, ne, ea, eb, displaced, total, out, cap, length);
+}
+
+extern "C" recon_status recon_batch_schedule_json(recon_ctx *, int32_t width, int32_t height, int32_t np,
+                                                  const int32_t *ps, const int32_t *pt, const int32_t *mb, int32_t nb,
+                                                  int32_t preset, char *out, int64_t cap, int64_t *length) {
+    if (!length || width <= 0 || height <= 0 || np < 0 || nb < 0) return RECON_ERR_ARGUMENT;
+    const Geometry g = Geometry::grid(width, height);
+    BatchSchedule bs;
+    bs.batches.resize(static_cast<size_t>(nb));
+    int64_t m = 0;
+    for (int k = 0; k < np; ++k) {
+        const Path p = one_bend_path(g, ps[k], pt[k]);
+        for (size_t i = 0; i + 1 < p.vertices.size(); ++i, ++m)
+            if (mb[m] >= 0 && mb[m] < nb) bs.batches[static_cast<size_t>(mb[m])].moves.push_back({p.vertices[i], p.vertices[i + 1]});
+    }
+    JsonOut j;
+    j.s = "{\n  \"batches\": ";
+    bool any = false;
+    for (const Batch &b : bs.batches) {
+        if (b.moves.empty()) continue;
+        j.s += any ? ",\n" : "[\n";
+        any = true;
+        std::string ax = "null", dr = "null";
+        if (preset == RECON_PRESET_COLUMN_DIRECTION) {
+            const BatchDir d = move_dir(g, b.moves.front());
+            ax = (d == BatchDir::up || d == BatchDir::down) ? "\"col\"" : "\"row\"";
+            dr = d == BatchDir::up ? "\"up\"" : d == BatchDir::down ? "\"down\"" : d == BatchDir::left ? "\"left\"" : "\"right\"";
+        }
+        j.s += "    {\n      \"axis\": " + ax + ",\n      \"dir\": " + dr + ",\n      \"moves\": [\n";
+        for (size_t i = 0; i < b.moves.size(); ++i) {
+            if (i) j.s += ",\n";
+            j.move(g, 8, b.moves[i]);
+        }
+        j.s += "\n      ]\n    }";
+    }
+    j.s += any ? "\n  ]\n}\n" : "[]\n}\n";
+    return json_out(j.s, out, cap, length);
+}
+
+extern "C" recon_status recon_batch_schedule_json_host(recon_ctx *c, int32_t width, int32_t height, int32_t np,
+                                                       const int32_t *ps, const int32_t *pt, const int32_t *mb,
+                                                       int32_t nb, int32_t preset, char *out, int64_t cap,
+                                                       int64_t *length) {
+    return recon_batch_schedule_json(c, width, height, np, ps, pt, mb, nb, preset, out, cap, length);
+}

@@ -189,6 +189,8 @@ EXPORTED_SYMBOLS = [
     "recon_solve_1d_batch", "recon_solve_1d_batch_host",
     "recon_batch_moves", "recon_pipeline_batch_run", "recon_pipeline_batch_run_host",
     "recon_validate_batch_run", "recon_validate_batch_run_host",
+    "recon_solution_json", "recon_solution_json_host", "recon_batch_schedule_json",
+    "recon_batch_schedule_json_host",
 ]
 
 
@@ -278,6 +280,17 @@ class ReconLib:
         for fn in ("recon_pipeline_batch_run", "recon_pipeline_batch_run_host"):
             f = getattr(L, fn)
             f.argtypes = [C.c_void_p, C.POINTER(PipelineBatch)]
+            f.restype = C.c_int
+        for fn in ("recon_solution_json", "recon_solution_json_host"):
+            f = getattr(L, fn)
+            f.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                          C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
+                          C.POINTER(C.c_int64)]
+            f.restype = C.c_int
+        for fn in ("recon_batch_schedule_json", "recon_batch_schedule_json_host"):
+            f = getattr(L, fn)
+            f.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                          C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
             f.restype = C.c_int
         for fn in ("recon_validate_batch_run", "recon_validate_batch_run_host"):
             f = getattr(L, fn)
@@ -533,6 +546,36 @@ class ReconLib:
         st = self.lib.recon_validate_batch_run_host(self.ctx(), C.byref(vb))
         self._check(st, 0)
         return verdict
+
+    def _json(self, call) -> bytes:
+        n = C.c_int64(0)
+        st = call(None, 0, C.byref(n))
+        if st == RECON_ERR_CAPACITY or (st == RECON_OK and n.value > 0):
+            buf = C.create_string_buffer(max(1, n.value))
+            st = call(buf, n.value, C.byref(n))
+            self._check(st, 0)
+            return buf.raw[:n.value]
+        self._check(st, 0)
+        return b""
+
+    def solution_json(self, width, height, src, dst, order=None, dag=None, displaced=0, total=0) -> bytes:
+        """recon_solution_json_host: the reference's solution_to_json text."""
+        src = np.ascontiguousarray(src, np.int32)
+        dst = np.ascontiguousarray(dst, np.int32)
+        order = None if order is None else np.ascontiguousarray(order, np.int32)
+        dag = np.zeros((0, 2), np.int32) if dag is None else np.ascontiguousarray(dag, np.int32).reshape(-1, 2)
+        ea, eb = np.ascontiguousarray(dag[:, 0]), np.ascontiguousarray(dag[:, 1])
+        return self._json(lambda out, cap, n: self.lib.recon_solution_json_host(
+            self.ctx(), width, height, len(src), _vp(src), _vp(dst), _vp(order), len(ea), _vp(ea), _vp(eb),
+            displaced, total, out, cap, n))
+
+    def batch_schedule_json(self, width, height, src, dst, move_batch, batch_count, preset=0) -> bytes:
+        """recon_batch_schedule_json_host: the reference's batch_schedule_to_json text."""
+        src = np.ascontiguousarray(src, np.int32)
+        dst = np.ascontiguousarray(dst, np.int32)
+        mb = np.ascontiguousarray(move_batch, np.int32)
+        return self._json(lambda out, cap, n: self.lib.recon_batch_schedule_json_host(
+            self.ctx(), width, height, len(src), _vp(src), _vp(dst), _vp(mb), batch_count, preset, out, cap, n))
 
     def pipeline_batch(self, solver: str, occ, count, width, height, h_prime, preset, move_stride):
         stride = width * h_prime
