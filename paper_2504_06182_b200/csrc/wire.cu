@@ -247,10 +247,43 @@ __global__ void k_measure(int sec, Sec s, int64_t n, int64_t *len) {
     }
 }
 
-__global__ void k_write(int sec, Sec s, int64_t n, const int64_t *off, char *out) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-        Writer<true> w{out + off[e]};
-        item(sec, s, w, e);
+// Writes 32 consecutive items per warp: each lane formats its item into the
+// warp's shared-memory buffer (co-aligned with the destination), then the
+// warp stores the group's bytes with 16-byte vector stores.  A group longer
+// than the buffer is written item by item.
+constexpr int kWriteWarps = 8, kWarpBuf = 8192;
+
+__global__ void __launch_bounds__(kWriteWarps * 32) k_write(int sec, Sec s, int64_t n, const int64_t *off, char *out) {
+    extern __shared__ __align__(16) char wbuf[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    char *buf = wbuf + (size_t)warp * (kWarpBuf + 16);
+    const int64_t ngroups = (n + 31) / 32;
+    for (int64_t g = (int64_t)blockIdx.x * kWriteWarps + warp; g < ngroups; g += (int64_t)gridDim.x * kWriteWarps) {
+        const int64_t e0 = g * 32, e1 = min(n, e0 + 32), e = e0 + lane;
+        const int64_t base = off[e0], tot = off[e1] - base;
+        char *dst = out + base;
+        if (tot > kWarpBuf) {
+            if (e < e1) {
+                Writer<true> w{out + off[e]};
+                item(sec, s, w, e);
+            }
+            continue;
+        }
+        const int mis = (int)((uintptr_t)dst & 15);
+        char *b = buf + mis;  // b[i] goes to dst[i]; buf + 16 and dst + (16 - mis) share alignment
+        if (e < e1) {
+            Writer<true> w{b + (off[e] - base)};
+            item(sec, s, w, e);
+        }
+        __syncwarp();
+        const int head = (int)min(tot, (int64_t)((16 - mis) & 15));
+        if (lane < head) dst[lane] = b[lane];
+        const int64_t nvec = (tot - head) / 16;
+        const uint4 *src4 = (const uint4 *)(b + head);
+        uint4 *dst4 = (uint4 *)(dst + head);
+        for (int64_t j = lane; j < nvec; j += 32) dst4[j] = src4[j];
+        for (int64_t i = head + nvec * 16 + lane; i < tot; i += 32) dst[i] = b[i];
+        __syncwarp();
     }
 }
 
@@ -331,7 +364,12 @@ recon_status assemble(Ctx *c, const std::vector<Piece> &pieces, const Sec &s, ch
             continue;
         }
         if (!p.n) continue;
-        k_write<<<blocks_for(p.n, c->sms), 256, 0, c->stream>>>(p.sec, s, p.n, len + seg[i], dout + start[i]);
+        const int smem = kWriteWarps * (kWarpBuf + 16);
+        CK(cudaFuncSetAttribute(k_write, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+        const int64_t groups = (p.n + 31) / 32;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((groups + kWriteWarps - 1) / kWriteWarps,
+                                                                       (int64_t)c->sms * 3));
+        k_write<<<grid, kWriteWarps * 32, smem, c->stream>>>(p.sec, s, p.n, len + seg[i], dout + start[i]);
         c->launches += 1;
     }
     CK(cudaGetLastError(), "json kernels");

@@ -106,7 +106,45 @@ def chains(n, k, tl, th, seed, count):
             "frac_hbm": bytes_ / mn / 1e6 / 6465.8}
 
 
+def json_case(solver, W, H, hp, k, seed, preset, ms_):
+    """solution + batch-schedule JSON of one pipeline instance, formatted on the device."""
+    occ = torch.from_numpy(sample_grids(seed, 1, W, H, k).view(np.int64)).to(dev)
+    S = W * hp
+    src = torch.empty(S, dtype=torch.int32, device=dev)
+    dst = torch.empty_like(src)
+    pc = torch.empty(1, dtype=torch.int32, device=dev)
+    td = torch.empty(1, dtype=torch.int64, device=dev)
+    st = torch.empty(1, dtype=torch.int32, device=dev)
+    de = torch.empty(1, dtype=torch.int32, device=dev)
+    mb = torch.empty(ms_, dtype=torch.int32, device=dev)
+    bc = torch.empty(1, dtype=torch.int32, device=dev)
+    g = GridBatch(occ.data_ptr(), 1, W, H, hp, src.data_ptr(), dst.data_ptr(), None, pc.data_ptr(),
+                  td.data_ptr(), st.data_ptr(), de.data_ptr(), None)
+    pb = PipelineBatch(g, 1 if solver == "bird" else 0, preset, ms_, mb.data_ptr(), bc.data_ptr())
+    assert lib.lib.recon_pipeline_batch_run(lib.ctx(), C.byref(pb)) == 0
+    torch.cuda.synchronize()
+    P, D, nb = int(pc.item()), int(td.item()), int(bc.item())
+    n = C.c_int64(0)
+    lib.lib.recon_solution_json(lib.ctx(), W, H, P, src.data_ptr(), dst.data_ptr(), None, 0, None, None, P, D,
+                                None, 0, C.byref(n))
+    out = torch.empty(n.value, dtype=torch.uint8, device=dev)
+    f = lambda: lib.lib.recon_solution_json(lib.ctx(), W, H, P, src.data_ptr(), dst.data_ptr(), None, 0, None, None,
+                                            P, D, out.data_ptr(), n.value, C.byref(n))
+    ms1, _ = timeit(f)
+    nb_ = C.c_int64(0)
+    lib.lib.recon_batch_schedule_json(lib.ctx(), W, H, P, src.data_ptr(), dst.data_ptr(), mb.data_ptr(), nb, preset,
+                                      None, 0, C.byref(nb_))
+    out2 = torch.empty(nb_.value, dtype=torch.uint8, device=dev)
+    f2 = lambda: lib.lib.recon_batch_schedule_json(lib.ctx(), W, H, P, src.data_ptr(), dst.data_ptr(), mb.data_ptr(),
+                                                   nb, preset, out2.data_ptr(), nb_.value, C.byref(nb_))
+    ms2, _ = timeit(f2)
+    return {"solution_json_MB": n.value / 1e6, "solution_json_ms": ms1, "solution_json_GBps": n.value / ms1 / 1e6,
+            "batch_json_MB": nb_.value / 1e6, "batch_json_ms": ms2, "batch_json_GBps": nb_.value / ms2 / 1e6}
+
+
 CASES = {
+    "c4_json": lambda: json_case("redrec", 256, 256, 153, 39322, 257, 0, 1_500_000),
+    "c5_json": lambda: json_case("bird", 512, 512, 307, 157286, 0x51200000, 0, 12_000_000),
     "c1_redrec": lambda: grid("redrec", 32, 32, 16, 614, 1, 4096),
     "c1_redrec_1": lambda: grid("redrec", 32, 32, 16, 614, 1, 1),
     "c4_redrec_h128_1": lambda: grid("redrec", 256, 256, 128, 39322, 256, 1),
