@@ -436,6 +436,60 @@ recon_status recon_batch_schedule_json_host(recon_ctx *ctx, int32_t width, int32
                                             char *out, int64_t capacity, int64_t *length);
 
 /* ------------------------------------------------------------------------- */
+/* Multi-cycle loss simulation (SPEC.md module `sim`; no reference code)      */
+/* ------------------------------------------------------------------------- */
+
+/*
+ * Monte Carlo trials of repeated reconfiguration under atom loss (SPEC.md
+ * [MODULE] sim: LossModel, run_trial, estimate_success).  Trial i starts from
+ * occ[i] (sample_initial: recon_sample_occ gives the reference's Rng draws)
+ * and repeats cycles: solve (red-rec or bird), optionally batch, execute the
+ * schedule with per-operation survival draws, let every atom decay over the
+ * cycle's elapsed time, re-measure.  A trial succeeds when the centered band
+ * is full, and fails when fewer than W*h' atoms remain, when the solver or the
+ * batching fails, or after max_cycles cycles.
+ *
+ * Execution model (SPEC design decisions):
+ *  - unbatched: each displaced token is one EDI cycle: extract (p_alpha), its
+ *    k moves (p_nu each), implant (p_alpha); elapsed 2 t_alpha + k t_nu;
+ *  - batched: an EDI cycle is a maximal run of consecutive batches moving the
+ *    same token set; each token of the run is extracted once and implanted
+ *    once per run; elapsed per run 2 t_alpha + (#batches) t_nu;
+ *  - a token lost mid-path vanishes and skips its remaining operations;
+ *    N_nu / N_alpha count the operations performed;
+ *  - NB_nu / NB_alpha count the scheduled displacement / transfer sequences
+ *    (batched: batches / runs; unbatched: moves / displaced tokens);
+ *  - after the moves every atom survives with exp(-(elapsed + t_meas) / tau)
+ *    (tau <= 0: no decay).
+ * Draws: include/recon_sim_rng.h (counter-based, order-independent).
+ */
+typedef struct recon_loss_model {
+    double p_nu, p_alpha; /* per-displacement / per-transfer survival */
+    double tau;           /* trapping lifetime (s); <= 0 disables decay */
+    double t_nu, t_alpha, t_meas;
+} recon_loss_model;
+
+typedef struct recon_sim_batch {
+    const uint64_t *occ;       /* initial configurations, count * width * wpc words (host) */
+    int32_t count;             /* trials */
+    int32_t width, height, h_prime;
+    uint64_t seed_base;        /* trial i draws with seed_base + i */
+    int32_t solver;            /* 0 = red-rec, 1 = bird */
+    int32_t batching;          /* 0 = off, 1 = on */
+    int32_t preset;            /* recon_preset when batching */
+    int32_t max_cycles;
+    recon_loss_model loss;
+    /* outputs, [count] each, host memory */
+    int32_t *success;          /* 1 = target reached */
+    int32_t *cycles;           /* reconfiguration cycles run */
+    int32_t *status;           /* RECON_OK, or the solver / batching status that ended the trial */
+    int64_t *n_nu, *n_alpha, *nb_nu, *nb_alpha, *atoms_lost;
+    double *elapsed;           /* model time (s) */
+} recon_sim_batch;
+
+recon_status recon_sim_run_host(recon_ctx *ctx, const recon_sim_batch *batch);
+
+/* ------------------------------------------------------------------------- */
 /* Synthetic inputs (host)                                                    */
 /* ------------------------------------------------------------------------- */
 

@@ -29,7 +29,10 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <math.h>
+
 #include "recon_b200.h"
+#include "recon_sim_rng.h"
 
 struct recon_ctx {
     int device;
@@ -2100,4 +2103,24 @@ recon_status recon_batch_schedule_json_host(recon_ctx *c, int32_t width, int32_t
                                             const int32_t *ps, const int32_t *pt, const int32_t *mb, int32_t nb,
                                             int32_t preset, char *out, int64_t cap, int64_t *length) {
     return recon_batch_schedule_json(c, width, height, np, ps, pt, mb, nb, preset, out, cap, length);
+}
+
+/* ======================================================================== */
+/* Loss simulation: oracle/sim_common.h with this library's own solvers     */
+/* ======================================================================== */
+
+static recon_status oracle_sim_solve(int batching, int solver, int preset, recon_grid_batch *g, int64_t ms,
+                                     int32_t *mb, int32_t *nb) {
+    if (batching) {
+        recon_pipeline_batch pb = {*g, solver, preset, ms, mb, nb};
+        return recon_pipeline_batch_run_host(NULL, &pb);
+    }
+    return solver == 1 ? recon_bird_solve_batch_host(NULL, g) : recon_redrec_solve_batch_host(NULL, g);
+}
+
+#include "sim_common.h"
+
+recon_status recon_sim_run_host(recon_ctx *c, const recon_sim_batch *b) {
+    (void)c;
+    return sim_run_checked(b, oracle_sim_solve);
 }

@@ -830,3 +830,30 @@ extern "C" recon_status recon_batch_schedule_json_host(recon_ctx *c, int32_t wid
                                                        int64_t *length) {
     return recon_batch_schedule_json(c, width, height, np, ps, pt, mb, nb, preset, out, cap, length);
 }
+
+// Loss simulation (SPEC.md [MODULE] sim; no reference code): the shared
+// sequential restatement (oracle/sim_common.h) driving the compiled
+// reference's own red_rec / bird / batch_moves.
+#include "sim_common.h"
+
+namespace {
+
+recon_status ref_sim_solve(int batching, int solver, int preset, recon_grid_batch *g, int64_t ms, int32_t *mb,
+                           int32_t *nb) {
+    if (batching) {
+        recon_pipeline_batch pb{*g, solver, preset, ms, mb, nb};
+        return recon_pipeline_batch_run(nullptr, &pb);
+    }
+    return solver == 1 ? recon_bird_solve_batch(nullptr, g) : recon_redrec_solve_batch(nullptr, g);
+}
+
+}  // namespace
+
+extern "C" recon_status recon_sim_run_host(recon_ctx *, const recon_sim_batch *b) {
+    if (!b || !b->occ || !b->success || !b->cycles || !b->status || !b->n_nu || !b->n_alpha || !b->nb_nu ||
+        !b->nb_alpha || !b->atoms_lost || !b->elapsed || b->width <= 0 || b->height <= 0 || b->h_prime <= 0 ||
+        b->h_prime >= b->height)
+        return RECON_ERR_ARGUMENT;
+    parallel_for(b->count, [&](int i) { simc_trial(b, i, ref_sim_solve); });
+    return RECON_OK;
+}

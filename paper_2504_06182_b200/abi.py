@@ -162,6 +162,22 @@ class ValidateBatch(C.Structure):
     ]
 
 
+class LossModel(C.Structure):
+    _fields_ = [("p_nu", C.c_double), ("p_alpha", C.c_double), ("tau", C.c_double), ("t_nu", C.c_double),
+                ("t_alpha", C.c_double), ("t_meas", C.c_double)]
+
+
+class SimBatch(C.Structure):
+    _fields_ = [
+        ("occ", C.c_void_p), ("count", C.c_int32), ("width", C.c_int32), ("height", C.c_int32),
+        ("h_prime", C.c_int32), ("seed_base", C.c_uint64), ("solver", C.c_int32), ("batching", C.c_int32),
+        ("preset", C.c_int32), ("max_cycles", C.c_int32), ("loss", LossModel),
+        ("success", C.c_void_p), ("cycles", C.c_void_p), ("status", C.c_void_p), ("n_nu", C.c_void_p),
+        ("n_alpha", C.c_void_p), ("nb_nu", C.c_void_p), ("nb_alpha", C.c_void_p), ("atoms_lost", C.c_void_p),
+        ("elapsed", C.c_void_p),
+    ]
+
+
 # recon_verdict bits (include/recon_b200.h)
 VERDICT_BITS = {
     "PATH_BOUNDS": 1 << 0, "SHARED_SOURCE": 1 << 1, "SHARED_TARGET": 1 << 2, "DAG_CYCLE": 1 << 3,
@@ -191,6 +207,7 @@ EXPORTED_SYMBOLS = [
     "recon_validate_batch_run", "recon_validate_batch_run_host",
     "recon_solution_json", "recon_solution_json_host", "recon_batch_schedule_json",
     "recon_batch_schedule_json_host",
+    "recon_sim_run_host",
 ]
 
 
@@ -292,6 +309,8 @@ class ReconLib:
             f.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                           C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
             f.restype = C.c_int
+        L.recon_sim_run_host.argtypes = [C.c_void_p, C.POINTER(SimBatch)]
+        L.recon_sim_run_host.restype = C.c_int
         for fn in ("recon_validate_batch_run", "recon_validate_batch_run_host"):
             f = getattr(L, fn)
             f.argtypes = [C.c_void_p, C.POINTER(ValidateBatch)]
@@ -576,6 +595,21 @@ class ReconLib:
         mb = np.ascontiguousarray(move_batch, np.int32)
         return self._json(lambda out, cap, n: self.lib.recon_batch_schedule_json_host(
             self.ctx(), width, height, len(src), _vp(src), _vp(dst), _vp(mb), batch_count, preset, out, cap, n))
+
+    def sim_run(self, occ, count, width, height, h_prime, seed_base, solver="redrec", batching=False, preset=0,
+                max_cycles=20, p_nu=0.985, p_alpha=0.985, tau=0.0, t_nu=100e-6, t_alpha=300e-6, t_meas=20e-3):
+        """recon_sim_run_host: one outcome record per trial (SPEC.md sim.run_trial)."""
+        occ = np.ascontiguousarray(occ, np.uint64)
+        out = {k: np.zeros(count, np.int32) for k in ("success", "cycles", "status")}
+        out.update({k: np.zeros(count, np.int64) for k in ("n_nu", "n_alpha", "nb_nu", "nb_alpha", "atoms_lost")})
+        out["elapsed"] = np.zeros(count, np.float64)
+        sb = SimBatch(_vp(occ).value, count, width, height, h_prime, seed_base, 1 if solver == "bird" else 0,
+                      1 if batching else 0, preset, max_cycles, LossModel(p_nu, p_alpha, tau, t_nu, t_alpha, t_meas),
+                      *[_vp(out[k]).value for k in ("success", "cycles", "status", "n_nu", "n_alpha", "nb_nu",
+                                                     "nb_alpha", "atoms_lost", "elapsed")])
+        st = self.lib.recon_sim_run_host(self.ctx(), C.byref(sb))
+        self._check(st, 0)
+        return out
 
     def pipeline_batch(self, solver: str, occ, count, width, height, h_prime, preset, move_stride):
         stride = width * h_prime
