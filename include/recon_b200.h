@@ -449,14 +449,15 @@ recon_status recon_batch_schedule_json_host(recon_ctx *ctx, int32_t width, int32
  * is full, and fails when fewer than W*h' atoms remain, when the solver or the
  * batching fails, or after max_cycles cycles.
  *
- * Execution model (SPEC design decisions):
- *  - unbatched: each displaced token is one EDI cycle: extract (p_alpha), its
- *    k moves (p_nu each), implant (p_alpha); elapsed 2 t_alpha + k t_nu;
- *  - batched: an EDI cycle is a maximal run of consecutive batches moving the
- *    same token set; each token of the run is extracted once and implanted
- *    once per run; elapsed per run 2 t_alpha + (#batches) t_nu;
- *  - a token lost mid-path vanishes and skips its remaining operations;
- *    N_nu / N_alpha count the operations performed;
+ * Execution model (SPEC design decisions and invariants):
+ *  - every displaced token is extracted (p_alpha), makes its k moves (p_nu
+ *    each) and is implanted (p_alpha); a token lost mid-path vanishes and
+ *    skips its remaining operations; N_nu / N_alpha count the operations
+ *    performed, so they are the same with and without batching (SPEC:
+ *    "batching conservation");
+ *  - unbatched, each displaced token is one EDI cycle (elapsed 2 t_alpha +
+ *    k t_nu); batched, an EDI cycle is a maximal run of consecutive batches
+ *    moving the same token set (elapsed 2 t_alpha + #batches t_nu);
  *  - NB_nu / NB_alpha count the scheduled displacement / transfer sequences
  *    (batched: batches / runs; unbatched: moves / displaced tokens);
  *  - after the moves every atom survives with exp(-(elapsed + t_meas) / tau)

@@ -115,35 +115,21 @@ static inline void simc_trial(const recon_sim_batch *b, int i, sim_solve_fn solv
         const int64_t before = atoms;
         memcpy(nxt, occ, words * 8);
         for (int32_t p = 0; p < pc; ++p) nxt[(size_t)(ps[p] / H) * wpc + (ps[p] % H) / 64] &= ~(1ULL << ((ps[p] % H) & 63));
-        for (int32_t p = 0; p < pc; ++p) {
+        for (int32_t p = 0; p < pc; ++p) { /* extract, k moves, implant (N counts are batching-independent) */
             const int64_t len = off[p + 1] - off[p];
-            int alive = 1, prev = -1;
-            uint64_t ord = 0;
             const uint64_t base = (uint64_t)p * 4096;
-            for (int64_t k = 0; k < len; ++k) {
-                const int r = b->batching ? runid[mb[off[p] + k]] : 0;
-                if (r != prev) {
-                    if (prev >= 0) {
-                        if (alive) {
-                            n_al++;
-                            alive = recon_sim_u01(seed, (uint32_t)cyc, RECON_DRAW_IMPLANT, base + ord) < L.p_alpha;
-                        }
-                        ord++;
-                    }
-                    if (alive) {
-                        n_al++;
-                        alive = recon_sim_u01(seed, (uint32_t)cyc, RECON_DRAW_EXTRACT, base + ord) < L.p_alpha;
-                    }
-                    prev = r;
-                }
-                if (alive) {
-                    n_nu++;
-                    alive = recon_sim_u01(seed, (uint32_t)cyc, RECON_DRAW_MOVE, base + (uint64_t)k) < L.p_nu;
-                }
+            int alive = 1;
+            if (len > 0) {
+                n_al++;
+                alive = recon_sim_u01(seed, (uint32_t)cyc, RECON_DRAW_EXTRACT, base) < L.p_alpha;
+            }
+            for (int64_t k = 0; k < len && alive; ++k) {
+                n_nu++;
+                alive = recon_sim_u01(seed, (uint32_t)cyc, RECON_DRAW_MOVE, base + (uint64_t)k) < L.p_nu;
             }
             if (len > 0 && alive) {
                 n_al++;
-                alive = recon_sim_u01(seed, (uint32_t)cyc, RECON_DRAW_IMPLANT, base + ord) < L.p_alpha;
+                alive = recon_sim_u01(seed, (uint32_t)cyc, RECON_DRAW_IMPLANT, base) < L.p_alpha;
             }
             if (alive) nxt[(size_t)(pt[p] / H) * wpc + (pt[p] % H) / 64] |= 1ULL << ((pt[p] % H) & 63);
         }

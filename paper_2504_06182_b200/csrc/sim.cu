@@ -149,36 +149,21 @@ __global__ void __launch_bounds__(kThreads) k_transport(SimArgs a) {
     const uint64_t seed = a.seed_base + (uint64_t)trial;
     const double pa = a.L.p_alpha, pn = a.L.p_nu;
     long long nu = 0, al = 0;
-    for (int p = tid; p < P; p += kThreads) {
+    for (int p = tid; p < P; p += kThreads) {  // extract, k moves, implant
         const int len = off[p + 1] - off[p];
-        bool alive = true;
-        int prev = -1;
-        uint64_t ord = 0;
         const uint64_t b4 = (uint64_t)p * 4096;
-        for (int k = 0; k < len; ++k) {
-            const int r = a.batching ? runid[mb[off[p] + k]] : 0;
-            if (r != prev) {
-                if (prev >= 0) {
-                    if (alive) {
-                        ++al;
-                        alive = recon_sim_u01(seed, (uint32_t)a.cyc, RECON_DRAW_IMPLANT, b4 + ord) < pa;
-                    }
-                    ++ord;
-                }
-                if (alive) {
-                    ++al;
-                    alive = recon_sim_u01(seed, (uint32_t)a.cyc, RECON_DRAW_EXTRACT, b4 + ord) < pa;
-                }
-                prev = r;
-            }
-            if (alive) {
-                ++nu;
-                alive = recon_sim_u01(seed, (uint32_t)a.cyc, RECON_DRAW_MOVE, b4 + (uint64_t)k) < pn;
-            }
+        bool alive = true;
+        if (len > 0) {
+            ++al;
+            alive = recon_sim_u01(seed, (uint32_t)a.cyc, RECON_DRAW_EXTRACT, b4) < pa;
+        }
+        for (int k = 0; k < len && alive; ++k) {
+            ++nu;
+            alive = recon_sim_u01(seed, (uint32_t)a.cyc, RECON_DRAW_MOVE, b4 + (uint64_t)k) < pn;
         }
         if (len > 0 && alive) {
             ++al;
-            alive = recon_sim_u01(seed, (uint32_t)a.cyc, RECON_DRAW_IMPLANT, b4 + ord) < pa;
+            alive = recon_sim_u01(seed, (uint32_t)a.cyc, RECON_DRAW_IMPLANT, b4) < pa;
         }
         if (alive) {
             const int v = dst[p];

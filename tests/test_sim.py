@@ -67,3 +67,18 @@ def test_device_paper_config(gpu, oracle):
     for k in FIELDS:
         assert np.array_equal(a[k][:8], b[k]), k
     assert 0 < a["success"].mean() < 1
+
+
+def test_batching_conservation(oracle):
+    """SPEC invariant: N_nu and N_alpha are identical with and without
+    batching on the same trial seed; only NB counts and elapsed time differ.
+    (Without lifetime decay: decay depends on the elapsed time, which batching
+    changes.)"""
+    W, H, hp, n = 16, 24, 12, 16
+    occ = sample_grids(0x51A0000, n, W, H, int(0.62 * W * H))
+    kw = dict(LOSSY, tau=0.0)
+    a = run(oracle, occ, n, W, H, hp, solver="bird", batching=False, **kw)
+    b = run(oracle, occ, n, W, H, hp, solver="bird", batching=True, preset=0, **kw)
+    for k in ("success", "cycles", "n_nu", "n_alpha", "atoms_lost"):
+        assert np.array_equal(a[k], b[k]), k
+    assert (b["nb_nu"] < a["nb_nu"]).all() and (b["elapsed"] < a["elapsed"]).all()
