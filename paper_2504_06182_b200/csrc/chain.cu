@@ -184,67 +184,72 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
             status = RECON_ERR_INFEASIBLE;
             detail = RECON_D_FEWER_SOURCES;
         } else {
-            // ---- candidate cuts (exact1d.cpp:219-247) as a prefix-max scan
+            // ---- candidate cuts (exact1d.cpp:219-247).  With D(v) = ps(v) -
+            // min(max(v - tl, 0), k) (ps = sources before v), an empty vertex
+            // outside the targets is a cut iff D(v) <= E and D(v) >= max(0,
+            // every earlier eligible D).  D = ps on the left of the targets and
+            // ps - k on the right, both nondecreasing, so the cuts are the empty
+            // vertices of two intervals: [0, min(tl, S[E] + 1)) and (max(th,
+            // S[k + max(0, Lmax) - 1]), n), Lmax = ps of the last left cut.  Cuts
+            // inside one run of empty vertices share ps, i.e. bound empty
+            // blocks, so one boundary per run start is enough.
             const int E = ns - k;
-            int lmax = INT_MIN, ncut = 0, nleft = 0;
+            const int lim_l = min(tl, (int)S[E] + 1);
+            int last_l = -1;  // last empty vertex in [0, lim_l)
+            for (int q = 0; q < per32; ++q) {
+                const int v0 = (lane * per32 + q) * 32;
+                const uint32_t em = ~w[q] & chunk_range(v0, 32, 0, min(lim_l, n));
+                if (em) last_l = v0 + 31 - __clz(em);
+            }
+            last_l = warp_max(last_l);
+            int Lmax = 0;  // max(0, ps(last left cut))
+            if (last_l >= 0) {  // ps(v) = #sources < v (binary search in S)
+                int lo = 0, hi = ns;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (S[mid] < last_l) lo = mid + 1;
+                    else hi = mid;
+                }
+                Lmax = lo;
+            }
+            const int lo_r = max(th, (int)S[k + Lmax - 1]);  // right cuts: v > lo_r
+            // run starts inside the two intervals, in vertex order
+            uint32_t st[4];
+            int ncnt = 0, nl = 0;
+            uint32_t prev_top = __shfl_up_sync(FULL, ~w[per32 - 1] >> 31, 1) & 1u;  // empty bit before this lane
+            if (lane == 0) prev_top = 0;
+            for (int q = 0; q < per32; ++q) {
+                const int v0 = (lane * per32 + q) * 32;
+                const uint32_t in = chunk_range(v0, 32, 0, min(lim_l, n)) | chunk_range(v0, 32, lo_r + 1, n);
+                const uint32_t em = ~w[q] & in;
+                const uint32_t prev_in = (in << 1) | (q == 0 ? (lane > 0 ? ((chunk_range(v0 - 1, 1, 0, min(lim_l, n)) |
+                                                                            chunk_range(v0 - 1, 1, lo_r + 1, n)) & 1u)
+                                                                       : 0u)
+                                                             : ((chunk_range(v0 - 32, 32, 0, min(lim_l, n)) |
+                                                                 chunk_range(v0 - 32, 32, lo_r + 1, n)) >> 31));
+                const uint32_t prev_e = (~w[q] << 1) | (q == 0 ? prev_top : (~w[q - 1] >> 31));
+                st[q] = em & ~(prev_e & prev_in);
+                ncnt += __popc(st[q]);
+                nl += __popc(st[q] & chunk_range(v0, 32, 0, tl));
+            }
+            int ncut;
+            int slot = 1 + warp_excl_scan(ncnt, &ncut);
+            const int nleft = warp_sum(nl);
             {
                 int ps = base_ps;
-                for (int q = 0; q < per32; ++q)
-                    for (int bb = 0; bb < 32; ++bb) {
-                        const int v = (lane * per32 + q) * 32 + bb;
-                        if (v >= n) break;
-                        const bool s = (w[q] >> bb) & 1u;
-                        const int D = ps - min(max(v - tl, 0), k);
-                        if (!s && (v < tl || v > th) && D <= E) lmax = max(lmax, D);
-                        ps += s;
+                for (int q = 0; q < per32; ++q) {
+                    for (uint32_t x = st[q]; x; x &= x - 1) {
+                        const int bit = __ffs(x) - 1;
+                        B[slot++] = (int16_t)(ps + __popc(w[q] & ((1u << bit) - 1u)));
                     }
-            }
-            int incl = lmax;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(FULL, incl, o);
-                if (lane >= o) incl = max(incl, y);
-            }
-            int run0 = __shfl_up_sync(FULL, incl, 1);
-            if (lane == 0) run0 = 0;
-            run0 = max(run0, 0);
-            for (int pass = 0; pass < 2; ++pass) {
-                int run = run0, ps = base_ps, slot = 0;
-                if (pass == 1) {
-                    int tot;
-                    slot = 1 + warp_excl_scan(ncut, &tot);
-                    if (lane == 0) {
-                        B[0] = 0;
-                        B[tot + 1] = (int16_t)ns;
-                    }
-                    ncut = tot;
+                    ps += __popc(w[q]);
                 }
-                int mine = 0;
-                for (int q = 0; q < per32; ++q)
-                    for (int bb = 0; bb < 32; ++bb) {
-                        const int v = (lane * per32 + q) * 32 + bb;
-                        if (v >= n) break;
-                        const bool s = (w[q] >> bb) & 1u;
-                        const int D = ps - min(max(v - tl, 0), k);
-                        if (!s && (v < tl || v > th) && D <= E && D >= run) {
-                            run = D;
-                            if (pass == 1) B[slot++] = (int16_t)ps;
-                            else {
-                                ++mine;
-                                nleft += v < tl;  // cuts left of the targets
-                            }
-                        }
-                        ps += s;
-                    }
-                if (pass == 0) ncut = mine;
+                if (lane == 0) {
+                    B[0] = 0;
+                    B[ncut + 1] = (int16_t)ns;
+                }
             }
             __syncwarp();
-            // boundaries B[0..ncut+1]; cut j is left of tl iff B[j] <= idxL and
-            // it was found before tl: count left cuts = cuts with vertex < tl.
-            // A cut at vertex v < tl has ps <= idxL; a cut at v > th has ps >= idxR.
-            // (idxL == idxR only if there are no residents; disambiguate via the
-            // number of left cuts computed from vertex positions.)
-            nleft = warp_sum(nleft);
             // non-empty blocks: [B[q], B[q+1]) for q in [0, ncut]; the target is
             // q == nleft (it holds the targets even without sources)
             int nb = 0, t = 0;

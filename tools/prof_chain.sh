@@ -1,0 +1,4 @@
+# ncu --set full of the chain band kernel (C2, 1M chains), source-correlated
+set -x
+mkdir -p gpurun_out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:chain_band -s 1 -c 1 -o gpurun_out/chain_full -f python tools/perf_probe.py c2_chains_1m > gpurun_out/ncu_c.log 2>&1; echo ncu rc=$?
