@@ -361,9 +361,12 @@ cudaError_t launch_chain_band(const ChainBandParams &p0, int sms, cudaStream_t s
     if (n <= 0 || n > 4096) return cudaErrorInvalidValue;
     const int k = p.t_hi - p.t_lo + 1;
     auto al = [](size_t x) { return (int)((x + 15) / 16 * 16); };
+    // block boundaries: one per run of empty vertices (runs are separated by
+    // sources), plus both ends -> at most (n + 1) / 2 + 2 entries
+    const size_t nbnd = (size_t)(n + 1) / 2 + 3;
     p.b_off = al((size_t)n * 2);
-    p.be_off = p.b_off + al((size_t)(n + 2) * 2);
-    p.ps_off = p.be_off + al((size_t)(n + 2) * 2);
+    p.be_off = p.b_off + al(nbnd * 2);
+    p.ps_off = p.be_off + al(nbnd * 2);
     p.hole_off = p.ps_off + al((size_t)(n + 1) * 4);
     p.warp_smem = p.hole_off + al((size_t)(k + 2) * 2);
     const int warps = 8;
