@@ -122,26 +122,25 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
         }
         int ns;
         const int base_ps = warp_excl_scan(cnt, &ns);
+        // sorted sources S and their prefix sums PS (one warp scan of the
+        // lanes' position sums), then the empty band cells
         {
+            int psum = 0;
+            for (int q = 0; q < per32; ++q)
+                for (uint32_t x = w[q]; x; x &= x - 1) psum += (lane * per32 + q) * 32 + __ffs(x) - 1;
+            int total;
+            int run = warp_excl_scan(psum, &total);
             int e = base_ps;
             for (int q = 0; q < per32; ++q)
-                for (uint32_t x = w[q]; x; x &= x - 1) S[e++] = (int16_t)((lane * per32 + q) * 32 + __ffs(x) - 1);
-        }
-        __syncwarp();
-        // prefix sums of the sorted sources and the empty band cells
-        {
-            int carry = 0;
-            for (int i0 = 0; i0 <= ns; i0 += 32) {
-                const int i = i0 + lane;
-                int x = (i > 0 && i <= ns) ? S[i - 1] : 0;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(FULL, x, o);
-                    if (lane >= o) x += y;
+                for (uint32_t x = w[q]; x; x &= x - 1) {
+                    const int v = (lane * per32 + q) * 32 + __ffs(x) - 1;
+                    S[e] = (int16_t)v;
+                    PS[e++] = run;
+                    run += v;
                 }
-                if (i <= ns) PS[i] = carry + x;
-                carry += __shfl_sync(FULL, x, 31);
-            }
+            if (lane == 31) PS[ns] = run;
+        }
+        {
             int hcnt = 0;
             uint32_t hm[4];
             for (int q = 0; q < per32; ++q) {
