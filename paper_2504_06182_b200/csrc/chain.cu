@@ -41,10 +41,13 @@ struct ChainCtx {
 // a-th empty band cell
 __device__ __forceinline__ int cnt_e_lt(const ChainCtx &c, int a) { return c.hole[a] - c.tl - a + 1; }
 
+// Integer ranges: n <= 4096 (launch_chain_band), so positions < 2^12, counts
+// < 2^12 and every sum of positions or cost below is < 2^25: 32-bit math.
+
 // Delta(a) = cost(a) - cost(a-1)
-__device__ __forceinline__ long long chain_delta(const ChainCtx &c, int a) {
+__device__ __forceinline__ int chain_delta(const ChainCtx &c, int a) {
     const int b = (c.k - c.R) - a;
-    return (long long)(c.tl + a - 1) - c.S[c.idxL - a] + 2LL * cnt_e_lt(c, a) - c.R - c.S[c.idxR + b] + c.th - b;
+    return (c.tl + a - 1) - c.S[c.idxL - a] + 2 * cnt_e_lt(c, a) - c.R - c.S[c.idxR + b] + c.th - b;
 }
 
 // largest a in [amin, amax] with Delta(a) <= 0 for all amin < a' <= a (32-ary search)
@@ -68,29 +71,29 @@ __device__ int chain_best_a(const ChainCtx &c, int amin, int amax) {
     return lo;
 }
 
-// split-rule cost at a (warp-cooperative range sums)
-__device__ long long chain_cost(const ChainCtx &c, int a) {
+// split-rule cost at a (range sums of the sources' prefix sums)
+__device__ int chain_cost(const ChainCtx &c, int a) {
     const int b = (c.k - c.R) - a;
     const int m = cnt_e_lt(c, a);
-    const long long top = (long long)c.PS[c.idxL] - c.PS[c.idxL - a];
-    const long long resm = (long long)c.PS[c.idxL + m] - c.PS[c.idxL];
-    const long long resR = (long long)c.PS[c.idxR] - c.PS[c.idxL];
-    const long long bot = (long long)c.PS[c.idxR + b] - c.PS[c.idxR];
-    const long long Em = resm - (long long)m * c.tl - (long long)m * (m - 1) / 2;
-    const long long ER = resR - (long long)c.R * c.tl - (long long)c.R * (c.R - 1) / 2;
-    long long cost = (long long)a * c.tl + (long long)a * (a - 1) / 2 - top;
-    cost += (long long)a * m - Em + (ER - Em) - (long long)a * (c.R - m);
-    cost += bot - ((long long)b * c.th - (long long)b * (b - 1) / 2);
+    const int top = c.PS[c.idxL] - c.PS[c.idxL - a];
+    const int resm = c.PS[c.idxL + m] - c.PS[c.idxL];
+    const int resR = c.PS[c.idxR] - c.PS[c.idxL];
+    const int bot = c.PS[c.idxR + b] - c.PS[c.idxR];
+    const int Em = resm - m * c.tl - m * (m - 1) / 2;
+    const int ER = resR - c.R * c.tl - c.R * (c.R - 1) / 2;
+    int cost = a * c.tl + a * (a - 1) / 2 - top;
+    cost += a * m - Em + (ER - Em) - a * (c.R - m);
+    cost += bot - (b * c.th - b * (b - 1) / 2);
     return cost;
 }
 
 // optimum over sources S[s0, s1) (holding every resident); *best_a = -1 if infeasible
-__device__ long long block_opt(const ChainCtx &c, int s0, int s1, int *best_a) {
+__device__ int block_opt(const ChainCtx &c, int s0, int s1, int *best_a) {
     const int holes = c.k - c.R;
     const int amin = max(0, holes - (s1 - c.idxR)), amax = min(c.idxL - s0, holes);
     if (amin > amax) {
         *best_a = -1;
-        return LLONG_MAX / 4;
+        return INT_MAX / 4;
     }
     const int a = chain_best_a(c, amin, amax);
     *best_a = a;
@@ -272,8 +275,8 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
             s1 = BE[t];
             if (nb > 1) {
                 int ga;
-                const long long global = block_opt(c, 0, ns, &ga);
-                long long wt = block_opt(c, s0, s1, &a);
+                const int global = block_opt(c, 0, ns, &ga);
+                int wt = block_opt(c, s0, s1, &a);
                 if (wt != global) {
                     // literal sweep (exact1d.cpp:269-289): blocks tL..tR form the
                     // target; list index i maps to the current merged list
@@ -289,7 +292,7 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
                         if (i > tL) break;  // only source-only pairs remain
                         int tmp;
                         if (i + 1 == tL) {  // (left neighbour, target)
-                            const long long wj = block_opt(c, B[tL - 1], BE[tR], &tmp);
+                            const int wj = block_opt(c, B[tL - 1], BE[tR], &tmp);
                             if (wj < wt) {
                                 --tL;
                                 wt = wj;
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
                                 ++i;
                             }
                         } else {  // i == tL: (target, right neighbour)
-                            const long long wj = block_opt(c, B[tL], BE[tR + 1], &tmp);
+                            const int wj = block_opt(c, B[tL], BE[tR + 1], &tmp);
                             if (wj < wt) {
                                 ++tR;
                                 wt = wj;
