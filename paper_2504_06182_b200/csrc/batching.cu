@@ -86,9 +86,28 @@ __device__ __forceinline__ LanePath load_lane_path(const ImplicitPaths &ip, cons
     return r;
 }
 
-__device__ __forceinline__ bool bit_get(const uint32_t *bm, int v) { return (bm[v >> 5] >> (v & 31)) & 1u; }
-__device__ __forceinline__ void bit_set(uint32_t *bm, int v) { atomicOr(&bm[v >> 5], 1u << (v & 31)); }
-__device__ __forceinline__ void bit_clr(uint32_t *bm, int v) { atomicAnd(&bm[v >> 5], ~(1u << (v & 31))); }
+// vertex bitmaps (occupancy, in-batch); SM = in shared memory, accessed with
+// ld.shared / atom.shared (a generic pointer would take the generic path)
+template <bool SM>
+struct Bits {
+    uint32_t *p;
+    uint32_t sa;  // shared-window address of p when SM
+    __device__ explicit Bits(uint32_t *q) : p(q), sa(SM ? (uint32_t)__cvta_generic_to_shared(q) : 0u) {}
+    __device__ __forceinline__ bool get(int v) const {
+        uint32_t x;
+        if (SM) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(sa + ((uint32_t)(v >> 5) << 2)));
+        else x = p[v >> 5];
+        return (x >> (v & 31)) & 1u;
+    }
+    __device__ __forceinline__ void set(int v) const {
+        if (SM) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(sa + ((uint32_t)(v >> 5) << 2)), "r"(1u << (v & 31)) : "memory");
+        else atomicOr(&p[v >> 5], 1u << (v & 31));
+    }
+    __device__ __forceinline__ void clr(int v) const {
+        if (SM) asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(sa + ((uint32_t)(v >> 5) << 2)), "r"(~(1u << (v & 31))) : "memory");
+        else atomicAnd(&p[v >> 5], ~(1u << (v & 31)));
+    }
+};
 
 // move_dir (batching.cpp:9-15): 0 up, 1 down, 2 left, 3 right
 __device__ __forceinline__ int move_dir(int H, int32_t a, int32_t b) {
@@ -140,11 +159,12 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t *a, int n, int x) {
 // the only possible vertex conflict inside a batch is a shared destination;
 // the minimum id wins (and, under column_direction, the class of the first
 // accepted move).  The general entry point keeps the literal pairwise checks.
-template <class Paths, bool FAST>
+template <class Paths, bool FAST, bool SM = false>
 __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
     const int lane = lane_id();
     const int P = J.P, H = J.H;
     BatchScratch s = J.s;
+    const Bits<SM> occ(s.occ), inb(s.inb);
     // ---- init: next = 0, blockers = in-degree (given), finish zero-length paths
     long long left = 0;
     for (int p = lane; p < P; p += 32) {
@@ -194,7 +214,7 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
                 fr = lp.v(H, lp.k);
                 to = lp.v(H, lp.k + 1);
             }
-            const bool cand = valid && !bit_get(s.occ, to);
+            const bool cand = valid && !occ.get(to);
             const unsigned cm = __ballot_sync(FULL, cand);
             if (!cm) {
                 status = RECON_ERR_INPUT;  // batching.cpp:127-128
@@ -210,9 +230,9 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
                 a = cand && (same & lanemask_lt()) == 0;
             }
             const unsigned acc = __ballot_sync(FULL, a);
-            if (a) bit_clr(s.occ, fr);
+            if (a) occ.clr(fr);
             __syncwarp();
-            if (a) bit_set(s.occ, to);
+            if (a) occ.set(to);
             bool fin = false;
             if (a) {
                 J.move_batch[lp.base + lp.k] = nb;
@@ -364,7 +384,7 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
                 k = s.next[p];
                 fr = paths.v(p, k);
                 to = paths.v(p, k + 1);
-                cand = !bit_get(s.occ, to) && !bit_get(s.inb, fr) && !bit_get(s.inb, to);
+                cand = !occ.get(to) && !inb.get(fr) && !inb.get(to);
                 if (cand && f_from >= 0) cand = compatible(J.preset, H, fr, to, f_from, f_to);
             }
             const unsigned cm_all = __ballot_sync(FULL, cand);
@@ -405,8 +425,8 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
                 }
             }
             if ((acc >> lane) & 1u) {
-                bit_set(s.inb, fr);
-                bit_set(s.inb, to);
+                inb.set(fr);
+                inb.set(to);
                 const int slot = nacc + __popc(acc & lanemask_lt());
                 s.mem[slot] = p;
                 s.mfr[slot] = fr;
@@ -426,12 +446,12 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
         }
         // ---- 3. atomic application
         for (int i = lane; i < nacc; i += 32) {
-            bit_clr(s.occ, s.mfr[i]);
-            bit_clr(s.inb, s.mfr[i]);
-            bit_clr(s.inb, s.mto[i]);
+            occ.clr(s.mfr[i]);
+            inb.clr(s.mfr[i]);
+            inb.clr(s.mto[i]);
         }
         __syncwarp();
-        for (int i = lane; i < nacc; i += 32) bit_set(s.occ, s.mto[i]);
+        for (int i = lane; i < nacc; i += 32) occ.set(s.mto[i]);
         __syncwarp();
         // ---- 4. advance, finish, release (newly -> next batch)
         int nnew = 0, nfin = 0;
@@ -744,7 +764,7 @@ cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *
     return cudaGetLastError();
 }
 
-__global__ void batch_pipeline_kernel(PipelineArgs a, int occ_in_smem) {
+__global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a, int occ_in_smem) {
     extern __shared__ __align__(16) uint32_t bsmem[];
     const int64_t S = (int64_t)a.W * a.k, nwb = ((int64_t)a.W * a.H + 31) / 32;
     const int nw = blockDim.x >> 5;
@@ -774,13 +794,17 @@ __global__ void batch_pipeline_kernel(PipelineArgs a, int occ_in_smem) {
         J.soff = a.soff + o;
         J.succ = a.succ;
         J.s.occ = a.occ + inst * nwb;
-        if (occ_in_smem) {  // the instance's occupancy bitmap lives in this warp's shared memory
-            uint32_t *mine = bsmem + (size_t)warp_id() * nwb;
-            for (int64_t w = lane_id(); w < nwb; w += 32) mine[w] = J.s.occ[w];
+        J.s.inb = a.inb + inst * nwb;
+        if (occ_in_smem) {  // the instance's occupancy and in-batch bitmaps live in this warp's shared memory
+            uint32_t *mine = bsmem + (size_t)warp_id() * 2 * nwb;
+            for (int64_t w = lane_id(); w < nwb; w += 32) {
+                mine[w] = J.s.occ[w];
+                mine[nwb + w] = 0u;
+            }
             __syncwarp();
             J.s.occ = mine;
+            J.s.inb = mine + nwb;
         }
-        J.s.inb = a.inb + inst * nwb;
         J.s.next = a.next + o;
         J.s.blockers = a.indeg + o;
         J.s.done = a.done + o;
@@ -796,7 +820,8 @@ __global__ void batch_pipeline_kernel(PipelineArgs a, int occ_in_smem) {
         J.status = a.status + inst;
         J.detail = a.detail ? a.detail + inst : nullptr;
         ImplicitPaths ip{a.path_src + o, a.path_dst + o, a.mbase + o, a.mbase[o], a.H};
-        batch_warp<ImplicitPaths, true>(J, ip);
+        if (occ_in_smem) batch_warp<ImplicitPaths, true, true>(J, ip);
+        else batch_warp<ImplicitPaths, true, false>(J, ip);
     }
 }
 
@@ -808,12 +833,12 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
     cudaMemsetAsync(a.inb, 0, (size_t)a.count * nwb * 4, st);
     cudaMemsetAsync(a.counter, 0, (size_t)a.count * 4, st);
     (void)N;
-    // occupancy bitmap in shared memory when a few warps' worth fits
-    const int64_t bm_bytes = nwb * 4;
+    // occupancy + in-batch bitmaps in shared memory when a few warps' worth fits
+    const int64_t bm_bytes = 2 * nwb * 4;
     int warps = 4, occ_smem = 0;
     size_t smem = 0;
-    if (bm_bytes <= 48 * 1024) {
-        warps = (int)std::max<int64_t>(1, std::min<int64_t>(8, (96 * 1024) / bm_bytes));
+    if (bm_bytes <= 96 * 1024) {
+        warps = (int)std::max<int64_t>(1, std::min<int64_t>(8, (200 * 1024) / bm_bytes));
         occ_smem = 1;
         smem = (size_t)warps * bm_bytes;
         cudaFuncSetAttribute(batch_pipeline_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
