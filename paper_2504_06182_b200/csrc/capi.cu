@@ -57,6 +57,9 @@ Ctx::~Ctx() {
         if (b.p) cudaFreeHost(b.p);
     for (auto &e : tev)
         if (e) cudaEventDestroy(e);
+    for (auto &e : cev)
+        if (e) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     if (stream) cudaStreamDestroy(stream);
 }
 

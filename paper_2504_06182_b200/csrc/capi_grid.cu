@@ -219,19 +219,47 @@ recon_status grid_batch(int solver, recon_ctx *ctx, const recon_grid_batch *b, b
         !p.total_displacement || !p.status || !p.detail || (b->events && !p.events))
         return cuda_fail(cudaErrorMemoryAllocation, "grid batch workspace", detail);
     CK(cudaMemcpyAsync(d_occ, b->occ, n * words * 8, cudaMemcpyHostToDevice, c->stream), "occ H2D");
-    CK(launch(c, solver, p, grid_blocks(c, solver, s, b->count)), "grid kernel launch");
-    CK(cudaMemcpyAsync(b->path_src, p.path_src, n * stride * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    CK(cudaMemcpyAsync(b->path_dst, p.path_dst, n * stride * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    if (b->path_event)
-        CK(cudaMemcpyAsync(b->path_event, p.path_event, n * stride * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    CK(cudaMemcpyAsync(b->path_count, p.path_count, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    CK(cudaMemcpyAsync(b->total_displacement, p.total_displacement, n * 8, cudaMemcpyDeviceToHost, c->stream),
-       "D2H");
-    CK(cudaMemcpyAsync(b->status, p.status, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    if (b->detail) CK(cudaMemcpyAsync(b->detail, p.detail, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    if (b->events)
-        CK(cudaMemcpyAsync(b->events, p.events, n * b->width * per * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    // Chunks of one wave of CTAs: chunk k's results go back on the copy stream
+    // while chunk k + 1 solves (the device-to-host copy of the path lists
+    // dominates, so it overlaps the solve instead of following it).
+    if (!c->copy_stream) CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "copy stream");
+    const size_t wave = (size_t)grid_blocks(c, solver, s, b->count);
+    const size_t chunk = std::max<size_t>(wave, (n + 7) / 8);
+    cudaStream_t cs = c->copy_stream;
+    for (size_t i0 = 0; i0 < n; i0 += chunk) {
+        const size_t m = std::min(chunk, n - i0);
+        GridParams q = p;
+        q.count = (int)m;
+        q.occ = d_occ + i0 * words;
+        q.path_src = p.path_src + i0 * stride;
+        q.path_dst = p.path_dst + i0 * stride;
+        q.path_event = p.path_event ? p.path_event + i0 * stride : nullptr;
+        q.path_count = p.path_count + i0;
+        q.total_displacement = p.total_displacement + i0;
+        q.status = p.status + i0;
+        q.detail = p.detail + i0;
+        q.events = p.events ? p.events + i0 * b->width * per : nullptr;
+        CK(launch(c, solver, q, grid_blocks(c, solver, s, (int)m)), "grid kernel launch");
+        cudaEvent_t ev = c->chunk_event();
+        if (!ev) return cuda_fail(cudaErrorMemoryAllocation, "chunk event", detail);
+        CK(cudaEventRecord(ev, c->stream), "event");
+        CK(cudaStreamWaitEvent(cs, ev, 0), "wait");
+        CK(cudaMemcpyAsync(b->path_src + i0 * stride, q.path_src, m * stride * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        CK(cudaMemcpyAsync(b->path_dst + i0 * stride, q.path_dst, m * stride * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        if (b->path_event)
+            CK(cudaMemcpyAsync(b->path_event + i0 * stride, q.path_event, m * stride * 4, cudaMemcpyDeviceToHost, cs),
+               "D2H");
+        CK(cudaMemcpyAsync(b->path_count + i0, q.path_count, m * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        CK(cudaMemcpyAsync(b->total_displacement + i0, q.total_displacement, m * 8, cudaMemcpyDeviceToHost, cs), "D2H");
+        CK(cudaMemcpyAsync(b->status + i0, q.status, m * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        if (b->detail) CK(cudaMemcpyAsync(b->detail + i0, q.detail, m * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        if (b->events)
+            CK(cudaMemcpyAsync(b->events + i0 * b->width * per, q.events, m * b->width * per * 4,
+                               cudaMemcpyDeviceToHost, cs),
+               "D2H");
+    }
     CK(cudaStreamSynchronize(c->stream), "grid batch");
+    CK(cudaStreamSynchronize(cs), "grid batch D2H");
     return RECON_OK;
 }
 

@@ -41,6 +41,14 @@ struct Ctx {
     bool timing = false;          // recon_ctx_set_kernel_timing
     bool timed_plan = false;      // the last timed solve launched the planner
     cudaEvent_t tev[3] = {};      // before planner, before executor, after executor
+    cudaStream_t copy_stream = nullptr;  // device-to-host copies overlapping the next chunk's solve
+    cudaEvent_t cev[64] = {};            // chunk-done events (reused round robin)
+    int cev_next = 0;
+    cudaEvent_t chunk_event() {
+        cudaEvent_t &e = cev[cev_next++ % 64];
+        if (!e && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        return e;
+    }
     DevBuf buf[S_NSLOTS];
     HostBuf hbuf[8];
     void *get(int slot, size_t bytes);
