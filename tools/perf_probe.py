@@ -155,6 +155,9 @@ CASES = {
     "r256_redrec_b2048": lambda: grid("redrec", 256, 256, 153, 39322, 0x25600000, 2048),
     "r256_bird_b2048": lambda: grid("bird", 256, 256, 153, 39322, 0x25600000, 2048),
     "c3_bird_solve": lambda: grid("bird", 64, 64, 40, 2662, 0x64000000, 4096),
+    "c3_redrec_solve": lambda: grid("redrec", 64, 64, 40, 2662, 0x64000000, 4096),
+    "r128_redrec_b4096": lambda: grid("redrec", 128, 128, 76, 9830, 0x12800000, 4096),
+    "r128_bird_b4096": lambda: grid("bird", 128, 128, 76, 9830, 0x12800000, 4096),
     "c3_pipeline_none": lambda: pipeline("bird", 64, 64, 40, 2662, 0x64000000, 4096, 0),
     "c3_pipeline_coldir": lambda: pipeline("bird", 64, 64, 40, 2662, 0x64000000, 1024, 1),
     "c5_pipeline_4": lambda: pipeline("bird", 512, 512, 307, 157286, 0x51200000, 4, 0, 12_000_000),
