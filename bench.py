@@ -177,7 +177,11 @@ def main():
 
     ws, rank, local = dist_env()
     if ws > 1:
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        # RECON_BENCH_BACKEND=gloo: functional runs with more ranks than GPUs
+        # (NCCL refuses two ranks on one device); timing values then mean nothing
+        backend = os.environ.get("RECON_BENCH_BACKEND", "nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group(backend)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     from paper_2504_06182_b200 import load_native
     from paper_2504_06182_b200.abi import GridBatch
@@ -246,9 +250,11 @@ def main():
         times = timed(lib.lib.recon_redrec_solve_batch, args.steps, args.warmup, kernels=True)
     launches = lib.launch_count() - launches0
     torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
     ms = sum(times) / len(times)
     if ws > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     counts = pcount.cpu().numpy()
@@ -289,7 +295,7 @@ def main():
             e2e.append(dt)
     e2e_s = statistics.median(e2e)
     if ws > 1:
-        t = torch.tensor([e2e_s], device=dev)
+        t = torch.tensor([e2e_s], device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     h2d = B * W * wpc * 8
