@@ -124,3 +124,44 @@ def test_error_statuses(gpu, solver):
         gpu.grid_solve(solver, occ, 2, 4, 4)
     with pytest.raises(InputError):
         gpu.grid_solve(solver, occ, 2, 4, 0)
+
+
+@pytest.mark.parametrize("solver", SOLVERS)
+def test_c4_batch_of_256_matches_reference(gpu, ref, solver):
+    """More instances than SMs: the 8-warp batch CTAs (and, for red-rec, the
+    planner kernel + executor on many instances at once), against the compiled
+    reference on every instance."""
+    W = H = 256
+    n = 160
+    occ = sample_grids(0x25600000, n, W, H, 39322)
+    g = gpu.grid_solve_batch(solver, occ, n, W, H, 153)
+    r = ref.grid_solve_batch(solver, occ, n, W, H, 153)
+    for key in ("path_count", "total_displacement", "status"):
+        assert np.array_equal(g[key], r[key]), key
+    S = W * 153
+    for i in range(n):
+        P = int(r["path_count"][i])
+        for key in ("path_src", "path_dst"):
+            assert np.array_equal(g[key][i * S:i * S + P], r[key][i * S:i * S + P]), (key, i)
+
+
+@pytest.mark.parametrize("solver", SOLVERS)
+def test_c5_512_matches_reference(gpu, ref, solver):
+    occ = sample_grids(0x51200000, 1, 512, 512, 157286)
+    g = gpu.grid_solve(solver, occ, 512, 512, 307, with_dag=True)
+    r = ref.grid_solve(solver, occ, 512, 512, 307, with_dag=True)
+    assert same_grid(g, r)
+
+
+@pytest.mark.parametrize("solver", SOLVERS)
+@pytest.mark.parametrize("W,H,hp,eps", [(1000, 8, 3, 0.5), (4, 1000, 500, 0.55), (1024, 64, 40, 0.66),
+                                         (96, 1024, 600, 0.62)])
+def test_extreme_shapes_match_oracle(gpu, oracle, solver, W, H, hp, eps):
+    occ = sample_grids(0xE57, 2, W, H, int(round(eps * W * H)))
+    wpc = (H + 63) // 64
+    for i in range(2):
+        o = occ[i * W * wpc:(i + 1) * W * wpc]
+        (g, eg), (r, er) = call(gpu, "grid_solve", solver, o, W, H, hp), call(oracle, "grid_solve", solver, o, W, H, hp)
+        assert eg == er
+        if g is not None:
+            assert same_grid(g, r)
