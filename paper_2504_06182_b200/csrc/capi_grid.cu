@@ -40,12 +40,12 @@ recon_status validate_grid(int W, int H, int hp, int32_t *detail) {
 // in flight per SM, which wins on small grids (red-rec up to 128^2, bird up
 // to 256^2, measured r01); larger grids keep 8.  A red-rec batch with no more
 // instances than SMs runs one CTA per SM anyway, so it takes up to 32 warps
-// to shorten phase 1/3 and the waves (bird: 8, its kernel's limit).
+// to shorten phase 1/3 and the waves (bird: 16, its window chunks in flight).
 // RECON_GRID_WARPS overrides.
 bool shape_for(Ctx *c, int solver, int W, int H, int hp, int count, GridShape &s) {
     const long long cells = (long long)W * H;
     int w = cells <= (solver == 0 ? 128 * 128 : 256 * 256) ? 4 : kWarps;
-    if (count <= c->sms) w = solver == 0 ? 32 : kWarps;  // latency: every warp on the instance
+    if (count <= c->sms) w = solver == 0 ? 32 : 16;  // latency: more warps on the instance
     if (const char *e = getenv("RECON_GRID_WARPS")) w = std::max(1, std::min(32, atoi(e)));
     const int floor_w = std::min(kWarps, w);
     for (; w >= floor_w; w /= 2)

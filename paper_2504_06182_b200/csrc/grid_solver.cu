@@ -23,7 +23,9 @@ static void (*redrec_exec(const GridShape &s))(GridParams) {
 }
 __global__ void redrec_plan_kernel(GridParams p);
 int64_t redrec_plan_smem(int W);
+template <bool LAT>
 __global__ void bird_kernel(GridParams p);
+static void (*bird_exec(const GridShape &s))(GridParams) { return s.nwarps > 8 ? bird_kernel<true> : bird_kernel<false>; }
 
 bool grid_shape(int W, int H, int k, int nwarps, GridShape &s) {
     if (W <= 0 || H <= 0 || W > 1024 || H > 1024) return false;
@@ -74,7 +76,7 @@ RedrecPlans redrec_plans_carve(void *base, int W, int count) {
 
 cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaStream_t stream, cudaEvent_t *ev) {
     const int threads = 32 * p.shape.nwarps;
-    void (*kern)(GridParams) = solver == 0 ? redrec_exec(p.shape) : bird_kernel;
+    void (*kern)(GridParams) = solver == 0 ? redrec_exec(p.shape) : bird_exec(p.shape);
     cudaError_t e;
     if (solver == 0) {
         // plans first: one warp per instance, all instances in parallel
@@ -101,7 +103,7 @@ cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaSt
 
 int grid_occupancy(int solver, const GridShape &s) {
     int nb = 0;
-    void (*kern)(GridParams) = solver == 0 ? redrec_exec(s) : bird_kernel;
+    void (*kern)(GridParams) = solver == 0 ? redrec_exec(s) : bird_exec(s);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s.smem_bytes);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32 * s.nwarps, s.smem_bytes);
     return nb;
