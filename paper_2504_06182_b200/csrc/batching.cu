@@ -427,8 +427,13 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
             if ((acc >> lane) & 1u) {
                 inb.set(fr);
                 inb.set(to);
+                // advance the accepted path here, while its state is in registers
+                J.move_batch[paths.move_base(p) + k] = nb;
+                s.next[p] = k + 1;
+                const bool fin = k + 1 == paths.len(p);
+                if (fin) s.done[p] = 1;
                 const int slot = nacc + __popc(acc & lanemask_lt());
-                s.mem[slot] = p;
+                s.mem[slot] = fin ? (int)(0x80000000u | (unsigned)p) : p;  // bit 31: path finished
                 s.mfr[slot] = fr;
                 s.mto[slot] = to;
             }
@@ -453,7 +458,8 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
         __syncwarp();
         for (int i = lane; i < nacc; i += 32) occ.set(s.mto[i]);
         __syncwarp();
-        // ---- 4. advance, finish, release (newly -> next batch)
+        // ---- 4. finish and release (newly -> next batch); the moves were
+        // recorded and the paths advanced during the scan
         int nnew = 0, nfin = 0;
         for (int i0 = 0; i0 < nacc; i0 += 32) {
             const int i = i0 + lane;
@@ -461,13 +467,10 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
             int p = -1;
             int64_t q0 = 0, q1 = 0;
             if (i < nacc) {
-                p = s.mem[i];
-                const int k = s.next[p];
-                J.move_batch[paths.move_base(p) + k] = nb;
-                s.next[p] = k + 1;
-                fin = k + 1 == paths.len(p);
+                const int m = s.mem[i];
+                p = m & 0x7fffffff;
+                fin = m < 0;
                 if (fin) {
-                    s.done[p] = 1;
                     q0 = J.soff[p];
                     q1 = J.soff[p + 1];
                 }
