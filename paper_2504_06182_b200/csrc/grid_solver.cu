@@ -50,7 +50,7 @@ bool grid_shape(int W, int H, int k, int nwarps, GridShape &s) {
     return s.smem_bytes <= 227 * 1024;
 }
 
-size_t grid_stage_ints(const GridShape &s) { return (size_t)s.W * s.k; }
+size_t grid_stage_ints(const GridShape &s) { return (size_t)s.W * stage_stride(s.k); }
 
 size_t redrec_plan_bytes(int W) {
     return (size_t)align_up(W, 16) + 3 * (size_t)align_up(2 * W, 16) + (size_t)align_up(4 * (W + 2), 16) + 32;

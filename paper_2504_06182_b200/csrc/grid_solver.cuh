@@ -52,6 +52,8 @@ bool grid_shape(int W, int H, int k, int nwarps, GridShape &s);
 cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaStream_t stream,
                                cudaEvent_t *ev = nullptr);
 int grid_occupancy(int solver, const GridShape &s);
+// per-event staging stride (ints): k rounded up to a 128-byte line
+__host__ __device__ inline int stage_stride(int k) { return (k + 31) & ~31; }
 size_t grid_stage_ints(const GridShape &s);
 size_t redrec_plan_bytes(int W);  // global plan bytes per instance
 RedrecPlans redrec_plans_carve(void *base, int W, int count);

@@ -562,8 +562,10 @@ __global__ void __launch_bounds__(MINB == 1 ? 1024 : 256, MINB) redrec_kernel(Gr
     const int warp = warp_id(), lane = lane_id(), nw = blockDim.x >> 5;
     int16_t *L = b.lists + (size_t)warp * 4 * g.LK;
     uint32_t *keys = b.keys + (size_t)warp * 2 * g.LK;
-    // event e's paths are staged (packed, emission order) at stage + k*e
-    uint32_t *const stage = p.stage + (size_t)blockIdx.x * g.W * g.k;
+    // event e's paths are staged (packed, emission order) at stage + ks*e,
+    // ks = k rounded to a 128-byte line so consumed lines can be discarded
+    const int ks = stage_stride(g.k);
+    uint32_t *const stage = p.stage + (size_t)blockIdx.x * g.W * ks;
     __shared__ long long s_tokens;
     __shared__ unsigned long long s_disp;
     __shared__ int s_status, s_detail, s_n1, s_n2, s_nlev, s_total, s_fail;
@@ -621,7 +623,7 @@ __global__ void __launch_bounds__(MINB == 1 ? 1024 : 256, MINB) redrec_kernel(Gr
                     if (lane == 0) s_fail = 1;
                     continue;
                 }
-                disp += own_emit(g, c, s, L, stage + (size_t)e * g.k, 0, e);
+                disp += own_emit(g, c, s, L, stage + (size_t)e * ks, 0, e);
                 if (lane == 0) b.ev_count[e] = s.n_right + s.n_left;
                 __syncwarp();
             }
@@ -631,7 +633,7 @@ __global__ void __launch_bounds__(MINB == 1 ? 1024 : 256, MINB) redrec_kernel(Gr
                     const int e = b.wave_list[q];
                     const int col = b.ev_col[e], aux = b.ev_aux[e];
                     uint64_t *mc = b.dep + (size_t)col * g.wpd;
-                    uint32_t *st = stage + (size_t)e * g.k;
+                    uint32_t *st = stage + (size_t)e * ks;
                     if (b.ev_type[e] == EV_OWN) {
                         OwnSolve s;
                         if (!own_solve(g, mc, L, -1, s)) {
@@ -672,7 +674,7 @@ __global__ void __launch_bounds__(MINB == 1 ? 1024 : 256, MINB) redrec_kernel(Gr
                     if (lane == 0) s_fail = 1;
                     continue;
                 }
-                disp += own_emit(g, c, s, L, stage + (size_t)e * g.k, 0, e);
+                disp += own_emit(g, c, s, L, stage + (size_t)e * ks, 0, e);
                 if (lane == 0) b.ev_count[e] = s.n_right + s.n_left;
                 __syncwarp();
             }
@@ -700,24 +702,29 @@ __global__ void __launch_bounds__(MINB == 1 ? 1024 : 256, MINB) redrec_kernel(Gr
                 for (int e = warp; e < W; e += nw) {
                     const int n = b.ev_count[e], off = b.ev_off[e];
                     const int dbase = b.ev_col[e] * g.H + g.H - 1;
-                    const uint32_t *st = stage + (size_t)e * g.k;
+                    const uint32_t *st = stage + (size_t)e * ks;
                     for (int i0 = 0; i0 < n; i0 += 128) {  // 4 loads in flight per lane
                         uint32_t v[4];
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const int i = i0 + 32 * u + lane;
-                            v[u] = i < n ? st[i] : 0u;
+                            v[u] = i < n ? __ldlu(st + i) : 0u;  // last use
                         }
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const int i = i0 + 32 * u + lane;
                             if (i < n) {
-                                osrc[off + i] = (int)(v[u] >> 20) * g.H + g.H - 1 - (int)((v[u] >> 10) & 1023);
-                                odst[off + i] = dbase - (int)(v[u] & 1023);
-                                if (oev) oev[off + i] = e;
+                                // streaming stores: the output must not evict the staging from L2
+                                __stcs(osrc + off + i, (int)(v[u] >> 20) * g.H + g.H - 1 - (int)((v[u] >> 10) & 1023));
+                                __stcs(odst + off + i, dbase - (int)(v[u] & 1023));
+                                if (oev) __stcs(oev + off + i, e);
                             }
                         }
                     }
+                    // the event's staged lines are dead: drop them from L2 without write-back
+                    __syncwarp();
+                    for (int l = lane; 32 * l < n; l += 32)
+                        asm volatile("discard.global.L2 [%0], 128;" ::"l"(st + 32 * l) : "memory");
                 }
             }
             __syncthreads();
