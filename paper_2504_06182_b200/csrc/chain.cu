@@ -35,6 +35,7 @@ struct ChainCtx {
     const int16_t *S;       // sorted sources
     const int32_t *PS;      // PS[i] = S[0] + ... + S[i-1]
     const int16_t *hole;    // hole[q] = q-th empty band cell (1-based), hole[0] = tl-1
+    int astar;              // largest a with Delta(a) <= 0 over the whole chain's range
 };
 
 // #(residents with e < a), e_r = S[idxL+r] - tl - r: the residents before the
@@ -87,7 +88,10 @@ __device__ int chain_cost(const ChainCtx &c, int a) {
     return cost;
 }
 
-// optimum over sources S[s0, s1) (holding every resident); *best_a = -1 if infeasible
+// optimum over sources S[s0, s1) (holding every resident); *best_a = -1 if
+// infeasible.  Delta does not depend on the block and is strictly increasing
+// in a, and every block's [amin, amax] lies inside the whole chain's, so the
+// block optimum is the chain-wide split point clamped to the block's range.
 __device__ int block_opt(const ChainCtx &c, int s0, int s1, int *best_a) {
     const int holes = c.k - c.R;
     const int amin = max(0, holes - (s1 - c.idxR)), amax = min(c.idxL - s0, holes);
@@ -95,7 +99,7 @@ __device__ int block_opt(const ChainCtx &c, int s0, int s1, int *best_a) {
         *best_a = -1;
         return INT_MAX / 4;
     }
-    const int a = chain_best_a(c, amin, amax);
+    const int a = min(max(c.astar, amin), amax);
     *best_a = a;
     return chain_cost(c, a);
 }
@@ -128,9 +132,11 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
         // sorted sources S and their prefix sums PS (one warp scan of the
         // lanes' position sums), then the empty band cells
         {
-            int psum = 0;
+            int psum = 0;  // sum of set-bit positions: popc per bit of the bit index
             for (int q = 0; q < per32; ++q)
-                for (uint32_t x = w[q]; x; x &= x - 1) psum += (lane * per32 + q) * 32 + __ffs(x) - 1;
+                psum += (lane * per32 + q) * 32 * __popc(w[q]) + __popc(w[q] & 0xAAAAAAAAu) +
+                        2 * __popc(w[q] & 0xCCCCCCCCu) + 4 * __popc(w[q] & 0xF0F0F0F0u) +
+                        8 * __popc(w[q] & 0xFF00FF00u) + 16 * __popc(w[q] & 0xFFFF0000u);
             int total;
             int run = warp_excl_scan(psum, &total);
             int e = base_ps;
@@ -180,6 +186,12 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
             c.idxR = warp_sum(r);
         }
         c.R = c.idxR - c.idxL;
+        c.astar = 0;
+        if (ns >= k) {
+            const int holes = k - c.R;
+            const int amin = max(0, holes - (ns - c.idxR)), amax = min(c.idxL, holes);
+            if (amin <= amax) c.astar = chain_best_a(c, amin, amax);
+        }
         int status = RECON_OK, detail = 0, a = -1;
         int s0 = 0, s1 = ns;
         if (ns < k) {  // validate_chain_instance (exact1d.cpp:311)
