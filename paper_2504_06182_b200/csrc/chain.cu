@@ -36,6 +36,7 @@ struct ChainCtx {
     const int32_t *PS;      // PS[i] = S[0] + ... + S[i-1]
     const int16_t *hole;    // hole[q] = q-th empty band cell (1-based), hole[0] = tl-1
     int astar;              // largest a with Delta(a) <= 0 over the whole chain's range
+    int psL, psR, ER;       // PS[idxL], PS[idxR], residents' excess (chain constants)
 };
 
 // #(residents with e < a), e_r = S[idxL+r] - tl - r: the residents before the
@@ -76,32 +77,32 @@ __device__ int chain_best_a(const ChainCtx &c, int amin, int amax) {
 __device__ int chain_cost(const ChainCtx &c, int a) {
     const int b = (c.k - c.R) - a;
     const int m = cnt_e_lt(c, a);
-    const int top = c.PS[c.idxL] - c.PS[c.idxL - a];
-    const int resm = c.PS[c.idxL + m] - c.PS[c.idxL];
-    const int resR = c.PS[c.idxR] - c.PS[c.idxL];
-    const int bot = c.PS[c.idxR + b] - c.PS[c.idxR];
+    const int top = c.psL - c.PS[c.idxL - a];
+    const int resm = c.PS[c.idxL + m] - c.psL;
+    const int bot = c.PS[c.idxR + b] - c.psR;
     const int Em = resm - m * c.tl - m * (m - 1) / 2;
-    const int ER = resR - c.R * c.tl - c.R * (c.R - 1) / 2;
     int cost = a * c.tl + a * (a - 1) / 2 - top;
-    cost += a * m - Em + (ER - Em) - a * (c.R - m);
+    cost += a * m - Em + (c.ER - Em) - a * (c.R - m);
     cost += bot - (b * c.th - b * (b - 1) / 2);
     return cost;
 }
 
-// optimum over sources S[s0, s1) (holding every resident); *best_a = -1 if
+// split point of sources S[s0, s1) (holding every resident), -1 if
 // infeasible.  Delta does not depend on the block and is strictly increasing
 // in a, and every block's [amin, amax] lies inside the whole chain's, so the
-// block optimum is the chain-wide split point clamped to the block's range.
-__device__ int block_opt(const ChainCtx &c, int s0, int s1, int *best_a) {
+// block optimum is the chain-wide split point clamped to the block's range;
+// the block cost is chain_cost at that point.
+__device__ __forceinline__ int block_a(const ChainCtx &c, int s0, int s1) {
     const int holes = c.k - c.R;
     const int amin = max(0, holes - (s1 - c.idxR)), amax = min(c.idxL - s0, holes);
-    if (amin > amax) {
-        *best_a = -1;
-        return INT_MAX / 4;
-    }
-    const int a = min(max(c.astar, amin), amax);
+    return amin > amax ? -1 : min(max(c.astar, amin), amax);
+}
+
+// optimum over sources S[s0, s1); *best_a = -1 if infeasible
+__device__ int block_opt(const ChainCtx &c, int s0, int s1, int *best_a) {
+    const int a = block_a(c, s0, s1);
     *best_a = a;
-    return chain_cost(c, a);
+    return a < 0 ? INT_MAX / 4 : chain_cost(c, a);
 }
 
 __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
@@ -187,6 +188,9 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
         }
         c.R = c.idxR - c.idxL;
         c.astar = 0;
+        c.psL = PS[c.idxL];
+        c.psR = PS[c.idxR];
+        c.ER = (c.psR - c.psL) - c.R * tl - c.R * (c.R - 1) / 2;
         if (ns >= k) {
             const int holes = k - c.R;
             const int amin = max(0, holes - (ns - c.idxR)), amax = min(c.idxL, holes);
@@ -302,9 +306,14 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
                             continue;
                         }
                         if (i > tL) break;  // only source-only pairs remain
+                        // a merge keeping the split point keeps the cost (not < wt)
+                        auto merged = [&](int s0m, int s1m, int *am) {
+                            *am = block_a(c, s0m, s1m);
+                            return *am == a ? wt : (*am < 0 ? INT_MAX / 4 : chain_cost(c, *am));
+                        };
                         int tmp;
                         if (i + 1 == tL) {  // (left neighbour, target)
-                            const int wj = block_opt(c, B[tL - 1], BE[tR], &tmp);
+                            const int wj = merged(B[tL - 1], BE[tR], &tmp);
                             if (wj < wt) {
                                 --tL;
                                 wt = wj;
@@ -314,7 +323,7 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
                                 ++i;
                             }
                         } else {  // i == tL: (target, right neighbour)
-                            const int wj = block_opt(c, B[tL], BE[tR + 1], &tmp);
+                            const int wj = merged(B[tL], BE[tR + 1], &tmp);
                             if (wj < wt) {
                                 ++tR;
                                 wt = wj;

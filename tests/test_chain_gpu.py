@@ -127,3 +127,21 @@ def test_chain_batch_infeasible_status(gpu):
     occ = sample_chains(7, 4, 64, 10)
     out = gpu.solve_1d_batch(occ, 4, 64, 10, 40)
     assert (out["status"] == 2).all()
+
+
+def test_band_batch_sweep_stress(gpu, ref):
+    """Batched band kernel vs the reference over many shapes and loadings,
+    from barely feasible (long certification sweeps, many blocks, cost ties)
+    to dense."""
+    rng = np.random.default_rng(0xc4a1)
+    for _ in range(40):
+        n = int(rng.integers(8, 700))
+        w = int(rng.integers(1, n + 1))
+        tl = int(rng.integers(0, n - w + 1))
+        k = int(rng.integers(w, n + 1)) if rng.integers(0, 2) else min(n, w + int(rng.integers(0, 4)))
+        count = 256
+        occ = sample_chains(int(rng.integers(0, 1 << 30)), count, n, k)
+        g = gpu.solve_1d_batch(occ, count, n, tl, tl + w - 1)
+        r = ref.solve_1d_batch(occ, count, n, tl, tl + w - 1)
+        for key in g:
+            assert np.array_equal(g[key], r[key]), (n, w, tl, k, key)
