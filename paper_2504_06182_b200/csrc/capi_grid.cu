@@ -49,8 +49,8 @@ bool shape_for(Ctx *c, int solver, int W, int H, int hp, int count, GridShape &s
     if (const char *e = getenv("RECON_GRID_WARPS")) w = std::max(1, std::min(32, atoi(e)));
     const int floor_w = std::min(kWarps, w);
     for (; w >= floor_w; w /= 2)
-        if (grid_shape(W, H, hp, w, s)) return true;
-    return grid_shape(W, H, hp, kWarps, s);
+        if (grid_shape(W, H, hp, w, solver, s)) return true;
+    return grid_shape(W, H, hp, kWarps, solver, s);
 }
 
 int grid_blocks(Ctx *c, int solver, const GridShape &s, int count) {

@@ -35,31 +35,29 @@ __host__ __device__ inline void grid_smem_layout(const GridShape &s, GridSmem &o
         off += bytes;
         return at;
     };
+    // arrays only one executor touches get no space in the other's layout
+    // (solver 0 = red-rec executor, 1 = bird, else both)
+    const int64_t R = s.solver != 1, Bd = s.solver != 0;
     o.dep = take((int64_t)s.W * s.wpd * 8, 16);
-    const int64_t keys_a = (int64_t)s.nwarps * 2 * s.LK * 4, keys_b = (int64_t)s.W * 8;
-    o.keys = take(keys_a > keys_b ? keys_a : keys_b, 16);
-    o.bal = take((int64_t)2 * s.nchunk * 64 * 4, 16);
+    const int64_t keys_a = (int64_t)s.nwarps * 2 * s.LK * 4;
+    o.keys = take(R * keys_a, 16);
+    o.bal = take(Bd * 2 * s.nchunk * 64 * 4, 16);
     o.sigma = take((int64_t)s.W * 4, 16);
     o.ev_count = take((int64_t)s.W * 4, 16);
     o.ev_off = take((int64_t)(s.W + 1) * 4, 16);
-    o.wave_off = take((int64_t)(s.W + 2) * 4, 16);
-    o.lvl_t = take((int64_t)s.LT * 4, 16);
-    o.lvl_b = take((int64_t)s.LB * 4, 16);
+    o.wave_off = take(R * (s.W + 2) * 4, 16);
+    o.lvl_t = take(Bd * s.LT * 4, 16);
+    o.lvl_b = take(Bd * s.LB * 4, 16);
     o.scal = take(32 * 8, 16);
     o.lists = take((int64_t)s.nwarps * 4 * s.LK * 2, 16);
-    o.plists = take((int64_t)2 * s.LK * 2, 16);
-    o.mark_next = take((int64_t)s.W * 2, 16);
+    o.plists = take(Bd * 2 * s.LK * 2, 16);
+    o.mark_next = take(R * s.W * 2, 16);
     o.mark_head = take((int64_t)s.W * 2, 16);
     o.ev_col = take((int64_t)s.W * 2, 16);
-    o.ev_aux = take((int64_t)s.W * 2, 16);
-    o.ev_a = take((int64_t)s.W * 2, 16);
-    o.ev_nr = take((int64_t)s.W * 2, 16);
-    o.ev_nl = take((int64_t)s.W * 2, 16);
-    o.ev_level = take((int64_t)s.W * 2, 16);
-    o.wave_list = take((int64_t)s.W * 2, 16);
-    o.lastc = take((int64_t)s.W * 2, 16);
-    o.lastm = take((int64_t)s.W * 2, 16);
-    o.ev_type = take(s.W, 16);
+    o.ev_aux = take(R * s.W * 2, 16);
+    o.ev_a = take(Bd * s.W * 2, 16);
+    o.wave_list = take(R * s.W * 2, 16);
+    o.ev_type = take(R * s.W, 16);
     o.solved = take(s.W, 16);
     o.total = align_up(off, 16);
 }
@@ -223,7 +221,7 @@ struct Block {
     uint64_t *dep;
     uint32_t *keys, *bal;
     int *sigma, *ev_count, *ev_off, *wave_off, *lvl_t, *lvl_b, *scal;
-    int16_t *lists, *plists, *mark_next, *mark_head, *ev_col, *ev_aux, *ev_a, *ev_nr, *ev_nl, *ev_level, *wave_list, *lastc, *lastm;
+    int16_t *lists, *plists, *mark_next, *mark_head, *ev_col, *ev_aux, *ev_a, *wave_list;
     uint8_t *ev_type, *solved;
 };
 
@@ -248,12 +246,7 @@ __device__ __forceinline__ Block carve(const GridShape &s, unsigned char *smem) 
     b.ev_col = (int16_t *)(smem + o.ev_col);
     b.ev_aux = (int16_t *)(smem + o.ev_aux);
     b.ev_a = (int16_t *)(smem + o.ev_a);
-    b.ev_nr = (int16_t *)(smem + o.ev_nr);
-    b.ev_nl = (int16_t *)(smem + o.ev_nl);
-    b.ev_level = (int16_t *)(smem + o.ev_level);
     b.wave_list = (int16_t *)(smem + o.wave_list);
-    b.lastc = (int16_t *)(smem + o.lastc);
-    b.lastm = (int16_t *)(smem + o.lastm);
     b.ev_type = (uint8_t *)(smem + o.ev_type);
     b.solved = (uint8_t *)(smem + o.solved);
     return b;

@@ -27,7 +27,7 @@ template <bool LAT>
 __global__ void bird_kernel(GridParams p);
 static void (*bird_exec(const GridShape &s))(GridParams) { return s.nwarps > 8 ? bird_kernel<true> : bird_kernel<false>; }
 
-bool grid_shape(int W, int H, int k, int nwarps, GridShape &s) {
+bool grid_shape(int W, int H, int k, int nwarps, int solver, GridShape &s) {
     if (W <= 0 || H <= 0 || W > 1024 || H > 1024) return false;
     s.W = W;
     s.H = H;
@@ -42,6 +42,7 @@ bool grid_shape(int W, int H, int k, int nwarps, GridShape &s) {
     s.LB = (int)align_up((H - 1 - hi) + W - 1 + 64, 64);
     s.nchunk = (2 * W - 1 + 31) / 32;
     s.nwarps = nwarps;
+    s.solver = solver;
     s.lo = lo;
     s.hi = hi;
     GridSmem o;

@@ -16,12 +16,13 @@ struct GridShape {
     int nchunk;       // 32-slot chunks covering 2W-1 group-order slots
     int nwarps;
     int lo, hi;       // band depths (rows from the top)
+    int solver;       // executor the shared-memory layout is for: 0 red-rec, 1 bird
     int64_t smem_bytes;
 };
 
 struct GridSmem {
     int64_t dep, keys, bal, sigma, ev_count, ev_off, wave_off, lvl_t, lvl_b, scal, lists, plists, mark_next, mark_head,
-        ev_col, ev_aux, ev_a, ev_nr, ev_nl, ev_level, wave_list, lastc, lastm, ev_type, solved, total;
+        ev_col, ev_aux, ev_a, wave_list, ev_type, solved, total;
 };
 
 // red-rec plans in global memory (redrec_plan_kernel -> redrec_kernel), per
@@ -46,7 +47,7 @@ struct GridParams {
     long long *phase_clock;  // optional: clock64 at phase boundaries of instance 0 (profiling)
 };
 
-bool grid_shape(int W, int H, int k, int nwarps, GridShape &s);
+bool grid_shape(int W, int H, int k, int nwarps, int solver, GridShape &s);
 // ev (optional): events recorded before the planner, before and after the
 // executor (bird: the last two)
 cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaStream_t stream,
