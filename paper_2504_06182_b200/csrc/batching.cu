@@ -159,7 +159,7 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t *a, int n, int x) {
 // the only possible vertex conflict inside a batch is a shared destination;
 // the minimum id wins (and, under column_direction, the class of the first
 // accepted move).  The general entry point keeps the literal pairwise checks.
-template <class Paths, bool FAST, bool SM = false>
+template <class Paths, bool FAST, bool SM = false, bool LOG = false>
 __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
     const int lane = lane_id();
     const int P = J.P, H = J.H;
@@ -191,7 +191,7 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
     }
     __syncwarp();
     int32_t *ready = s.ready, *ready2 = s.ready2;
-    int nb = 0, status = RECON_OK;
+    int nb = 0, nlog = 0, status = RECON_OK;
     // Register-resident frontier (FAST path, <= 32 ready paths): lane i keeps
     // ready path i (ascending id) with its step and endpoints in registers, so
     // a batch costs one occupancy probe plus fire-and-forget atomics.
@@ -235,10 +235,16 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
             if (a) occ.set(to);
             bool fin = false;
             if (a) {
-                J.move_batch[lp.base + lp.k] = nb;
+                if (LOG) {
+                    const int r = __popc(acc & lanemask_lt());
+                    J.mlog[nlog + r] = (int)lp.base + lp.k | (r == 0 ? (int)0x80000000u : 0);
+                } else {
+                    J.move_batch[lp.base + lp.k] = nb;
+                }
                 ++lp.k;
                 fin = lp.k == lp.len;
             }
+            nlog += __popc(acc);
             left -= __popc(acc);
             const unsigned fm = __ballot_sync(FULL, fin);
             if (fm) {
@@ -428,11 +434,12 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
                 inb.set(fr);
                 inb.set(to);
                 // advance the accepted path here, while its state is in registers
-                J.move_batch[paths.move_base(p) + k] = nb;
+                const int slot = nacc + __popc(acc & lanemask_lt());
+                if (LOG) J.mlog[nlog + slot] = (int)(paths.move_base(p) + k) | (slot == 0 ? (int)0x80000000u : 0);
+                else J.move_batch[paths.move_base(p) + k] = nb;
                 s.next[p] = k + 1;
                 const bool fin = k + 1 == paths.len(p);
                 if (fin) s.done[p] = 1;
-                const int slot = nacc + __popc(acc & lanemask_lt());
                 s.mem[slot] = fin ? (int)(0x80000000u | (unsigned)p) : p;  // bit 31: path finished
                 s.mfr[slot] = fr;
                 s.mto[slot] = to;
@@ -503,6 +510,7 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
             __syncwarp();
         }
         left -= nacc;
+        nlog += nacc;
         __syncwarp();
         if (!J.edge_level && (nfin > 0 || nnew > 0)) {
             // ready' = (ready - finished) U newly, sorted
@@ -547,6 +555,7 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
         if (REG && nready <= 32) enter_regmode();
     }
     if (lane == 0) {
+        if (J.nlog) *J.nlog = nlog;
         *J.batch_count = status == RECON_OK ? nb : 0;
         *J.status = status;
         if (J.detail) *J.detail = status == RECON_OK ? 0 : RECON_D_BATCH_NO_PROGRESS;
@@ -742,7 +751,7 @@ size_t pipeline_temp_bytes(int64_t n) {
     return t;
 }
 
-cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *edges_host) {
+cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *counts_host) {
     const int64_t S = (int64_t)a.W * a.k, WH = (int64_t)a.W * a.H, N = (int64_t)a.count * S;
     cudaMemsetAsync(a.source_of, 0xff, (size_t)a.count * WH * 4, st);
     cudaMemsetAsync(a.target_of, 0xff, (size_t)a.count * WH * 4, st);
@@ -760,14 +769,19 @@ cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *
     cudaMemsetAsync(a.mbase + N, 0, 8, st);
     tb = a.temp_bytes;
     cub::DeviceScan::ExclusiveSum(a.temp, tb, a.mbase, a.mbase, (int)(N + 1), st);
-    cudaError_t e = cudaMemcpyAsync(edges_host, a.soff + N, 8, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaMemcpyAsync(counts_host, a.soff + N, 8, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyAsync(counts_host + 1, a.mbase + N, 8, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) return e;
     e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
-__global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a, int occ_in_smem) {
+// MODE 0: bitmaps in global memory; 1: bitmaps in shared memory; 2: 1 + move log
+template <int MODE>
+__global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) {
+    constexpr bool occ_in_smem = MODE >= 1;
     extern __shared__ __align__(16) uint32_t bsmem[];
     const int64_t S = (int64_t)a.W * a.k, nwb = ((int64_t)a.W * a.H + 31) / 32;
     const int nw = blockDim.x >> 5;
@@ -819,12 +833,51 @@ __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a, 
         J.s.mto = a.mto + o;
         J.s.counter = a.counter + inst;
         J.move_batch = a.move_batch + (int64_t)inst * a.move_stride;
+        if (MODE == 2) {
+            J.mlog = a.mlog + a.mbase[o];
+            J.nlog = a.counter + inst;
+        }
         J.batch_count = a.batch_count + inst;
         J.status = a.status + inst;
         J.detail = a.detail ? a.detail + inst : nullptr;
         ImplicitPaths ip{a.path_src + o, a.path_dst + o, a.mbase + o, a.mbase[o], a.H};
-        if (occ_in_smem) batch_warp<ImplicitPaths, true, true>(J, ip);
-        else batch_warp<ImplicitPaths, true, false>(J, ip);
+        batch_warp<ImplicitPaths, true, MODE >= 1, MODE == 2>(J, ip);
+    }
+}
+
+// move log -> move_batch, one CTA per instance: a batch index is the number
+// of batch-start flags up to the entry, minus one.  The instance's move_batch
+// region is written within one CTA's pass, so L2 merges the scattered 4-byte
+// stores into full sectors before they reach DRAM.
+__global__ void __launch_bounds__(256) pipeline_scatter_moves(PipelineArgs a) {
+    __shared__ int wsum[8];
+    __shared__ int carry;
+    const int lane = lane_id(), warp = warp_id();
+    for (int inst = blockIdx.x; inst < a.count; inst += gridDim.x) {
+        const int n = a.counter[inst];
+        const int32_t *log = a.mlog + a.mbase[(int64_t)inst * a.W * a.k];
+        int32_t *mb = a.move_batch + (int64_t)inst * a.move_stride;
+        if (threadIdx.x == 0) carry = -1;
+        __syncthreads();
+        for (int i0 = 0; i0 < n; i0 += 256) {
+            const int i = i0 + threadIdx.x;
+            const int v = i < n ? __ldcs(log + i) : 0;
+            const int f = v < 0;
+            int incl = f;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) wsum[warp] = incl;
+            __syncthreads();
+            int before = carry;
+            for (int w = 0; w < warp; ++w) before += wsum[w];
+            if (i < n) mb[v & 0x7fffffff] = before + incl;
+            __syncthreads();
+            if (threadIdx.x == 255) carry = before + incl;
+            __syncthreads();
+        }
     }
 }
 
@@ -844,10 +897,14 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
         warps = (int)std::max<int64_t>(1, std::min<int64_t>(8, (200 * 1024) / bm_bytes));
         occ_smem = 1;
         smem = (size_t)warps * bm_bytes;
-        cudaFuncSetAttribute(batch_pipeline_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(batch_pipeline_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(batch_pipeline_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
     const int grid = (int)std::min<int64_t>(((int64_t)a.count + warps - 1) / warps, (int64_t)sms * 32);
-    batch_pipeline_kernel<<<grid, warps * 32, smem, st>>>(a, occ_smem);
+    if (!occ_smem) batch_pipeline_kernel<0><<<grid, warps * 32, smem, st>>>(a);
+    else if (!a.mlog) batch_pipeline_kernel<1><<<grid, warps * 32, smem, st>>>(a);
+    else batch_pipeline_kernel<2><<<grid, warps * 32, smem, st>>>(a);
+    if (a.mlog) pipeline_scatter_moves<<<(int)std::min<int64_t>(a.count, (int64_t)sms * 8), 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 

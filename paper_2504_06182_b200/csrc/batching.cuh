@@ -27,6 +27,10 @@ struct BatchJob {
     const int64_t *in_need;
     BatchScratch s;
     int32_t *move_batch;  // path-major, one per elementary move
+    // move log (pipeline): accepted moves' path-major slots in batch order, bit
+    // 31 on a batch's first entry; pipeline_scatter_moves turns it into
+    // move_batch.  Null: move_batch is written directly.
+    int32_t *mlog, *nlog;
     int32_t *batch_count, *status, *detail;
 };
 
@@ -61,14 +65,16 @@ struct PipelineArgs {
     uint32_t *occ, *inb;                 // [count * ceil(W*H/32)]
     int32_t *next, *ready, *ready2, *newly, *mem, *mfr, *mto;  // [count * W*k]
     uint8_t *done;                       // [count * W*k]
-    int32_t *counter;                    // [count]
+    int32_t *counter;                    // [count] move-log length
+    int32_t *mlog;                       // [total moves] move log, instance i at mbase[i*W*k]
     const uint64_t *grid_occ;            // [count * W * wpc] initial occupancy (occ bits)
     void *temp;
     size_t temp_bytes;
 };
 
 size_t pipeline_temp_bytes(int64_t n);
-cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *edges_host);
+// counts_host[0] = DAG edges, counts_host[1] = elementary moves (all instances)
+cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *counts_host);
 cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t st);
 
 // occ bits (column-major, bit y) -> vertex-id bitmap

@@ -2,6 +2,7 @@
 // batching pipeline over device-resident instances.
 
 #include <algorithm>
+#include <cstdlib>
 #include <cub/device/device_scan.cuh>
 #include <vector>
 
@@ -106,12 +107,26 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool 
     a.temp_bytes = pipeline_temp_bytes((int64_t)(n * S + 1));
     a.temp = c->get(S_TEMP, a.temp_bytes);
     if (!a.temp) return cuda_fail(cudaErrorMemoryAllocation, "pipeline temp", detail);
-    int64_t edges = 0;
-    CK(pipeline_dag_count(a, c->stream, &edges), "pipeline dag");
+    int64_t counts[2] = {0, 0};
+    CK(pipeline_dag_count(a, c->stream, counts), "pipeline dag");
     c->launches += 5;
+    const int64_t edges = counts[0];
     a.succ = c->dev<int32_t>(S_BM_AUX5, (size_t)edges + 1);
     a.edge_capacity = edges;
     if (!a.succ) return cuda_fail(cudaErrorMemoryAllocation, "pipeline succ", detail);
+    // move log (pipeline_scatter_moves) for many small instances, whose
+    // scattered move_batch stores otherwise miss L2 one 4-byte store at a time;
+    // large instances write move_batch directly.  RECON_BATCH_LOG=0/1 forces.
+    static const int log_env = [] {
+        const char *e = getenv("RECON_BATCH_LOG");
+        return e ? atoi(e) : -1;
+    }();
+    const bool use_log = log_env >= 0 ? log_env == 1 : (n >= (size_t)c->sms * 4 && 2 * nwb * 4 <= 96 * 1024);
+    a.mlog = nullptr;
+    if (use_log) {
+        a.mlog = c->dev<int32_t>(S_BM_AUX6, (size_t)counts[1] + 1);
+        if (!a.mlog) return cuda_fail(cudaErrorMemoryAllocation, "pipeline move log", detail);
+    }
     CK(pipeline_run_batching(a, c->sms, c->stream), "pipeline batching");
     c->launches += 3;
     if (!host) return RECON_OK;

@@ -52,7 +52,12 @@ def grid(solver, W, H, hp, k, seed, count):
     mn, avg = timeit(lambda: fn(lib.ctx(), C.byref(b)))
     assert int((st != 0).sum()) == 0
     P = int(pc.sum())
-    return {"ms": mn, "grids_per_s": count / mn * 1e3, "us_per_grid": mn * 1e3 / count,
+    lib.set_kernel_timing(True)
+    fn(lib.ctx(), C.byref(b))
+    torch.cuda.synchronize()
+    kt = lib.kernel_times()
+    lib.set_kernel_timing(False)
+    return {"ms": mn, "plan_ms": kt[0], "exec_ms": kt[1], "grids_per_s": count / mn * 1e3, "us_per_grid": mn * 1e3 / count,
             "paths_per_grid": P / count, "GBps_alg": (count * W * H / 8 + 8 * P + 32 * count) / mn / 1e6}
 
 
@@ -154,6 +159,10 @@ CASES = {
     "c4_bird_2048": lambda: grid("bird", 256, 256, 153, 39322, 0x25600000, 2048),
     "r256_redrec_b2048": lambda: grid("redrec", 256, 256, 153, 39322, 0x25600000, 2048),
     "r256_bird_b2048": lambda: grid("bird", 256, 256, 153, 39322, 0x25600000, 2048),
+    "r256_redrec_b1776": lambda: grid("redrec", 256, 256, 153, 39322, 0x25600000, 1776),
+    "r256_redrec_b2368": lambda: grid("redrec", 256, 256, 153, 39322, 0x25600000, 2368),
+    "r256_redrec_b8192": lambda: grid("redrec", 256, 256, 153, 39322, 0x25600000, 8192),
+    "r256_bird_b8192": lambda: grid("bird", 256, 256, 153, 39322, 0x25600000, 8192),
     "c3_bird_solve": lambda: grid("bird", 64, 64, 40, 2662, 0x64000000, 4096),
     "c3_redrec_solve": lambda: grid("redrec", 64, 64, 40, 2662, 0x64000000, 4096),
     "r128_redrec_b4096": lambda: grid("redrec", 128, 128, 76, 9830, 0x12800000, 4096),
