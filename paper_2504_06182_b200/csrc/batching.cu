@@ -740,6 +740,158 @@ __global__ void pl_walk_kernel(PipelineArgs a) {
     }
 }
 
+// ---- small instances: the occupancy DAG per instance in one CTA, with the
+// source / target maps and the degree counters in shared memory (the global
+// variant above walks every path twice through L2-missing maps and atomics).
+// PASS 0 counts degrees (indeg, outdeg to global) and the instance's edge and
+// move totals; PASS 1 lays out soff / mbase from the instance bases and fills
+// the successor lists.
+
+__host__ __device__ inline int64_t al16(int64_t x) { return (x + 15) / 16 * 16; }
+
+int64_t pipeline_small_dag_smem(int W, int H, int k) {
+    const int64_t WH = (int64_t)W * H, S = (int64_t)W * k;
+    if (S >= 32768) return 0;  // int16 maps
+    const int64_t bytes = al16(WH * 2 * 2) + (2 * S + 2) * 4 + 64;
+    return bytes <= 160 * 1024 ? bytes : 0;
+}
+
+// exclusive scan of v over the CTA (256 threads) in chunk order; returns the
+// chunk total through *tot (all threads)
+__device__ __forceinline__ int cta_excl_scan256(int v, int *wsum, int *tot) {
+    const int lane = lane_id(), warp = warp_id();
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        before += w < warp ? wsum[w] : 0;
+        all += wsum[w];
+    }
+    __syncthreads();
+    *tot = all;
+    return before + incl - v;
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(256) pl_dag_small_kernel(PipelineArgs a) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ int wsum[8];
+    const int W = a.W, H = a.H, WH = W * H, S = W * a.k;
+    int16_t *so = (int16_t *)dsm, *to = so + WH;
+    int *deg0 = (int *)(dsm + al16((int64_t)WH * 4)), *deg1 = deg0 + S + 1;
+    for (int inst = blockIdx.x; inst < a.count; inst += gridDim.x) {
+        const int64_t o = (int64_t)inst * S;
+        const int P = a.solve_status[inst] != 0 ? 0 : a.path_count[inst];
+        const int32_t *src = a.path_src + o, *dst = a.path_dst + o;
+        for (int v = threadIdx.x; v < WH; v += blockDim.x) so[v] = to[v] = -1;
+        for (int p = threadIdx.x; p <= S; p += blockDim.x) deg0[p] = deg1[p] = 0;
+        __syncthreads();
+        for (int p = threadIdx.x; p < P; p += blockDim.x) {
+            so[src[p]] = (int16_t)p;
+            to[dst[p]] = (int16_t)p;
+        }
+        if (PASS == 1) {
+            // local CSR offsets (deg0) from the out-degrees of pass 0
+            int run = 0;
+            for (int p0 = 0; p0 < P; p0 += blockDim.x) {
+                const int p = p0 + threadIdx.x;
+                int tot;
+                const int ex = cta_excl_scan256(p < P ? a.outdeg[o + p] : 0, wsum, &tot);
+                if (p < P) deg0[p] = run + ex;
+                run += tot;
+            }
+        }
+        __syncthreads();
+        const int64_t eb = PASS == 1 ? a.ebase[inst] : 0;
+        int moves = 0;
+        for (int i = threadIdx.x; i < P; i += blockDim.x) {
+            const int32_t s = src[i], tt = dst[i];
+            const int xs = s / H, ys = s % H, xt = tt / H, yt = tt % H;
+            moves += abs(xt - xs) + abs(yt - ys);
+            const int dx = xt > xs ? 1 : -1, dy = yt > ys ? 1 : -1;
+            int x = xs, y = ys;
+            for (;;) {
+                const int v = x * H + y;
+                const int pa = so[v];
+                if (pa >= 0 && pa != i) {  // (pa, i)
+                    if (PASS == 0) {
+                        atomicAdd(&deg0[pa], 1);
+                        atomicAdd(&deg1[i], 1);
+                    } else {
+                        a.succ[eb + deg0[pa] + atomicAdd(&deg1[pa], 1)] = i;
+                    }
+                }
+                const int pb = to[v];
+                if (pb >= 0 && pb != i && !on_path2(H, src[pb], dst[pb], s)) {  // (i, pb)
+                    if (PASS == 0) {
+                        atomicAdd(&deg0[i], 1);
+                        atomicAdd(&deg1[pb], 1);
+                    } else {
+                        a.succ[eb + deg0[i] + atomicAdd(&deg1[i], 1)] = pb;
+                    }
+                }
+                if (x != xt) x += dx;
+                else if (y != yt) y += dy;
+                else break;
+            }
+        }
+        __syncthreads();
+        if (PASS == 0) {
+            int edges = 0;
+            for (int p = threadIdx.x; p < P; p += blockDim.x) {
+                a.outdeg[o + p] = deg0[p];
+                a.indeg[o + p] = deg1[p];
+                edges += deg0[p];
+            }
+            edges = warp_sum(edges);
+            moves = warp_sum(moves);
+            if (lane_id() == 0) wsum[warp_id()] = edges;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int e = 0;
+                for (int w = 0; w < 8; ++w) e += wsum[w];
+                a.inst_edges[inst] = e;
+            }
+            __syncthreads();
+            if (lane_id() == 0) wsum[warp_id()] = moves;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int m = 0;
+                for (int w = 0; w < 8; ++w) m += wsum[w];
+                a.inst_moves[inst] = m;
+            }
+        } else {
+            // soff / mbase: instance base + local prefix, for p in [0, P]
+            // (p = P is the instance's end, which the batching reads)
+            const int64_t mb = a.mvbase[inst];
+            int run = 0;
+            for (int p0 = 0; p0 <= P; p0 += blockDim.x) {
+                const int p = p0 + threadIdx.x;
+                int len = 0;
+                if (p < P) {
+                    const int32_t s = src[p], tt = dst[p];
+                    len = abs(tt / H - s / H) + abs(tt % H - s % H);
+                }
+                int tot;
+                const int ex = cta_excl_scan256(len, wsum, &tot);
+                if (p <= P) {
+                    a.soff[o + p] = eb + (p < P ? deg0[p] : a.inst_edges[inst]);
+                    a.mbase[o + p] = mb + run + ex;
+                }
+                run += tot;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void widen32_kernel(int64_t n, const int32_t *in, int64_t *out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         out[i] = in[i];
@@ -753,6 +905,26 @@ size_t pipeline_temp_bytes(int64_t n) {
 
 cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *counts_host) {
     const int64_t S = (int64_t)a.W * a.k, WH = (int64_t)a.W * a.H, N = (int64_t)a.count * S;
+    if (a.small_dag) {
+        const int64_t smem = pipeline_small_dag_smem(a.W, a.H, a.k);
+        cudaFuncSetAttribute(pl_dag_small_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(pl_dag_small_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int grid = (int)std::min<int64_t>(a.count, 148 * 16);
+        pl_dag_small_kernel<0><<<grid, 256, smem, st>>>(a);
+        cudaMemsetAsync(a.inst_edges + a.count, 0, 8, st);
+        cudaMemsetAsync(a.inst_moves + a.count, 0, 8, st);
+        size_t tb = a.temp_bytes;
+        cub::DeviceScan::ExclusiveSum(a.temp, tb, a.inst_edges, a.ebase, a.count + 1, st);
+        tb = a.temp_bytes;
+        cub::DeviceScan::ExclusiveSum(a.temp, tb, a.inst_moves, a.mvbase, a.count + 1, st);
+        cudaError_t e = cudaMemcpyAsync(counts_host, a.ebase + a.count, 8, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) return e;
+        e = cudaMemcpyAsync(counts_host + 1, a.mvbase + a.count, 8, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) return e;
+        e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return e;
+        return cudaGetLastError();
+    }
     cudaMemsetAsync(a.source_of, 0xff, (size_t)a.count * WH * 4, st);
     cudaMemsetAsync(a.target_of, 0xff, (size_t)a.count * WH * 4, st);
     cudaMemsetAsync(a.outdeg, 0, (size_t)N * 4, st);
@@ -884,7 +1056,12 @@ __global__ void __launch_bounds__(256) pipeline_scatter_moves(PipelineArgs a) {
 cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t st) {
     const int64_t S = (int64_t)a.W * a.k, N = (int64_t)a.count * S, nwb = ((int64_t)a.W * a.H + 31) / 32;
     const int blocks = 148 * 8;
-    pl_walk_kernel<1><<<blocks, 256, 0, st>>>(a);
+    if (a.small_dag) {
+        const int64_t smem = pipeline_small_dag_smem(a.W, a.H, a.k);
+        pl_dag_small_kernel<1><<<(int)std::min<int64_t>(a.count, 148 * 16), 256, smem, st>>>(a);
+    } else {
+        pl_walk_kernel<1><<<blocks, 256, 0, st>>>(a);
+    }
     occ_to_vertex_bits<<<blocks, 256, 0, st>>>(a.count, a.W, a.H, a.grid_occ, a.occ);
     cudaMemsetAsync(a.inb, 0, (size_t)a.count * nwb * 4, st);
     cudaMemsetAsync(a.counter, 0, (size_t)a.count * 4, st);

@@ -67,6 +67,10 @@ struct PipelineArgs {
     uint8_t *done;                       // [count * W*k]
     int32_t *counter;                    // [count] move-log length
     int32_t *mlog;                       // [total moves] move log, instance i at mbase[i*W*k]
+    // small instances (pipeline_small_dag): per-instance edge / move totals and
+    // their exclusive scans over instances, [count + 1] each
+    int small_dag;
+    int64_t *inst_edges, *inst_moves, *ebase, *mvbase;
     const uint64_t *grid_occ;            // [count * W * wpc] initial occupancy (occ bits)
     void *temp;
     size_t temp_bytes;
@@ -76,6 +80,8 @@ size_t pipeline_temp_bytes(int64_t n);
 // counts_host[0] = DAG edges, counts_host[1] = elementary moves (all instances)
 cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *counts_host);
 cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t st);
+// shared memory of the per-instance DAG builder, or 0 when an instance does not fit
+int64_t pipeline_small_dag_smem(int W, int H, int k);
 
 // occ bits (column-major, bit y) -> vertex-id bitmap
 __global__ void occ_to_vertex_bits(int count, int W, int H, const uint64_t *occ, uint32_t *bits);

@@ -72,7 +72,7 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool 
     a.grid_occ = g.occ;
     const size_t nwb = (WH + 31) / 32;
     int32_t *i32 = c->dev<int32_t>(S_BM_AUX0, n * WH * 2 + n * S * 10 + n * 2 + 8);
-    int64_t *i64 = c->dev<int64_t>(S_BM_AUX1, (n * S + 1) * 2 + 4);
+    int64_t *i64 = c->dev<int64_t>(S_BM_AUX1, (n * S + 1) * 2 + 4 * (n + 1) + 4);
     uint32_t *bits = c->dev<uint32_t>(S_BM_AUX2, n * nwb * 2 + 4);
     uint8_t *done = c->dev<uint8_t>(S_BM_AUX3, n * S + 16);
     int32_t *mb = host ? c->dev<int32_t>(S_BM_OUT, n * (size_t)pb->move_stride) : pb->move_batch;
@@ -97,6 +97,15 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool 
     a.counter = q + 10 * n * S;
     a.soff = i64;
     a.mbase = i64 + n * S + 1;
+    static const int small_env = [] {
+        const char *e = getenv("RECON_SMALL_DAG");
+        return e ? atoi(e) : 1;
+    }();
+    a.small_dag = small_env && pipeline_small_dag_smem(a.W, a.H, a.k) > 0;
+    a.inst_edges = i64 + 2 * (n * S + 1);
+    a.inst_moves = a.inst_edges + (n + 1);
+    a.ebase = a.inst_moves + (n + 1);
+    a.mvbase = a.ebase + (n + 1);
     a.occ = bits;
     a.inb = bits + n * nwb;
     a.done = done;
