@@ -950,6 +950,394 @@ cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *
     return cudaGetLastError();
 }
 
+// --------------------------------------------------------------------------
+// pipeline batching with the ready list as records
+// --------------------------------------------------------------------------
+// A ready path is a record {p (-1 once finished), k | len << 16,
+// xs | ys << 16, xt | yt << 16} plus its move base in a parallel array, kept
+// in ascending p.  A batch reads its candidates with coalesced loads and
+// advances them in place; only newly released paths touch the per-path
+// arrays (src, dst, mbase).  Same acceptance, application and release as
+// batch_warp (FAST, implicit paths); records replace next / done / ready ids.
+
+__device__ __forceinline__ int4 make_rec(const ImplicitPaths &ip, int p, int *base) {
+    const int s = ip.src[p], t = ip.dst[p];
+    const int xs = s / ip.H, ys = s - xs * ip.H, xt = t / ip.H, yt = t - xt * ip.H;
+    const int len = abs(xt - xs) + abs(yt - ys);
+    *base = (int)ip.move_base(p);
+    return make_int4(p, len << 16, xs | (ys << 16), xt | (yt << 16));
+}
+
+__device__ __forceinline__ LanePath rec_lane(int4 r, int base) {
+    LanePath l;
+    l.p = r.x;
+    l.k = r.y & 0xffff;
+    l.len = r.y >> 16;
+    l.xs = r.z & 0xffff;
+    l.ys = r.z >> 16;
+    l.xt = r.w & 0xffff;
+    l.yt = r.w >> 16;
+    l.base = base;
+    return l;
+}
+
+__device__ __forceinline__ int4 lane_rec(const LanePath &l) {
+    return make_int4(l.p, l.k | (l.len << 16), l.xs | (l.ys << 16), l.xt | (l.yt << 16));
+}
+
+// #records with p < x in a p-ascending record array
+__device__ __forceinline__ int lower_bound_rec(const int4 *a, int n, int x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if (a[m].x < x) lo = m + 1;
+        else hi = m;
+    }
+    return lo;
+}
+
+// successors of the finished paths (fin lanes, CSR range [q0, q1)) lose one
+// blocker; the released ones are appended to newly; returns the new count
+__device__ __forceinline__ int release_successors(const BatchJob &J, int32_t *blockers, int32_t *newly, int nnew,
+                                                  bool fin, int64_t q0, int64_t q1) {
+    const int lane = lane_id();
+    if (!fin) q0 = q1 = 0;
+    int tot;
+    const int base = warp_excl_scan((int)(q1 - q0), &tot);
+    for (int t0 = 0; t0 < tot; t0 += 32) {
+        const int t = t0 + lane;
+        int owner = 0;  // largest lane with base <= t
+#pragma unroll
+        for (int st = 16; st > 0; st >>= 1) {
+            const int cl = owner + st;
+            if (__shfl_sync(FULL, base, cl) <= t) owner = cl;
+        }
+        const int64_t oq0 = __shfl_sync(FULL, q0, owner);
+        const int ob = __shfl_sync(FULL, base, owner);
+        bool released = false;
+        int sc = -1;
+        if (t < tot) {
+            sc = J.succ[oq0 + (t - ob)];
+            released = atomicSub(&blockers[sc], 1) == 1;
+        }
+        const unsigned rm = __ballot_sync(FULL, released);
+        if (released) newly[nnew + __popc(rm & lanemask_lt())] = sc;
+        nnew += __popc(rm);
+    }
+    return nnew;
+}
+
+// sorts newly[0, n) ascending in place (mem: scratch of n)
+__device__ __forceinline__ void sort_newly(int32_t *newly, int32_t *mem, int n) {
+    const int lane = lane_id();
+    if (n <= 32) {
+        int v = lane < n ? newly[lane] : INT_MAX;
+        v = warp_sort32(v);
+        if (lane < n) newly[lane] = v;
+    } else {
+        for (int q = lane; q < n; q += 32) {
+            const int x = newly[q];
+            int lt = 0;
+            for (int r2 = 0; r2 < n; ++r2) lt += newly[r2] < x;
+            mem[lt] = x;
+        }
+        __syncwarp();
+        for (int q = lane; q < n; q += 32) newly[q] = mem[q];
+    }
+    __syncwarp();
+}
+
+// ready = (kept records rec2[0, nkeep)) U (records of newly[0, nnew)), by rank
+__device__ __forceinline__ void merge_ready(const ImplicitPaths &paths, const PipeRecords &R, const int32_t *newly,
+                                            int nkeep, int nnew) {
+    const int lane = lane_id();
+    for (int i = lane; i < nkeep; i += 32) {
+        const int4 x = R.rec2[i];
+        const int at = i + lower_bound_i32(newly, nnew, x.x);
+        R.rec[at] = x;
+        R.rb[at] = R.rb2[i];
+    }
+    for (int j = lane; j < nnew; j += 32) {
+        const int y = newly[j];
+        int b;
+        const int4 r = make_rec(paths, y, &b);
+        const int at = j + lower_bound_rec(R.rec2, nkeep, y);
+        R.rec[at] = r;
+        R.rb[at] = b;
+    }
+    __syncwarp();
+}
+
+template <bool SM, bool LOG>
+__device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, const PipeRecords R) {
+    const int lane = lane_id();
+    const int P = J.P, H = J.H;
+    BatchScratch s = J.s;
+    const Bits<SM> occ(s.occ), inb(s.inb);
+    // ---- init: blockers = in-degree (given); zero-length paths finish at once
+    long long left = 0;
+    for (int p = lane; p < P; p += 32) {
+        const int len = paths.len(p);
+        left += len;
+        if (len == 0)
+            for (int64_t q = J.soff[p]; q < J.soff[p + 1]; ++q) atomicSub(&s.blockers[J.succ[q]], 1);
+    }
+    left = warp_sum64(left);
+    __syncwarp();
+    __threadfence_block();
+    int nready = 0;
+    for (int p0 = 0; p0 < P; p0 += 32) {
+        const int p = p0 + lane;
+        const bool r = p < P && s.blockers[p] == 0 && paths.len(p) > 0;
+        const unsigned m = __ballot_sync(FULL, r);
+        if (r) {
+            int b;
+            const int4 rc = make_rec(paths, p, &b);
+            const int at = nready + __popc(m & lanemask_lt());
+            R.rec[at] = rc;
+            R.rb[at] = b;
+        }
+        nready += __popc(m);
+    }
+    __syncwarp();
+    int nb = 0, nlog = 0, status = RECON_OK;
+    // register-resident frontier (<= 32 ready paths), as in batch_warp
+    bool regmode = false;
+    LanePath lp;
+    lp.p = INT_MAX;
+    auto enter_regmode = [&]() {
+        lp.p = INT_MAX;
+        if (lane < nready) lp = rec_lane(R.rec[lane], R.rb[lane]);
+        regmode = true;
+    };
+    auto put_move = [&](int64_t slot, int rank_in_batch) {
+        if (LOG) J.mlog[nlog + rank_in_batch] = (int)slot | (rank_in_batch == 0 ? (int)0x80000000u : 0);
+        else J.move_batch[slot] = nb;
+    };
+    if (nready <= 32) enter_regmode();
+    while (left > 0) {
+        if (regmode) {
+            const bool valid = lp.p != INT_MAX;
+            int32_t fr = -1, to = -1;
+            if (valid) {
+                fr = lp.v(H, lp.k);
+                to = lp.v(H, lp.k + 1);
+            }
+            const bool cand = valid && !occ.get(to);
+            const unsigned cm = __ballot_sync(FULL, cand);
+            if (!cm) {
+                status = RECON_ERR_INPUT;  // batching.cpp:127-128
+                break;
+            }
+            bool a;
+            if (J.preset != 0) {
+                const int first = __ffs(cm) - 1;
+                const int32_t ff = __shfl_sync(FULL, fr, first), ft = __shfl_sync(FULL, to, first);
+                a = cand && compatible(J.preset, H, fr, to, ff, ft);
+            } else {
+                const unsigned same = __match_any_sync(FULL, cand ? to : -2 - lane);
+                a = cand && (same & lanemask_lt()) == 0;
+            }
+            const unsigned acc = __ballot_sync(FULL, a);
+            if (a) occ.clr(fr);
+            __syncwarp();
+            if (a) occ.set(to);
+            bool fin = false;
+            int64_t q0 = 0, q1 = 0;
+            if (a) {
+                put_move(lp.base + lp.k, __popc(acc & lanemask_lt()));
+                ++lp.k;
+                fin = lp.k == lp.len;
+                if (fin) {
+                    q0 = J.soff[lp.p];
+                    q1 = J.soff[lp.p + 1];
+                }
+            }
+            nlog += __popc(acc);
+            left -= __popc(acc);
+            const unsigned fm = __ballot_sync(FULL, fin);
+            if (fm) {
+                const int nnew = release_successors(J, s.blockers, s.newly, 0, fin, q0, q1);
+                if (fin) lp.p = INT_MAX;
+                __syncwarp();
+                const unsigned live = __ballot_sync(FULL, lp.p != INT_MAX);
+                const int nlive = __popc(live);
+                if (nlive + nnew > 32) {
+                    // spill to the record list: live lanes are ascending
+                    if (lp.p != INT_MAX) {
+                        const int at = __popc(live & lanemask_lt());
+                        R.rec2[at] = lane_rec(lp);
+                        R.rb2[at] = (int)lp.base;
+                    }
+                    __syncwarp();
+                    sort_newly(s.newly, s.mem, nnew);
+                    merge_ready(paths, R, s.newly, nlive, nnew);
+                    nready = nlive + nnew;
+                    regmode = false;
+                } else if (nnew > 0) {
+                    // newly released paths take the empty lanes, then sort lanes by id
+                    const int erank = __popc(~live & lanemask_lt());
+                    if (lp.p == INT_MAX && erank < nnew) {
+                        int b;
+                        const int4 r = make_rec(paths, s.newly[erank], &b);
+                        lp = rec_lane(r, b);
+                    }
+                    int key = lp.p == INT_MAX ? INT_MAX : (lp.p << 5) | lane;
+                    key = warp_sort32(key);
+                    const int src = key == INT_MAX ? lane : (key & 31);
+                    LanePath q;
+                    q.p = __shfl_sync(FULL, lp.p, src);
+                    q.k = __shfl_sync(FULL, lp.k, src);
+                    q.len = __shfl_sync(FULL, lp.len, src);
+                    q.xs = __shfl_sync(FULL, lp.xs, src);
+                    q.ys = __shfl_sync(FULL, lp.ys, src);
+                    q.xt = __shfl_sync(FULL, lp.xt, src);
+                    q.yt = __shfl_sync(FULL, lp.yt, src);
+                    q.base = __shfl_sync(FULL, lp.base, src);
+                    lp = key == INT_MAX ? LanePath{INT_MAX, 0, 0, 0, 0, 0, 0, 0} : q;
+                } else {
+                    // finished lanes leave gaps: lane L takes the L-th live lane
+                    int src = lane;
+                    for (int st = 0; st < 32; ++st)
+                        if (((live >> st) & 1u) && __popc(live & ((1u << st) - 1u)) == lane) src = st;
+                    LanePath q;
+                    q.p = __shfl_sync(FULL, lp.p, src);
+                    q.k = __shfl_sync(FULL, lp.k, src);
+                    q.len = __shfl_sync(FULL, lp.len, src);
+                    q.xs = __shfl_sync(FULL, lp.xs, src);
+                    q.ys = __shfl_sync(FULL, lp.ys, src);
+                    q.xt = __shfl_sync(FULL, lp.xt, src);
+                    q.yt = __shfl_sync(FULL, lp.yt, src);
+                    q.base = __shfl_sync(FULL, lp.base, src);
+                    lp = lane < nlive ? q : LanePath{INT_MAX, 0, 0, 0, 0, 0, 0, 0};
+                }
+            }
+            __syncwarp();
+            ++nb;
+            continue;
+        }
+        // ---- general: candidate scan over the records (ascending id)
+        int nacc = 0;
+        int32_t f_from = -1, f_to = -1;  // first accepted move of the batch
+        for (int c0 = 0; c0 < nready; c0 += 32) {
+            const int idx = c0 + lane;
+            const bool valid = idx < nready;
+            LanePath l;
+            l.p = -1;
+            int32_t fr = -1, to = -1;
+            bool cand = false;
+            if (valid) {
+                l = rec_lane(R.rec[idx], R.rb[idx]);
+                fr = l.v(H, l.k);
+                to = l.v(H, l.k + 1);
+                cand = !occ.get(to) && !inb.get(fr) && !inb.get(to);
+                if (cand && f_from >= 0) cand = compatible(J.preset, H, fr, to, f_from, f_to);
+            }
+            const unsigned cm_all = __ballot_sync(FULL, cand);
+            if (!cm_all) continue;
+            bool a;
+            if (J.preset != 0) {
+                const int first = __ffs(cm_all) - 1;
+                const int32_t ff = f_from >= 0 ? f_from : __shfl_sync(FULL, fr, first);
+                const int32_t ft = f_from >= 0 ? f_to : __shfl_sync(FULL, to, first);
+                a = cand && compatible(J.preset, H, fr, to, ff, ft);
+            } else {
+                const unsigned same = __match_any_sync(FULL, cand ? to : -2 - lane);
+                a = cand && (same & lanemask_lt()) == 0;
+            }
+            const unsigned acc = __ballot_sync(FULL, a);
+            if (a) {
+                inb.set(fr);
+                inb.set(to);
+                const int slot = nacc + __popc(acc & lanemask_lt());
+                put_move(l.base + l.k, slot);
+                const bool fin = l.k + 1 == l.len;
+                int *rw = reinterpret_cast<int *>(R.rec + idx);
+                if (fin) rw[0] = -1;  // finished: dropped at the next merge
+                else rw[1] = (l.k + 1) | (l.len << 16);
+                s.mem[slot] = fin ? (int)(0x80000000u | (unsigned)l.p) : l.p;
+                s.mfr[slot] = fr;
+                s.mto[slot] = to;
+            }
+            if (acc && f_from < 0) {
+                const int first = __ffs(acc) - 1;
+                f_from = __shfl_sync(FULL, fr, first);
+                f_to = __shfl_sync(FULL, to, first);
+            }
+            nacc += __popc(acc);
+            __syncwarp();
+        }
+        if (nacc == 0) {
+            status = RECON_ERR_INPUT;  // batching.cpp:127-128
+            break;
+        }
+        // ---- atomic application
+        for (int i = lane; i < nacc; i += 32) {
+            occ.clr(s.mfr[i]);
+            inb.clr(s.mfr[i]);
+            inb.clr(s.mto[i]);
+        }
+        __syncwarp();
+        for (int i = lane; i < nacc; i += 32) occ.set(s.mto[i]);
+        __syncwarp();
+        // ---- release (newly -> next batch)
+        int nnew = 0, nfin = 0;
+        for (int i0 = 0; i0 < nacc; i0 += 32) {
+            const int i = i0 + lane;
+            bool fin = false;
+            int64_t q0 = 0, q1 = 0;
+            if (i < nacc) {
+                const int m = s.mem[i];
+                fin = m < 0;
+                if (fin) {
+                    const int p = m & 0x7fffffff;
+                    q0 = J.soff[p];
+                    q1 = J.soff[p + 1];
+                }
+            }
+            nfin += __popc(__ballot_sync(FULL, fin));
+            nnew = release_successors(J, s.blockers, s.newly, nnew, fin, q0, q1);
+            __syncwarp();
+        }
+        left -= nacc;
+        nlog += nacc;
+        __syncwarp();
+        if (nfin > 0 || nnew > 0) {
+            // ready' = (ready - finished) U newly, by rank
+            int nkeep = 0;
+            for (int c0 = 0; c0 < nready; c0 += 32) {
+                const int idx = c0 + lane;
+                int4 x = make_int4(-1, 0, 0, 0);
+                int b = 0;
+                if (idx < nready) {
+                    x = R.rec[idx];
+                    b = R.rb[idx];
+                }
+                const bool keep = x.x >= 0;
+                const unsigned m = __ballot_sync(FULL, keep);
+                if (keep) {
+                    const int at = nkeep + __popc(m & lanemask_lt());
+                    R.rec2[at] = x;
+                    R.rb2[at] = b;
+                }
+                nkeep += __popc(m);
+            }
+            __syncwarp();
+            sort_newly(s.newly, s.mem, nnew);
+            merge_ready(paths, R, s.newly, nkeep, nnew);
+            nready = nkeep + nnew;
+        }
+        ++nb;
+        if (nready <= 32) enter_regmode();
+    }
+    if (lane == 0) {
+        if (J.nlog) *J.nlog = nlog;
+        *J.batch_count = status == RECON_OK ? nb : 0;
+        *J.status = status;
+        if (J.detail) *J.detail = status == RECON_OK ? 0 : RECON_D_BATCH_NO_PROGRESS;
+    }
+}
+
 // MODE 0: bitmaps in global memory; 1: bitmaps in shared memory; 2: 1 + move log
 template <int MODE>
 __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) {
@@ -1013,7 +1401,8 @@ __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) 
         J.status = a.status + inst;
         J.detail = a.detail ? a.detail + inst : nullptr;
         ImplicitPaths ip{a.path_src + o, a.path_dst + o, a.mbase + o, a.mbase[o], a.H};
-        batch_warp<ImplicitPaths, true, MODE >= 1, MODE == 2>(J, ip);
+        const PipeRecords R{a.rec + o, a.rec2 + o, a.rb + o, a.rb2 + o};
+        batch_warp_pipe<MODE >= 1, MODE == 2>(J, ip, R);
     }
 }
 

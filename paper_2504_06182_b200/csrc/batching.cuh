@@ -18,6 +18,11 @@ struct BatchScratch {
     int32_t *counter;   // [1], zero
 };
 
+struct PipeRecords {  // one instance's ready records (batch_warp_pipe)
+    int4 *rec, *rec2;
+    int32_t *rb, *rb2;
+};
+
 struct BatchJob {
     int P, W, H, preset, edge_level;
     const int64_t *soff;  // [P+1] successor CSR offsets (global edge index)
@@ -70,6 +75,8 @@ struct PipelineArgs {
     // small instances (pipeline_small_dag): per-instance edge / move totals and
     // their exclusive scans over instances, [count + 1] each
     int small_dag;
+    int4 *rec, *rec2;    // [count * W*k] ready-path records (batch_warp_pipe)
+    int32_t *rb, *rb2;   // [count * W*k] their move bases
     int64_t *inst_edges, *inst_moves, *ebase, *mvbase;
     const uint64_t *grid_occ;            // [count * W * wpc] initial occupancy (occ bits)
     void *temp;

@@ -101,6 +101,14 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool 
         const char *e = getenv("RECON_SMALL_DAG");
         return e ? atoi(e) : 1;
     }();
+    {
+        unsigned char *r = c->dev<unsigned char>(S_BM_AUX7, n * S * 40 + 64);
+        if (!r) return cuda_fail(cudaErrorMemoryAllocation, "pipeline records", detail);
+        a.rec = (int4 *)r;
+        a.rec2 = a.rec + n * S;
+        a.rb = (int32_t *)(a.rec2 + n * S);
+        a.rb2 = a.rb + n * S;
+    }
     a.small_dag = small_env && pipeline_small_dag_smem(a.W, a.H, a.k) > 0;
     a.inst_edges = i64 + 2 * (n * S + 1);
     a.inst_moves = a.inst_edges + (n + 1);
