@@ -996,9 +996,37 @@ __device__ __forceinline__ int lower_bound_rec(const int4 *a, int n, int x) {
     return lo;
 }
 
+// per-path blocker counts: global int32, or (BSM) u16 halves of u32 words in
+// shared memory, decremented with a 32-bit atomic add of -(1 << 16*half) (a
+// count is >= 1 before each decrement, so no borrow crosses halves)
+template <bool BSM>
+struct Blockers {
+    int32_t *g;
+    uint32_t sa;
+    __device__ Blockers(int32_t *gp, uint32_t *sp) : g(gp), sa(BSM ? (uint32_t)__cvta_generic_to_shared(sp) : 0u) {}
+    __device__ __forceinline__ int get(int p) const {
+        if (!BSM) return g[p];
+        uint32_t x;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(sa + ((uint32_t)(p >> 1) << 2)));
+        return (int)((x >> ((p & 1) * 16)) & 0xffffu);
+    }
+    // one predecessor of p finished; true when it was the last
+    __device__ __forceinline__ bool release(int p) const {
+        if (!BSM) return atomicSub(&g[p], 1) == 1;
+        const uint32_t sh = (uint32_t)(p & 1) * 16u;
+        uint32_t old;
+        asm volatile("atom.shared.add.u32 %0, [%1], %2;"
+                     : "=r"(old)
+                     : "r"(sa + ((uint32_t)(p >> 1) << 2)), "r"(0u - (1u << sh))
+                     : "memory");
+        return ((old >> sh) & 0xffffu) == 1u;
+    }
+};
+
 // successors of the finished paths (fin lanes, CSR range [q0, q1)) lose one
 // blocker; the released ones are appended to newly; returns the new count
-__device__ __forceinline__ int release_successors(const BatchJob &J, int32_t *blockers, int32_t *newly, int nnew,
+template <class BL>
+__device__ __forceinline__ int release_successors(const BatchJob &J, const BL &blockers, int32_t *newly, int nnew,
                                                   bool fin, int64_t q0, int64_t q1) {
     const int lane = lane_id();
     if (!fin) q0 = q1 = 0;
@@ -1018,7 +1046,7 @@ __device__ __forceinline__ int release_successors(const BatchJob &J, int32_t *bl
         int sc = -1;
         if (t < tot) {
             sc = J.succ[oq0 + (t - ob)];
-            released = atomicSub(&blockers[sc], 1) == 1;
+            released = blockers.release(sc);
         }
         const unsigned rm = __ballot_sync(FULL, released);
         if (released) newly[nnew + __popc(rm & lanemask_lt())] = sc;
@@ -1068,19 +1096,20 @@ __device__ __forceinline__ void merge_ready(const ImplicitPaths &paths, const Pi
     __syncwarp();
 }
 
-template <bool SM, bool LOG>
+template <bool SM, bool LOG, bool BSM>
 __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, const PipeRecords R) {
     const int lane = lane_id();
     const int P = J.P, H = J.H;
     BatchScratch s = J.s;
     const Bits<SM> occ(s.occ), inb(s.inb);
+    const Blockers<BSM> blk(s.blockers, s.blk_sm);  // BSM: filled by the caller
     // ---- init: blockers = in-degree (given); zero-length paths finish at once
     long long left = 0;
     for (int p = lane; p < P; p += 32) {
         const int len = paths.len(p);
         left += len;
         if (len == 0)
-            for (int64_t q = J.soff[p]; q < J.soff[p + 1]; ++q) atomicSub(&s.blockers[J.succ[q]], 1);
+            for (int64_t q = J.soff[p]; q < J.soff[p + 1]; ++q) blk.release(J.succ[q]);
     }
     left = warp_sum64(left);
     __syncwarp();
@@ -1088,7 +1117,7 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, c
     int nready = 0;
     for (int p0 = 0; p0 < P; p0 += 32) {
         const int p = p0 + lane;
-        const bool r = p < P && s.blockers[p] == 0 && paths.len(p) > 0;
+        const bool r = p < P && blk.get(p) == 0 && paths.len(p) > 0;
         const unsigned m = __ballot_sync(FULL, r);
         if (r) {
             int b;
@@ -1157,7 +1186,7 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, c
             left -= __popc(acc);
             const unsigned fm = __ballot_sync(FULL, fin);
             if (fm) {
-                const int nnew = release_successors(J, s.blockers, s.newly, 0, fin, q0, q1);
+                const int nnew = release_successors(J, blk, s.newly, 0, fin, q0, q1);
                 if (fin) lp.p = INT_MAX;
                 __syncwarp();
                 const unsigned live = __ballot_sync(FULL, lp.p != INT_MAX);
@@ -1296,7 +1325,7 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, c
                 }
             }
             nfin += __popc(__ballot_sync(FULL, fin));
-            nnew = release_successors(J, s.blockers, s.newly, nnew, fin, q0, q1);
+            nnew = release_successors(J, blk, s.newly, nnew, fin, q0, q1);
             __syncwarp();
         }
         left -= nacc;
@@ -1338,7 +1367,8 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, c
     }
 }
 
-// MODE 0: bitmaps in global memory; 1: bitmaps in shared memory; 2: 1 + move log
+// MODE 0: bitmaps in global memory; 1: bitmaps in shared memory; 2: 1 + move
+// log; 3: 2 + blocker counts in shared memory (u16, after the bitmaps)
 template <int MODE>
 __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) {
     constexpr bool occ_in_smem = MODE >= 1;
@@ -1372,8 +1402,9 @@ __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) 
         J.succ = a.succ;
         J.s.occ = a.occ + inst * nwb;
         J.s.inb = a.inb + inst * nwb;
+        const int64_t nbw = MODE == 3 ? (S + 1) / 2 : 0;
         if (occ_in_smem) {  // the instance's occupancy and in-batch bitmaps live in this warp's shared memory
-            uint32_t *mine = bsmem + (size_t)warp_id() * 2 * nwb;
+            uint32_t *mine = bsmem + (size_t)warp_id() * (2 * nwb + nbw);
             for (int64_t w = lane_id(); w < nwb; w += 32) {
                 mine[w] = J.s.occ[w];
                 mine[nwb + w] = 0u;
@@ -1393,7 +1424,7 @@ __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) 
         J.s.mto = a.mto + o;
         J.s.counter = a.counter + inst;
         J.move_batch = a.move_batch + (int64_t)inst * a.move_stride;
-        if (MODE == 2) {
+        if (MODE >= 2) {
             J.mlog = a.mlog + a.mbase[o];
             J.nlog = a.counter + inst;
         }
@@ -1402,7 +1433,19 @@ __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) 
         J.detail = a.detail ? a.detail + inst : nullptr;
         ImplicitPaths ip{a.path_src + o, a.path_dst + o, a.mbase + o, a.mbase[o], a.H};
         const PipeRecords R{a.rec + o, a.rec2 + o, a.rb + o, a.rb2 + o};
-        batch_warp_pipe<MODE >= 1, MODE == 2>(J, ip, R);
+        if (MODE == 3) {
+            uint32_t *bw = bsmem + (size_t)warp_id() * (2 * nwb + nbw) + 2 * nwb;
+            const int P = J.P;
+            for (int64_t w = lane_id(); w < nbw; w += 32) {
+                const int p = (int)(2 * w);
+                const uint32_t lo = p < P ? (uint32_t)J.s.blockers[p] : 0u;
+                const uint32_t hi = p + 1 < P ? (uint32_t)J.s.blockers[p + 1] : 0u;
+                bw[w] = lo | (hi << 16);
+            }
+            __syncwarp();
+            J.s.blk_sm = bw;
+        }
+        batch_warp_pipe<MODE >= 1, MODE >= 2, MODE == 3>(J, ip, R);
     }
 }
 
@@ -1456,20 +1499,29 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
     cudaMemsetAsync(a.counter, 0, (size_t)a.count * 4, st);
     (void)N;
     // occupancy + in-batch bitmaps in shared memory when a few warps' worth fits
-    const int64_t bm_bytes = 2 * nwb * 4;
-    int warps = 4, occ_smem = 0;
+    // (MODE 3) the blocker counts too, when the move log is on and they fit
+    const int64_t bm_bytes = 2 * nwb * 4, blk_bytes = (S + 1) / 2 * 4;
+    static const int bsm_env = [] {
+        const char *e = getenv("RECON_BATCH_BSM");
+        return e ? atoi(e) : 1;
+    }();
+    int warps = 4, mode = 0;
     size_t smem = 0;
     if (bm_bytes <= 96 * 1024) {
-        warps = (int)std::max<int64_t>(1, std::min<int64_t>(8, (200 * 1024) / bm_bytes));
-        occ_smem = 1;
-        smem = (size_t)warps * bm_bytes;
+        mode = a.mlog ? 2 : 1;
+        if (mode == 2 && bsm_env && S < 65536 && bm_bytes + blk_bytes <= 32 * 1024) mode = 3;
+        const int64_t per = bm_bytes + (mode == 3 ? blk_bytes : 0);
+        warps = (int)std::max<int64_t>(1, std::min<int64_t>(8, (200 * 1024) / per));
+        smem = (size_t)warps * per;
         cudaFuncSetAttribute(batch_pipeline_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(batch_pipeline_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(batch_pipeline_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
     const int grid = (int)std::min<int64_t>(((int64_t)a.count + warps - 1) / warps, (int64_t)sms * 32);
-    if (!occ_smem) batch_pipeline_kernel<0><<<grid, warps * 32, smem, st>>>(a);
-    else if (!a.mlog) batch_pipeline_kernel<1><<<grid, warps * 32, smem, st>>>(a);
-    else batch_pipeline_kernel<2><<<grid, warps * 32, smem, st>>>(a);
+    if (mode == 0) batch_pipeline_kernel<0><<<grid, warps * 32, smem, st>>>(a);
+    else if (mode == 1) batch_pipeline_kernel<1><<<grid, warps * 32, smem, st>>>(a);
+    else if (mode == 2) batch_pipeline_kernel<2><<<grid, warps * 32, smem, st>>>(a);
+    else batch_pipeline_kernel<3><<<grid, warps * 32, smem, st>>>(a);
     if (a.mlog) pipeline_scatter_moves<<<(int)std::min<int64_t>(a.count, (int64_t)sms * 8), 256, 0, st>>>(a);
     return cudaGetLastError();
 }

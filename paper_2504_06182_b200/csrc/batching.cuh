@@ -16,6 +16,7 @@ struct BatchScratch {
     uint8_t *done;      // [P]
     int32_t *ready, *ready2, *newly, *mem, *mfr, *mto;  // [P] each
     int32_t *counter;   // [1], zero
+    uint32_t *blk_sm;   // pipeline: blocker counts in shared memory (u16 pairs), or null
 };
 
 struct PipeRecords {  // one instance's ready records (batch_warp_pipe)
