@@ -159,7 +159,7 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t *a, int n, int x) {
 // the only possible vertex conflict inside a batch is a shared destination;
 // the minimum id wins (and, under column_direction, the class of the first
 // accepted move).  The general entry point keeps the literal pairwise checks.
-template <class Paths, bool FAST, bool SM = false, bool LOG = false>
+template <class Paths, bool FAST, bool SM = false>
 __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
     const int lane = lane_id();
     const int P = J.P, H = J.H;
@@ -191,7 +191,7 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
     }
     __syncwarp();
     int32_t *ready = s.ready, *ready2 = s.ready2;
-    int nb = 0, nlog = 0, status = RECON_OK;
+    int nb = 0, status = RECON_OK;
     // Register-resident frontier (FAST path, <= 32 ready paths): lane i keeps
     // ready path i (ascending id) with its step and endpoints in registers, so
     // a batch costs one occupancy probe plus fire-and-forget atomics.
@@ -235,16 +235,10 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
             if (a) occ.set(to);
             bool fin = false;
             if (a) {
-                if (LOG) {
-                    const int r = __popc(acc & lanemask_lt());
-                    J.mlog[nlog + r] = (int)lp.base + lp.k | (r == 0 ? (int)0x80000000u : 0);
-                } else {
-                    J.move_batch[lp.base + lp.k] = nb;
-                }
+                J.move_batch[lp.base + lp.k] = nb;
                 ++lp.k;
                 fin = lp.k == lp.len;
             }
-            nlog += __popc(acc);
             left -= __popc(acc);
             const unsigned fm = __ballot_sync(FULL, fin);
             if (fm) {
@@ -435,8 +429,7 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
                 inb.set(to);
                 // advance the accepted path here, while its state is in registers
                 const int slot = nacc + __popc(acc & lanemask_lt());
-                if (LOG) J.mlog[nlog + slot] = (int)(paths.move_base(p) + k) | (slot == 0 ? (int)0x80000000u : 0);
-                else J.move_batch[paths.move_base(p) + k] = nb;
+                J.move_batch[paths.move_base(p) + k] = nb;
                 s.next[p] = k + 1;
                 const bool fin = k + 1 == paths.len(p);
                 if (fin) s.done[p] = 1;
@@ -510,7 +503,6 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
             __syncwarp();
         }
         left -= nacc;
-        nlog += nacc;
         __syncwarp();
         if (!J.edge_level && (nfin > 0 || nnew > 0)) {
             // ready' = (ready - finished) U newly, sorted
@@ -555,7 +547,6 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
         if (REG && nready <= 32) enter_regmode();
     }
     if (lane == 0) {
-        if (J.nlog) *J.nlog = nlog;
         *J.batch_count = status == RECON_OK ? nb : 0;
         *J.status = status;
         if (J.detail) *J.detail = status == RECON_OK ? 0 : RECON_D_BATCH_NO_PROGRESS;
@@ -1140,7 +1131,7 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, c
         regmode = true;
     };
     auto put_move = [&](int64_t slot, int rank_in_batch) {
-        if (LOG) J.mlog[nlog + rank_in_batch] = (int)slot | (rank_in_batch == 0 ? (int)0x80000000u : 0);
+        if (LOG) J.mlog[nlog + rank_in_batch] = make_int2((int)slot, nb);
         else J.move_batch[slot] = nb;
     };
     if (nready <= 32) enter_regmode();
@@ -1449,38 +1440,17 @@ __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) 
     }
 }
 
-// move log -> move_batch, one CTA per instance: a batch index is the number
-// of batch-start flags up to the entry, minus one.  The instance's move_batch
+// move log -> move_batch, one CTA per instance: the instance's move_batch
 // region is written within one CTA's pass, so L2 merges the scattered 4-byte
 // stores into full sectors before they reach DRAM.
 __global__ void __launch_bounds__(256) pipeline_scatter_moves(PipelineArgs a) {
-    __shared__ int wsum[8];
-    __shared__ int carry;
-    const int lane = lane_id(), warp = warp_id();
     for (int inst = blockIdx.x; inst < a.count; inst += gridDim.x) {
         const int n = a.counter[inst];
-        const int32_t *log = a.mlog + a.mbase[(int64_t)inst * a.W * a.k];
+        const int2 *log = a.mlog + a.mbase[(int64_t)inst * a.W * a.k];
         int32_t *mb = a.move_batch + (int64_t)inst * a.move_stride;
-        if (threadIdx.x == 0) carry = -1;
-        __syncthreads();
-        for (int i0 = 0; i0 < n; i0 += 256) {
-            const int i = i0 + threadIdx.x;
-            const int v = i < n ? __ldcs(log + i) : 0;
-            const int f = v < 0;
-            int incl = f;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(FULL, incl, o);
-                if (lane >= o) incl += y;
-            }
-            if (lane == 31) wsum[warp] = incl;
-            __syncthreads();
-            int before = carry;
-            for (int w = 0; w < warp; ++w) before += wsum[w];
-            if (i < n) mb[v & 0x7fffffff] = before + incl;
-            __syncthreads();
-            if (threadIdx.x == 255) carry = before + incl;
-            __syncthreads();
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const int2 e = __ldcs(log + i);
+            mb[e.x] = e.y;
         }
     }
 }

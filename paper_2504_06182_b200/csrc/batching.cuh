@@ -33,10 +33,11 @@ struct BatchJob {
     const int64_t *in_need;
     BatchScratch s;
     int32_t *move_batch;  // path-major, one per elementary move
-    // move log (pipeline): accepted moves' path-major slots in batch order, bit
-    // 31 on a batch's first entry; pipeline_scatter_moves turns it into
-    // move_batch.  Null: move_batch is written directly.
-    int32_t *mlog, *nlog;
+    // move log (pipeline): {path-major slot, batch} of the accepted moves in
+    // batch order; pipeline_scatter_moves turns it into move_batch.  Null:
+    // move_batch is written directly.
+    int2 *mlog;
+    int32_t *nlog;
     int32_t *batch_count, *status, *detail;
 };
 
@@ -72,7 +73,7 @@ struct PipelineArgs {
     int32_t *next, *ready, *ready2, *newly, *mem, *mfr, *mto;  // [count * W*k]
     uint8_t *done;                       // [count * W*k]
     int32_t *counter;                    // [count] move-log length
-    int32_t *mlog;                       // [total moves] move log, instance i at mbase[i*W*k]
+    int2 *mlog;                          // [total moves] move log, instance i at mbase[i*W*k]
     // small instances (pipeline_small_dag): per-instance edge / move totals and
     // their exclusive scans over instances, [count + 1] each
     int small_dag;

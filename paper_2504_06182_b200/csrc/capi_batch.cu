@@ -141,7 +141,7 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool 
     const bool use_log = log_env >= 0 ? log_env == 1 : (n >= (size_t)c->sms * 4 && 2 * nwb * 4 <= 96 * 1024);
     a.mlog = nullptr;
     if (use_log) {
-        a.mlog = c->dev<int32_t>(S_BM_AUX6, (size_t)counts[1] + 1);
+        a.mlog = c->dev<int2>(S_BM_AUX6, (size_t)counts[1] + 1);
         if (!a.mlog) return cuda_fail(cudaErrorMemoryAllocation, "pipeline move log", detail);
     }
     CK(pipeline_run_batching(a, c->sms, c->stream), "pipeline batching");
