@@ -263,13 +263,14 @@ def main():
     plan_ms = sum(k[0] for k in ktimes) / len(ktimes)
     exec_ms = sum(k[1] for k in ktimes) / len(ktimes)
     achieved_gbs = alg_bytes / (exec_ms * 1e-3) / 1e9  # dominant kernel: the executor
-    traffic = None
+    traffic = warp_inst = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             tr = json.load(f).get("redrec_kernel", {})
         if tr.get("batch") == B and tr.get("workload_seed") == hex(SEED_BASE):
             traffic = tr.get("dram_bytes")
+            warp_inst = tr.get("warp_inst")
     value = ws * B / (ms * 1e-3)
 
     # bird on the same grids (secondary)
@@ -327,6 +328,18 @@ def main():
                "sample": f"first {args.ref_sample} grids of the batch, compiled reference red_rec "
                          f"(oracle/_ref), std::thread pool over all host threads"}
 
+    # the executor is latency / issue bound, not HBM bound: its instruction
+    # issue rate against the SMs' peak (4 warp-instructions per SM per clock)
+    # says how close it runs to that ceiling
+    issue = None
+    clocks = clk.summary()
+    if warp_inst and clocks.get("sm_mhz"):
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak_i = sms * 4 * clocks["sm_mhz"] * 1e6
+        ach_i = warp_inst / (exec_ms * 1e-3)
+        issue = {"warp_inst_per_launch": warp_inst, "achieved_ginst_s": ach_i / 1e9, "peak_ginst_s": peak_i / 1e9,
+                 "frac": ach_i / peak_i, "source": "ncu smsp__inst_executed.sum of the same launch (profiles/traffic.json)"}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "grids/s", "n_gpus": ws, "steps": args.steps,
@@ -341,12 +354,12 @@ def main():
                          "frac": achieved_gbs / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "rb::redrec_kernel (executor)", "kernel_ms": exec_ms,
                          "algorithmic_bytes_per_launch": alg_bytes,
-                         "planner_kernel_ms": plan_ms},
+                         "planner_kernel_ms": plan_ms, "issue": issue},
             "e2e": {"value": ws * B / e2e_s, "unit": "grids/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "bird": {"grids_per_s": ws * B / (bird_ms * 1e-3), "ms_per_step": bird_ms},
             "latency_single_grid": lat,
-            "clocks": clk.summary(),
+            "clocks": clocks,
         }
         if cpu:
             line["cpu_baseline"] = cpu
