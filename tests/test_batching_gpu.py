@@ -120,3 +120,17 @@ def test_batch_moves_random_matches_reference(gpu, ref):
                 assert er == eg
                 if r is not None:
                     assert r[1] == g[1] and np.array_equal(r[0], g[0]), (it, preset, el)
+
+
+@pytest.mark.parametrize("solver,W,hp,k,n", [("bird", 64, 40, 2662, 700), ("redrec", 32, 16, 614, 1200)])
+@pytest.mark.parametrize("preset", [0, 1])
+def test_pipeline_many_instances_matches_reference(gpu, ref, solver, W, hp, k, n, preset):
+    """Batches of >= 4 instances per SM take the many-instance pipeline: the
+    shared-memory DAG build, the move log + scatter, blocker counts in shared
+    memory and the record ready list."""
+    occ = sample_grids(0x64100000 + W, n, W, W, k)
+    ms = W * W * 12
+    g = gpu.pipeline_batch(solver, occ, n, W, W, hp, preset, ms)
+    r = ref.pipeline_batch(solver, occ, n, W, W, hp, preset, ms)
+    _cmp_pipeline(g, r, ms)
+    assert (g["status"] == 0).sum() > n // 2
