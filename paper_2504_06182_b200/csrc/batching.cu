@@ -1358,11 +1358,11 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, c
     }
 }
 
-// MODE 0: bitmaps in global memory; 1: bitmaps in shared memory; 2: 1 + move
-// log; 3: 2 + blocker counts in shared memory (u16, after the bitmaps)
+// MODE bits: 1 = occupancy / in-batch bitmaps in shared memory, 2 = move log,
+// 4 = blocker counts in shared memory (u16, after the bitmaps; needs 1)
 template <int MODE>
 __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) {
-    constexpr bool occ_in_smem = MODE >= 1;
+    constexpr bool occ_in_smem = MODE & 1, LOG = MODE & 2, BSM = MODE & 4;
     extern __shared__ __align__(16) uint32_t bsmem[];
     const int64_t S = (int64_t)a.W * a.k, nwb = ((int64_t)a.W * a.H + 31) / 32;
     const int nw = blockDim.x >> 5;
@@ -1393,7 +1393,7 @@ __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) 
         J.succ = a.succ;
         J.s.occ = a.occ + inst * nwb;
         J.s.inb = a.inb + inst * nwb;
-        const int64_t nbw = MODE == 3 ? (S + 1) / 2 : 0;
+        const int64_t nbw = BSM ? (S + 1) / 2 : 0;
         if (occ_in_smem) {  // the instance's occupancy and in-batch bitmaps live in this warp's shared memory
             uint32_t *mine = bsmem + (size_t)warp_id() * (2 * nwb + nbw);
             for (int64_t w = lane_id(); w < nwb; w += 32) {
@@ -1415,7 +1415,7 @@ __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) 
         J.s.mto = a.mto + o;
         J.s.counter = a.counter + inst;
         J.move_batch = a.move_batch + (int64_t)inst * a.move_stride;
-        if (MODE >= 2) {
+        if (LOG) {
             J.mlog = a.mlog + a.mbase[o];
             J.nlog = a.counter + inst;
         }
@@ -1424,7 +1424,7 @@ __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) 
         J.detail = a.detail ? a.detail + inst : nullptr;
         ImplicitPaths ip{a.path_src + o, a.path_dst + o, a.mbase + o, a.mbase[o], a.H};
         const PipeRecords R{a.rec + o, a.rec2 + o, a.rb + o, a.rb2 + o};
-        if (MODE == 3) {
+        if (BSM) {
             uint32_t *bw = bsmem + (size_t)warp_id() * (2 * nwb + nbw) + 2 * nwb;
             const int P = J.P;
             for (int64_t w = lane_id(); w < nbw; w += 32) {
@@ -1436,7 +1436,7 @@ __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) 
             __syncwarp();
             J.s.blk_sm = bw;
         }
-        batch_warp_pipe<MODE >= 1, MODE >= 2, MODE == 3>(J, ip, R);
+        batch_warp_pipe<occ_in_smem, LOG, BSM>(J, ip, R);
     }
 }
 
@@ -1469,7 +1469,8 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
     cudaMemsetAsync(a.counter, 0, (size_t)a.count * 4, st);
     (void)N;
     // occupancy + in-batch bitmaps in shared memory when a few warps' worth fits
-    // (MODE 3) the blocker counts too, when the move log is on and they fit
+    // bitmaps in shared memory when a few warps' worth fits; then the blocker
+    // counts too when they fit in u16 and the CTA keeps at least two warps
     const int64_t bm_bytes = 2 * nwb * 4, blk_bytes = (S + 1) / 2 * 4;
     static const int bsm_env = [] {
         const char *e = getenv("RECON_BATCH_BSM");
@@ -1478,20 +1479,18 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
     int warps = 4, mode = 0;
     size_t smem = 0;
     if (bm_bytes <= 96 * 1024) {
-        mode = a.mlog ? 2 : 1;
-        if (mode == 2 && bsm_env && S < 65536 && bm_bytes + blk_bytes <= 32 * 1024) mode = 3;
-        const int64_t per = bm_bytes + (mode == 3 ? blk_bytes : 0);
+        mode = 1 | (a.mlog ? 2 : 0);
+        if (bsm_env && S < 65536 && bm_bytes + blk_bytes <= 100 * 1024) mode |= 4;
+        const int64_t per = bm_bytes + ((mode & 4) ? blk_bytes : 0);
         warps = (int)std::max<int64_t>(1, std::min<int64_t>(8, (200 * 1024) / per));
         smem = (size_t)warps * per;
-        cudaFuncSetAttribute(batch_pipeline_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(batch_pipeline_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(batch_pipeline_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
+    void (*kern)(PipelineArgs) = mode == 0 ? batch_pipeline_kernel<0> : mode == 1 ? batch_pipeline_kernel<1>
+                               : mode == 3 ? batch_pipeline_kernel<3> : mode == 5 ? batch_pipeline_kernel<5>
+                                                                       : batch_pipeline_kernel<7>;
+    if (smem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int grid = (int)std::min<int64_t>(((int64_t)a.count + warps - 1) / warps, (int64_t)sms * 32);
-    if (mode == 0) batch_pipeline_kernel<0><<<grid, warps * 32, smem, st>>>(a);
-    else if (mode == 1) batch_pipeline_kernel<1><<<grid, warps * 32, smem, st>>>(a);
-    else if (mode == 2) batch_pipeline_kernel<2><<<grid, warps * 32, smem, st>>>(a);
-    else batch_pipeline_kernel<3><<<grid, warps * 32, smem, st>>>(a);
+    kern<<<grid, warps * 32, smem, st>>>(a);
     if (a.mlog) pipeline_scatter_moves<<<(int)std::min<int64_t>(a.count, (int64_t)sms * 8), 256, 0, st>>>(a);
     return cudaGetLastError();
 }
