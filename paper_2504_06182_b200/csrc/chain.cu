@@ -33,10 +33,9 @@ struct ChainCtx {
     int tl, th, k;
     int ns, idxL, idxR, R;  // sources; #S < tl; #S <= th; residents
     const int16_t *S;       // sorted sources
-    const int32_t *PS;      // PS[i] = S[0] + ... + S[i-1]
     const int16_t *hole;    // hole[q] = q-th empty band cell (1-based), hole[0] = tl-1
     int astar;              // largest a with Delta(a) <= 0 over the whole chain's range
-    int psL, psR, ER;       // PS[idxL], PS[idxR], residents' excess (chain constants)
+    int zp;                 // largest a with Delta(a) < 0 (astar, or astar - 1 when Delta(astar) == 0)
 };
 
 // #(residents with e < a), e_r = S[idxL+r] - tl - r: the residents before the
@@ -73,36 +72,36 @@ __device__ int chain_best_a(const ChainCtx &c, int amin, int amax) {
     return lo;
 }
 
-// split-rule cost at a (range sums of the sources' prefix sums)
-__device__ int chain_cost(const ChainCtx &c, int a) {
-    const int b = (c.k - c.R) - a;
-    const int m = cnt_e_lt(c, a);
-    const int top = c.psL - c.PS[c.idxL - a];
-    const int resm = c.PS[c.idxL + m] - c.psL;
-    const int bot = c.PS[c.idxR + b] - c.psR;
-    const int Em = resm - m * c.tl - m * (m - 1) / 2;
-    int cost = a * c.tl + a * (a - 1) / 2 - top;
-    cost += a * m - Em + (c.ER - Em) - a * (c.R - m);
-    cost += bot - (b * c.th - b * (b - 1) / 2);
-    return cost;
-}
-
 // split point of sources S[s0, s1) (holding every resident), -1 if
 // infeasible.  Delta does not depend on the block and is strictly increasing
 // in a, and every block's [amin, amax] lies inside the whole chain's, so the
-// block optimum is the chain-wide split point clamped to the block's range;
-// the block cost is chain_cost at that point.
+// block optimum is the chain-wide split point clamped to the block's range
+// (its cost is the split-rule cost there; see cost_rank).
 __device__ __forceinline__ int block_a(const ChainCtx &c, int s0, int s1) {
     const int holes = c.k - c.R;
     const int amin = max(0, holes - (s1 - c.idxR)), amax = min(c.idxL - s0, holes);
     return amin > amax ? -1 : min(max(c.astar, amin), amax);
 }
 
+// Block costs only meet in comparisons (the sweep's strict `<` and the final
+// test against the whole chain), so an order-equivalent surrogate of the
+// split-rule cost F(a) replaces it.  Delta is strictly increasing (each step
+// of a adds >= 4), so F strictly decreases up to zp, is flat on [zp, astar]
+// and strictly increases past astar.  A block's split lies on one side of
+// astar and every merge the sweep tries keeps it on that side (the clamp
+// moves one bound toward astar), so comparisons never cross sides:
+//   G(a) = zp - a (a < zp), 0 (zp <= a <= astar), a - astar (a > astar),
+// and INT_MAX / 4 for an infeasible block.
+__device__ __forceinline__ int cost_rank(const ChainCtx &c, int a) {
+    if (a < 0) return INT_MAX / 4;
+    return a < c.zp ? c.zp - a : (a > c.astar ? a - c.astar : 0);
+}
+
 // optimum over sources S[s0, s1); *best_a = -1 if infeasible
 __device__ int block_opt(const ChainCtx &c, int s0, int s1, int *best_a) {
     const int a = block_a(c, s0, s1);
     *best_a = a;
-    return a < 0 ? INT_MAX / 4 : chain_cost(c, a);
+    return cost_rank(c, a);
 }
 
 __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
@@ -114,7 +113,6 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
     int16_t *S = (int16_t *)(smem + (size_t)warp * p.warp_smem);
     int16_t *B = (int16_t *)(smem + (size_t)warp * p.warp_smem + p.b_off);   // block boundaries
     int16_t *BE = (int16_t *)(smem + (size_t)warp * p.warp_smem + p.be_off);  // kept block ends
-    int32_t *PS = (int32_t *)(smem + (size_t)warp * p.warp_smem + p.ps_off);  // prefix sums of S
     int16_t *HL = (int16_t *)(smem + (size_t)warp * p.warp_smem + p.hole_off); // empty band cells
     for (int ch = blockIdx.x * nw + warp; ch < p.count; ch += gridDim.x * nw) {
         const uint32_t *bits = (const uint32_t *)(p.occ + (size_t)ch * words64);
@@ -130,25 +128,11 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
         }
         int ns;
         const int base_ps = warp_excl_scan(cnt, &ns);
-        // sorted sources S and their prefix sums PS (one warp scan of the
-        // lanes' position sums), then the empty band cells
+        // sorted sources S, then the empty band cells
         {
-            int psum = 0;  // sum of set-bit positions: popc per bit of the bit index
-            for (int q = 0; q < per32; ++q)
-                psum += (lane * per32 + q) * 32 * __popc(w[q]) + __popc(w[q] & 0xAAAAAAAAu) +
-                        2 * __popc(w[q] & 0xCCCCCCCCu) + 4 * __popc(w[q] & 0xF0F0F0F0u) +
-                        8 * __popc(w[q] & 0xFF00FF00u) + 16 * __popc(w[q] & 0xFFFF0000u);
-            int total;
-            int run = warp_excl_scan(psum, &total);
             int e = base_ps;
             for (int q = 0; q < per32; ++q)
-                for (uint32_t x = w[q]; x; x &= x - 1) {
-                    const int v = (lane * per32 + q) * 32 + __ffs(x) - 1;
-                    S[e] = (int16_t)v;
-                    PS[e++] = run;
-                    run += v;
-                }
-            if (lane == 31) PS[ns] = run;
+                for (uint32_t x = w[q]; x; x &= x - 1) S[e++] = (int16_t)((lane * per32 + q) * 32 + __ffs(x) - 1);
         }
         {
             int hcnt = 0;
@@ -174,7 +158,6 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
         c.k = k;
         c.ns = ns;
         c.S = S;
-        c.PS = PS;
         c.hole = HL;
         {
             int l = 0, r = 0;
@@ -187,14 +170,14 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
             c.idxR = warp_sum(r);
         }
         c.R = c.idxR - c.idxL;
-        c.astar = 0;
-        c.psL = PS[c.idxL];
-        c.psR = PS[c.idxR];
-        c.ER = (c.psR - c.psL) - c.R * tl - c.R * (c.R - 1) / 2;
+        c.astar = c.zp = 0;
         if (ns >= k) {
             const int holes = k - c.R;
             const int amin = max(0, holes - (ns - c.idxR)), amax = min(c.idxL, holes);
-            if (amin <= amax) c.astar = chain_best_a(c, amin, amax);
+            if (amin <= amax) {
+                c.astar = c.zp = chain_best_a(c, amin, amax);
+                if (c.astar > amin && chain_delta(c, c.astar) == 0) c.zp = c.astar - 1;
+            }
         }
         int status = RECON_OK, detail = 0, a = -1;
         int s0 = 0, s1 = ns;
@@ -306,10 +289,9 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
                             continue;
                         }
                         if (i > tL) break;  // only source-only pairs remain
-                        // a merge keeping the split point keeps the cost (not < wt)
                         auto merged = [&](int s0m, int s1m, int *am) {
                             *am = block_a(c, s0m, s1m);
-                            return *am == a ? wt : (*am < 0 ? INT_MAX / 4 : chain_cost(c, *am));
+                            return cost_rank(c, *am);
                         };
                         int tmp;
                         if (i + 1 == tL) {  // (left neighbour, target)
@@ -389,8 +371,7 @@ cudaError_t launch_chain_band(const ChainBandParams &p0, int sms, cudaStream_t s
     const size_t nbnd = (size_t)(n + 1) / 2 + 3;
     p.b_off = al((size_t)n * 2);
     p.be_off = p.b_off + al(nbnd * 2);
-    p.ps_off = p.be_off + al(nbnd * 2);
-    p.hole_off = p.ps_off + al((size_t)(n + 1) * 4);
+    p.hole_off = p.be_off + al(nbnd * 2);
     p.warp_smem = p.hole_off + al((size_t)(k + 2) * 2);
     const int warps = 8;
     const size_t smem = (size_t)warps * p.warp_smem;

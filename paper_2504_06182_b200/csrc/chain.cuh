@@ -14,7 +14,7 @@ struct ChainBandParams {
     int64_t *total_displacement;
     int32_t *displaced, *status, *detail;
     int32_t *use_first;  // optional: index of the first used sorted source
-    int b_off, be_off, ps_off, hole_off, warp_smem;  // set by launch_chain_band
+    int b_off, be_off, hole_off, warp_smem;  // set by launch_chain_band
 };
 
 cudaError_t launch_chain_band(const ChainBandParams &p, int sms, cudaStream_t st);
