@@ -1404,11 +1404,7 @@ __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) 
             J.s.occ = mine;
             J.s.inb = mine + nwb;
         }
-        J.s.next = a.next + o;
         J.s.blockers = a.indeg + o;
-        J.s.done = a.done + o;
-        J.s.ready = a.ready + o;
-        J.s.ready2 = a.ready2 + o;
         J.s.newly = a.newly + o;
         J.s.mem = a.mem + o;
         J.s.mfr = a.mfr + o;

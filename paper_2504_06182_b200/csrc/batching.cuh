@@ -70,8 +70,7 @@ struct PipelineArgs {
     int32_t *succ;                       // [edge capacity]
     int64_t edge_capacity;
     uint32_t *occ, *inb;                 // [count * ceil(W*H/32)]
-    int32_t *next, *ready, *ready2, *newly, *mem, *mfr, *mto;  // [count * W*k]
-    uint8_t *done;                       // [count * W*k]
+    int32_t *newly, *mem, *mfr, *mto;    // [count * W*k]
     int32_t *counter;                    // [count] move-log length
     int2 *mlog;                          // [total moves] move log, instance i at mbase[i*W*k]
     // small instances (pipeline_small_dag): per-instance edge / move totals and

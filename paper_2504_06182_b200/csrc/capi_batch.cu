@@ -71,52 +71,46 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool 
     a.move_stride = pb->move_stride;
     a.grid_occ = g.occ;
     const size_t nwb = (WH + 31) / 32;
-    int32_t *i32 = c->dev<int32_t>(S_BM_AUX0, n * WH * 2 + n * S * 10 + n * 2 + 8);
-    int64_t *i64 = c->dev<int64_t>(S_BM_AUX1, (n * S + 1) * 2 + 4 * (n + 1) + 4);
-    uint32_t *bits = c->dev<uint32_t>(S_BM_AUX2, n * nwb * 2 + 4);
-    uint8_t *done = c->dev<uint8_t>(S_BM_AUX3, n * S + 16);
-    int32_t *mb = host ? c->dev<int32_t>(S_BM_OUT, n * (size_t)pb->move_stride) : pb->move_batch;
-    int32_t *bc = host ? c->dev<int32_t>(S_BM_AUX4, n * 3) : pb->batch_count;
-    int32_t *bst = host ? bc + n : g.status;  // batching status (device variant reuses solve status)
-    int32_t *bdet = host ? bc + 2 * n : g.detail;
-    if (!i32 || !i64 || !bits || !done || !mb || !bc) return cuda_fail(cudaErrorMemoryAllocation, "pipeline", detail);
-    if (host) CK(cudaMemsetAsync(mb, 0xff, n * (size_t)pb->move_stride * 4, c->stream), "memset");
-    a.source_of = i32;
-    a.target_of = i32 + n * WH;
-    int32_t *q = i32 + 2 * n * WH;
-    a.outdeg = q;
-    a.indeg = q + n * S;
-    a.fill = q + 2 * n * S;
-    a.next = q + 3 * n * S;
-    a.ready = q + 4 * n * S;
-    a.ready2 = q + 5 * n * S;
-    a.newly = q + 6 * n * S;
-    a.mem = q + 7 * n * S;
-    a.mfr = q + 8 * n * S;
-    a.mto = q + 9 * n * S;
-    a.counter = q + 10 * n * S;
-    a.soff = i64;
-    a.mbase = i64 + n * S + 1;
     static const int small_env = [] {
         const char *e = getenv("RECON_SMALL_DAG");
         return e ? atoi(e) : 1;
     }();
-    {
-        unsigned char *r = c->dev<unsigned char>(S_BM_AUX7, n * S * 40 + 64);
-        if (!r) return cuda_fail(cudaErrorMemoryAllocation, "pipeline records", detail);
-        a.rec = (int4 *)r;
-        a.rec2 = a.rec + n * S;
-        a.rb = (int32_t *)(a.rec2 + n * S);
-        a.rb2 = a.rb + n * S;
-    }
     a.small_dag = small_env && pipeline_small_dag_smem(a.W, a.H, a.k) > 0;
+    // per-instance vertex maps only for the global DAG walk
+    const size_t maps = a.small_dag ? 0 : n * WH * 2;
+    int32_t *i32 = c->dev<int32_t>(S_BM_AUX0, maps + n * S * 9 + n * 2 + 8);
+    int64_t *i64 = c->dev<int64_t>(S_BM_AUX1, (n * S + 1) * 2 + 4 * (n + 1) + 4);
+    uint32_t *bits = c->dev<uint32_t>(S_BM_AUX2, n * nwb * 2 + 4);
+    int4 *rec = c->dev<int4>(S_BM_AUX7, n * S * 2 + 4);
+    int32_t *mb = host ? c->dev<int32_t>(S_BM_OUT, n * (size_t)pb->move_stride) : pb->move_batch;
+    int32_t *bc = host ? c->dev<int32_t>(S_BM_AUX4, n * 3) : pb->batch_count;
+    int32_t *bst = host ? bc + n : g.status;  // batching status (device variant reuses solve status)
+    int32_t *bdet = host ? bc + 2 * n : g.detail;
+    if (!i32 || !i64 || !bits || !rec || !mb || !bc) return cuda_fail(cudaErrorMemoryAllocation, "pipeline", detail);
+    if (host) CK(cudaMemsetAsync(mb, 0xff, n * (size_t)pb->move_stride * 4, c->stream), "memset");
+    a.source_of = maps ? i32 : nullptr;
+    a.target_of = maps ? i32 + n * WH : nullptr;
+    int32_t *q = i32 + maps;
+    a.outdeg = q;
+    a.indeg = q + n * S;
+    a.fill = q + 2 * n * S;
+    a.newly = q + 3 * n * S;
+    a.mem = q + 4 * n * S;
+    a.mfr = q + 5 * n * S;
+    a.mto = q + 6 * n * S;
+    a.rb = q + 7 * n * S;   // ready records' move bases (batch_warp_pipe)
+    a.rb2 = q + 8 * n * S;
+    a.counter = q + 9 * n * S;
+    a.rec = rec;  // ready records
+    a.rec2 = rec + n * S;
+    a.soff = i64;
+    a.mbase = i64 + n * S + 1;
     a.inst_edges = i64 + 2 * (n * S + 1);
     a.inst_moves = a.inst_edges + (n + 1);
     a.ebase = a.inst_moves + (n + 1);
     a.mvbase = a.ebase + (n + 1);
     a.occ = bits;
     a.inb = bits + n * nwb;
-    a.done = done;
     a.move_batch = mb;
     a.batch_count = bc;
     a.status = bst;
