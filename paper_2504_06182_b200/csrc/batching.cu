@@ -1350,6 +1350,15 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, c
         ++nb;
         if (nready <= 32) enter_regmode();
     }
+    if (LOG) {
+        // the instance's log -> move_batch in one burst: its region is written
+        // back to back, so L2 merges the scattered 4-byte stores into sectors
+        __syncwarp();
+        for (int i = lane; i < nlog; i += 32) {
+            const int2 e = __ldcs(J.mlog + i);
+            J.move_batch[e.x] = e.y;
+        }
+    }
     if (lane == 0) {
         if (J.nlog) *J.nlog = nlog;
         *J.batch_count = status == RECON_OK ? nb : 0;
@@ -1436,21 +1445,6 @@ __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) 
     }
 }
 
-// move log -> move_batch, one CTA per instance: the instance's move_batch
-// region is written within one CTA's pass, so L2 merges the scattered 4-byte
-// stores into full sectors before they reach DRAM.
-__global__ void __launch_bounds__(256) pipeline_scatter_moves(PipelineArgs a) {
-    for (int inst = blockIdx.x; inst < a.count; inst += gridDim.x) {
-        const int n = a.counter[inst];
-        const int2 *log = a.mlog + a.mbase[(int64_t)inst * a.W * a.k];
-        int32_t *mb = a.move_batch + (int64_t)inst * a.move_stride;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const int2 e = __ldcs(log + i);
-            mb[e.x] = e.y;
-        }
-    }
-}
-
 cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t st) {
     const int64_t S = (int64_t)a.W * a.k, N = (int64_t)a.count * S, nwb = ((int64_t)a.W * a.H + 31) / 32;
     const int blocks = 148 * 8;
@@ -1487,7 +1481,6 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
     if (smem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int grid = (int)std::min<int64_t>(((int64_t)a.count + warps - 1) / warps, (int64_t)sms * 32);
     kern<<<grid, warps * 32, smem, st>>>(a);
-    if (a.mlog) pipeline_scatter_moves<<<(int)std::min<int64_t>(a.count, (int64_t)sms * 8), 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 
