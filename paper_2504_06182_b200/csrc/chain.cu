@@ -276,9 +276,51 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
                 int ga;
                 const int global = block_opt(c, 0, ns, &ga);
                 int wt = block_opt(c, s0, s1, &a);
-                if (wt != global) {
-                    // literal sweep (exact1d.cpp:269-289): blocks tL..tR form the
-                    // target; list index i maps to the current merged list
+                if (wt != global && a >= 0) {
+                    // Feasible target: the sweep's outcome in closed form.  Its
+                    // split lies on one side of a*; merges on the other side
+                    // leave the split (and the rank) unchanged, and every merge
+                    // on this side moves the split toward a* by the merged
+                    // block's sources, i.e. strictly improves until the rank is
+                    // 0.  Left side (a < zp): the target grows left to the
+                    // nearest block start B[j] <= idxL - zp; right side
+                    // (a > a*): right to the nearest end BE[j] >= idxR + holes
+                    // - a* (or the last block, rank still > 0).
+                    int tL = t, tR = t;
+                    if (a < c.zp) {
+                        const int lim = c.idxL - c.zp;
+                        for (int j1 = t; j1 > 0; j1 -= 32) {
+                            const int j = j1 - 32 + lane;
+                            const unsigned m = __ballot_sync(FULL, j >= 0 && B[j] <= lim);
+                            if (m) {
+                                tL = j1 - 32 + 31 - __clz(m);
+                                break;
+                            }
+                        }
+                    } else {
+                        const int lim = c.idxR + (k - c.R) - c.astar;
+                        tR = nb - 1;
+                        for (int j0 = t + 1; j0 < nb; j0 += 32) {
+                            const int j = j0 + lane;
+                            const unsigned m = __ballot_sync(FULL, j < nb && BE[j] >= lim);
+                            if (m) {
+                                tR = j0 + __ffs(m) - 1;
+                                break;
+                            }
+                        }
+                    }
+                    s0 = B[tL];
+                    s1 = BE[tR];
+                    a = block_a(c, s0, s1);
+                    if (cost_rank(c, a) != global) {  // whole chain (exact1d.cpp:293-296)
+                        s0 = 0;
+                        s1 = ns;
+                        a = ga;
+                    }
+                } else if (wt != global) {
+                    // infeasible target: the literal sweep (exact1d.cpp:269-289);
+                    // blocks tL..tR form the target, list index i maps to the
+                    // current merged list
                     int tL = t, tR = t, i = tL >= 1 ? tL - 1 : 0;
                     const int nb0 = nb;
                     for (;;) {

@@ -134,7 +134,7 @@ def test_band_batch_sweep_stress(gpu, ref):
     from barely feasible (long certification sweeps, many blocks, cost ties)
     to dense."""
     rng = np.random.default_rng(0xc4a1)
-    for _ in range(40):
+    for _ in range(150):
         n = int(rng.integers(8, 700))
         w = int(rng.integers(1, n + 1))
         tl = int(rng.integers(0, n - w + 1))
