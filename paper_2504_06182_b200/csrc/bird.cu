@@ -176,8 +176,10 @@ __device__ __forceinline__ uint64_t win_mask(bool top, int w, int lim) {
     return top ? low << (size - n) : low;  // top: bit i <-> level win_hi - 1 - i
 }
 
-// counts one window of one side with the warps [g0, g0 + gn) of the CTA
-__device__ void count_window(const Geo &g, const uint64_t *dep, int c, bool top, int w, int *lvl, int g0, int gn) {
+// counts one window of one side with the warps [g0, g0 + gn) of the CTA and
+// leaves its transposed slot words in T (as transpose_window would)
+__device__ void count_window(const Geo &g, const uint64_t *dep, int c, bool top, int w, int *lvl, uint32_t *T,
+                             int g0, int gn) {
     const int warp = warp_id(), lane = lane_id();
     if (warp < g0 || warp >= g0 + gn) return;
     const int V0 = win_V0(g, top, w), nslots = win_nslots(g, win_hi(w)), nch = (nslots + 31) / 32;
@@ -186,9 +188,10 @@ __device__ void count_window(const Geo &g, const uint64_t *dep, int c, bool top,
     for (int ch = warp - g0; ch < nch; ch += gn) {
         int col, dist;
         const uint64_t word = slot_word(g, dep, c, ch * 32 + lane, nslots, V0, top, &col, &dist, wmask);
-        if (!__any_sync(FULL, word != 0ull)) continue;
-        uint32_t t_lo, t_hi;
-        transpose64(word, t_lo, t_hi);
+        uint32_t t_lo = 0u, t_hi = 0u;
+        if (__any_sync(FULL, word != 0ull)) transpose64(word, t_lo, t_hi);
+        T[ch * 64 + lane] = t_lo;
+        T[ch * 64 + 32 + lane] = t_hi;
         acc_lo += __popc(t_lo);
         acc_hi += __popc(t_hi);
     }
@@ -336,8 +339,9 @@ __device__ int pooled_event(const Geo &g, uint64_t *dep, int *sigma, int c, int1
         const bool wt = S[sWantT], wb = S[sWantB];
         const int wtop = S[sWT], wbot = S[sWB];
         const int half = nw / 2;
-        if (wt) count_window(g, dep, c, true, wtop, ps.lvl_t, 0, wb ? half : nw);
-        if (wb) count_window(g, dep, c, false, wbot, ps.lvl_b, wt ? half : 0, wt ? nw - half : nw);
+        if (wt) count_window(g, dep, c, true, wtop, ps.lvl_t, ps.bal, 0, wb ? half : nw);
+        if (wb) count_window(g, dep, c, false, wbot, ps.lvl_b, ps.bal + (size_t)g.nchunk * 64, wt ? half : 0,
+                             wt ? nw - half : nw);
         __syncthreads();
         if (warp == 0 && wt) {
             const int f = finish_window(g, true, wtop, ps.lvl_t, S[sFoundT], ps.otop, holes);
@@ -438,12 +442,18 @@ __device__ int pooled_event(const Geo &g, uint64_t *dep, int *sigma, int c, int1
     long long disp = 0;
     const int last_t = vt_li >= 0 ? win_of(vt_li) : -1, last_b = vb_li >= 0 ? win_of(vb_li) : -1;
     uint32_t *Tt = ps.bal, *Tb = ps.bal + (size_t)g.nchunk * 64;
-    for (int w = 0; w <= max(last_t, last_b); ++w) {
+    // windows in reverse: each side's last counted window still has its
+    // transposed words in T from the count (rows of levels <= v* are the same
+    // with the emission's narrower mask: farther slots reach no such level);
+    // windows hold disjoint levels, so the emission order does not matter
+    bool cached_t = last_t >= 0 && last_t == S[sWT] - 1, cached_b = last_b >= 0 && last_b == S[sWB] - 1;
+    for (int w = max(last_t, last_b); w >= 0; --w) {
         const bool dt = w <= last_t, db = w <= last_b;
+        const bool tt = dt && !(cached_t && w == last_t), tb = db && !(cached_b && w == last_b);
         const int half = nw / 2;
-        if (dt) transpose_window(g, dep, c, true, w, vt_li, Tt, 0, db ? half : nw);
-        if (db) transpose_window(g, dep, c, false, w, vb_li, Tb, dt ? half : 0, dt ? nw - half : nw);
-        __syncthreads();
+        if (tt) transpose_window(g, dep, c, true, w, vt_li, Tt, 0, db ? half : nw);
+        if (tb) transpose_window(g, dep, c, false, w, vb_li, Tb, dt ? half : 0, dt ? nw - half : nw);
+        if (tt || tb) __syncthreads();
         if (dt)
             disp += emit_window(g, dep, sigma, c, true, w, a, a, R, n_right, n_left, ps.lvl_t, Tt, vt_li, rt, o, off,
                                 evid, 0, db ? half : nw);
