@@ -1468,7 +1468,11 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
     }();
     int warps = 4, mode = 0;
     size_t smem = 0;
-    if (bm_bytes <= 96 * 1024) {
+    static const int occ_env = [] {
+        const char *e = getenv("RECON_BATCH_OCC_SMEM");
+        return e ? atoi(e) : 1;
+    }();
+    if (occ_env && bm_bytes <= 96 * 1024) {
         mode = 1 | (a.mlog ? 2 : 0);
         if (bsm_env && S < 65536 && bm_bytes + blk_bytes <= 100 * 1024) mode |= 4;
         const int64_t per = bm_bytes + ((mode & 4) ? blk_bytes : 0);
