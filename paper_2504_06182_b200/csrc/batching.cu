@@ -1087,12 +1087,13 @@ __device__ __forceinline__ void merge_ready(const ImplicitPaths &paths, const Pi
     __syncwarp();
 }
 
-template <bool SM, bool LOG, bool BSM>
+template <bool SM, bool SMI, bool LOG, bool BSM>
 __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, const PipeRecords R) {
     const int lane = lane_id();
     const int P = J.P, H = J.H;
     BatchScratch s = J.s;
-    const Bits<SM> occ(s.occ), inb(s.inb);
+    const Bits<SM> occ(s.occ);
+    const Bits<SMI> inb(s.inb);
     const Blockers<BSM> blk(s.blockers, s.blk_sm);  // BSM: filled by the caller
     // ---- init: blockers = in-degree (given); zero-length paths finish at once
     long long left = 0;
@@ -1368,10 +1369,12 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, c
 }
 
 // MODE bits: 1 = occupancy / in-batch bitmaps in shared memory, 2 = move log,
-// 4 = blocker counts in shared memory (u16, after the bitmaps; needs 1)
+// 4 = blocker counts in shared memory (u16, after the bitmaps; needs 1),
+// 8 = the in-batch bitmap stays in global memory (only the candidate scan of
+// the general path touches it), halving a large grid's shared memory
 template <int MODE>
 __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) {
-    constexpr bool occ_in_smem = MODE & 1, LOG = MODE & 2, BSM = MODE & 4;
+    constexpr bool occ_in_smem = MODE & 1, LOG = MODE & 2, BSM = MODE & 4, INB_SM = occ_in_smem && !(MODE & 8);
     extern __shared__ __align__(16) uint32_t bsmem[];
     const int64_t S = (int64_t)a.W * a.k, nwb = ((int64_t)a.W * a.H + 31) / 32;
     const int nw = blockDim.x >> 5;
@@ -1402,16 +1405,16 @@ __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) 
         J.succ = a.succ;
         J.s.occ = a.occ + inst * nwb;
         J.s.inb = a.inb + inst * nwb;
-        const int64_t nbw = BSM ? (S + 1) / 2 : 0;
-        if (occ_in_smem) {  // the instance's occupancy and in-batch bitmaps live in this warp's shared memory
-            uint32_t *mine = bsmem + (size_t)warp_id() * (2 * nwb + nbw);
+        const int64_t nbw = BSM ? (S + 1) / 2 : 0, nib = INB_SM ? nwb : 0, per = nwb + nib + nbw;
+        if (occ_in_smem) {  // the instance's occupancy (and in-batch) bitmaps live in this warp's shared memory
+            uint32_t *mine = bsmem + (size_t)warp_id() * per;
             for (int64_t w = lane_id(); w < nwb; w += 32) {
                 mine[w] = J.s.occ[w];
-                mine[nwb + w] = 0u;
+                if (INB_SM) mine[nwb + w] = 0u;
             }
             __syncwarp();
             J.s.occ = mine;
-            J.s.inb = mine + nwb;
+            if (INB_SM) J.s.inb = mine + nwb;
         }
         J.s.blockers = a.indeg + o;
         J.s.newly = a.newly + o;
@@ -1430,7 +1433,7 @@ __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) 
         ImplicitPaths ip{a.path_src + o, a.path_dst + o, a.mbase + o, a.mbase[o], a.H};
         const PipeRecords R{a.rec + o, a.rec2 + o, a.rb + o, a.rb2 + o};
         if (BSM) {
-            uint32_t *bw = bsmem + (size_t)warp_id() * (2 * nwb + nbw) + 2 * nwb;
+            uint32_t *bw = bsmem + (size_t)warp_id() * per + nwb + nib;
             const int P = J.P;
             for (int64_t w = lane_id(); w < nbw; w += 32) {
                 const int p = (int)(2 * w);
@@ -1441,7 +1444,7 @@ __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) 
             __syncwarp();
             J.s.blk_sm = bw;
         }
-        batch_warp_pipe<occ_in_smem, LOG, BSM>(J, ip, R);
+        batch_warp_pipe<occ_in_smem, INB_SM, LOG, BSM>(J, ip, R);
     }
 }
 
@@ -1475,13 +1478,20 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
     if (occ_env && bm_bytes <= 96 * 1024) {
         mode = 1 | (a.mlog ? 2 : 0);
         if (bsm_env && S < 65536 && bm_bytes + blk_bytes <= 100 * 1024) mode |= 4;
-        const int64_t per = bm_bytes + ((mode & 4) ? blk_bytes : 0);
+        int64_t per = bm_bytes + ((mode & 4) ? blk_bytes : 0);
         warps = (int)std::max<int64_t>(1, std::min<int64_t>(8, (200 * 1024) / per));
+        // more instances than the SMs hold with both bitmaps: keep only the
+        // occupancy in shared memory, for twice the warps per SM
+        if (mode == 1 && warps < 8 && a.count > (int64_t)warps * sms) {
+            mode |= 8;
+            per = bm_bytes / 2;
+            warps = (int)std::max<int64_t>(1, std::min<int64_t>(8, (200 * 1024) / per));
+        }
         smem = (size_t)warps * per;
     }
     void (*kern)(PipelineArgs) = mode == 0 ? batch_pipeline_kernel<0> : mode == 1 ? batch_pipeline_kernel<1>
-                               : mode == 3 ? batch_pipeline_kernel<3> : mode == 5 ? batch_pipeline_kernel<5>
-                                                                       : batch_pipeline_kernel<7>;
+                               : mode == 9 ? batch_pipeline_kernel<9> : mode == 3 ? batch_pipeline_kernel<3>
+                               : mode == 5 ? batch_pipeline_kernel<5> : batch_pipeline_kernel<7>;
     if (smem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int grid = (int)std::min<int64_t>(((int64_t)a.count + warps - 1) / warps, (int64_t)sms * 32);
     kern<<<grid, warps * 32, smem, st>>>(a);

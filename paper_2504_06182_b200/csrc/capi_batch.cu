@@ -125,14 +125,16 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool 
     a.succ = c->dev<int32_t>(S_BM_AUX5, (size_t)edges + 1);
     a.edge_capacity = edges;
     if (!a.succ) return cuda_fail(cudaErrorMemoryAllocation, "pipeline succ", detail);
-    // move log (pipeline_scatter_moves) for many small instances, whose
-    // scattered move_batch stores otherwise miss L2 one 4-byte store at a time;
-    // large instances write move_batch directly.  RECON_BATCH_LOG=0/1 forces.
+    // move log (scattered into move_batch by each warp when its instance
+    // finishes) for many small instances, whose scattered move_batch stores
+    // otherwise miss L2 one 4-byte store at a time; large instances (whose log
+    // would cost 8 B per move of HBM) write move_batch directly.
+    // RECON_BATCH_LOG=0/1 forces.
     static const int log_env = [] {
         const char *e = getenv("RECON_BATCH_LOG");
         return e ? atoi(e) : -1;
     }();
-    const bool use_log = log_env >= 0 ? log_env == 1 : (n >= (size_t)c->sms * 4 && 2 * nwb * 4 <= 96 * 1024);
+    const bool use_log = log_env >= 0 ? log_env == 1 : (n >= (size_t)c->sms * 4 && 2 * nwb * 4 <= 32 * 1024);
     a.mlog = nullptr;
     if (use_log) {
         a.mlog = c->dev<int2>(S_BM_AUX6, (size_t)counts[1] + 1);

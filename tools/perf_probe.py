@@ -169,6 +169,7 @@ CASES = {
     "r128_bird_b4096": lambda: grid("bird", 128, 128, 76, 9830, 0x12800000, 4096),
     "c3_pipeline_none": lambda: pipeline("bird", 64, 64, 40, 2662, 0x64000000, 4096, 0),
     "c3_pipeline_coldir": lambda: pipeline("bird", 64, 64, 40, 2662, 0x64000000, 1024, 1),
+    "c5_pipeline_512": lambda: pipeline("bird", 512, 512, 307, 157286, 0x51200000, 512, 0, 11_000_000),
     "c5_pipeline_256": lambda: pipeline("bird", 512, 512, 307, 157286, 0x51200000, 256, 0, 11_000_000),
     "c5_pipeline_4": lambda: pipeline("bird", 512, 512, 307, 157286, 0x51200000, 4, 0, 12_000_000),
     "c5_pipeline_4_validate": lambda: pipeline("bird", 512, 512, 307, 157286, 0x51200000, 4, 0, 12_000_000, True),
