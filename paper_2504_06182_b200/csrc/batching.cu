@@ -1126,9 +1126,18 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, c
     bool regmode = false;
     LanePath lp;
     lp.p = INT_MAX;
+    // the lane's current move (fr -> to), advanced incrementally on acceptance
+    int32_t fr = -1, to = -1;
+    auto lane_move = [&]() {
+        if (lp.p != INT_MAX) {
+            fr = lp.v(H, lp.k);
+            to = lp.v(H, lp.k + 1);
+        }
+    };
     auto enter_regmode = [&]() {
         lp.p = INT_MAX;
         if (lane < nready) lp = rec_lane(R.rec[lane], R.rb[lane]);
+        lane_move();
         regmode = true;
     };
     auto put_move = [&](int64_t slot, int rank_in_batch) {
@@ -1139,11 +1148,6 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, c
     while (left > 0) {
         if (regmode) {
             const bool valid = lp.p != INT_MAX;
-            int32_t fr = -1, to = -1;
-            if (valid) {
-                fr = lp.v(H, lp.k);
-                to = lp.v(H, lp.k + 1);
-            }
             const bool cand = valid && !occ.get(to);
             const unsigned cm = __ballot_sync(FULL, cand);
             if (!cm) {
@@ -1173,6 +1177,10 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, c
                     q0 = J.soff[lp.p];
                     q1 = J.soff[lp.p + 1];
                 }
+                // next move: horizontal steps first (virtual_line.cpp:150-173)
+                const int dx = abs(lp.xt - lp.xs);
+                fr = to;
+                to += lp.k < dx ? (lp.xt > lp.xs ? H : -H) : (lp.yt > lp.ys ? 1 : -1);
             }
             nlog += __popc(acc);
             left -= __popc(acc);
@@ -1232,6 +1240,7 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, c
                     q.base = __shfl_sync(FULL, lp.base, src);
                     lp = lane < nlive ? q : LanePath{INT_MAX, 0, 0, 0, 0, 0, 0, 0};
                 }
+                lane_move();  // lanes were reloaded / reordered
             }
             __syncwarp();
             ++nb;
