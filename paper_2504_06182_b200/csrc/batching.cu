@@ -72,20 +72,6 @@ struct LanePath {
     }
 };
 
-__device__ __forceinline__ LanePath load_lane_path(const ImplicitPaths &ip, const int32_t *next, int p) {
-    LanePath r;
-    r.p = p;
-    r.k = next[p];
-    const int s = ip.src[p], t = ip.dst[p];
-    r.xs = s / ip.H;
-    r.ys = s - r.xs * ip.H;
-    r.xt = t / ip.H;
-    r.yt = t - r.xt * ip.H;
-    r.len = abs(r.xt - r.xs) + abs(r.yt - r.ys);
-    r.base = ip.move_base(p);
-    return r;
-}
-
 // vertex bitmaps (occupancy, in-batch); SM = in shared memory, accessed with
 // ld.shared / atom.shared (a generic pointer would take the generic path)
 template <bool SM>
@@ -155,16 +141,14 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t *a, int n, int x) {
     return lo;
 }
 
-// FAST: paths are solver output (every source occupied, distinct tokens), so
-// the only possible vertex conflict inside a batch is a shared destination;
-// the minimum id wins (and, under column_direction, the class of the first
-// accepted move).  The general entry point keeps the literal pairwise checks.
-template <class Paths, bool FAST, bool SM = false>
+// The general entry point (arbitrary paths, given dag): the literal
+// pairwise checks.  (The solver pipeline runs batch_warp_pipe below.)
+template <class Paths>
 __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
     const int lane = lane_id();
     const int P = J.P, H = J.H;
     BatchScratch s = J.s;
-    const Bits<SM> occ(s.occ), inb(s.inb);
+    const Bits<false> occ(s.occ), inb(s.inb);
     // ---- init: next = 0, blockers = in-degree (given), finish zero-length paths
     long long left = 0;
     for (int p = lane; p < P; p += 32) {
@@ -192,166 +176,7 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
     __syncwarp();
     int32_t *ready = s.ready, *ready2 = s.ready2;
     int nb = 0, status = RECON_OK;
-    // Register-resident frontier (FAST path, <= 32 ready paths): lane i keeps
-    // ready path i (ascending id) with its step and endpoints in registers, so
-    // a batch costs one occupancy probe plus fire-and-forget atomics.
-    constexpr bool REG = FAST && std::is_same<Paths, ImplicitPaths>::value;
-    bool regmode = false;
-    LanePath lp;
-    lp.p = INT_MAX;
-    auto enter_regmode = [&]() {
-        lp.p = INT_MAX;
-        if (lane < nready) lp = load_lane_path(reinterpret_cast<const ImplicitPaths &>(paths), s.next, ready[lane]);
-        regmode = true;
-        __syncwarp();
-    };
-    if (REG && nready <= 32) enter_regmode();
     while (left > 0) {
-        if (REG && regmode) {
-            const bool valid = lp.p != INT_MAX;
-            int32_t fr = -1, to = -1;
-            if (valid) {
-                fr = lp.v(H, lp.k);
-                to = lp.v(H, lp.k + 1);
-            }
-            const bool cand = valid && !occ.get(to);
-            const unsigned cm = __ballot_sync(FULL, cand);
-            if (!cm) {
-                status = RECON_ERR_INPUT;  // batching.cpp:127-128
-                break;
-            }
-            bool a;
-            if (J.preset != 0) {
-                const int first = __ffs(cm) - 1;
-                const int32_t ff = __shfl_sync(FULL, fr, first), ft = __shfl_sync(FULL, to, first);
-                a = cand && compatible(J.preset, H, fr, to, ff, ft);
-            } else {
-                const unsigned same = __match_any_sync(FULL, cand ? to : -2 - lane);
-                a = cand && (same & lanemask_lt()) == 0;
-            }
-            const unsigned acc = __ballot_sync(FULL, a);
-            if (a) occ.clr(fr);
-            __syncwarp();
-            if (a) occ.set(to);
-            bool fin = false;
-            if (a) {
-                J.move_batch[lp.base + lp.k] = nb;
-                ++lp.k;
-                fin = lp.k == lp.len;
-            }
-            left -= __popc(acc);
-            const unsigned fm = __ballot_sync(FULL, fin);
-            if (fm) {
-                int64_t q0 = 0, q1 = 0;
-                if (fin) {
-                    s.done[lp.p] = 1;
-                    q0 = J.soff[lp.p];
-                    q1 = J.soff[lp.p + 1];
-                }
-                int nnew = 0, tot;
-                const int basei = warp_excl_scan((int)(q1 - q0), &tot);
-                for (int t0 = 0; t0 < tot; t0 += 32) {
-                    const int t = t0 + lane;
-                    int owner = 0;
-#pragma unroll
-                    for (int st = 16; st > 0; st >>= 1) {
-                        const int cl = owner + st;
-                        if (__shfl_sync(FULL, basei, cl) <= t) owner = cl;
-                    }
-                    const int64_t oq0 = __shfl_sync(FULL, q0, owner);
-                    const int ob = __shfl_sync(FULL, basei, owner);
-                    bool released = false;
-                    int sc = -1;
-                    if (t < tot) {
-                        sc = J.succ[oq0 + (t - ob)];
-                        released = atomicSub(&s.blockers[sc], 1) == 1;
-                    }
-                    const unsigned rm = __ballot_sync(FULL, released);
-                    if (released) s.newly[nnew + __popc(rm & lanemask_lt())] = sc;
-                    nnew += __popc(rm);
-                }
-                if (fin) lp.p = INT_MAX;
-                __syncwarp();
-                const unsigned live = __ballot_sync(FULL, lp.p != INT_MAX);
-                const int nlive = __popc(live);
-                if (nlive + nnew > 32) {
-                    // spill to the shared-list path: live lanes are ascending
-                    if (lp.p != INT_MAX) {
-                        s.next[lp.p] = lp.k;
-                        ready2[__popc(live & lanemask_lt())] = lp.p;
-                    }
-                    __syncwarp();
-                    if (nnew <= 32) {
-                        int v = lane < nnew ? s.newly[lane] : INT_MAX;
-                        v = warp_sort32(v);
-                        if (lane < nnew) s.newly[lane] = v;
-                    } else {
-                        for (int q = lane; q < nnew; q += 32) {
-                            const int x = s.newly[q];
-                            int lt = 0;
-                            for (int r2 = 0; r2 < nnew; ++r2) lt += s.newly[r2] < x;
-                            s.mem[lt] = x;
-                        }
-                        __syncwarp();
-                        for (int q = lane; q < nnew; q += 32) s.newly[q] = s.mem[q];
-                    }
-                    __syncwarp();
-                    for (int i = lane; i < nlive; i += 32) {
-                        const int x = ready2[i];
-                        ready[i + lower_bound_i32(s.newly, nnew, x)] = x;
-                    }
-                    for (int j = lane; j < nnew; j += 32) {
-                        const int y = s.newly[j];
-                        ready[j + lower_bound_i32(ready2, nlive, y)] = y;
-                    }
-                    __syncwarp();
-                    nready = nlive + nnew;
-                    regmode = false;
-                } else if (nnew > 0) {
-                    // newly released paths take the empty lanes, then sort lanes by id
-                    const unsigned empty = ~live;
-                    const int erank = __popc(empty & lanemask_lt());
-                    if (lp.p == INT_MAX && erank < nnew)
-                        lp = load_lane_path(reinterpret_cast<const ImplicitPaths &>(paths), s.next, s.newly[erank]);
-                    int key = lp.p == INT_MAX ? INT_MAX : (lp.p << 5) | lane;
-                    key = warp_sort32(key);
-                    const int src = key == INT_MAX ? lane : (key & 31);
-                    LanePath q;
-                    q.p = __shfl_sync(FULL, lp.p, src);
-                    q.k = __shfl_sync(FULL, lp.k, src);
-                    q.len = __shfl_sync(FULL, lp.len, src);
-                    q.xs = __shfl_sync(FULL, lp.xs, src);
-                    q.ys = __shfl_sync(FULL, lp.ys, src);
-                    q.xt = __shfl_sync(FULL, lp.xt, src);
-                    q.yt = __shfl_sync(FULL, lp.yt, src);
-                    q.base = __shfl_sync(FULL, lp.base, src);
-                    lp = key == INT_MAX ? LanePath{INT_MAX, 0, 0, 0, 0, 0, 0, 0} : q;
-                } else {
-                    // finished lanes leave gaps: compact live lanes (order kept)
-                    const int dst_rank = __popc(live & lanemask_lt());
-                    int src = lane;
-                    // lane L takes the L-th live lane
-                    for (int st = 0; st < 32; ++st) {
-                        const bool hit = ((live >> st) & 1u) && __popc(live & ((1u << st) - 1u)) == lane;
-                        if (hit) src = st;
-                    }
-                    (void)dst_rank;
-                    LanePath q;
-                    q.p = __shfl_sync(FULL, lp.p, src);
-                    q.k = __shfl_sync(FULL, lp.k, src);
-                    q.len = __shfl_sync(FULL, lp.len, src);
-                    q.xs = __shfl_sync(FULL, lp.xs, src);
-                    q.ys = __shfl_sync(FULL, lp.ys, src);
-                    q.xt = __shfl_sync(FULL, lp.xt, src);
-                    q.yt = __shfl_sync(FULL, lp.yt, src);
-                    q.base = __shfl_sync(FULL, lp.base, src);
-                    lp = lane < nlive ? q : LanePath{INT_MAX, 0, 0, 0, 0, 0, 0, 0};
-                }
-            }
-            __syncwarp();
-            ++nb;
-            continue;
-        }
         // ---- 1. candidate scan (ascending id), greedy acceptance
         int nacc = 0;
         int32_t f_from = -1, f_to = -1;  // first accepted move of the batch
@@ -390,39 +215,21 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
             const unsigned cm_all = __ballot_sync(FULL, cand);
             if (!cm_all) continue;
             unsigned acc = 0;
-            if (FAST) {
-                bool a;
-                if (J.preset != 0) {
-                    // column_direction: every candidate in the class (direction + column/row)
-                    // of the batch's first move; a shared destination needs two directions,
-                    // so it cannot occur inside one class
-                    const int first = __ffs(cm_all) - 1;
-                    const int32_t ff = f_from >= 0 ? f_from : __shfl_sync(FULL, fr, first);
-                    const int32_t ft = f_from >= 0 ? f_to : __shfl_sync(FULL, to, first);
-                    a = cand && compatible(J.preset, H, fr, to, ff, ft);
-                } else {
-                    // shared destination: the lowest lane (= lowest id) of each group wins
-                    const unsigned same = __match_any_sync(FULL, cand ? to : -2 - lane);
-                    a = cand && (same & lanemask_lt()) == 0;
+            // literal batching.cpp:107-125 greedy: pairwise vertex-disjointness
+            // and the constraint predicate against earlier accepted lanes
+            unsigned cm = 0;
+            for (unsigned m = cm_all; m; m &= m - 1) {
+                const int i = __ffs(m) - 1;
+                const int32_t ofr = __shfl_sync(FULL, fr, i), oto = __shfl_sync(FULL, to, i);
+                if (i < lane && cand) {
+                    const bool share = ofr == fr || ofr == to || oto == fr || oto == to;
+                    if (share || !compatible(J.preset, H, fr, to, ofr, oto)) cm |= 1u << i;
                 }
-                acc = __ballot_sync(FULL, a);
-            } else {
-                // literal batching.cpp:107-125 greedy: pairwise vertex-disjointness
-                // and the constraint predicate against earlier accepted lanes
-                unsigned cm = 0;
-                for (unsigned m = cm_all; m; m &= m - 1) {
-                    const int i = __ffs(m) - 1;
-                    const int32_t ofr = __shfl_sync(FULL, fr, i), oto = __shfl_sync(FULL, to, i);
-                    if (i < lane && cand) {
-                        const bool share = ofr == fr || ofr == to || oto == fr || oto == to;
-                        if (share || !compatible(J.preset, H, fr, to, ofr, oto)) cm |= 1u << i;
-                    }
-                }
-                for (unsigned m = cm_all; m; m &= m - 1) {
-                    const int i = __ffs(m) - 1;
-                    const bool a = __shfl_sync(FULL, cand && !(cm & acc), i);
-                    if (a) acc |= 1u << i;
-                }
+            }
+            for (unsigned m = cm_all; m; m &= m - 1) {
+                const int i = __ffs(m) - 1;
+                const bool a = __shfl_sync(FULL, cand && !(cm & acc), i);
+                if (a) acc |= 1u << i;
             }
             if ((acc >> lane) & 1u) {
                 inb.set(fr);
@@ -544,7 +351,6 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
             nready = nkeep + nnew;
         }
         ++nb;
-        if (REG && nready <= 32) enter_regmode();
     }
     if (lane == 0) {
         *J.batch_count = status == RECON_OK ? nb : 0;
@@ -554,7 +360,7 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
 }
 
 __global__ void batch_explicit_kernel(BatchJob J, ExplicitPaths paths) {
-    if (threadIdx.x < 32) batch_warp<ExplicitPaths, false>(J, paths);
+    if (threadIdx.x < 32) batch_warp<ExplicitPaths>(J, paths);
 }
 
 cudaError_t launch_batch_explicit(const BatchJob &J, const int64_t *off, const int32_t *verts, cudaStream_t st) {
@@ -948,8 +754,12 @@ cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *
 // xs | ys << 16, xt | yt << 16} plus its move base in a parallel array, kept
 // in ascending p.  A batch reads its candidates with coalesced loads and
 // advances them in place; only newly released paths touch the per-path
-// arrays (src, dst, mbase).  Same acceptance, application and release as
-// batch_warp (FAST, implicit paths); records replace next / done / ready ids.
+// arrays (src, dst, mbase).  Acceptance: the paths are solver output (every
+// source occupied, distinct tokens), so the only possible vertex conflict
+// inside a batch is a shared destination and the minimum id wins (under
+// column_direction, the class of the batch's first move); application and
+// release as in batch_warp.  With <= 32 ready paths, lane i keeps path i in
+// registers (register-resident frontier).
 
 __device__ __forceinline__ int4 make_rec(const ImplicitPaths &ip, int p, int *base) {
     const int s = ip.src[p], t = ip.dst[p];
