@@ -3,6 +3,9 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "grid_common.cuh"
 
@@ -26,6 +29,57 @@ int64_t redrec_plan_smem(int W);
 template <bool LAT>
 __global__ void bird_kernel(GridParams p);
 static void (*bird_exec(const GridShape &s))(GridParams) { return s.nwarps > 8 ? bird_kernel<true> : bird_kernel<false>; }
+
+// Launch-attribute caches: a lone small instance's latency is a few kernel
+// durations, so per-call cudaFuncSetAttribute / occupancy / attribute queries
+// (each a driver round trip) are done once per (device, kernel, size).
+namespace {
+std::mutex g_attr_mu;
+std::map<std::pair<int, const void *>, int> g_smem_set;
+std::map<std::tuple<int, const void *, int, int64_t>, int> g_occ;
+std::map<int, int> g_sms;
+
+int cur_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
+cudaError_t ensure_smem(const void *kern, int64_t smem) {
+    const int dev = cur_device();
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    int &have = g_smem_set[{dev, kern}];
+    if (smem <= have) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) have = (int)smem;
+    return e;
+}
+
+int occupancy(const void *kern, int threads, int64_t smem) {
+    const int dev = cur_device();
+    {
+        std::lock_guard<std::mutex> lk(g_attr_mu);
+        auto it = g_occ.find({dev, kern, threads, smem});
+        if (it != g_occ.end()) return it->second;
+    }
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem);
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    g_occ[{dev, kern, threads, smem}] = nb;
+    return nb;
+}
+
+int sm_count() {
+    const int dev = cur_device();
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto it = g_sms.find(dev);
+    if (it != g_sms.end()) return it->second;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    g_sms[dev] = sms;
+    return sms;
+}
+}  // namespace
 
 bool grid_shape(int W, int H, int k, int nwarps, int solver, GridShape &s) {
     if (W <= 0 || H <= 0 || W > 1024 || H > 1024) return false;
@@ -83,18 +137,15 @@ cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaSt
         // plans first: one warp per instance, all instances in parallel
         const int pw = 4;
         const int64_t psmem = pw * redrec_plan_smem(p.shape.W);
-        e = cudaFuncSetAttribute(redrec_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+        e = ensure_smem((const void *)redrec_plan_kernel, psmem);
         if (e != cudaSuccess) return e;
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, redrec_plan_kernel, 32 * pw, psmem);
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int per_sm = occupancy((const void *)redrec_plan_kernel, 32 * pw, psmem);
+        const int sms = sm_count();
         const int pgrid = std::max(1, std::min((p.count + pw - 1) / pw, std::max(1, per_sm) * sms));
         if (ev) cudaEventRecord(ev[0], stream);
         redrec_plan_kernel<<<pgrid, 32 * pw, psmem, stream>>>(p);
     }
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.shape.smem_bytes);
+    e = ensure_smem((const void *)kern, p.shape.smem_bytes);
     if (e != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[1], stream);
     kern<<<grid, threads, p.shape.smem_bytes, stream>>>(p);
@@ -103,11 +154,9 @@ cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaSt
 }
 
 int grid_occupancy(int solver, const GridShape &s) {
-    int nb = 0;
     void (*kern)(GridParams) = solver == 0 ? redrec_exec(s) : bird_exec(s);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s.smem_bytes);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32 * s.nwarps, s.smem_bytes);
-    return nb;
+    ensure_smem((const void *)kern, s.smem_bytes);
+    return occupancy((const void *)kern, 32 * s.nwarps, s.smem_bytes);
 }
 
 }  // namespace rb
