@@ -23,6 +23,7 @@
 //     are a contiguous run of the sorted sources.
 
 #include <climits>
+#include <cstdint>
 
 #include "chain.cuh"
 #include "common.cuh"
@@ -380,15 +381,28 @@ __global__ void __launch_bounds__(256) chain_band_kernel(ChainBandParams p) {
             const int first = c.idxL - a;
             int32_t *ps_out = p.path_src + (size_t)ch * k;
             int32_t *pd_out = p.path_dst + (size_t)ch * k;
-            for (int i = lane; i < k; i += 32) {
-                const int src = S[first + i];
-                const int dst = tl + i;
-                ps_out[i] = src;
-                pd_out[i] = dst;
-                disp += src > dst ? src - dst : dst - src;
-                displaced += src != dst;
+            int d32 = 0;  // <= k * n <= 2^24
+            if ((k & 3) == 0 && ((reinterpret_cast<uintptr_t>(ps_out) | reinterpret_cast<uintptr_t>(pd_out)) & 15) == 0) {
+                // 4 paths per lane per step: 128-bit stores
+                for (int i = 4 * lane; i < k; i += 128) {
+                    const int s0 = S[first + i], s1 = S[first + i + 1], s2 = S[first + i + 2], s3 = S[first + i + 3];
+                    const int t0 = tl + i;
+                    *reinterpret_cast<int4 *>(ps_out + i) = make_int4(s0, s1, s2, s3);
+                    *reinterpret_cast<int4 *>(pd_out + i) = make_int4(t0, t0 + 1, t0 + 2, t0 + 3);
+                    d32 += abs(s0 - t0) + abs(s1 - t0 - 1) + abs(s2 - t0 - 2) + abs(s3 - t0 - 3);
+                    displaced += (s0 != t0) + (s1 != t0 + 1) + (s2 != t0 + 2) + (s3 != t0 + 3);
+                }
+            } else {
+                for (int i = lane; i < k; i += 32) {
+                    const int src = S[first + i];
+                    const int dst = tl + i;
+                    ps_out[i] = src;
+                    pd_out[i] = dst;
+                    d32 += src > dst ? src - dst : dst - src;
+                    displaced += src != dst;
+                }
             }
-            disp = warp_sum64(disp);
+            disp = warp_sum(d32);
             displaced = warp_sum(displaced);
         }
         if (lane == 0) {
