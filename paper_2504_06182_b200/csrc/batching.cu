@@ -1207,7 +1207,7 @@ __global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) 
         }
         const int64_t o = (int64_t)inst * S;
         const int64_t moves = a.mbase[o + a.path_count[inst]] - a.mbase[o];
-        if (moves > a.move_stride) {
+        if (moves > a.move_stride || moves >= INT_MAX) {  // (records hold 32-bit move slots)
             if (lane_id() == 0) {
                 a.status[inst] = RECON_ERR_CAPACITY;
                 a.batch_count[inst] = 0;
