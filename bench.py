@@ -157,6 +157,57 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def other_configs(lib, torch, dev, stream, reps=3):
+    """C2 (1M chains of 1024, band [256, 767]) and C3 (4096 bird 64x64 h'40 +
+    batching, preset none), each timed over `reps` runs after one warm-up."""
+    import ctypes as C
+    from paper_2504_06182_b200.abi import ChainBatch, GridBatch, PipelineBatch
+    from paper_2504_06182_b200.inputs import sample_chains, sample_grids
+
+    def run(fn):
+        fn()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            st = fn()
+            e1.record(stream)
+            e1.synchronize()
+            if st != 0:
+                raise RuntimeError(f"config run failed {st}: {lib.last_cuda_error()}")
+            ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
+    out = {}
+    n, k, tl, th, cnt = 1024, 563, 256, 767, 1 << 20
+    occ = torch.from_numpy(sample_chains(0x1D000000, cnt, n, k).view(np.int64)).to(dev)
+    nt = th - tl + 1
+    src = torch.empty(cnt * nt, dtype=torch.int32, device=dev)
+    dst = torch.empty_like(src)
+    i64 = torch.empty(cnt, dtype=torch.int64, device=dev)
+    i32 = torch.empty(3 * cnt, dtype=torch.int32, device=dev)
+    cb = ChainBatch(occ.data_ptr(), cnt, n, tl, th, src.data_ptr(), dst.data_ptr(), i64.data_ptr(), i32.data_ptr(),
+                    i32.data_ptr() + 4 * cnt, i32.data_ptr() + 8 * cnt)
+    ms = run(lambda: lib.lib.recon_solve_1d_batch(lib.ctx(), C.byref(cb)))
+    out["c2_1m_chains"] = {"ms": ms, "chains_per_s": cnt / ms * 1e3}
+    del occ, src, dst, i64, i32
+    W = H = 64
+    cnt = 4096
+    occ = torch.from_numpy(sample_grids(0x64000000, cnt, W, H, 2662).view(np.int64)).to(dev)
+    S, mst = W * 40, W * H * 12
+    src = torch.empty(cnt * S, dtype=torch.int32, device=dev)
+    dst = torch.empty_like(src)
+    td = torch.empty(cnt, dtype=torch.int64, device=dev)
+    i32 = torch.empty(4 * cnt, dtype=torch.int32, device=dev)
+    mb = torch.empty(cnt * mst, dtype=torch.int32, device=dev)
+    g = GridBatch(occ.data_ptr(), cnt, W, H, 40, src.data_ptr(), dst.data_ptr(), None, i32.data_ptr(), td.data_ptr(),
+                  i32.data_ptr() + 4 * cnt, i32.data_ptr() + 8 * cnt, None)
+    pb = PipelineBatch(g, 1, 0, mst, mb.data_ptr(), i32.data_ptr() + 12 * cnt)
+    ms = run(lambda: lib.lib.recon_pipeline_batch_run(lib.ctx(), C.byref(pb)))
+    out["c3_bird_batching_4096"] = {"ms": ms, "grids_per_s": cnt / ms * 1e3}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -166,6 +217,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--ref-sample", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C2 / C3 side measurements")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -321,6 +373,12 @@ def main():
                 ts.append(e0.elapsed_time(e1) * 1000.0)
         lat[f"h{hp}_seed{seed}_us"] = statistics.median(ts)
 
+    # the other BASELINE configs at their own sizes (device-resident inputs,
+    # CUDA events on the context stream; informative, the headline is above)
+    others = None
+    if rank == 0 and ws == 1 and not args.no_configs:
+        others = other_configs(lib, torch, dev, stream)
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         v, cores, _ = cpu_reference(occ_h, args.ref_sample)
@@ -359,6 +417,7 @@ def main():
                     "d2h_bytes_per_step": d2h},
             "bird": {"grids_per_s": ws * B / (bird_ms * 1e-3), "ms_per_step": bird_ms},
             "latency_single_grid": lat,
+            "other_configs": others,
             "clocks": clocks,
         }
         if cpu:
