@@ -36,15 +36,15 @@ recon_status validate_grid(int W, int H, int hp, int32_t *detail) {
     return RECON_OK;
 }
 
-// Warps per CTA.  Batches: more, smaller CTAs (4 warps) keep more instances
-// in flight per SM, which wins on small grids (red-rec up to 128^2, bird up
-// to 256^2, measured r01); larger grids keep 8.  A red-rec batch with no more
-// instances than SMs runs one CTA per SM anyway, so it takes up to 32 warps
-// to shorten phase 1/3 and the waves (bird: 16, its window chunks in flight).
-// RECON_GRID_WARPS overrides.
+// Warps per CTA.  Batches: more, smaller CTAs keep more instances in flight
+// per SM and wait less at the wave / window barriers: 2 warps up to 128^2,
+// 4 up to 256^2, 8 beyond (both solvers, measured r01 with the per-solver
+// shared-memory layouts).  A batch with no more instances than SMs runs one
+// CTA per SM anyway, so it takes up to 32 warps (bird: 16) to shorten the
+// instance's own critical path.  RECON_GRID_WARPS overrides.
 bool shape_for(Ctx *c, int solver, int W, int H, int hp, int count, GridShape &s) {
     const long long cells = (long long)W * H;
-    int w = cells <= (solver == 0 ? 128 * 128 : 256 * 256) ? 4 : kWarps;
+    int w = cells <= 128 * 128 ? 2 : (cells <= 256 * 256 ? 4 : kWarps);
     if (count <= c->sms) w = solver == 0 ? 32 : 16;  // latency: more warps on the instance
     if (const char *e = getenv("RECON_GRID_WARPS")) w = std::max(1, std::min(32, atoi(e)));
     const int floor_w = std::min(kWarps, w);

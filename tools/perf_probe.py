@@ -163,6 +163,8 @@ CASES = {
     "r256_redrec_b2368": lambda: grid("redrec", 256, 256, 153, 39322, 0x25600000, 2368),
     "r256_redrec_b8192": lambda: grid("redrec", 256, 256, 153, 39322, 0x25600000, 8192),
     "r256_bird_b8192": lambda: grid("bird", 256, 256, 153, 39322, 0x25600000, 8192),
+    "r128_bird_b4096": lambda: grid("bird", 128, 128, 77, 9830, 0x12800000, 4096),
+    "r128_redrec_b4096": lambda: grid("redrec", 128, 128, 77, 9830, 0x12800000, 4096),
     "c3_bird_solve": lambda: grid("bird", 64, 64, 40, 2662, 0x64000000, 4096),
     "c3_redrec_solve": lambda: grid("redrec", 64, 64, 40, 2662, 0x64000000, 4096),
     "r128_redrec_b4096": lambda: grid("redrec", 128, 128, 76, 9830, 0x12800000, 4096),
