@@ -179,6 +179,7 @@ CASES = {
     "c4_pipeline_redrec_64_validate": lambda: pipeline("redrec", 256, 256, 153, 39322, 257, 64, 0, 1_500_000, True),
     "c4_pipeline_redrec_64": lambda: pipeline("redrec", 256, 256, 153, 39322, 257, 64, 0, 1_500_000),
     "c5_bird_solve_64": lambda: grid("bird", 512, 512, 307, 157286, 0x51200000, 64),
+    "c5_bird_solve_512": lambda: grid("bird", 512, 512, 307, 157286, 0x51200000, 512),
     "c5_bird_solve_1": lambda: grid("bird", 512, 512, 307, 157286, 0x51200000, 1),
     "c2_chains_1m": lambda: chains(1024, 563, 256, 767, 0x1D000000, 1 << 20),
 }
