@@ -510,7 +510,8 @@ __global__ void __launch_bounds__(LAT ? 1024 : 256, LAT ? 1 : 3) bird_kernel(Gri
     ps.lvl_b = b.lvl_b;
     ps.bal = b.bal;
     ps.scal = b.scal;
-    for (int inst = blockIdx.x; inst < p.count; inst += gridDim.x) {
+    __shared__ int s_next;
+    for (int inst = blockIdx.x; inst < p.count; inst = next_instance(p, inst, &s_next)) {
         const size_t pbase = (size_t)inst * g.W * g.k;
         PathOut o{p.path_src + pbase, p.path_dst + pbase, p.path_event ? p.path_event + pbase : nullptr};
         if (threadIdx.x == 0) {

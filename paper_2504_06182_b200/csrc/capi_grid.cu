@@ -60,6 +60,14 @@ int grid_blocks(Ctx *c, int solver, const GridShape &s, int count) {
 
 // launches with the per-CTA staging scratch and the plans the red-rec kernels need
 cudaError_t launch(Ctx *c, int solver, GridParams &p, int grid) {
+    // dynamic instance scheduling when CTAs take more than one instance
+    p.work = nullptr;
+    if (p.count > grid) {
+        p.work = c->dev<int>(S_WORK, 1);
+        if (!p.work) return cudaErrorMemoryAllocation;
+        cudaError_t e = cudaMemsetAsync(p.work, 0, sizeof(int), c->stream);
+        if (e != cudaSuccess) return e;
+    }
     if (solver == 0) {
         p.stage = c->dev<uint32_t>(S_STAGE, (size_t)grid * grid_stage_ints(p.shape));
         if (!p.stage) return cudaErrorMemoryAllocation;

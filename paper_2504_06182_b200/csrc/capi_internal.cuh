@@ -23,7 +23,7 @@ enum Slot {
     S_SRCOF, S_TGTOF, S_DCNT, S_DOFF, S_KEYS, S_KEYS2, S_TEMP, S_EA, S_EB,
     S_CHAIN_A, S_CHAIN_B, S_CHAIN_C, S_CHAIN_D, S_CHAIN_E,
     S_BM_OFF, S_BM_VERT, S_BM_ES, S_BM_ED, S_BM_OUT, S_BM_AUX0, S_BM_AUX1, S_BM_AUX2, S_BM_AUX3,
-    S_BM_AUX4, S_BM_AUX5, S_BM_AUX6, S_BM_AUX7, S_STAGE, S_PLAN,
+    S_BM_AUX4, S_BM_AUX5, S_BM_AUX6, S_BM_AUX7, S_STAGE, S_WORK, S_PLAN,
     S_V_VERDICT, S_V_STATE, S_V_SRCOF, S_V_DSTOF, S_V_FIN, S_V_LEN, S_V_MB, S_V_EV, S_V_EV2, S_V_BCNT,
     S_V_BMIN, S_V_BMAX, S_V_ECNT, S_V_ALIVE, S_V_PRED, S_V_TOK, S_V_BEGAN,
     S_W_LEN, S_W_OUT, S_W_MOFF, S_W_VOFF, S_W_MB, S_W_K0, S_W_K1, S_W_I0, S_W_I1,

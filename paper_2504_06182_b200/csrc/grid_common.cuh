@@ -280,6 +280,17 @@ __device__ __forceinline__ void load_instance(const Geo &g, const uint64_t *occ,
     if (lane_id() == 0 && tot) atomicAdd((unsigned long long *)total_tokens, (unsigned long long)tot);
 }
 
+// next instance of a persistent CTA: the static stride, or (p.work) the next
+// unclaimed instance of a global counter -- instance costs vary, and a static
+// split leaves the last round's CTAs idle behind the slowest ones
+__device__ __forceinline__ int next_instance(const GridParams &p, int inst, int *s_next) {
+    if (!p.work) return inst + gridDim.x;
+    __syncthreads();
+    if (threadIdx.x == 0) *s_next = gridDim.x + atomicAdd(p.work, 1);
+    __syncthreads();
+    return *s_next;
+}
+
 // exclusive scan of vals[idx[i]] for i in [0, n) into out[idx[i]] (warp 0); returns the total
 __device__ __forceinline__ int scan_indexed(const int *vals, const int16_t *idx, int n, int *out, int base) {
     int run = base;

@@ -45,6 +45,7 @@ struct GridParams {
     uint32_t *stage;         // red-rec: per-CTA packed path staging, W*k words per CTA (grid-sized)
     RedrecPlans plans;       // red-rec: [count] plans
     long long *phase_clock;  // optional: clock64 at phase boundaries of instance 0 (profiling)
+    int *work;               // optional: zeroed instance counter (dynamic instance scheduling)
 };
 
 bool grid_shape(int W, int H, int k, int nwarps, int solver, GridShape &s);

@@ -569,7 +569,8 @@ __global__ void __launch_bounds__(MINB == 1 ? 1024 : 256, MINB) redrec_kernel(Gr
     __shared__ long long s_tokens;
     __shared__ unsigned long long s_disp;
     __shared__ int s_status, s_detail, s_n1, s_n2, s_nlev, s_total, s_fail;
-    for (int inst = blockIdx.x; inst < p.count; inst += gridDim.x) {
+    __shared__ int s_next;
+    for (int inst = blockIdx.x; inst < p.count; inst = next_instance(p, inst, &s_next)) {
         if (threadIdx.x == 0) {
             s_tokens = 0;
             s_disp = 0;
