@@ -106,6 +106,7 @@ def chains(n, k, tl, th, seed, count):
     b = ChainBatch(occ.data_ptr(), count, n, tl, th, src.data_ptr(), dst.data_ptr(), td.data_ptr(), ds.data_ptr(),
                    st.data_ptr(), de.data_ptr())
     mn, avg = timeit(lambda: lib.lib.recon_solve_1d_batch(lib.ctx(), C.byref(b)))
+    assert int((st != 0).sum()) == 0, "chain batch failed"
     bytes_ = count * (n // 8 + 8 * nt + 32)
     return {"ms": mn, "chains_per_s": count / mn * 1e3, "GBps_alg": bytes_ / mn / 1e6,
             "frac_hbm": bytes_ / mn / 1e6 / 6465.8}
