@@ -29,7 +29,7 @@ def main():
     W, H, hp, k, seed = [int(x, 0) for x in sys.argv[1:6]] if len(sys.argv) > 5 else (256, 256, 153, 39322, 257)
     lib = ReconLib(LIB_PATH, "b200")
     occ = sample_grids(seed, 1, W, H, k)
-    ms = W * H * 20
+    ms = W * H * 48
     t0 = time.perf_counter()
     pipe = lib.pipeline_batch("redrec", occ, 1, W, H, hp, 0, ms)
     t_pipe = time.perf_counter() - t0
@@ -42,6 +42,7 @@ def main():
         mb, nb = lib.batch_moves(W, H, occ, paths, edges, 0)
         t_exp = time.perf_counter() - t0
     D = int(pipe["total_displacement"][0])
+    assert int(pipe["status"][0]) == 0, ("pipeline status", int(pipe["status"][0]))
     same = nb == int(pipe["batch_count"][0]) and np.array_equal(mb, pipe["move_batch"][:D])
     print({"W": W, "H": H, "paths": P, "moves": D, "edges": len(edges), "batches": nb,
            "explicit_batch_moves_s": round(t_exp, 4), "pipeline_s (solve+dag+batch, host)": round(t_pipe, 4),
