@@ -553,20 +553,23 @@ __global__ void __launch_bounds__(LAT ? 1024 : 256, LAT ? 1 : 3) bird_kernel(Gri
             __syncthreads();
             own_emit_range(g, b, 0, n1, 0, o, 0, true, &s_disp);
             __syncthreads();
-            // row pass: pooled events, strictly sequential
+            // row pass: pooled events, strictly sequential.  An event's path
+            // count is CTA-uniform (read from shared state after its last
+            // barrier), so every thread keeps the running offset itself.
+            int off = s_off;
             for (int e = n1; e < g.W; ++e) {
                 const int c = b.ev_col[e];
                 long long *dbg = (p.phase_clock && inst == 0) ? p.phase_clock + 8 + 8 * (e - n1) : nullptr;
-                const int cnt = pooled_event(g, b.dep, b.sigma, c, b.lists, ps, o, s_off, e, &s_disp, dbg);
+                const int cnt = pooled_event(g, b.dep, b.sigma, c, b.lists, ps, o, off, e, &s_disp, dbg);
                 if (cnt < 0) {
                     if (threadIdx.x == 0) s_fail = 1;
                     __syncthreads();
                     break;
                 }
-                __syncthreads();
-                if (threadIdx.x == 0) s_off += cnt;
-                __syncthreads();
+                off += cnt;
             }
+            __syncthreads();
+            if (threadIdx.x == 0) s_off = off;
             if (s_fail && threadIdx.x == 0) {
                 s_status = RECON_ERR_INFEASIBLE;
                 s_detail = RECON_D_GEN_NO_ASSIGNMENT;
