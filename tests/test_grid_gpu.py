@@ -128,7 +128,7 @@ def test_error_statuses(gpu, solver):
 
 @pytest.mark.parametrize("solver", SOLVERS)
 def test_c4_batch_of_256_matches_reference(gpu, ref, solver):
-    """More instances than SMs: the 8-warp batch CTAs (and, for red-rec, the
+    """More instances than SMs: the 4-warp batch CTAs (and, for red-rec, the
     planner kernel + executor on many instances at once), against the compiled
     reference on every instance."""
     W = H = 256
@@ -139,6 +139,24 @@ def test_c4_batch_of_256_matches_reference(gpu, ref, solver):
     for key in ("path_count", "total_displacement", "status"):
         assert np.array_equal(g[key], r[key]), key
     S = W * 153
+    for i in range(n):
+        P = int(r["path_count"][i])
+        for key in ("path_src", "path_dst"):
+            assert np.array_equal(g[key][i * S:i * S + P], r[key][i * S:i * S + P]), (key, i)
+
+
+@pytest.mark.parametrize("solver", SOLVERS)
+def test_more_instances_than_ctas_matches_reference(gpu, ref, solver):
+    """More instances than resident CTAs (2-warp CTAs at 128^2): CTAs claim
+    further instances from the global counter (dynamic scheduling)."""
+    W = H = 128
+    n = 3000
+    occ = sample_grids(0x12800000, n, W, H, 9830)
+    g = gpu.grid_solve_batch(solver, occ, n, W, H, 77)
+    r = ref.grid_solve_batch(solver, occ, n, W, H, 77)
+    for key in ("path_count", "total_displacement", "status"):
+        assert np.array_equal(g[key], r[key]), key
+    S = W * 77
     for i in range(n):
         P = int(r["path_count"][i])
         for key in ("path_src", "path_dst"):
