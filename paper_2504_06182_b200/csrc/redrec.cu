@@ -704,15 +704,15 @@ __global__ void __launch_bounds__(MINB == 1 ? 1024 : 256, MINB) redrec_kernel(Gr
                     const int n = b.ev_count[e], off = b.ev_off[e];
                     const int dbase = b.ev_col[e] * g.H + g.H - 1;
                     const uint32_t *st = stage + (size_t)e * ks;
-                    for (int i0 = 0; i0 < n; i0 += 128) {  // 4 loads in flight per lane
-                        uint32_t v[4];
+                    for (int i0 = 0; i0 < n; i0 += 256) {  // 8 loads in flight per lane
+                        uint32_t v[8];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
+                        for (int u = 0; u < 8; ++u) {
                             const int i = i0 + 32 * u + lane;
                             v[u] = i < n ? __ldlu(st + i) : 0u;  // last use
                         }
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
+                        for (int u = 0; u < 8; ++u) {
                             const int i = i0 + 32 * u + lane;
                             if (i < n) {
                                 // streaming stores: the output must not evict the staging from L2
