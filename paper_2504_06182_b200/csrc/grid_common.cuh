@@ -186,6 +186,7 @@ __device__ __forceinline__ long long own_emit(const Geo &g, int col, const OwnSo
                                               int off, int evid) {
     const int16_t *otop = L, *obot = L + g.LK, *res = L + 3 * g.LK;
     long long disp = 0;
+#pragma unroll 2
     for (int j = lane_id(); j < g.k; j += 32) {
         const bool right = j < s.n_right, left = j >= g.k - s.n_left;
         if (!right && !left) continue;
