@@ -262,10 +262,15 @@ __device__ long long emit_window(const Geo &g, uint64_t *dep, int *sigma, int c,
         if (cleared) {
             uint64_t *m = dep + (size_t)col * g.wpd;
             const int start = top ? V0 + dist : V0 - dist;
-            // top and bottom windows run concurrently and may share a word / a column
-            for (uint64_t x = cleared; x; x &= x - 1) {
-                const int dpt = start + __ffsll((long long)x) - 1;
-                atomicAnd((unsigned long long *)&m[dpt >> 6], ~(1ull << (dpt & 63)));
+            // top and bottom windows run concurrently and may share a word / a
+            // column: the window's bits (depths start + i, all >= 0) cover at
+            // most two plane words, one atomic AND each
+            if (start >= 0) {
+                const int w0 = start >> 6, sh = start & 63;
+                atomicAnd((unsigned long long *)&m[w0], ~(cleared << sh));
+                if (sh && (cleared >> (64 - sh))) atomicAnd((unsigned long long *)&m[w0 + 1], ~(cleared >> (64 - sh)));
+            } else {
+                atomicAnd((unsigned long long *)&m[0], ~(cleared >> (-start)));
             }
             if (col != c) atomicSub(&sigma[col], __popcll(cleared));
         }
