@@ -34,8 +34,8 @@ struct BatchJob {
     BatchScratch s;
     int32_t *move_batch;  // path-major, one per elementary move
     // move log (pipeline): {path-major slot, batch} of the accepted moves in
-    // batch order; pipeline_scatter_moves turns it into move_batch.  Null:
-    // move_batch is written directly.
+    // batch order; the warp scatters it into move_batch when its instance
+    // finishes.  Null: move_batch is written directly.
     int2 *mlog;
     int32_t *nlog;
     int32_t *batch_count, *status, *detail;
