@@ -500,7 +500,7 @@ __device__ int pooled_event(const Geo &g, uint64_t *dep, int *sigma, int c, int1
 
 // LAT: a lone instance gets up to 32 warps (more chunks of a window in flight)
 template <bool LAT>
-__global__ void __launch_bounds__(LAT ? 1024 : 256, LAT ? 1 : 3) bird_kernel(GridParams p) {
+__global__ void __launch_bounds__(LAT ? 512 : 256, LAT ? 1 : 3) bird_kernel(GridParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geo g = make_geo(p.shape);
     Block b = carve(p.shape, smem);

@@ -47,6 +47,7 @@ bool shape_for(Ctx *c, int solver, int W, int H, int hp, int count, GridShape &s
     int w = cells <= 128 * 128 ? 2 : (cells <= 256 * 256 ? 4 : kWarps);
     if (count <= c->sms) w = solver == 0 ? 32 : 16;  // latency: more warps on the instance
     if (const char *e = getenv("RECON_GRID_WARPS")) w = std::max(1, std::min(32, atoi(e)));
+    if (solver == 1) w = std::min(w, 16);  // bird_kernel<true>: at most 512 threads
     const int floor_w = std::min(kWarps, w);
     for (; w >= floor_w; w /= 2)
         if (grid_shape(W, H, hp, w, solver, s)) return true;
