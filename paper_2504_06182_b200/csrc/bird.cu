@@ -498,9 +498,11 @@ __device__ int pooled_event(const Geo &g, uint64_t *dep, int *sigma, int c, int1
     return n_right + n_left;
 }
 
-// LAT: a lone instance gets up to 32 warps (more chunks of a window in flight)
-template <bool LAT>
-__global__ void __launch_bounds__(LAT ? 512 : 256, LAT ? 1 : 3) bird_kernel(GridParams p) {
+// MODE 1 (lone instance): up to 16 warps (more chunks of a window in flight),
+// up to 128 registers.  Batches: MODE 0 (up to 85 registers; the compiler
+// keeps 64, best on small grids) or MODE 2 (up to 128; better from 128^2).
+template <int MODE>
+__global__ void __launch_bounds__(MODE == 1 ? 512 : 256, MODE == 0 ? 3 : (MODE == 1 ? 1 : 2)) bird_kernel(GridParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geo g = make_geo(p.shape);
     Block b = carve(p.shape, smem);
@@ -594,7 +596,8 @@ __global__ void __launch_bounds__(LAT ? 512 : 256, LAT ? 1 : 3) bird_kernel(Grid
     }
 }
 
-template __global__ void bird_kernel<false>(GridParams);
-template __global__ void bird_kernel<true>(GridParams);
+template __global__ void bird_kernel<0>(GridParams);
+template __global__ void bird_kernel<1>(GridParams);
+template __global__ void bird_kernel<2>(GridParams);
 
 }  // namespace rb

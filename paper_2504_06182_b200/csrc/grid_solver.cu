@@ -26,9 +26,12 @@ static void (*redrec_exec(const GridShape &s))(GridParams) {
 }
 __global__ void redrec_plan_kernel(GridParams p);
 int64_t redrec_plan_smem(int W);
-template <bool LAT>
+template <int MODE>
 __global__ void bird_kernel(GridParams p);
-static void (*bird_exec(const GridShape &s))(GridParams) { return s.nwarps > 8 ? bird_kernel<true> : bird_kernel<false>; }
+static void (*bird_exec(const GridShape &s))(GridParams) {
+    if (s.nwarps > 8) return bird_kernel<1>;
+    return (long long)s.W * s.H >= 128 * 128 ? bird_kernel<2> : bird_kernel<0>;
+}
 
 // Launch-attribute caches: a lone small instance's latency is a few kernel
 // durations, so per-call cudaFuncSetAttribute / occupancy / attribute queries
