@@ -1192,7 +1192,7 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, c
 // 8 = the in-batch bitmap stays in global memory (only the candidate scan of
 // the general path touches it), halving a large grid's shared memory
 template <int MODE>
-__global__ void __launch_bounds__(256, 4) batch_pipeline_kernel(PipelineArgs a) {
+__global__ void __launch_bounds__(256, (MODE & 2) ? 4 : 1) batch_pipeline_kernel(PipelineArgs a) {
     constexpr bool occ_in_smem = MODE & 1, LOG = MODE & 2, BSM = MODE & 4, INB_SM = occ_in_smem && !(MODE & 8);
     extern __shared__ __align__(16) uint32_t bsmem[];
     const int64_t S = (int64_t)a.W * a.k, nwb = ((int64_t)a.W * a.H + 31) / 32;
