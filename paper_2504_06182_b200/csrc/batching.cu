@@ -1059,15 +1059,35 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, c
         // ---- general: candidate scan over the records (ascending id)
         int nacc = 0;
         int32_t f_from = -1, f_to = -1;  // first accepted move of the batch
+        // large grids (no move log): records one chunk ahead (a chunk only
+        // rewrites its own records); small grids keep their registers
+        constexpr bool PREFETCH = !LOG;
+        int4 nrec = make_int4(0, 0, 0, 0);
+        int nrb = 0;
+        if (PREFETCH && lane < nready) {
+            nrec = R.rec[lane];
+            nrb = R.rb[lane];
+        }
         for (int c0 = 0; c0 < nready; c0 += 32) {
             const int idx = c0 + lane;
             const bool valid = idx < nready;
+            int4 crec = nrec;
+            int crb = nrb;
+            if (PREFETCH) {
+                if (idx + 32 < nready) {
+                    nrec = R.rec[idx + 32];
+                    nrb = R.rb[idx + 32];
+                }
+            } else if (valid) {
+                crec = R.rec[idx];
+                crb = R.rb[idx];
+            }
             LanePath l;
             l.p = -1;
             int32_t fr = -1, to = -1;
             bool cand = false;
             if (valid) {
-                l = rec_lane(R.rec[idx], R.rb[idx]);
+                l = rec_lane(crec, crb);
                 fr = l.v(H, l.k);
                 to = l.v(H, l.k + 1);
                 cand = !occ.get(to) && !inb.get(fr) && !inb.get(to);
