@@ -37,18 +37,19 @@ recon_status validate_grid(int W, int H, int hp, int32_t *detail) {
 }
 
 // Warps per CTA.  Batches: more, smaller CTAs keep more instances in flight
-// per SM and wait less at the wave / window barriers: 2 warps up to 128^2,
-// 4 up to 256^2, 8 beyond (both solvers, measured r01 with the per-solver
-// shared-memory layouts).  A batch with no more instances than SMs runs one
+// per SM and wait less at the wave / window barriers: 2 warps up to 128^2
+// (red-rec: 1 up to 64^2; bird needs 2 for its top / bottom halves), 4 up to
+// 256^2, 8 beyond (measured r01 with the per-solver shared-memory layouts).  A batch with no more instances than SMs runs one
 // CTA per SM anyway, so it takes up to 32 warps (bird: 16) to shorten the
 // instance's own critical path.  RECON_GRID_WARPS overrides.
 bool shape_for(Ctx *c, int solver, int W, int H, int hp, int count, GridShape &s) {
     const long long cells = (long long)W * H;
     int w = cells <= 128 * 128 ? 2 : (cells <= 256 * 256 ? 4 : kWarps);
+    if (solver == 0 && cells <= 64 * 64) w = 1;  // red-rec: one warp per tiny instance
     if (count <= c->sms) w = solver == 0 ? 32 : 16;  // latency: more warps on the instance
     if (const char *e = getenv("RECON_GRID_WARPS")) w = std::max(1, std::min(32, atoi(e)));
-    if (solver == 1) w = std::min(w, 16);  // bird_kernel<true>: at most 512 threads
-    const int floor_w = std::min(kWarps, w);
+    if (solver == 1) w = std::max(2, std::min(w, 16));  // bird: 2..16 warps (top/bottom halves, 512 threads)
+    const int floor_w = std::min(kWarps, w);  // (shape retries halve w down to this)
     for (; w >= floor_w; w /= 2)
         if (grid_shape(W, H, hp, w, solver, s)) return true;
     return grid_shape(W, H, hp, kWarps, solver, s);

@@ -152,6 +152,7 @@ CASES = {
     "c4_json": lambda: json_case("redrec", 256, 256, 153, 39322, 257, 0, 1_500_000),
     "c5_json": lambda: json_case("bird", 512, 512, 307, 157286, 0x51200000, 0, 12_000_000),
     "c1_redrec": lambda: grid("redrec", 32, 32, 16, 614, 1, 4096),
+    "c1_bird": lambda: grid("bird", 32, 32, 16, 614, 1, 4096),
     "c1_redrec_1": lambda: grid("redrec", 32, 32, 16, 614, 1, 1),
     "c4_redrec_h128_1": lambda: grid("redrec", 256, 256, 128, 39322, 256, 1),
     "c4_redrec_h153_1": lambda: grid("redrec", 256, 256, 153, 39322, 257, 1),
