@@ -877,9 +877,52 @@ __device__ __forceinline__ void sort_newly(int32_t *newly, int32_t *mem, int n) 
 }
 
 // ready = (kept records rec2[0, nkeep)) U (records of newly[0, nnew)), by rank
+// (kr: scratch of >= 32 ints.)  With <= 32 newly released paths, their ids
+// stay in registers: a kept record's rank among them is a shuffle binary
+// search, and the kept ranks place each newly released record, so neither
+// side searches global memory.
 __device__ __forceinline__ void merge_ready(const ImplicitPaths &paths, const PipeRecords &R, const int32_t *newly,
-                                            int nkeep, int nnew) {
+                                            int nkeep, int nnew, int32_t *kr) {
     const int lane = lane_id();
+    if (nnew <= 32) {
+        const int ny = lane < nnew ? newly[lane] : INT_MAX;  // ascending, INT_MAX padded
+        if (lane < nnew) kr[lane] = nkeep;  // #kept below newly j (default: all)
+        __syncwarp();
+        const int ny31 = __shfl_sync(FULL, ny, 31);
+        int prev_r = 0;
+        for (int i0 = 0; i0 < nkeep; i0 += 32) {
+            const int i = i0 + lane;
+            int4 x = make_int4(INT_MAX, 0, 0, 0);
+            int xb = 0;
+            if (i < nkeep) {
+                x = R.rec2[i];
+                xb = R.rb2[i];
+            }
+            int r = 0;  // #newly < x.x
+#pragma unroll
+            for (int st = 16; st; st >>= 1)
+                if (__shfl_sync(FULL, ny, r + st - 1) < x.x) r += st;
+            if (r == 31 && ny31 < x.x) r = 32;
+            int rp = __shfl_up_sync(FULL, r, 1);
+            if (lane == 0) rp = prev_r;
+            if (i < nkeep) {
+                R.rec[i + r] = x;
+                R.rb[i + r] = xb;
+                for (int j = rp; j < r; ++j) kr[j] = i;  // newly j sits right before kept i
+            }
+            prev_r = __shfl_sync(FULL, r, 31);
+        }
+        __syncwarp();
+        if (lane < nnew) {
+            int b;
+            const int4 rr = make_rec(paths, ny, &b);
+            const int at = lane + kr[lane];
+            R.rec[at] = rr;
+            R.rb[at] = b;
+        }
+        __syncwarp();
+        return;
+    }
     for (int i = lane; i < nkeep; i += 32) {
         const int4 x = R.rec2[i];
         const int at = i + lower_bound_i32(newly, nnew, x.x);
@@ -1010,7 +1053,7 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, c
                     }
                     __syncwarp();
                     sort_newly(s.newly, s.mem, nnew);
-                    merge_ready(paths, R, s.newly, nlive, nnew);
+                    merge_ready(paths, R, s.newly, nlive, nnew, s.mfr);
                     nready = nlive + nnew;
                     regmode = false;
                 } else if (nnew > 0) {
@@ -1184,7 +1227,7 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, c
             }
             __syncwarp();
             sort_newly(s.newly, s.mem, nnew);
-            merge_ready(paths, R, s.newly, nkeep, nnew);
+            merge_ready(paths, R, s.newly, nkeep, nnew, s.mfr);
             nready = nkeep + nnew;
         }
         ++nb;
