@@ -941,7 +941,7 @@ __device__ __forceinline__ void merge_ready(const ImplicitPaths &paths, const Pi
 }
 
 template <bool SM, bool SMI, bool LOG, bool BSM>
-__device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, const PipeRecords R) {
+__device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, PipeRecords R) {
     const int lane = lane_id();
     const int P = J.P, H = J.H;
     BatchScratch s = J.s;
@@ -1205,7 +1205,64 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, c
         left -= nacc;
         nlog += nacc;
         __syncwarp();
-        if (nfin > 0 || nnew > 0) {
+        if ((nfin > 0 || nnew > 0) && nnew <= 32) {
+            // ready' = (ready - finished) U newly in one pass into the other
+            // record buffer (then the buffers swap): a kept record goes to its
+            // kept index + its rank among the newly released ids (registers,
+            // shuffle search); kept ranks place the newly released records
+            sort_newly(s.newly, s.mem, nnew);
+            int32_t *kr = s.mfr;  // free after the application step
+            const int ny = lane < nnew ? s.newly[lane] : INT_MAX;
+            if (lane < nnew) kr[lane] = -1;  // -> all kept below: set after the pass
+            __syncwarp();
+            const int ny31 = __shfl_sync(FULL, ny, 31);
+            int nkeep = 0, prev_r = 0;
+            for (int c0 = 0; c0 < nready; c0 += 32) {
+                const int idx = c0 + lane;
+                int4 x = make_int4(-1, 0, 0, 0);
+                int b = 0;
+                if (idx < nready) {
+                    x = R.rec[idx];
+                    b = R.rb[idx];
+                }
+                const bool keep = x.x >= 0;
+                const unsigned m = __ballot_sync(FULL, keep);
+                const int key = keep ? x.x : INT_MAX;
+                int r = 0;  // #newly < key
+#pragma unroll
+                for (int st = 16; st; st >>= 1)
+                    if (__shfl_sync(FULL, ny, r + st - 1) < key) r += st;
+                if (r == 31 && ny31 < key) r = 32;
+                const int ki = nkeep + __popc(m & lanemask_lt());
+                // rank of the previous kept element (this chunk's, else the last one's)
+                const unsigned before = m & lanemask_lt();
+                const int rsh = __shfl_sync(FULL, r, before ? 31 - __clz(before) : lane);
+                const int rp = before ? rsh : prev_r;
+                if (keep) {
+                    R.rec2[ki + r] = x;
+                    R.rb2[ki + r] = b;
+                    for (int j = rp; j < r; ++j) kr[j] = ki;  // newly j sits right before kept ki
+                }
+                if (m) prev_r = __shfl_sync(FULL, r, 31 - __clz(m));
+                nkeep += __popc(m);
+            }
+            __syncwarp();
+            if (lane < nnew) {
+                int bb;
+                const int4 rr = make_rec(paths, ny, &bb);
+                const int k = kr[lane] < 0 ? nkeep : kr[lane];
+                R.rec2[lane + k] = rr;
+                R.rb2[lane + k] = bb;
+            }
+            __syncwarp();
+            int4 *tr = R.rec;
+            R.rec = R.rec2;
+            R.rec2 = tr;
+            int32_t *tb = R.rb;
+            R.rb = R.rb2;
+            R.rb2 = tb;
+            nready = nkeep + nnew;
+        } else if (nfin > 0 || nnew > 0) {
             // ready' = (ready - finished) U newly, by rank
             int nkeep = 0;
             for (int c0 = 0; c0 < nready; c0 += 32) {
