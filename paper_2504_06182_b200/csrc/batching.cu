@@ -1174,23 +1174,20 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
             status = RECON_ERR_INPUT;  // batching.cpp:127-128
             break;
         }
-        // ---- atomic application
-        for (int i = lane; i < nacc; i += 32) {
-            occ.clr(s.mfr[i]);
-            inb.clr(s.mfr[i]);
-            inb.clr(s.mto[i]);
-        }
-        __syncwarp();
-        for (int i = lane; i < nacc; i += 32) occ.set(s.mto[i]);
-        __syncwarp();
-        // ---- release (newly -> next batch)
+        // ---- atomic application and release (newly -> next batch), one pass:
+        // the accepted moves' sources are occupied and their destinations
+        // empty, so the sets are disjoint and each update is independent
         int nnew = 0, nfin = 0;
         for (int i0 = 0; i0 < nacc; i0 += 32) {
             const int i = i0 + lane;
             bool fin = false;
             int64_t q0 = 0, q1 = 0;
             if (i < nacc) {
-                const int m = s.mem[i];
+                const int m = s.mem[i], fr = s.mfr[i], to = s.mto[i];
+                occ.clr(fr);
+                occ.set(to);
+                inb.clr(fr);
+                inb.clr(to);
                 fin = m < 0;
                 if (fin) {
                     const int p = m & 0x7fffffff;
