@@ -210,6 +210,18 @@ recon_status recon_bird_solve_batch(recon_ctx *ctx, const recon_grid_batch *batc
 recon_status recon_redrec_solve_batch_host(recon_ctx *ctx, const recon_grid_batch *batch);
 recon_status recon_bird_solve_batch_host(recon_ctx *ctx, const recon_grid_batch *batch);
 
+/* Same as *_batch_host, but the path list comes back packed: one uint32 per
+ * path slot, src | dst << 16, in path_packed[count * width * h_prime] (slot
+ * layout as path_src).  Grids of at most 65,536 cells (RECON_ERR_ARGUMENT
+ * otherwise); batch->path_src / path_dst are not used and may be NULL.  The
+ * device-to-host copy of the path lists bounds the host call (8 bytes per
+ * path over the host link), and this halves it.  Same paths, same order:
+ * the reference-side shim widens them back into Path (redrec.hpp:67). */
+recon_status recon_redrec_solve_batch_host_packed(recon_ctx *ctx, const recon_grid_batch *batch,
+                                                  uint32_t *path_packed);
+recon_status recon_bird_solve_batch_host_packed(recon_ctx *ctx, const recon_grid_batch *batch,
+                                                uint32_t *path_packed);
+
 /* occupancy_dag over explicit vertex lists (paths of any shape, CSR
  * off[P+1] into verts); edges sorted by (src, dst), deduplicated. */
 recon_status recon_occupancy_dag_paths(recon_ctx *ctx, int32_t width, int32_t height, int32_t path_count,

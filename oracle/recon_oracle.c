@@ -741,6 +741,35 @@ recon_status recon_bird_solve_batch_host(recon_ctx *c, const recon_grid_batch *b
     return grid_batch(1, b);
 }
 
+/* *_batch_host_packed (include/recon_b200.h): the same solve, paths packed as
+ * src | dst << 16 (grids of at most 65,536 cells). */
+static recon_status grid_batch_packed(int pooled, const recon_grid_batch *b, uint32_t *packed) {
+    if (!packed || !b) return RECON_ERR_ARGUMENT;
+    if ((int64_t)b->width * b->height > 65536) return RECON_ERR_ARGUMENT;
+    const size_t n = (size_t)(b->count > 0 ? b->count : 0) * (size_t)b->width * (size_t)b->h_prime;
+    recon_grid_batch t = *b;
+    t.path_src = (int32_t *)malloc((n ? n : 1) * sizeof(int32_t));
+    t.path_dst = (int32_t *)malloc((n ? n : 1) * sizeof(int32_t));
+    recon_status st = RECON_ERR_ARGUMENT;
+    if (t.path_src && t.path_dst) {
+        memset(t.path_src, 0, (n ? n : 1) * sizeof(int32_t));
+        memset(t.path_dst, 0, (n ? n : 1) * sizeof(int32_t));
+        st = grid_batch(pooled, &t);
+        for (size_t i = 0; i < n; ++i) packed[i] = (uint32_t)t.path_src[i] | (uint32_t)t.path_dst[i] << 16;
+    }
+    free(t.path_src);
+    free(t.path_dst);
+    return st;
+}
+recon_status recon_redrec_solve_batch_host_packed(recon_ctx *c, const recon_grid_batch *b, uint32_t *packed) {
+    (void)c;
+    return grid_batch_packed(0, b, packed);
+}
+recon_status recon_bird_solve_batch_host_packed(recon_ctx *c, const recon_grid_batch *b, uint32_t *packed) {
+    (void)c;
+    return grid_batch_packed(1, b, packed);
+}
+
 /* ======================================================================== */
 /* Exact 1D (exact1d.cpp)                                                    */
 /* ======================================================================== */

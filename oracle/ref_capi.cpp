@@ -355,6 +355,24 @@ recon_status recon_bird_solve_batch(recon_ctx *, const recon_grid_batch *b) { re
 recon_status recon_redrec_solve_batch_host(recon_ctx *, const recon_grid_batch *b) { return grid_batch(b, false); }
 recon_status recon_bird_solve_batch_host(recon_ctx *, const recon_grid_batch *b) { return grid_batch(b, true); }
 
+static recon_status grid_batch_packed(const recon_grid_batch *b, bool pooled, uint32_t *packed) {
+    if (!packed || !b || static_cast<int64_t>(b->width) * b->height > 65536) return RECON_ERR_ARGUMENT;
+    const size_t n = static_cast<size_t>(std::max(b->count, 0)) * b->width * b->h_prime;
+    std::vector<int32_t> src(n), dst(n);
+    recon_grid_batch t = *b;
+    t.path_src = src.data();
+    t.path_dst = dst.data();
+    const recon_status st = grid_batch(&t, pooled);
+    for (size_t i = 0; i < n; ++i) packed[i] = static_cast<uint32_t>(src[i]) | static_cast<uint32_t>(dst[i]) << 16;
+    return st;
+}
+recon_status recon_redrec_solve_batch_host_packed(recon_ctx *, const recon_grid_batch *b, uint32_t *packed) {
+    return grid_batch_packed(b, false, packed);
+}
+recon_status recon_bird_solve_batch_host_packed(recon_ctx *, const recon_grid_batch *b, uint32_t *packed) {
+    return grid_batch_packed(b, true, packed);
+}
+
 recon_status recon_assign_1d(recon_ctx *, int32_t n, const int32_t *S, int32_t ns, const int32_t *T,
                              int32_t nt, int64_t *weight, int64_t *pair_src, int64_t *pair_dst,
                              int32_t *use_count, int32_t *detail) {

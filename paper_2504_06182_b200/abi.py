@@ -201,6 +201,7 @@ EXPORTED_SYMBOLS = [
     "recon_redrec_solve", "recon_bird_solve", "recon_occupancy_dag",
     "recon_redrec_solve_batch", "recon_bird_solve_batch",
     "recon_redrec_solve_batch_host", "recon_bird_solve_batch_host",
+    "recon_redrec_solve_batch_host_packed", "recon_bird_solve_batch_host_packed",
     "recon_assign_1d", "recon_assign_1d_generalized", "recon_solve_1d",
     "recon_solve_1d_batch", "recon_solve_1d_batch_host",
     "recon_batch_moves", "recon_pipeline_batch_run", "recon_pipeline_batch_run_host",
@@ -276,6 +277,10 @@ class ReconLib:
                    "recon_redrec_solve_batch_host", "recon_bird_solve_batch_host"):
             f = getattr(L, fn)
             f.argtypes = [C.c_void_p, C.POINTER(GridBatch)]
+            f.restype = C.c_int
+        for fn in ("recon_redrec_solve_batch_host_packed", "recon_bird_solve_batch_host_packed"):
+            f = getattr(L, fn)
+            f.argtypes = [C.c_void_p, C.POINTER(GridBatch), C.c_void_p]
             f.restype = C.c_int
         L.recon_assign_1d.argtypes = [C.c_void_p, C.c_int32, I32P, C.c_int32, I32P, C.c_int32,
                                       I64P, I64P, I64P, I32P, I32P]
@@ -433,6 +438,27 @@ class ReconLib:
         else:
             fn = self.lib.recon_bird_solve_batch_host if host else self.lib.recon_bird_solve_batch
         st = fn(self.ctx(), C.byref(b))
+        self._check(st, 0)
+        return out
+
+    def grid_solve_batch_packed(self, solver: str, occ: np.ndarray, count: int, width: int, height: int,
+                                h_prime: int):
+        """Batched solve through *_batch_host_packed: path_packed[i] = src | dst << 16."""
+        stride = width * h_prime
+        out = {
+            "path_packed": np.zeros(count * stride, np.uint32),
+            "path_count": np.zeros(count, np.int32),
+            "total_displacement": np.zeros(count, np.int64),
+            "status": np.zeros(count, np.int32),
+            "detail": np.zeros(count, np.int32),
+        }
+        occ = np.ascontiguousarray(occ, np.uint64)
+        b = GridBatch(_vp(occ).value, count, width, height, h_prime, None, None, None,
+                      _vp(out["path_count"]).value, _vp(out["total_displacement"]).value,
+                      _vp(out["status"]).value, _vp(out["detail"]).value, None)
+        fn = (self.lib.recon_redrec_solve_batch_host_packed if solver == "redrec"
+              else self.lib.recon_bird_solve_batch_host_packed)
+        st = fn(self.ctx(), C.byref(b), _vp(out["path_packed"]).value)
         self._check(st, 0)
         return out
 

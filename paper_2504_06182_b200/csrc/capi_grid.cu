@@ -189,13 +189,38 @@ recon_status grid_single(int solver, recon_ctx *ctx, const uint64_t *occ, int W,
     return RECON_OK;
 }
 
-recon_status grid_batch(int solver, recon_ctx *ctx, const recon_grid_batch *b, bool host) {
+// Packed path list for the host copy: one u32 per path slot, src | dst << 16
+// (grids of at most 65,536 cells).  Streaming loads/stores; the 8-byte
+// {src, dst} slots are read once and 4 bytes go back over the host link.
+__global__ void __launch_bounds__(256) pack_paths_kernel(const int32_t *__restrict__ src,
+                                                         const int32_t *__restrict__ dst,
+                                                         uint32_t *__restrict__ out, size_t n) {
+    const size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x, step = (size_t)gridDim.x * blockDim.x;
+    const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) |
+                       reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    size_t done = 0;
+    if (vec) {
+        const size_t n4 = n / 4;
+        const int4 *s4 = reinterpret_cast<const int4 *>(src), *d4 = reinterpret_cast<const int4 *>(dst);
+        uint4 *o4 = reinterpret_cast<uint4 *>(out);
+        for (size_t i = t0; i < n4; i += step) {
+            const int4 a = __ldcs(s4 + i), b = __ldcs(d4 + i);
+            __stcs(o4 + i, make_uint4((uint32_t)a.x | (uint32_t)b.x << 16, (uint32_t)a.y | (uint32_t)b.y << 16,
+                                      (uint32_t)a.z | (uint32_t)b.z << 16, (uint32_t)a.w | (uint32_t)b.w << 16));
+        }
+        done = n4 * 4;
+    }
+    for (size_t i = done + t0; i < n; i += step) out[i] = (uint32_t)src[i] | (uint32_t)dst[i] << 16;
+}
+
+recon_status grid_batch(int solver, recon_ctx *ctx, const recon_grid_batch *b, bool host, uint32_t *packed = nullptr) {
     int32_t *detail = nullptr;
-    if (!b || !b->occ || !b->path_src || !b->path_dst || !b->path_count || !b->total_displacement || !b->status)
-        return RECON_ERR_ARGUMENT;
+    if (!b || !b->occ || !b->path_count || !b->total_displacement || !b->status) return RECON_ERR_ARGUMENT;
+    if (!packed && (!b->path_src || !b->path_dst)) return RECON_ERR_ARGUMENT;
     int32_t dummy = 0;
     recon_status st = validate_grid(b->width, b->height, b->h_prime, &dummy);
     if (st != RECON_OK) return st;
+    if (packed && (int64_t)b->width * b->height > 65536) return RECON_ERR_ARGUMENT;
     if (b->count <= 0) return RECON_OK;
     Ctx *c = resolve(ctx);
     if (!c) return RECON_ERR_CUDA;
@@ -230,19 +255,25 @@ recon_status grid_batch(int solver, recon_ctx *ctx, const recon_grid_batch *b, b
     p.status = c->dev<int32_t>(S_STATUS, n);
     p.detail = c->dev<int32_t>(S_DETAIL, n);
     p.events = b->events ? c->dev<int32_t>(S_EVENTS, n * b->width * per) : nullptr;
-    if (!d_occ || !p.path_src || !p.path_dst || (b->path_event && !p.path_event) || !p.path_count ||
+    uint32_t *d_pack = packed ? c->dev<uint32_t>(S_PPACK, n * stride) : nullptr;
+    if (!d_occ || !p.path_src || !p.path_dst || (packed && !d_pack) || (b->path_event && !p.path_event) || !p.path_count ||
         !p.total_displacement || !p.status || !p.detail || (b->events && !p.events))
         return cuda_fail(cudaErrorMemoryAllocation, "grid batch workspace", detail);
-    CK(cudaMemcpyAsync(d_occ, b->occ, n * words * 8, cudaMemcpyHostToDevice, c->stream), "occ H2D");
-    // Chunks of one wave of CTAs: chunk k's results go back on the copy stream
-    // while chunk k + 1 solves (the device-to-host copy of the path lists
-    // dominates, so it overlaps the solve instead of following it).
+    // Chunks: chunk k's results go back on the copy stream while chunk k + 1
+    // solves (the device-to-host copy of the path lists dominates, so it
+    // overlaps the solve instead of following it).  Chunk sizes start at one
+    // instance per SM and double up to a wave of CTAs, so the copy engine
+    // starts after a short first solve; each chunk's inputs go up just
+    // before its launch (the other direction of the link).
     if (!c->copy_stream) CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "copy stream");
     const size_t wave = (size_t)grid_blocks(c, solver, s, b->count);
-    const size_t chunk = std::max<size_t>(wave, (n + 7) / 8);
+    const size_t chunk_max = std::max<size_t>(wave, (n + 7) / 8);
+    size_t chunk = std::min<size_t>(std::max(c->sms, 1), chunk_max);
     cudaStream_t cs = c->copy_stream;
-    for (size_t i0 = 0; i0 < n; i0 += chunk) {
-        const size_t m = std::min(chunk, n - i0);
+    for (size_t i0 = 0, m = 0; i0 < n; i0 += m, chunk = std::min(chunk * 2, chunk_max)) {
+        m = std::min(chunk, n - i0);
+        CK(cudaMemcpyAsync(d_occ + i0 * words, b->occ + i0 * words, m * words * 8, cudaMemcpyHostToDevice, c->stream),
+           "occ H2D");
         GridParams q = p;
         q.count = (int)m;
         q.occ = d_occ + i0 * words;
@@ -255,12 +286,22 @@ recon_status grid_batch(int solver, recon_ctx *ctx, const recon_grid_batch *b, b
         q.detail = p.detail + i0;
         q.events = p.events ? p.events + i0 * b->width * per : nullptr;
         CK(launch(c, solver, q, grid_blocks(c, solver, s, (int)m)), "grid kernel launch");
+        if (packed) {
+            pack_paths_kernel<<<c->sms * 8, 256, 0, c->stream>>>(q.path_src, q.path_dst, d_pack + i0 * stride, m * stride);
+            ++c->launches;
+            CK(cudaGetLastError(), "pack kernel launch");
+        }
         cudaEvent_t ev = c->chunk_event();
         if (!ev) return cuda_fail(cudaErrorMemoryAllocation, "chunk event", detail);
         CK(cudaEventRecord(ev, c->stream), "event");
         CK(cudaStreamWaitEvent(cs, ev, 0), "wait");
-        CK(cudaMemcpyAsync(b->path_src + i0 * stride, q.path_src, m * stride * 4, cudaMemcpyDeviceToHost, cs), "D2H");
-        CK(cudaMemcpyAsync(b->path_dst + i0 * stride, q.path_dst, m * stride * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        if (packed) {
+            CK(cudaMemcpyAsync(packed + i0 * stride, d_pack + i0 * stride, m * stride * 4, cudaMemcpyDeviceToHost, cs),
+               "D2H");
+        } else {
+            CK(cudaMemcpyAsync(b->path_src + i0 * stride, q.path_src, m * stride * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+            CK(cudaMemcpyAsync(b->path_dst + i0 * stride, q.path_dst, m * stride * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        }
         if (b->path_event)
             CK(cudaMemcpyAsync(b->path_event + i0 * stride, q.path_event, m * stride * 4, cudaMemcpyDeviceToHost, cs),
                "D2H");
@@ -296,6 +337,14 @@ recon_status recon_redrec_solve_batch(recon_ctx *ctx, const recon_grid_batch *b)
 recon_status recon_bird_solve_batch(recon_ctx *ctx, const recon_grid_batch *b) { return grid_batch(1, ctx, b, false); }
 recon_status recon_redrec_solve_batch_host(recon_ctx *ctx, const recon_grid_batch *b) { return grid_batch(0, ctx, b, true); }
 recon_status recon_bird_solve_batch_host(recon_ctx *ctx, const recon_grid_batch *b) { return grid_batch(1, ctx, b, true); }
+recon_status recon_redrec_solve_batch_host_packed(recon_ctx *ctx, const recon_grid_batch *b, uint32_t *path_packed) {
+    if (!path_packed) return RECON_ERR_ARGUMENT;
+    return grid_batch(0, ctx, b, true, path_packed);
+}
+recon_status recon_bird_solve_batch_host_packed(recon_ctx *ctx, const recon_grid_batch *b, uint32_t *path_packed) {
+    if (!path_packed) return RECON_ERR_ARGUMENT;
+    return grid_batch(1, ctx, b, true, path_packed);
+}
 
 recon_status recon_occupancy_dag(recon_ctx *ctx, int32_t width, int32_t height, const int32_t *path_src,
                                  const int32_t *path_dst, int64_t path_count, int32_t *dag_src, int32_t *dag_dst,

@@ -164,6 +164,30 @@ def test_more_instances_than_ctas_matches_reference(gpu, ref, solver):
 
 
 @pytest.mark.parametrize("solver", SOLVERS)
+@pytest.mark.parametrize("W,hp,n,k,seed", [(256, 153, 160, 39322, 0x25600000), (128, 77, 3000, 9830, 0x12800000)])
+def test_packed_host_api_matches_reference(gpu, ref, solver, W, hp, n, k, seed):
+    """*_batch_host_packed (src | dst << 16 per path, several copy chunks at
+    128^2) against the compiled reference on every instance."""
+    occ = sample_grids(seed, n, W, W, k)
+    g = gpu.grid_solve_batch_packed(solver, occ, n, W, W, hp)
+    r = ref.grid_solve_batch(solver, occ, n, W, W, hp)
+    for key in ("path_count", "total_displacement", "status"):
+        assert np.array_equal(g[key], r[key]), key
+    S = W * hp
+    for i in range(n):
+        P = int(r["path_count"][i])
+        pk = g["path_packed"][i * S:i * S + P]
+        assert np.array_equal((pk & 0xFFFF).astype(np.int32), r["path_src"][i * S:i * S + P]), ("src", i)
+        assert np.array_equal((pk >> 16).astype(np.int32), r["path_dst"][i * S:i * S + P]), ("dst", i)
+
+
+def test_packed_host_api_rejects_large_grids(gpu):
+    occ = sample_grids(1, 1, 512, 512, 157286)
+    with pytest.raises(Exception):
+        gpu.grid_solve_batch_packed("redrec", occ, 1, 512, 512, 307)
+
+
+@pytest.mark.parametrize("solver", SOLVERS)
 def test_c5_512_matches_reference(gpu, ref, solver):
     occ = sample_grids(0x51200000, 1, 512, 512, 157286)
     g = gpu.grid_solve(solver, occ, 512, 512, 307, with_dag=True)
