@@ -156,7 +156,28 @@ cudaError_t launch_grid_solver(int solver, const GridParams &p, int grid, cudaSt
     e = ensure_smem((const void *)kern, p.shape.smem_bytes);
     if (e != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[1], stream);
-    kern<<<grid, threads, p.shape.smem_bytes, stream>>>(p);
+    if (solver == 0 && !ev && p.count <= grid) {
+        // programmatic dependent launch: executor CTAs start as planner CTAs
+        // trigger, load and transpose their first instance, and wait for the
+        // plans (griddepcontrol.wait) only before reading them.  Only when
+        // every CTA takes one instance (latency: C4 h'128 67 -> 62 us); on
+        // large batches the executor CTAs cannot co-reside with the planner
+        // and the step was not faster.
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = p.shape.smem_bytes;
+        cfg.stream = stream;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, kern, p);
+        if (e != cudaSuccess) return e;
+    } else {
+        kern<<<grid, threads, p.shape.smem_bytes, stream>>>(p);
+    }
     if (ev) cudaEventRecord(ev[2], stream);
     return cudaGetLastError();
 }

@@ -507,6 +507,9 @@ __global__ void __launch_bounds__(128) redrec_plan_kernel(GridParams p) {
     PlanView v = carve_plan(smem + (size_t)warp * plan_warp_bytes(g.W), g.W);
     const RedrecPlans pg = p.plans;
     const uint64_t last_mask = (g.H & 63) ? ((1ull << (g.H & 63)) - 1ull) : ~0ull;
+    // the executor (launched as a programmatic dependent) may start loading
+    // its instances now; it waits for this grid before reading the plans
+    asm volatile("griddepcontrol.launch_dependents;");
     for (int inst = blockIdx.x * wpb + warp; inst < p.count; inst += gridDim.x * wpb) {
         const uint64_t *occ = p.occ + (size_t)inst * g.W * g.wpd;
         long long tot = 0;
@@ -587,7 +590,10 @@ __global__ void __launch_bounds__(MINB == 1 ? 1024 : 256, MINB) redrec_kernel(Gr
         }
         __syncthreads();
         if (p.phase_clock && inst == 0 && threadIdx.x == 0) p.phase_clock[0] = clock64();
-        // the instance's plan (redrec_plan_kernel) -> shared memory
+        // the instance's plan (redrec_plan_kernel) -> shared memory; under
+        // programmatic dependent launch, wait for the planner grid first
+        // (returns at once when it has completed, or without the attribute)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         {
             const RedrecPlans pg = p.plans;
             const int *meta = pg.meta + (size_t)inst * 8;
