@@ -372,6 +372,21 @@ def main():
         pk = packed_pin[c0:c0 + n0]
         assert torch.equal(pk & 0xFFFF, pin["src"][c0:c0 + n0]) and torch.equal((pk >> 16) & 0xFFFF, pin["dst"][c0:c0 + n0])
     e2e_p_s = statistics.median(e2e_p)
+    # the host link's own device-to-host rate into pinned memory (the bound of
+    # the e2e call): one copy of the packed path lists' size, CUDA events
+    link = []
+    dsrc = bufs["src"].view(torch.int32)
+    for i in range(4):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            packed_pin.copy_(dsrc, non_blocking=True)
+            e1.record(stream)
+        e1.synchronize()
+        if i:
+            link.append(packed_pin.numel() * 4 / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    link_gbs = statistics.median(link)
     if ws > 1:
         t = torch.tensor([e2e_s, e2e_p_s], device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -441,7 +456,9 @@ def main():
                          "planner_kernel_ms": plan_ms, "issue": issue},
             "e2e": {"value": ws * B / e2e_p_s, "unit": "grids/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h_p, "call": "recon_redrec_solve_batch_host_packed (pinned host buffers)",
-                    "path_format": "u32 src | dst << 16 per path"},
+                    "path_format": "u32 src | dst << 16 per path",
+                    "link_d2h_gbs": link_gbs, "achieved_d2h_gbs": d2h_p / e2e_p_s / 1e9,
+                    "link_frac": d2h_p / e2e_p_s / 1e9 / link_gbs},
             "e2e_unpacked": {"value": ws * B / e2e_s, "unit": "grids/s", "h2d_bytes_per_step": h2d,
                              "d2h_bytes_per_step": d2h, "call": "recon_redrec_solve_batch_host (pinned host buffers)",
                              "path_format": "i32 path_src[] + i32 path_dst[]"},
