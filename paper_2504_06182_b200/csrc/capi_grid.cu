@@ -276,6 +276,13 @@ recon_status grid_batch(int solver, recon_ctx *ctx, const recon_grid_batch *b, b
            "occ H2D");
         GridParams q = p;
         q.count = (int)m;
+        // the first chunk (one instance per SM) takes the lone-instance shape
+        // (more warps per instance, shorter critical path): the copy engine
+        // starts sooner; later chunks overlap copies and keep the batch shape
+        GridShape sq = s;
+        if (i0 == 0 && m <= (size_t)c->sms && m < n && !shape_for(c, solver, b->width, b->height, b->h_prime, (int)m, sq))
+            sq = s;
+        q.shape = sq;
         q.occ = d_occ + i0 * words;
         q.path_src = p.path_src + i0 * stride;
         q.path_dst = p.path_dst + i0 * stride;
@@ -285,7 +292,7 @@ recon_status grid_batch(int solver, recon_ctx *ctx, const recon_grid_batch *b, b
         q.status = p.status + i0;
         q.detail = p.detail + i0;
         q.events = p.events ? p.events + i0 * b->width * per : nullptr;
-        CK(launch(c, solver, q, grid_blocks(c, solver, s, (int)m)), "grid kernel launch");
+        CK(launch(c, solver, q, grid_blocks(c, solver, sq, (int)m)), "grid kernel launch");
         if (packed) {
             pack_paths_kernel<<<c->sms * 8, 256, 0, c->stream>>>(q.path_src, q.path_dst, d_pack + i0 * stride, m * stride);
             ++c->launches;
