@@ -73,3 +73,25 @@ def test_pipeline_random(oracle, ref, preset):
                 d = int(r["total_displacement"][0])
                 assert o["batch_count"][0] == r["batch_count"][0]
                 assert np.array_equal(o["move_batch"][:d], r["move_batch"][:d])
+
+
+@pytest.mark.parametrize("solver", ["redrec", "bird"])
+def test_packed_batch_format(oracle, ref, solver):
+    """*_batch_host_packed (src | dst << 16 per path) in both CPU libraries
+    against the unpacked batch call; grids over 65,536 cells are refused."""
+    from paper_2504_06182_b200.inputs import sample_grids
+    W, H, hp, n = 24, 20, 10, 12
+    occ = sample_grids(0x9ac, n, W, H, 300)
+    r = ref.grid_solve_batch(solver, occ, n, W, H, hp)
+    for lib in (oracle, ref):
+        p = lib.grid_solve_batch_packed(solver, occ, n, W, H, hp)
+        for key in ("path_count", "total_displacement", "status"):
+            assert np.array_equal(p[key], r[key]), key
+        S = W * hp
+        for i in range(n):
+            c = int(r["path_count"][i])
+            pk = p["path_packed"][i * S:i * S + c]
+            assert np.array_equal((pk & 0xFFFF).astype(np.int32), r["path_src"][i * S:i * S + c])
+            assert np.array_equal((pk >> 16).astype(np.int32), r["path_dst"][i * S:i * S + c])
+        with pytest.raises(Exception):
+            lib.grid_solve_batch_packed(solver, sample_grids(1, 1, 300, 300, 50000), 1, 300, 300, 100)
