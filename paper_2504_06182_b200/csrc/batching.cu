@@ -64,6 +64,7 @@ struct ImplicitPaths {
 struct LanePath {
     int p, k, len, xs, ys, xt, yt;
     int64_t base;
+    int64_t q0, q1;  // successor CSR range, prefetched when the lane is filled (leap mode)
     __device__ __forceinline__ int32_t v(int H, int kk) const {
         const int dx = abs(xt - xs);
         if (kk <= dx) return (xs + (xt > xs ? kk : -kk)) * H + ys;
@@ -476,65 +477,90 @@ __device__ __forceinline__ bool on_path2(int H, int32_t s, int32_t t, int32_t v)
     return false;
 }
 
-__global__ void pl_mark_kernel(PipelineArgs a) {
+// ---- large instances: one WARP per path, lanes over the route's vertices.
+// The source/target owners of every vertex sit in one int2 map, column-major
+// (x*H + y, read along vertical segments) and row-major (y*W + x, read along
+// horizontal segments), so a route is read with contiguous 256-byte warp
+// loads instead of one scattered load per vertex and thread.  Path i's
+// out-list is [rule-2 edges (i, pb), written by i itself | rule-1 edges
+// (i, j), appended by the paths j that cross source(i)], so only rule-1 edges
+// need a fill counter (virtual_line.cpp:241-268 edge rules; order inside a
+// list is irrelevant to batching).
+
+__global__ void pl_mark2_kernel(PipelineArgs a, int32_t *mc, int32_t *mr) {
     const int64_t S = (int64_t)a.W * a.k, WH = (int64_t)a.W * a.H;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)a.count * S;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t inst = t / S;
         const int p = (int)(t % S);
         if (a.solve_status[inst] != 0 || p >= a.path_count[inst]) continue;
-        a.source_of[inst * WH + a.path_src[t]] = p;
-        a.target_of[inst * WH + a.path_dst[t]] = p;
+        const int s = a.path_src[t], d = a.path_dst[t];
+        const int xs = s / a.H, ys = s - xs * a.H, xd = d / a.H, yd = d - xd * a.H;
+        int32_t *c = mc + inst * WH * 2, *r = mr + inst * WH * 2;
+        c[2 * (int64_t)s] = p;
+        c[2 * (int64_t)d + 1] = p;
+        r[2 * ((int64_t)ys * a.W + xs)] = p;
+        r[2 * ((int64_t)yd * a.W + xd) + 1] = p;
     }
 }
 
-// pass 0: degrees + path lengths; pass 1: successor fill (virtual_line.cpp:241-268 edge rules)
 template <int PASS>
-__global__ void pl_walk_kernel(PipelineArgs a) {
-    const int64_t S = (int64_t)a.W * a.k, WH = (int64_t)a.W * a.H;
-    const int H = a.H;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)a.count * S;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t inst = t / S;
-        const int i = (int)(t % S);
+__global__ void __launch_bounds__(256) pl_walk_warp_kernel(PipelineArgs a, const int2 *mc, const int2 *mr) {
+    const int lane = lane_id();
+    const int W = a.W, H = a.H;
+    const int64_t S = (int64_t)W * a.k, WH = (int64_t)W * H, N = (int64_t)a.count * S;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp_id(); t < N; t += nwarps) {
+        const int64_t inst = t / S, o = inst * S;
+        const int i = (int)(t - o);
         if (a.solve_status[inst] != 0 || i >= a.path_count[inst]) {
-            if (PASS == 0) a.mbase[t] = 0;
+            if (PASS == 0 && lane == 0) {
+                a.mbase[t] = 0;
+                a.mfr[t] = 0;
+            }
             continue;
         }
-        const int32_t *src = a.path_src + inst * S, *dst = a.path_dst + inst * S;
-        const int32_t *so = a.source_of + inst * WH, *to = a.target_of + inst * WH;
-        const int32_t s = src[i], tt = dst[i];
-        const int xs = s / H, ys = s % H, xt = tt / H, yt = tt % H;
-        if (PASS == 0) a.mbase[t] = abs(xt - xs) + abs(yt - ys);
-        const int dx = xt > xs ? 1 : -1, dy = yt > ys ? 1 : -1;
-        int x = xs, y = ys;
-        for (;;) {
-            const int32_t v = x * H + y;
-            const int32_t pa = so[v];
-            if (pa >= 0 && pa != i) {  // (pa, i)
-                if (PASS == 0) {
-                    atomicAdd(&a.outdeg[inst * S + pa], 1);
-                    atomicAdd(&a.indeg[t], 1);
-                } else {
-                    const int slot = atomicAdd(&a.fill[inst * S + pa], 1);
-                    a.succ[a.soff[inst * S + pa] + slot] = i;
-                }
+        const int32_t *src = a.path_src + o, *dst = a.path_dst + o;
+        const int s = src[i], d = dst[i];
+        const int xs = s / H, ys = s - xs * H, xt = d / H, yt = d - xt * H;
+        const int dx = abs(xt - xs), len = dx + abs(yt - ys), sx = xt > xs ? 1 : -1, sy = yt > ys ? 1 : -1;
+        const int2 *mci = mc + inst * WH, *mri = mr + inst * WH;
+        int in1 = 0, out2 = 0;
+        const int64_t my_off = PASS == 1 ? a.soff[t] : 0;
+        for (int j0 = 0; j0 <= len; j0 += 32) {
+            const int j = j0 + lane;
+            int2 m = make_int2(-1, -1);
+            if (j <= len) m = j <= dx ? mri[(int64_t)ys * W + xs + sx * j] : mci[(int64_t)xt * H + ys + sy * (j - dx)];
+            const bool r1 = m.x >= 0 && m.x != i;  // (m.x, i): i crosses source(m.x)
+            bool r2 = m.y >= 0 && m.y != i;        // (i, m.y): i crosses target(m.y) ...
+            if (r2) r2 = !on_path2(H, src[m.y], dst[m.y], s);  // ... unless rule 1 already gives it
+            if (PASS == 0) {
+                if (r1) atomicAdd(&a.outdeg[o + m.x], 1);
+                if (r2) atomicAdd(&a.indeg[o + m.y], 1);
+                in1 += r1;
+                out2 += r2;
+            } else {
+                if (r1) a.succ[a.soff[o + m.x] + a.mfr[o + m.x] + atomicAdd(&a.fill[o + m.x], 1)] = i;
+                const unsigned b2 = __ballot_sync(FULL, r2);
+                if (r2) a.succ[my_off + out2 + __popc(b2 & lanemask_lt())] = m.y;
+                out2 += __popc(b2);
             }
-            const int32_t pb = to[v];
-            if (pb >= 0 && pb != i && !on_path2(H, src[pb], dst[pb], s)) {  // (i, pb), not already rule 1
-                if (PASS == 0) {
-                    atomicAdd(&a.outdeg[t], 1);
-                    atomicAdd(&a.indeg[inst * S + pb], 1);
-                } else {
-                    const int slot = atomicAdd(&a.fill[t], 1);
-                    a.succ[a.soff[t] + slot] = pb;
-                }
+        }
+        if (PASS == 0) {
+            in1 = warp_sum(in1);
+            out2 = warp_sum(out2);
+            if (lane == 0) {
+                if (in1) atomicAdd(&a.indeg[t], in1);
+                a.mfr[t] = out2;  // rule-2 out-degree, written only by i
+                a.mbase[t] = len;
             }
-            if (x != xt) x += dx;
-            else if (y != yt) y += dy;
-            else break;
         }
     }
+}
+
+__global__ void sum2_widen_kernel(int64_t n, const int32_t *a, const int32_t *b, int64_t *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int64_t)a[i] + b[i];
 }
 
 // ---- small instances: the occupancy DAG per instance in one CTA, with the
@@ -722,16 +748,17 @@ cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *
         if (e != cudaSuccess) return e;
         return cudaGetLastError();
     }
-    cudaMemsetAsync(a.source_of, 0xff, (size_t)a.count * WH * 4, st);
-    cudaMemsetAsync(a.target_of, 0xff, (size_t)a.count * WH * 4, st);
+    // maps: {source owner, target owner} per vertex, column-major then row-major
+    int32_t *mc = a.source_of, *mr = a.source_of + (size_t)a.count * WH * 2;
+    cudaMemsetAsync(mc, 0xff, (size_t)a.count * WH * 16, st);
     cudaMemsetAsync(a.outdeg, 0, (size_t)N * 4, st);
     cudaMemsetAsync(a.indeg, 0, (size_t)N * 4, st);
     cudaMemsetAsync(a.fill, 0, (size_t)N * 4, st);
     const int blocks = 148 * 8;
-    pl_mark_kernel<<<blocks, 256, 0, st>>>(a);
-    pl_walk_kernel<0><<<blocks, 256, 0, st>>>(a);
-    // soff = exclusive scan of outdeg (global edge index); mbase = exclusive scan of lengths
-    widen32_kernel<<<blocks, 256, 0, st>>>(N, a.outdeg, a.soff);
+    pl_mark2_kernel<<<blocks, 256, 0, st>>>(a, mc, mr);
+    pl_walk_warp_kernel<0><<<blocks, 256, 0, st>>>(a, (const int2 *)mc, (const int2 *)mr);
+    // soff = exclusive scan of the out-degrees (rule 1 + rule 2); mbase = exclusive scan of lengths
+    sum2_widen_kernel<<<blocks, 256, 0, st>>>(N, a.outdeg, a.mfr, a.soff);
     cudaMemsetAsync(a.soff + N, 0, 8, st);
     size_t tb = a.temp_bytes;
     cub::DeviceScan::ExclusiveSum(a.temp, tb, a.soff, a.soff, (int)(N + 1), st);
@@ -940,27 +967,285 @@ __device__ __forceinline__ void merge_ready(const ImplicitPaths &paths, const Pi
     __syncwarp();
 }
 
-template <bool SM, bool SMI, bool LOG, bool BSM>
-__device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, PipeRecords R) {
+// a lane path moved between lanes (q0/q1 only in leap mode)
+__device__ __forceinline__ LanePath shfl_lane(const LanePath &lp, int src, bool with_succ) {
+    LanePath q;
+    q.p = __shfl_sync(FULL, lp.p, src);
+    q.k = __shfl_sync(FULL, lp.k, src);
+    q.len = __shfl_sync(FULL, lp.len, src);
+    q.xs = __shfl_sync(FULL, lp.xs, src);
+    q.ys = __shfl_sync(FULL, lp.ys, src);
+    q.xt = __shfl_sync(FULL, lp.xt, src);
+    q.yt = __shfl_sync(FULL, lp.yt, src);
+    q.base = __shfl_sync(FULL, lp.base, src);
+    if (with_succ) {
+        q.q0 = __shfl_sync(FULL, lp.q0, src);
+        q.q1 = __shfl_sync(FULL, lp.q1, src);
+    } else {
+        q.q0 = q.q1 = 0;
+    }
+    return q;
+}
+
+// release_successors for leap mode: every successor id of the chunk group is
+// loaded first, then every blocker decremented, so a finish costs two
+// dependent round trips instead of two per 32 successors.  Released ids go to
+// the warp's shared buffer (cap entries) when every successor fits, else to
+// the global one; *out = the buffer used.
+template <class BL>
+__device__ __forceinline__ int release_successors_buf(const BatchJob &J, const BL &blockers, int32_t *sm, int cap,
+                                                      int32_t *g, bool fin, int64_t q0, int64_t q1, int32_t **out) {
+    constexpr int G = 8;  // chunks of 32 successors in flight
+    const int lane = lane_id();
+    if (!fin) q0 = q1 = 0;
+    int tot;
+    const int base = warp_excl_scan((int)(q1 - q0), &tot);
+    int32_t *buf = tot <= cap ? sm : g;
+    *out = buf;
+    int nnew = 0;
+    for (int g0 = 0; g0 < tot; g0 += 32 * G) {
+        int sc[G];
+#pragma unroll
+        for (int c = 0; c < G; ++c) {
+            const int t = g0 + c * 32 + lane;
+            int owner = 0;  // largest lane with base <= t
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1) {
+                const int cl = owner + st;
+                if (__shfl_sync(FULL, base, cl) <= t) owner = cl;
+            }
+            const int64_t oq0 = __shfl_sync(FULL, q0, owner);
+            const int ob = __shfl_sync(FULL, base, owner);
+            sc[c] = t < tot ? __ldg(J.succ + oq0 + (t - ob)) : -1;
+        }
+        bool rel[G];
+#pragma unroll
+        for (int c = 0; c < G; ++c) rel[c] = sc[c] >= 0 && blockers.release(sc[c]);
+#pragma unroll
+        for (int c = 0; c < G; ++c) {
+            const unsigned rm = __ballot_sync(FULL, rel[c]);
+            if (rel[c]) buf[nnew + __popc(rm & lanemask_lt())] = sc[c];
+            nnew += __popc(rm);
+        }
+    }
+    return nnew;
+}
+
+// occupancy update without ordering: a token moving a -> b toggles both bits
+// (red.xor commutes, so a vacated and a refilled vertex need no fence)
+template <bool SM>
+__device__ __forceinline__ void occ_toggle(const Bits<SM> &b, int v) {
+    if (SM) asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(b.sa + ((uint32_t)(v >> 5) << 2)), "r"(1u << (v & 31)) : "memory");
+    else asm volatile("red.global.xor.b32 [%0], %1;" ::"l"(b.p + (v >> 5)), "r"(1u << (v & 31)) : "memory");
+}
+
+// phase cycle counters of batch_warp_pipe (experiments: -DRECON_BATCH_PROF)
+__device__ unsigned long long g_batch_prof[16];
+#ifdef RECON_BATCH_PROF
+#define BPROF_T0() long long bp_t0_ = clock64()
+#define BPROF_ADD(i)                  \
+    do {                              \
+        const long long t_ = clock64(); \
+        bprof[i] += t_ - bp_t0_;      \
+        bp_t0_ = t_;                  \
+    } while (0)
+#define BPROF_CNT(i) (bprof[i] += 1)
+#else
+#define BPROF_T0() (void)0
+#define BPROF_ADD(i) (void)0
+#define BPROF_CNT(i) (void)0
+#endif
+
+// ---- leap mode (preset none, register frontier): the batches in which
+// every ready path moves are skipped in one step.
+//
+// Between two "events" — a path's final move, or a ready path that is not
+// accepted — every ready path advances one vertex per batch, so batch
+// nb + t moves every live path's (k + t)-th edge.  An event is found without
+// stepping:
+//  * path p's final move happens at offset f_p = len_p - k_p - 1;
+//  * p is not accepted at offset t iff its destination P(t+1) is occupied
+//    pre-batch, or another ready path q wants the same vertex
+//    (batching.cpp:111-113).  Occupied means a ready path's current vertex,
+//    P(t+1) == Q(t), or a stationary token.  A stationary token can never
+//    lie on a ready path's remaining route under the occupancy dag
+//    (virtual_line.cpp:241-268): an unstarted path's source on p's route is a
+//    dag predecessor of p (so it already left), a finished path's target on
+//    p's route is a dag successor of p (so it has not arrived), and a token
+//    no path moves cannot lie on any route of a collision-free solution.
+// With one-bend routes (horizontal, then vertical; virtual_line.cpp:150-173)
+// P(t) and Q(t) are two linear pieces each, so the first meeting time is a
+// small integer solve per piece pair.  delta = min over live paths of
+// min(f_p + 1, first stall) batches are applied at once; delta == 0 runs the
+// literal batch.  Bit-identical to the literal loop (tests/test_batching_gpu.py).
+struct Seg {
+    int x0, y0, vx, vy, t0, t1;  // position (x0 + vx t, y0 + vy t) for t in [t0, t1]
+};
+
+__device__ __forceinline__ void lane_segs(int k, int len, int xs, int ys, int xt, int yt, Seg &h, Seg &v) {
+    const int dx = abs(xt - xs), sx = xt > xs ? 1 : -1, sy = yt > ys ? 1 : -1;
+    h = Seg{xs + sx * k, ys, sx, 0, 0, dx - k};
+    v = Seg{xt, ys + sy * (k - dx), 0, sy, max(0, dx - k), len - k};
+}
+
+// t / c for c in {+-1, +-2}; false when not an integer
+__device__ __forceinline__ bool div12(int r, int c, int *t) {
+    if (c & 1) {
+        *t = r * c;
+        return true;
+    }
+    if (r & 1) return false;
+    *t = (r >> 1) * (c >> 1);
+    return true;
+}
+
+// min t in [lo, hi] with (ax + avx t, ay + avy t) == (bx + bvx t, by + bvy t)
+__device__ __forceinline__ int meet(int ax, int ay, int avx, int avy, int bx, int by, int bvx, int bvy, int lo,
+                                    int hi) {
+    const int cx = avx - bvx, rx = bx - ax, cy = avy - bvy, ry = by - ay;
+    int t;
+    if (cx == 0) {
+        if (rx != 0) return INT_MAX;
+    } else {
+        if (!div12(rx, cx, &t)) return INT_MAX;
+        lo = max(lo, t);
+        hi = min(hi, t);
+    }
+    if (cy == 0) {
+        if (ry != 0) return INT_MAX;
+    } else {
+        if (!div12(ry, cy, &t)) return INT_MAX;
+        lo = max(lo, t);
+        hi = min(hi, t);
+    }
+    return lo <= hi ? lo : INT_MAX;
+}
+
+// first offset t in [0, T] at which p (pieces a) is blocked by q (pieces b):
+// P(t+1) == Q(t) (q's pre-batch vertex) or P(t+1) == Q(t+1) (same destination)
+__device__ __forceinline__ int pair_event(const Seg *a, const Seg *b, int T) {
+    int best = INT_MAX;
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+            const Seg &A = a[u], &B = b[w];
+            int lo = max(max(A.t0 - 1, B.t0), 0), hi = min(min(A.t1 - 1, B.t1), T);
+            if (lo <= hi) best = min(best, meet(A.x0 + A.vx, A.y0 + A.vy, A.vx, A.vy, B.x0, B.y0, B.vx, B.vy, lo, hi));
+            lo = max(max(A.t0, B.t0), 1);
+            hi = min(min(A.t1, B.t1), T + 1);
+            if (lo <= hi) {
+                const int s = meet(A.x0, A.y0, A.vx, A.vy, B.x0, B.y0, B.vx, B.vy, lo, hi);
+                if (s != INT_MAX) best = min(best, s - 1);
+            }
+        }
+    return best;
+}
+
+// Deadlocked lanes.  A lane whose next vertex holds another lane's token is
+// blocked; the blocked lanes whose blocker is itself blocked, closed under
+// that relation, form cycles (head-on riders, batching.cpp:127-128's
+// no-progress case) plus the lanes queued behind them.  None of them can ever
+// move again, so they are frozen: their tokens act as fixed obstacles and the
+// leap runs over the remaining lanes (the movers).  A lane blocked by a mover
+// only waits one batch: delta = 0 then.
+// Returns delta (0: run the batch literally) and the movers' lane mask.
+__device__ __forceinline__ int leap_delta(const LanePath &lp, int H, int32_t fr, int32_t to, unsigned *movers) {
+    const int lane = lane_id();
+    const bool valid = lp.p != INT_MAX;
+    const unsigned vm = __ballot_sync(FULL, valid);
+    int blocker = -1;
+    for (unsigned m = vm; m; m &= m - 1) {
+        const int q = __ffs(m) - 1;
+        if (__shfl_sync(FULL, fr, q) == to) blocker = q;
+    }
+    bool frozen = valid && blocker >= 0;
+    unsigned fm = __ballot_sync(FULL, frozen);
+    const unsigned blocked = fm;
+    if (fm) {
+        for (;;) {  // greatest set closed under "blocked by a member"
+            frozen = frozen && ((fm >> blocker) & 1u);
+            const unsigned nfm = __ballot_sync(FULL, frozen);
+            if (nfm == fm) break;
+            fm = nfm;
+        }
+        if (blocked != fm) {  // someone waits for a mover: one literal batch
+            *movers = vm & ~fm;
+            return 0;
+        }
+    }
+    const unsigned mv = vm & ~fm;
+    *movers = mv;
+    if (!mv) return 0;  // only frozen lanes: the literal batch reports no progress
+    const bool mover = (mv >> lane) & 1u;
+    int best = mover ? lp.len - lp.k : INT_MAX;  // f + 1
+    Seg mine[2];
+    lane_segs(lp.k, lp.len, lp.xs, lp.ys, lp.xt, lp.yt, mine[0], mine[1]);
+    // remaining route's bounding box: no meeting outside both boxes
+    const int xc = mine[0].t1 >= 0 ? mine[0].x0 : lp.xt;  // column now
+    const int bx0 = min(xc, lp.xt), bx1 = max(xc, lp.xt);
+    const int yc = mine[1].y0 + mine[1].vy * mine[1].t0;  // row at the bend (or now)
+    const int by0 = min(yc, lp.yt), by1 = max(yc, lp.yt);
+    const int pk = lp.k | (lp.len << 16), pxs = lp.xs | (lp.ys << 16), pxt = lp.xt | (lp.yt << 16);
+    const int pb0 = bx0 | (by0 << 16), pb1 = bx1 | (by1 << 16);
+    const unsigned others = __popc(vm) > 1 ? vm : 0u;
+    for (unsigned m = others; m; m &= m - 1) {
+        const int q = __ffs(m) - 1;
+        const int qk = __shfl_sync(FULL, pk, q), qxs = __shfl_sync(FULL, pxs, q), qxt = __shfl_sync(FULL, pxt, q);
+        const int qb0 = __shfl_sync(FULL, pb0, q), qb1 = __shfl_sync(FULL, pb1, q);
+        const int qfr = __shfl_sync(FULL, fr, q);
+        const bool qfrozen = (fm >> q) & 1u;
+        if (!mover || q == lane) continue;
+        if (qfrozen) {
+            // a frozen token is a fixed obstacle: the first t with P(t+1) on it
+            const int qx = qfr / H, qy = qfr - qx * H;
+            if (qx >= bx0 && qx <= bx1 && qy >= by0 && qy <= by1) {
+                const Seg pt[2] = {Seg{qx, qy, 0, 0, 0, INT_MAX / 2}, Seg{qx, qy, 0, 0, 0, INT_MAX / 2}};
+                best = min(best, pair_event(mine, pt, lp.len - lp.k - 1));
+            }
+            continue;
+        }
+        const bool overlap = (qb0 & 0xffff) <= bx1 && (qb1 & 0xffff) >= bx0 && (qb0 >> 16) <= by1 && (qb1 >> 16) >= by0;
+        if (overlap) {
+            const int k = qk & 0xffff, len = qk >> 16;
+            Seg other[2];
+            lane_segs(k, len, qxs & 0xffff, qxs >> 16, qxt & 0xffff, qxt >> 16, other[0], other[1]);
+            best = min(best, pair_event(mine, other, min(lp.len - lp.k - 1, len - k - 1)));
+        }
+    }
+    return __reduce_min_sync(FULL, mover ? best : INT_MAX);
+}
+
+template <bool SM, bool SMI, bool LOG, bool BSM, bool LEAP = false>
+__device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, PipeRecords R, const int64_t *wst) {
     const int lane = lane_id();
     const int P = J.P, H = J.H;
     BatchScratch s = J.s;
     const Bits<SM> occ(s.occ);
     const Bits<SMI> inb(s.inb);
     const Blockers<BSM> blk(s.blockers, s.blk_sm);  // BSM: filled by the caller
-    // ---- init: blockers = in-degree (given); zero-length paths finish at once
+    // the wide phase (batch_wide.cu) ran the first batches: continue from its
+    // ready records, bitmap, blocker counts and counters
+    const bool resumed = wst && wst[0] == 1;
     long long left = 0;
-    for (int p = lane; p < P; p += 32) {
+    int nready = 0;
+    int nb = 0, nlog = 0, status = RECON_OK;
+    if (resumed) {
+        nb = (int)wst[1];
+        left = wst[2];
+        nready = (int)wst[3];
+    }
+    // ---- init: blockers = in-degree (given); zero-length paths finish at once
+    for (int p = lane; p < P && !resumed; p += 32) {
         const int len = paths.len(p);
         left += len;
         if (len == 0)
             for (int64_t q = J.soff[p]; q < J.soff[p + 1]; ++q) blk.release(J.succ[q]);
     }
-    left = warp_sum64(left);
+    if (!resumed) left = warp_sum64(left);
     __syncwarp();
     __threadfence_block();
-    int nready = 0;
-    for (int p0 = 0; p0 < P; p0 += 32) {
+    for (int p0 = 0; p0 < P && !resumed; p0 += 32) {
         const int p = p0 + lane;
         const bool r = p < P && blk.get(p) == 0 && paths.len(p) > 0;
         const unsigned m = __ballot_sync(FULL, r);
@@ -974,7 +1259,10 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
         nready += __popc(m);
     }
     __syncwarp();
-    int nb = 0, nlog = 0, status = RECON_OK;
+#ifdef RECON_BATCH_PROF
+    long long bprof[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const long long bp_start = clock64();
+#endif
     // register-resident frontier (<= 32 ready paths), as in batch_warp
     bool regmode = false;
     LanePath lp;
@@ -989,7 +1277,13 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
     };
     auto enter_regmode = [&]() {
         lp.p = INT_MAX;
-        if (lane < nready) lp = rec_lane(R.rec[lane], R.rb[lane]);
+        if (lane < nready) {
+            lp = rec_lane(R.rec[lane], R.rb[lane]);
+            if (LEAP) {
+                lp.q0 = J.soff[lp.p];
+                lp.q1 = J.soff[lp.p + 1];
+            }
+        }
         lane_move();
         regmode = true;
     };
@@ -1000,46 +1294,101 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
     if (nready <= 32) enter_regmode();
     while (left > 0) {
         if (regmode) {
-            const bool valid = lp.p != INT_MAX;
-            const bool cand = valid && !occ.get(to);
-            const unsigned cm = __ballot_sync(FULL, cand);
-            if (!cm) {
-                status = RECON_ERR_INPUT;  // batching.cpp:127-128
-                break;
-            }
-            bool a;
-            if (J.preset != 0) {
-                const int first = __ffs(cm) - 1;
-                const int32_t ff = __shfl_sync(FULL, fr, first), ft = __shfl_sync(FULL, to, first);
-                a = cand && compatible(J.preset, H, fr, to, ff, ft);
-            } else {
-                const unsigned same = __match_any_sync(FULL, cand ? to : -2 - lane);
-                a = cand && (same & lanemask_lt()) == 0;
-            }
-            const unsigned acc = __ballot_sync(FULL, a);
-            if (a) occ.clr(fr);
-            __syncwarp();
-            if (a) occ.set(to);
             bool fin = false;
             int64_t q0 = 0, q1 = 0;
-            if (a) {
-                put_move(lp.base + lp.k, __popc(acc & lanemask_lt()));
-                ++lp.k;
-                fin = lp.k == lp.len;
-                if (fin) {
-                    q0 = J.soff[lp.p];
-                    q1 = J.soff[lp.p + 1];
+            BPROF_T0();
+            unsigned movers = 0;
+            const int delta = LEAP ? leap_delta(lp, H, fr, to, &movers) : 0;
+            BPROF_ADD(0);
+            if (delta > 0) {
+                BPROF_CNT(5);
+                // batches nb .. nb+delta-1 move every mover one vertex each
+                // (frozen lanes stay put)
+                const bool valid = (movers >> lane) & 1u;
+                const unsigned vm = movers;
+                for (unsigned m = vm; m; m &= m - 1) {
+                    const int o = __ffs(m) - 1;
+                    const int64_t b = __shfl_sync(FULL, lp.base + lp.k, o);
+                    for (int i = lane; i < delta; i += 32) __stcs(J.move_batch + b + i, nb + i);
                 }
-                // next move: horizontal steps first (virtual_line.cpp:150-173)
-                const int dx = abs(lp.xt - lp.xs);
-                fr = to;
-                to += lp.k < dx ? (lp.xt > lp.xs ? H : -H) : (lp.yt > lp.ys ? 1 : -1);
+                if (valid) {
+                    occ_toggle(occ, fr);
+                    lp.k += delta;
+                    fr = lp.v(H, lp.k);
+                    occ_toggle(occ, fr);
+                    fin = lp.k == lp.len;
+                    if (fin) {
+                        q0 = lp.q0;
+                        q1 = lp.q1;
+                    } else {
+                        to = lp.v(H, lp.k + 1);
+                    }
+                }
+                nb += delta;
+                left -= (long long)__popc(vm) * delta;
+                BPROF_ADD(1);
+            } else {
+                BPROF_CNT(6);
+                const bool valid = lp.p != INT_MAX;
+                bool cand;
+                if (LEAP) {
+                    bool held = false;  // a ready path's token sits on my destination
+                    for (unsigned m = __ballot_sync(FULL, valid); m; m &= m - 1)
+                        held |= __shfl_sync(FULL, fr, __ffs(m) - 1) == to;
+                    cand = valid && !held;
+                } else {
+                    cand = valid && !occ.get(to);
+                }
+                const unsigned cm = __ballot_sync(FULL, cand);
+                if (!cm) {
+                    status = RECON_ERR_INPUT;  // batching.cpp:127-128
+                    break;
+                }
+                bool a;
+                if (J.preset != 0) {
+                    const int first = __ffs(cm) - 1;
+                    const int32_t ff = __shfl_sync(FULL, fr, first), ft = __shfl_sync(FULL, to, first);
+                    a = cand && compatible(J.preset, H, fr, to, ff, ft);
+                } else {
+                    const unsigned same = __match_any_sync(FULL, cand ? to : -2 - lane);
+                    a = cand && (same & lanemask_lt()) == 0;
+                }
+                const unsigned acc = __ballot_sync(FULL, a);
+                if (LEAP) {
+                    if (a) {
+                        occ_toggle(occ, fr);
+                        occ_toggle(occ, to);
+                    }
+                } else {
+                    if (a) occ.clr(fr);
+                    __syncwarp();
+                    if (a) occ.set(to);
+                }
+                if (a) {
+                    put_move(lp.base + lp.k, __popc(acc & lanemask_lt()));
+                    ++lp.k;
+                    fin = lp.k == lp.len;
+                    if (fin) {
+                        q0 = LEAP ? lp.q0 : J.soff[lp.p];
+                        q1 = LEAP ? lp.q1 : J.soff[lp.p + 1];
+                    }
+                    // next move: horizontal steps first (virtual_line.cpp:150-173)
+                    const int dx = abs(lp.xt - lp.xs);
+                    fr = to;
+                    to += lp.k < dx ? (lp.xt > lp.xs ? H : -H) : (lp.yt > lp.ys ? 1 : -1);
+                }
+                nlog += __popc(acc);
+                left -= __popc(acc);
+                ++nb;
+                BPROF_ADD(2);
             }
-            nlog += __popc(acc);
-            left -= __popc(acc);
             const unsigned fm = __ballot_sync(FULL, fin);
             if (fm) {
-                const int nnew = release_successors(J, blk, s.newly, 0, fin, q0, q1);
+                BPROF_CNT(8);
+                // leap mode: released ids go to the warp's shared buffer when they fit
+                int32_t *newly = s.newly;
+                const int nnew = LEAP ? release_successors_buf(J, blk, s.newly_sm, NEWLY_SM, s.newly, fin, q0, q1, &newly)
+                                      : release_successors(J, blk, s.newly, 0, fin, q0, q1);
                 if (fin) lp.p = INT_MAX;
                 __syncwarp();
                 const unsigned live = __ballot_sync(FULL, lp.p != INT_MAX);
@@ -1052,53 +1401,45 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
                         R.rb2[at] = (int)lp.base;
                     }
                     __syncwarp();
-                    sort_newly(s.newly, s.mem, nnew);
-                    merge_ready(paths, R, s.newly, nlive, nnew, s.mfr);
+                    sort_newly(newly, s.mem, nnew);
+                    merge_ready(paths, R, newly, nlive, nnew, s.mfr);
                     nready = nlive + nnew;
                     regmode = false;
+                    if (LEAP) __threadfence();  // the general path reads the toggled bitmap
                 } else if (nnew > 0) {
                     // newly released paths take the empty lanes, then sort lanes by id
                     const int erank = __popc(~live & lanemask_lt());
                     if (lp.p == INT_MAX && erank < nnew) {
                         int b;
-                        const int4 r = make_rec(paths, s.newly[erank], &b);
+                        const int np = newly[erank];
+                        const int4 r = make_rec(paths, np, &b);
                         lp = rec_lane(r, b);
+                        if (LEAP) {
+                            lp.q0 = J.soff[np];
+                            lp.q1 = J.soff[np + 1];
+                        }
                     }
                     int key = lp.p == INT_MAX ? INT_MAX : (lp.p << 5) | lane;
                     key = warp_sort32(key);
                     const int src = key == INT_MAX ? lane : (key & 31);
-                    LanePath q;
-                    q.p = __shfl_sync(FULL, lp.p, src);
-                    q.k = __shfl_sync(FULL, lp.k, src);
-                    q.len = __shfl_sync(FULL, lp.len, src);
-                    q.xs = __shfl_sync(FULL, lp.xs, src);
-                    q.ys = __shfl_sync(FULL, lp.ys, src);
-                    q.xt = __shfl_sync(FULL, lp.xt, src);
-                    q.yt = __shfl_sync(FULL, lp.yt, src);
-                    q.base = __shfl_sync(FULL, lp.base, src);
-                    lp = key == INT_MAX ? LanePath{INT_MAX, 0, 0, 0, 0, 0, 0, 0} : q;
+                    LanePath q = shfl_lane(lp, src, LEAP);
+                    if (key == INT_MAX) q.p = INT_MAX;
+                    lp = q;
                 } else {
                     // finished lanes leave gaps: lane L takes the L-th live lane
-                    int src = lane;
-                    for (int st = 0; st < 32; ++st)
-                        if (((live >> st) & 1u) && __popc(live & ((1u << st) - 1u)) == lane) src = st;
-                    LanePath q;
-                    q.p = __shfl_sync(FULL, lp.p, src);
-                    q.k = __shfl_sync(FULL, lp.k, src);
-                    q.len = __shfl_sync(FULL, lp.len, src);
-                    q.xs = __shfl_sync(FULL, lp.xs, src);
-                    q.ys = __shfl_sync(FULL, lp.ys, src);
-                    q.xt = __shfl_sync(FULL, lp.xt, src);
-                    q.yt = __shfl_sync(FULL, lp.yt, src);
-                    q.base = __shfl_sync(FULL, lp.base, src);
-                    lp = lane < nlive ? q : LanePath{INT_MAX, 0, 0, 0, 0, 0, 0, 0};
+                    const int src = lane < nlive ? (int)__fns(live, 0, lane + 1) : lane;
+                    LanePath q = shfl_lane(lp, src, LEAP);
+                    if (lane >= nlive) q.p = INT_MAX;
+                    lp = q;
                 }
                 lane_move();  // lanes were reloaded / reordered
+                BPROF_ADD(3);
             }
             __syncwarp();
-            ++nb;
             continue;
         }
+        BPROF_T0();
+        BPROF_CNT(7);
         // ---- general: candidate scan over the records (ascending id)
         int nacc = 0;
         int32_t f_from = -1, f_to = -1;  // first accepted move of the batch
@@ -1286,7 +1627,13 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
         }
         ++nb;
         if (nready <= 32) enter_regmode();
+        BPROF_ADD(4);
     }
+#ifdef RECON_BATCH_PROF
+    bprof[9] = clock64() - bp_start;
+    if (lane == 0)
+        for (int i = 0; i < 10; ++i) atomicAdd(&g_batch_prof[i], (unsigned long long)bprof[i]);
+#endif
     if (LOG) {
         // the instance's log -> move_batch in one burst: its region is written
         // back to back, so L2 merges the scattered 4-byte stores into sectors
@@ -1307,11 +1654,15 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
 // MODE bits: 1 = occupancy / in-batch bitmaps in shared memory, 2 = move log,
 // 4 = blocker counts in shared memory (u16, after the bitmaps; needs 1),
 // 8 = the in-batch bitmap stays in global memory (only the candidate scan of
-// the general path touches it), halving a large grid's shared memory
+// the general path touches it), halving a large grid's shared memory,
+// 16 = leap mode (preset none; no move log)
 template <int MODE>
 __global__ void __launch_bounds__(256, (MODE & 2) ? 4 : 1) batch_pipeline_kernel(PipelineArgs a) {
     constexpr bool occ_in_smem = MODE & 1, LOG = MODE & 2, BSM = MODE & 4, INB_SM = occ_in_smem && !(MODE & 8);
+    constexpr bool LEAP = MODE & 16;
+    static_assert(!(LEAP && LOG), "leap mode writes move_batch directly");
     extern __shared__ __align__(16) uint32_t bsmem[];
+    __shared__ int32_t newly_buf[LEAP ? 8 : 1][LEAP ? NEWLY_SM : 1];
     const int64_t S = (int64_t)a.W * a.k, nwb = ((int64_t)a.W * a.H + 31) / 32;
     const int nw = blockDim.x >> 5;
     for (int inst = blockIdx.x * nw + warp_id(); inst < a.count; inst += gridDim.x * nw) {
@@ -1322,6 +1673,8 @@ __global__ void __launch_bounds__(256, (MODE & 2) ? 4 : 1) batch_pipeline_kernel
             }
             continue;
         }
+        const int64_t *wst = a.wstate ? a.wstate + (int64_t)inst * 4 : nullptr;
+        if (wst && wst[0] == 2) continue;  // the wide phase finished the instance
         const int64_t o = (int64_t)inst * S;
         const int64_t moves = a.mbase[o + a.path_count[inst]] - a.mbase[o];
         if (moves > a.move_stride || moves >= INT_MAX) {  // (records hold 32-bit move slots)
@@ -1354,6 +1707,7 @@ __global__ void __launch_bounds__(256, (MODE & 2) ? 4 : 1) batch_pipeline_kernel
         }
         J.s.blockers = a.indeg + o;
         J.s.newly = a.newly + o;
+        J.s.newly_sm = LEAP ? newly_buf[warp_id()] : nullptr;
         J.s.mem = a.mem + o;
         J.s.mfr = a.mfr + o;
         J.s.mto = a.mto + o;
@@ -1380,7 +1734,7 @@ __global__ void __launch_bounds__(256, (MODE & 2) ? 4 : 1) batch_pipeline_kernel
             __syncwarp();
             J.s.blk_sm = bw;
         }
-        batch_warp_pipe<occ_in_smem, INB_SM, LOG, BSM>(J, ip, R);
+        batch_warp_pipe<occ_in_smem, INB_SM, LOG, BSM, LEAP>(J, ip, R, wst);
     }
 }
 
@@ -1391,12 +1745,31 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
         const int64_t smem = pipeline_small_dag_smem(a.W, a.H, a.k);
         pl_dag_small_kernel<1><<<(int)std::min<int64_t>(a.count, 148 * 16), 256, smem, st>>>(a);
     } else {
-        pl_walk_kernel<1><<<blocks, 256, 0, st>>>(a);
+        const int32_t *mc = a.source_of, *mr = a.source_of + (size_t)a.count * a.W * a.H * 2;
+        pl_walk_warp_kernel<1><<<blocks, 256, 0, st>>>(a, (const int2 *)mc, (const int2 *)mr);
     }
     occ_to_vertex_bits<<<blocks, 256, 0, st>>>(a.count, a.W, a.H, a.grid_occ, a.occ);
     cudaMemsetAsync(a.inb, 0, (size_t)a.count * nwb * 4, st);
     cudaMemsetAsync(a.counter, 0, (size_t)a.count * 4, st);
     (void)N;
+    if (a.wide) {
+        // wide phase first: the batches whose ready set exceeds a warp
+        int rmax = 0, hbits = 0;
+        size_t wsmem = 0;
+        static const int wide_smem_env = [] {
+            const char *e = getenv("RECON_WIDE_SMEM_KB");
+            return e ? atoi(e) : 0;
+        }();
+        const int64_t budget = wide_smem_env > 0 ? (int64_t)wide_smem_env * 1024 : 113 * 1024;  // 2 CTAs per SM
+        if (pipeline_wide_config(a.W, a.H, budget, &rmax, &hbits, &wsmem) ||
+            pipeline_wide_config(a.W, a.H, 220 * 1024, &rmax, &hbits, &wsmem)) {
+            cudaMemsetAsync(a.vmin, 0x7f, (size_t)a.count * a.W * a.H * 4, st);
+            cudaError_t e = launch_batch_wide(a, sms, rmax, hbits, wsmem, st);
+            if (e != cudaSuccess) return e;
+        } else {
+            cudaMemsetAsync(a.wstate, 0, (size_t)a.count * 32, st);
+        }
+    }
     // occupancy + in-batch bitmaps in shared memory when a few warps' worth fits
     // bitmaps in shared memory when a few warps' worth fits; then the blocker
     // counts too when they fit in u16 and the CTA keeps at least two warps
@@ -1411,7 +1784,20 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
         const char *e = getenv("RECON_BATCH_OCC_SMEM");
         return e ? atoi(e) : 1;
     }();
-    if (occ_env && bm_bytes <= 96 * 1024) {
+    if (a.leap) {
+        // leap mode reads the bitmaps only in literal batches and the general
+        // (> 32 ready) path: shared memory only when it costs no warps
+        mode = 16;
+        int64_t per = bm_bytes + (S < 65536 ? blk_bytes : 0);
+        if (occ_env && per <= 24 * 1024) {
+            mode |= 1 | ((bsm_env && S < 65536) ? 4 : 0);
+            if (!(mode & 4)) per = bm_bytes;
+            warps = 8;
+            smem = (size_t)warps * per;
+        } else {
+            warps = 4;
+        }
+    } else if (occ_env && bm_bytes <= 96 * 1024) {
         mode = 1 | (a.mlog ? 2 : 0);
         if (bsm_env && S < 65536 && bm_bytes + blk_bytes <= 100 * 1024) mode |= 4;
         int64_t per = bm_bytes + ((mode & 4) ? blk_bytes : 0);
@@ -1427,7 +1813,9 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
     }
     void (*kern)(PipelineArgs) = mode == 0 ? batch_pipeline_kernel<0> : mode == 1 ? batch_pipeline_kernel<1>
                                : mode == 9 ? batch_pipeline_kernel<9> : mode == 3 ? batch_pipeline_kernel<3>
-                               : mode == 5 ? batch_pipeline_kernel<5> : batch_pipeline_kernel<7>;
+                               : mode == 5 ? batch_pipeline_kernel<5> : mode == 16 ? batch_pipeline_kernel<16>
+                               : mode == 17 ? batch_pipeline_kernel<17> : mode == 21 ? batch_pipeline_kernel<21>
+                               : batch_pipeline_kernel<7>;
     if (smem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int grid = (int)std::min<int64_t>(((int64_t)a.count + warps - 1) / warps, (int64_t)sms * 32);
     kern<<<grid, warps * 32, smem, st>>>(a);
@@ -1435,3 +1823,13 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
 }
 
 }  // namespace rb
+
+// experiments: the phase counters above (zero unless built with -DRECON_BATCH_PROF)
+extern "C" int recon_debug_batch_prof(unsigned long long *out, int reset) {
+    if (cudaMemcpyFromSymbol(out, rb::g_batch_prof, sizeof(rb::g_batch_prof)) != cudaSuccess) return -1;
+    if (reset) {
+        static const unsigned long long z[16] = {};
+        if (cudaMemcpyToSymbol(rb::g_batch_prof, z, sizeof(z)) != cudaSuccess) return -1;
+    }
+    return 0;
+}

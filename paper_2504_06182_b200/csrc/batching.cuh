@@ -17,7 +17,10 @@ struct BatchScratch {
     int32_t *ready, *ready2, *newly, *mem, *mfr, *mto;  // [P] each
     int32_t *counter;   // [1], zero
     uint32_t *blk_sm;   // pipeline: blocker counts in shared memory (u16 pairs), or null
+    int32_t *newly_sm;  // pipeline leap mode: the warp's shared buffer of released ids
 };
+
+constexpr int NEWLY_SM = 128;  // released ids per warp kept in shared memory (leap mode)
 
 struct PipeRecords {  // one instance's ready records (batch_warp_pipe)
     int4 *rec, *rec2;
@@ -56,6 +59,10 @@ __global__ void need_kernel(int64_t E, const int32_t *es, const int32_t *ed, con
 // fused pipeline over `count` grid instances already solved on the device
 struct PipelineArgs {
     int count, W, H, k, preset;
+    int leap;                            // leap mode (preset none): batching.cu
+    int wide;                            // wide phase first (batch_wide.cu)
+    int64_t *wstate;                     // [count * 4] wide -> warp hand-off {phase, nb, left, nready}
+    int32_t *vmin;                       // [count * W*H] wide: per-vertex min id (0x7f7f7f7f = empty)
     const int32_t *path_src, *path_dst;  // [count * W*k] (instance stride W*k)
     const int32_t *path_count;           // [count]
     const int32_t *solve_status;         // [count]
@@ -90,6 +97,10 @@ cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *
 cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t st);
 // shared memory of the per-instance DAG builder, or 0 when an instance does not fit
 int64_t pipeline_small_dag_smem(int W, int H, int k);
+
+// wide phase (batch_wide.cu): CTA per instance while the ready set exceeds a warp
+bool pipeline_wide_config(int W, int H, int64_t smem_budget, int *rmax, int *hbits, size_t *smem);
+cudaError_t launch_batch_wide(const PipelineArgs &a, int sms, int rmax, int hbits, size_t smem, cudaStream_t st);
 
 // occ bits (column-major, bit y) -> vertex-id bitmap
 __global__ void occ_to_vertex_bits(int count, int W, int H, const uint64_t *occ, uint32_t *bits);

@@ -70,14 +70,33 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool 
     a.solve_status = g.status;
     a.move_stride = pb->move_stride;
     a.grid_occ = g.occ;
+    // leap mode (batching.cu) for preset none; RECON_BATCH_LEAP=0 forces the
+    // batch-by-batch loop
+    static const int leap_env = [] {
+        const char *e = getenv("RECON_BATCH_LEAP");
+        return e ? atoi(e) : 1;
+    }();
+    a.leap = leap_env && pb->preset == 0;
+    // wide phase (batch_wide.cu) for large instances; RECON_BATCH_WIDE=0/1 forces
+    static const int wide_env = [] {
+        const char *e = getenv("RECON_BATCH_WIDE");
+        return e ? atoi(e) : -1;
+    }();
+    a.wide = wide_env >= 0 ? wide_env : (S >= 16384 ? 1 : 0);
+    if (a.wide) {
+        a.wstate = c->dev<int64_t>(S_BM_WSTATE, n * 4);
+        a.vmin = c->dev<int32_t>(S_BM_VMIN, n * WH);
+        if (!a.wstate || !a.vmin) return cuda_fail(cudaErrorMemoryAllocation, "pipeline wide", detail);
+    }
     const size_t nwb = (WH + 31) / 32;
     static const int small_env = [] {
         const char *e = getenv("RECON_SMALL_DAG");
         return e ? atoi(e) : 1;
     }();
     a.small_dag = small_env && pipeline_small_dag_smem(a.W, a.H, a.k) > 0;
-    // per-instance vertex maps only for the global DAG walk
-    const size_t maps = a.small_dag ? 0 : n * WH * 2;
+    // per-instance vertex maps only for the global DAG walk: {source, target}
+    // owner per vertex, column-major and row-major
+    const size_t maps = a.small_dag ? 0 : n * WH * 4;
     int32_t *i32 = c->dev<int32_t>(S_BM_AUX0, maps + n * S * 9 + n * 2 + 8);
     int64_t *i64 = c->dev<int64_t>(S_BM_AUX1, (n * S + 1) * 2 + 4 * (n + 1) + 4);
     uint32_t *bits = c->dev<uint32_t>(S_BM_AUX2, n * nwb * 2 + 4);
@@ -88,8 +107,8 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool 
     int32_t *bdet = host ? bc + 2 * n : g.detail;
     if (!i32 || !i64 || !bits || !rec || !mb || !bc) return cuda_fail(cudaErrorMemoryAllocation, "pipeline", detail);
     if (host) CK(cudaMemsetAsync(mb, 0xff, n * (size_t)pb->move_stride * 4, c->stream), "memset");
-    a.source_of = maps ? i32 : nullptr;
-    a.target_of = maps ? i32 + n * WH : nullptr;
+    a.source_of = maps ? i32 : nullptr;  // int2 maps (batching.cu pl_mark2_kernel)
+    a.target_of = nullptr;
     int32_t *q = i32 + maps;
     a.outdeg = q;
     a.indeg = q + n * S;
@@ -134,7 +153,7 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool 
         const char *e = getenv("RECON_BATCH_LOG");
         return e ? atoi(e) : -1;
     }();
-    const bool use_log = log_env >= 0 ? log_env == 1 : (n >= (size_t)c->sms * 4 && 2 * nwb * 4 <= 32 * 1024);
+    const bool use_log = !a.leap && (log_env >= 0 ? log_env == 1 : (n >= (size_t)c->sms * 4 && 2 * nwb * 4 <= 32 * 1024));
     a.mlog = nullptr;
     if (use_log) {
         a.mlog = c->dev<int2>(S_BM_AUX6, (size_t)counts[1] + 1);

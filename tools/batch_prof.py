@@ -1,0 +1,44 @@
+"""Phase cycle breakdown of the pipeline batching warp (library built with
+RECON_NVCC_EXTRA=-DRECON_BATCH_PROF).
+
+  python tools/batch_prof.py c5 [count]
+"""
+import ctypes as C
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2504_06182_b200 import load_native  # noqa: E402
+from paper_2504_06182_b200.inputs import sample_grids  # noqa: E402
+
+CASES = {
+    "c3": ("bird", 64, 64, 40, 2662, 0x64000000, 0, 64 * 64 * 12),
+    "c4": ("redrec", 256, 256, 153, 39322, 0x25600000, 0, 1_500_000),
+    "c5": ("bird", 512, 512, 307, 157286, 0x51200000, 0, 12_000_000),
+}
+gpu = load_native()
+name = sys.argv[1]
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+solver, W, H, hp, k, seed, preset, ms = CASES[name]
+occ = sample_grids(seed, n, W, H, k)
+buf = (C.c_ulonglong * 16)()
+gpu.lib.recon_debug_batch_prof(buf, 1)
+t = time.time()
+g = gpu.pipeline_batch(solver, occ, n, W, H, hp, preset, ms)
+dt = time.time() - t
+gpu.lib.recon_debug_batch_prof(buf, 1)
+v = list(buf)
+names = ["leap_delta", "leap_apply", "literal", "finish", "general", "n_leap", "n_literal", "n_general", "n_finish",
+         "total"]
+out = {names[i]: v[i] for i in range(10)}
+cyc = {k2: out[k2] / n for k2 in names[:5] + ["total"]}
+print(name, n, f"wall {dt:.2f}s", "per-instance Mcycles:", {k2: round(c / 1e6, 2) for k2, c in cyc.items()})
+print("counts per instance:", {k2: out[k2] / n for k2 in names[5:9]})
+for a, b in (("leap_delta", "n_leap"), ("literal", "n_literal"), ("general", "n_general"), ("finish", "n_finish")):
+    if out[b]:
+        print(f"  {a}: {out[a] / max(1, out[b] if a != 'leap_delta' else out['n_leap'] + out['n_literal']):.0f} cycles per")
+print("batch_count", g["batch_count"][:4], "status", np.unique(g["status"]))
