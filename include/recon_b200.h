@@ -340,6 +340,35 @@ recon_status recon_pipeline_batch_run(recon_ctx *ctx, const recon_pipeline_batch
 /* Same with every pointer in `batch` in host memory. */
 recon_status recon_pipeline_batch_run_host(recon_ctx *ctx, const recon_pipeline_batch *batch);
 
+/*
+ * Per-instance result record of a pipeline run (device): SolutionStats
+ * {displaced_tokens, total_displacement} (path_system.hpp:74-77), the batch
+ * count (BatchSchedule::batches.size(), batching.hpp:23-27), the status and
+ * digest64, a 64-bit fingerprint of the canonical path list and the whole
+ * batch schedule (identical across GPU counts and chunkings):
+ *   mix(z)       = splitmix64 finaliser (z += 0x9e3779b97f4a7c15; ...)
+ *   e(tag, i, v) = mix(mix((tag << 48) ^ i) ^ (uint32)v)
+ *   status == 0: digest = mix( sum_i e(1,i,src[i]) + e(2,i,dst[i])  (i < P)
+ *                              + sum_j e(3,j,move_batch[j])          (j < D)
+ *                              + e(5,0,P) + e(6,0,D & 0xffffffff) + e(7,0,D >> 32) + e(8,0,nb) )  (mod 2^64)
+ *   else:        digest = mix(e(4,0,status))
+ * (tests/digest.py is the same formula in numpy.)
+ */
+typedef struct recon_instance_stats {
+    int32_t status;              /* recon_status of the instance (solve or batching) */
+    int32_t detail;              /* recon_detail */
+    int32_t path_count;          /* P */
+    int32_t displaced_tokens;    /* paths of length > 0 (PathSystem::displaced_count) */
+    int64_t total_displacement;  /* D */
+    int64_t batch_count;         /* nb */
+    uint64_t digest;             /* digest64 */
+} recon_instance_stats;
+
+/* Stats of a finished recon_pipeline_batch_run: `batch` holds the run's device
+ * pointers, `stats` is a device array of batch->grid.count records.  Enqueued
+ * on the context's stream. */
+recon_status recon_pipeline_stats(recon_ctx *ctx, const recon_pipeline_batch *batch, recon_instance_stats *stats);
+
 /* ------------------------------------------------------------------------- */
 /* Validators (device)                                                        */
 /* ------------------------------------------------------------------------- */

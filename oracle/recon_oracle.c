@@ -33,6 +33,7 @@
 
 #include "recon_b200.h"
 #include "recon_sim_rng.h"
+#include "digest_cpu.h"
 
 struct recon_ctx {
     int device;
@@ -2152,4 +2153,10 @@ static recon_status oracle_sim_solve(int batching, int solver, int preset, recon
 recon_status recon_sim_run_host(recon_ctx *c, const recon_sim_batch *b) {
     (void)c;
     return sim_run_checked(b, oracle_sim_solve);
+}
+
+/* recon_pipeline_stats over host pointers (digest_cpu.h) */
+recon_status recon_pipeline_stats(recon_ctx *ctx, const recon_pipeline_batch *pb, recon_instance_stats *stats) {
+    (void)ctx;
+    return recon_dg_stats(pb, stats);
 }

@@ -23,6 +23,8 @@
 #include <thread>
 #include <vector>
 
+#include "digest_cpu.h"
+
 #include "recon/batching.hpp"
 #include "recon/bird.hpp"
 #include "recon/exact1d.hpp"
@@ -874,4 +876,9 @@ extern "C" recon_status recon_sim_run_host(recon_ctx *, const recon_sim_batch *b
         return RECON_ERR_ARGUMENT;
     parallel_for(b->count, [&](int i) { simc_trial(b, i, ref_sim_solve); });
     return RECON_OK;
+}
+
+// recon_pipeline_stats over host pointers (digest_cpu.h)
+extern "C" recon_status recon_pipeline_stats(recon_ctx *, const recon_pipeline_batch *pb, recon_instance_stats *stats) {
+    return recon_dg_stats(pb, stats);
 }

@@ -151,6 +151,20 @@ class PipelineBatch(C.Structure):
     ]
 
 
+class InstanceStats(C.Structure):
+    """recon_instance_stats (include/recon_b200.h)."""
+    _fields_ = [
+        ("status", C.c_int32), ("detail", C.c_int32), ("path_count", C.c_int32), ("displaced_tokens", C.c_int32),
+        ("total_displacement", C.c_int64), ("batch_count", C.c_int64), ("digest", C.c_uint64),
+    ]
+
+
+STATS_DTYPE = np.dtype([("status", np.int32), ("detail", np.int32), ("path_count", np.int32),
+                        ("displaced_tokens", np.int32), ("total_displacement", np.int64),
+                        ("batch_count", np.int64), ("digest", np.uint64)])
+assert STATS_DTYPE.itemsize == C.sizeof(InstanceStats) == 40
+
+
 class ValidateBatch(C.Structure):
     _fields_ = [
         ("occ", C.c_void_p), ("count", C.c_int32), ("width", C.c_int32), ("height", C.c_int32),
@@ -303,6 +317,8 @@ class ReconLib:
             f = getattr(L, fn)
             f.argtypes = [C.c_void_p, C.POINTER(PipelineBatch)]
             f.restype = C.c_int
+        L.recon_pipeline_stats.argtypes = [C.c_void_p, C.POINTER(PipelineBatch), C.c_void_p]
+        L.recon_pipeline_stats.restype = C.c_int
         for fn in ("recon_solution_json", "recon_solution_json_host"):
             f = getattr(L, fn)
             f.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -636,6 +652,18 @@ class ReconLib:
         st = self.lib.recon_sim_run_host(self.ctx(), C.byref(sb))
         self._check(st, 0)
         return out
+
+    def pipeline_stats_host(self, out: dict, count, width, h_prime, move_stride) -> np.ndarray:
+        """recon_pipeline_stats over a pipeline_batch result held in host memory
+        (the CPU checkers: oracle / compiled reference)."""
+        g = GridBatch(None, count, width, 0, h_prime, _vp(out["path_src"]).value, _vp(out["path_dst"]).value, None,
+                      _vp(out["path_count"]).value, _vp(out["total_displacement"]).value,
+                      _vp(out["status"]).value, _vp(out["detail"]).value, None)
+        pb = PipelineBatch(g, 0, 0, move_stride, _vp(out["move_batch"]).value, _vp(out["batch_count"]).value)
+        st = np.zeros(count, STATS_DTYPE)
+        r = self.lib.recon_pipeline_stats(None, C.byref(pb), st.ctypes.data)
+        self._check(r, 0)
+        return st
 
     def pipeline_batch(self, solver: str, occ, count, width, height, h_prime, preset, move_stride):
         stride = width * h_prime

@@ -558,6 +558,23 @@ __global__ void __launch_bounds__(256) pl_walk_warp_kernel(PipelineArgs a, const
     }
 }
 
+// per-path records for leap mode: {src, dst, move base, successor offset},
+// relative to the instance; entry P closes the last path's ranges
+__global__ void prec_kernel(PipelineArgs a) {
+    const int64_t S = (int64_t)a.W * a.k, S1 = S + 1;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)a.count * S1;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t inst = t / S1;
+        const int p = (int)(t - inst * S1);
+        const int P = a.solve_status[inst] != 0 ? 0 : a.path_count[inst];
+        if (p > P) continue;
+        const int64_t o = inst * S;
+        const int64_t e0 = a.soff[o], m0 = a.mbase[o];
+        a.prec[t] = make_int4(p < P ? a.path_src[o + p] : 0, p < P ? a.path_dst[o + p] : 0,
+                              (int)(a.mbase[o + p] - m0), (int)(a.soff[o + p] - e0));
+    }
+}
+
 __global__ void sum2_widen_kernel(int64_t n, const int32_t *a, const int32_t *b, int64_t *out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         out[i] = (int64_t)a[i] + b[i];
@@ -1031,6 +1048,98 @@ __device__ __forceinline__ int release_successors_buf(const BatchJob &J, const B
     return nnew;
 }
 
+// Leap-mode finish: the finished lanes' successors are released as in
+// release_successors_buf, and every successor's path record
+// {src, dst, move base, successor offset} (prec, built with the dag) is loaded
+// together with its blocker decrement, so a released path needs no further
+// round trip: it goes straight into an empty lane (lanes are not kept in id
+// order in leap mode).  Released ids also go to `buf` for the rare spill.
+// Returns the number released; *filled = whether every one got a lane.
+template <class BL>
+__device__ __forceinline__ int release_into_lanes(const BatchJob &J, const BL &blockers, int32_t *sm, int cap,
+                                                  int32_t *g, bool fin, int64_t q0, int64_t q1, int32_t **out,
+                                                  LanePath &lp, bool *filled) {
+    constexpr int G = 8;  // chunks of 32 successors in flight
+    const int lane = lane_id();
+    const unsigned fmask = __ballot_sync(FULL, fin);
+    const int tot = __reduce_add_sync(FULL, fin ? (unsigned)(q1 - q0) : 0u);
+    int32_t *buf = tot <= cap ? sm : g;
+    *out = buf;
+    const unsigned empty = __ballot_sync(FULL, lp.p == INT_MAX);
+    const int erank = __popc(empty & lanemask_lt());  // my rank among the empty lanes
+    const int nempty = __popc(empty);
+    const bool is_empty = (empty >> lane) & 1u;
+    bool took = false;
+    int nnew = 0;
+    int sc[G];
+    int nsl = 0;  // chunks loaded (warp-uniform)
+    // decrement, prefetch and hand out the loaded chunks
+    auto flush = [&]() {
+        int4 pr[G];
+        int qe[G];
+        bool rel[G];
+#pragma unroll
+        for (int c = 0; c < G; ++c) {
+            rel[c] = false;
+            pr[c] = make_int4(0, 0, 0, 0);
+            qe[c] = 0;
+            if (c < nsl && sc[c] >= 0) {
+                pr[c] = __ldg(J.prec + sc[c]);
+                qe[c] = __ldg(&J.prec[sc[c] + 1].w);
+                rel[c] = blockers.release(sc[c]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < G; ++c) {
+            if (c >= nsl) break;
+            const unsigned rm = __ballot_sync(FULL, rel[c]);
+            if (!rm) continue;
+            if (rel[c]) buf[nnew + __popc(rm & lanemask_lt())] = sc[c];
+            // the empty lane of rank e takes released item e - nnew of this chunk
+            const int j = erank - nnew;
+            const bool take = is_empty && j >= 0 && j < __popc(rm);
+            const int srcl = take ? (int)__fns(rm, 0, j + 1) : lane;
+            const int np = __shfl_sync(FULL, sc[c], srcl);
+            const int4 r = make_int4(__shfl_sync(FULL, pr[c].x, srcl), __shfl_sync(FULL, pr[c].y, srcl),
+                                     __shfl_sync(FULL, pr[c].z, srcl), __shfl_sync(FULL, pr[c].w, srcl));
+            const int e = __shfl_sync(FULL, qe[c], srcl);
+            if (take) {
+                const int H = J.H;
+                took = true;
+                lp.p = np;
+                lp.k = 0;
+                lp.xs = r.x / H;
+                lp.ys = r.x - lp.xs * H;
+                lp.xt = r.y / H;
+                lp.yt = r.y - lp.xt * H;
+                lp.len = abs(lp.xt - lp.xs) + abs(lp.yt - lp.ys);
+                lp.base = r.z;
+                lp.q0 = J.e0 + r.w;
+                lp.q1 = J.e0 + e;
+            }
+            nnew += __popc(rm);
+        }
+        nsl = 0;
+    };
+    // successor ids, finished lane by finished lane, 32 at a time
+    for (unsigned m = fmask; m; m &= m - 1) {
+        const int f = __ffs(m) - 1;
+        const int64_t fq0 = __shfl_sync(FULL, q0, f);
+        const int fn = (int)(__shfl_sync(FULL, q1, f) - fq0);
+        for (int j0 = 0; j0 < fn; j0 += 32) {
+            const int v = j0 + lane < fn ? __ldg(J.succ + fq0 + j0 + lane) : -1;
+#pragma unroll
+            for (int c = 0; c < G; ++c)
+                if (c == nsl) sc[c] = v;
+            if (++nsl == G) flush();
+        }
+    }
+    if (nsl) flush();
+    *filled = nnew <= nempty;
+    if (!*filled && took) lp.p = INT_MAX;  // the spill takes every released id from buf
+    return nnew;
+}
+
 // occupancy update without ordering: a token moving a -> b toggles both bits
 // (red.xor commutes, so a vacated and a refilled vertex need no fence)
 template <bool SM>
@@ -1349,6 +1458,11 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
                     const int first = __ffs(cm) - 1;
                     const int32_t ff = __shfl_sync(FULL, fr, first), ft = __shfl_sync(FULL, to, first);
                     a = cand && compatible(J.preset, H, fr, to, ff, ft);
+                } else if (LEAP) {
+                    // lanes are not in id order in leap mode: the minimum id of
+                    // each destination group wins (batching.cpp:112-113)
+                    const unsigned same = __match_any_sync(FULL, cand ? to : -2 - lane);
+                    a = cand && __reduce_min_sync(same, (unsigned)lp.p) == (unsigned)lp.p;
                 } else {
                     const unsigned same = __match_any_sync(FULL, cand ? to : -2 - lane);
                     a = cand && (same & lanemask_lt()) == 0;
@@ -1385,12 +1499,39 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
             const unsigned fm = __ballot_sync(FULL, fin);
             if (fm) {
                 BPROF_CNT(8);
-                // leap mode: released ids go to the warp's shared buffer when they fit
                 int32_t *newly = s.newly;
-                const int nnew = LEAP ? release_successors_buf(J, blk, s.newly_sm, NEWLY_SM, s.newly, fin, q0, q1, &newly)
-                                      : release_successors(J, blk, s.newly, 0, fin, q0, q1);
-                if (fin) lp.p = INT_MAX;
+                int nnew;
+                bool filled = false;
+                if (LEAP) {
+                    if (fin) lp.p = INT_MAX;
+                    nnew = release_into_lanes(J, blk, s.newly_sm, NEWLY_SM, s.newly, fin, q0, q1, &newly, lp, &filled);
+                } else {
+                    nnew = release_successors(J, blk, s.newly, 0, fin, q0, q1);
+                    if (fin) lp.p = INT_MAX;
+                }
                 __syncwarp();
+                if (LEAP && filled) {
+                    // released paths already sit in the empty lanes
+                } else if (LEAP) {
+                    // more ready paths than lanes (release_into_lanes emptied
+                    // the lanes it had filled): the live lanes in id order and
+                    // the released ids become the sorted record list
+                    int key = lp.p != INT_MAX ? (lp.p << 5) | lane : INT_MAX;
+                    key = warp_sort32(key);
+                    const int srcl = key == INT_MAX ? lane : (key & 31);
+                    const LanePath q = shfl_lane(lp, srcl, true);
+                    const int nlive = __popc(__ballot_sync(FULL, key != INT_MAX));
+                    if (lane < nlive) {
+                        R.rec2[lane] = lane_rec(q);
+                        R.rb2[lane] = (int)q.base;
+                    }
+                    __syncwarp();
+                    sort_newly(newly, s.mem, nnew);
+                    merge_ready(paths, R, newly, nlive, nnew, s.mfr);
+                    nready = nlive + nnew;
+                    regmode = false;
+                    __threadfence();  // the general path reads the toggled bitmap
+                } else {
                 const unsigned live = __ballot_sync(FULL, lp.p != INT_MAX);
                 const int nlive = __popc(live);
                 if (nlive + nnew > 32) {
@@ -1405,7 +1546,6 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
                     merge_ready(paths, R, newly, nlive, nnew, s.mfr);
                     nready = nlive + nnew;
                     regmode = false;
-                    if (LEAP) __threadfence();  // the general path reads the toggled bitmap
                 } else if (nnew > 0) {
                     // newly released paths take the empty lanes, then sort lanes by id
                     const int erank = __popc(~live & lanemask_lt());
@@ -1414,23 +1554,20 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
                         const int np = newly[erank];
                         const int4 r = make_rec(paths, np, &b);
                         lp = rec_lane(r, b);
-                        if (LEAP) {
-                            lp.q0 = J.soff[np];
-                            lp.q1 = J.soff[np + 1];
-                        }
                     }
                     int key = lp.p == INT_MAX ? INT_MAX : (lp.p << 5) | lane;
                     key = warp_sort32(key);
                     const int src = key == INT_MAX ? lane : (key & 31);
-                    LanePath q = shfl_lane(lp, src, LEAP);
+                    LanePath q = shfl_lane(lp, src, false);
                     if (key == INT_MAX) q.p = INT_MAX;
                     lp = q;
                 } else {
                     // finished lanes leave gaps: lane L takes the L-th live lane
                     const int src = lane < nlive ? (int)__fns(live, 0, lane + 1) : lane;
-                    LanePath q = shfl_lane(lp, src, LEAP);
+                    LanePath q = shfl_lane(lp, src, false);
                     if (lane >= nlive) q.p = INT_MAX;
                     lp = q;
+                }
                 }
                 lane_move();  // lanes were reloaded / reordered
                 BPROF_ADD(3);
@@ -1670,6 +1807,7 @@ __global__ void __launch_bounds__(256, (MODE & 2) ? 4 : 1) batch_pipeline_kernel
             if (lane_id() == 0) {
                 a.status[inst] = a.solve_status[inst];
                 a.batch_count[inst] = 0;
+                if (a.detail && a.solve_detail && a.detail != a.solve_detail) a.detail[inst] = a.solve_detail[inst];
             }
             continue;
         }
@@ -1681,6 +1819,7 @@ __global__ void __launch_bounds__(256, (MODE & 2) ? 4 : 1) batch_pipeline_kernel
             if (lane_id() == 0) {
                 a.status[inst] = RECON_ERR_CAPACITY;
                 a.batch_count[inst] = 0;
+                if (a.detail) a.detail[inst] = RECON_D_NONE;
             }
             continue;
         }
@@ -1691,6 +1830,8 @@ __global__ void __launch_bounds__(256, (MODE & 2) ? 4 : 1) batch_pipeline_kernel
         J.preset = a.preset;
         J.edge_level = 0;
         J.soff = a.soff + o;
+        J.prec = a.prec ? a.prec + (int64_t)inst * (S + 1) : nullptr;
+        J.e0 = a.soff[o];
         J.succ = a.succ;
         J.s.occ = a.occ + inst * nwb;
         J.s.inb = a.inb + inst * nwb;
@@ -1748,6 +1889,7 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
         const int32_t *mc = a.source_of, *mr = a.source_of + (size_t)a.count * a.W * a.H * 2;
         pl_walk_warp_kernel<1><<<blocks, 256, 0, st>>>(a, (const int2 *)mc, (const int2 *)mr);
     }
+    if (a.prec) prec_kernel<<<blocks, 256, 0, st>>>(a);
     occ_to_vertex_bits<<<blocks, 256, 0, st>>>(a.count, a.W, a.H, a.grid_occ, a.occ);
     cudaMemsetAsync(a.inb, 0, (size_t)a.count * nwb * 4, st);
     cudaMemsetAsync(a.counter, 0, (size_t)a.count * 4, st);

@@ -31,6 +31,8 @@ struct BatchJob {
     int P, W, H, preset, edge_level;
     const int64_t *soff;  // [P+1] successor CSR offsets (global edge index)
     const int32_t *succ;
+    const int4 *prec;     // pipeline: [P+1] {src, dst, move base, soff - e0} per path
+    int64_t e0;           // pipeline: soff[0]
     const int64_t *in_off;  // edge-level only: incoming CSR
     const int32_t *in_src;
     const int64_t *in_need;
@@ -66,6 +68,7 @@ struct PipelineArgs {
     const int32_t *path_src, *path_dst;  // [count * W*k] (instance stride W*k)
     const int32_t *path_count;           // [count]
     const int32_t *solve_status;         // [count]
+    const int32_t *solve_detail;         // [count] (may be null)
     int64_t move_stride;
     int32_t *move_batch;                 // [count * move_stride]
     int32_t *batch_count, *status, *detail;
@@ -84,6 +87,7 @@ struct PipelineArgs {
     // their exclusive scans over instances, [count + 1] each
     int small_dag;
     int4 *rec, *rec2;    // [count * W*k] ready-path records (batch_warp_pipe)
+    int4 *prec;          // [count * (W*k + 1)] path records {src, dst, move base, soff} (leap mode)
     int32_t *rb, *rb2;   // [count * W*k] their move bases
     int64_t *inst_edges, *inst_moves, *ebase, *mvbase;
     const uint64_t *grid_occ;            // [count * W * wpc] initial occupancy (occ bits)

@@ -68,6 +68,7 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool 
     a.path_dst = g.path_dst;
     a.path_count = g.path_count;
     a.solve_status = g.status;
+    a.solve_detail = g.detail;
     a.move_stride = pb->move_stride;
     a.grid_occ = g.occ;
     // leap mode (batching.cu) for preset none; RECON_BATCH_LEAP=0 forces the
@@ -83,6 +84,11 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool 
         return e ? atoi(e) : -1;
     }();
     a.wide = wide_env >= 0 ? wide_env : (S >= 16384 ? 1 : 0);
+    a.prec = nullptr;
+    if (a.leap) {
+        a.prec = c->dev<int4>(S_BM_PREC, n * (S + 1));
+        if (!a.prec) return cuda_fail(cudaErrorMemoryAllocation, "pipeline prec", detail);
+    }
     if (a.wide) {
         a.wstate = c->dev<int64_t>(S_BM_WSTATE, n * 4);
         a.vmin = c->dev<int32_t>(S_BM_VMIN, n * WH);

@@ -29,7 +29,7 @@ enum Slot {
     S_W_LEN, S_W_OUT, S_W_MOFF, S_W_VOFF, S_W_MB, S_W_K0, S_W_K1, S_W_I0, S_W_I1,
     S_SIM_OCC, S_SIM_CUR, S_SIM_NXT, S_SIM_CYC, S_SIM_ST, S_SIM_SUC, S_SIM_ACC, S_SIM_EL, S_SIM_LIVE, S_SIM_CODE,
     S_SIM_CEL, S_SIM_PDEC, S_SIM_SRC, S_SIM_DST, S_SIM_PC, S_SIM_PST, S_SIM_DET, S_SIM_NB, S_SIM_TD, S_SIM_OFF,
-    S_SIM_MB, S_SIM_BCNT, S_SIM_RUN, S_SIM_ALLC, S_PPACK, S_BM_WSTATE, S_BM_VMIN,
+    S_SIM_MB, S_SIM_BCNT, S_SIM_RUN, S_SIM_ALLC, S_PPACK, S_BM_WSTATE, S_BM_VMIN, S_BM_PREC,
     S_NSLOTS
 };
 

@@ -1,0 +1,109 @@
+// Per-instance result record of a pipeline run, on the device:
+// SolutionStats {displaced_tokens, total_displacement} (path_system.hpp:74-77,
+// path_system.cpp:41-44), the batch count (BatchSchedule::batches.size(),
+// batching.hpp:23-27), the status, and digest64 over the canonical path list
+// and the whole batch schedule (the digest definition is in
+// include/recon_b200.h).  One CTA per instance; the element hashes are summed
+// (mod 2^64) by a block reduction, so the value is independent of the
+// reduction order.  SURVEY.md §5 / §8(d): the 32-byte stats record, plus the
+// digest that cross-GPU-count identity is checked with.
+
+#include "capi_internal.cuh"
+#include "common.cuh"
+
+namespace {
+
+using namespace rb;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint64_t elem(uint64_t tag, uint64_t i, int32_t v) {
+    return mix64(mix64((tag << 48) ^ i) ^ (uint64_t)(uint32_t)v);
+}
+
+constexpr int ST = 256;
+
+__global__ void __launch_bounds__(ST) pipeline_stats_kernel(recon_pipeline_batch pb, recon_instance_stats *out) {
+    __shared__ unsigned long long s_sum;
+    __shared__ int s_disp;
+    const recon_grid_batch &g = pb.grid;
+    const int64_t S = (int64_t)g.width * g.h_prime;
+    for (int inst = blockIdx.x; inst < g.count; inst += gridDim.x) {
+        const int32_t st = g.status[inst];
+        recon_instance_stats r{};
+        r.status = st;
+        r.detail = g.detail ? g.detail[inst] : 0;
+        if (st != RECON_OK) {
+            if (threadIdx.x == 0) {
+                r.digest = mix64(elem(4, 0, st));
+                out[inst] = r;
+            }
+            continue;
+        }
+        const int P = g.path_count[inst];
+        const int64_t D = g.total_displacement[inst];
+        const int32_t nb = pb.batch_count[inst];
+        if (threadIdx.x == 0) {
+            s_sum = 0;
+            s_disp = 0;
+        }
+        __syncthreads();
+        const int32_t *src = g.path_src + inst * S, *dst = g.path_dst + inst * S;
+        const int32_t *mb = pb.move_batch + inst * pb.move_stride;
+        uint64_t acc = 0;
+        int disp = 0;
+        for (int i = threadIdx.x; i < P; i += ST) {
+            const int32_t s = __ldg(src + i), t = __ldg(dst + i);
+            acc += elem(1, i, s) + elem(2, i, t);
+            disp += s != t;
+        }
+        for (int64_t j = threadIdx.x; j < D; j += ST) acc += elem(3, (uint64_t)j, __ldcs(mb + j));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            acc += __shfl_xor_sync(FULL, acc, o);
+            disp += __shfl_xor_sync(FULL, disp, o);
+        }
+        if (lane_id() == 0) {
+            atomicAdd(&s_sum, (unsigned long long)acc);
+            atomicAdd(&s_disp, disp);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t a = s_sum;
+            a += elem(5, 0, P) + elem(6, 0, (int32_t)(uint32_t)(D & 0xffffffffll)) + elem(7, 0, (int32_t)(D >> 32)) +
+                 elem(8, 0, nb);
+            r.path_count = P;
+            r.displaced_tokens = s_disp;
+            r.total_displacement = D;
+            r.batch_count = nb;
+            r.digest = mix64(a);
+            out[inst] = r;
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+extern "C" recon_status recon_pipeline_stats(recon_ctx *ctx, const recon_pipeline_batch *pb, recon_instance_stats *stats) {
+    int32_t *detail = nullptr;
+    if (!pb || !stats || !pb->grid.status || !pb->grid.path_count || !pb->grid.path_src || !pb->grid.path_dst ||
+        !pb->grid.total_displacement || !pb->move_batch || !pb->batch_count)
+        return RECON_ERR_ARGUMENT;
+    if (pb->grid.count <= 0) return RECON_OK;
+    Ctx *c = resolve(ctx);
+    if (!c) return RECON_ERR_CUDA;
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice", detail);
+    const int grid = pb->grid.count < c->sms * 8 ? pb->grid.count : c->sms * 8;
+    pipeline_stats_kernel<<<grid, ST, 0, c->stream>>>(*pb, stats);
+    c->launches += 1;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "pipeline stats", detail);
+    return RECON_OK;
+}
