@@ -2,19 +2,26 @@
 """bench.py — headline benchmark of the B200 atom-reconfiguration core.
 
 Metric (BASELINE.json): "red-rec/bird solve µs per 256×256 grid; grids/sec at
-1/2/4/8 B200".  One step = one batched red-rec solve (recon_redrec_solve_batch)
-of B independent 256×256 grids, h'=153 (ε-critical: ~113 deficit columns, the
-pairing loop runs), 39,322 atoms each (ε=0.6), seeds 0x25600000 + global index,
-all resident in HBM.  value = grids/s over all ranks (weak scaling: each rank
-solves its own B grids; instances are independent, so no collective runs on
-the data path — torch.distributed only carries the timing max).
+1/2/4/8 B200".  The grids/sec clause is quoted on C5: bird + batching
+(preset none, the reference default) on 512×512 grids, h'=307 (ε-critical),
+157,286 atoms (ε=0.6), seeds 0x51200000 + global instance index, 65,536
+instances sharded across 1/2/4/8 B200.
 
-Side measurements on the same line: bird on the same grids, single-grid
-latency (µs) for red-rec at h'=128 / 153 (C4), the roofline of the solve
-kernel against MEASURED_PEAKS.json, e2e through the host-buffer C-ABI call
-(recon_redrec_solve_batch_host: H2D of the grids + D2H of the paths inside the
-timed region), and the reference CPU implementation (oracle/_ref, compiled
-from the reference's own sources) timed on this host.
+One step = one HBM-resident chunk of B C5 instances per GPU through the fused
+device pipeline (recon_pipeline_batch_run: bird solve -> occupancy DAG ->
+batching), inputs already in HBM.  value = grids/s over all ranks (weak
+scaling: rank r owns instances [r*B, (r+1)*B); instances are independent, so
+no collective runs on the data path — torch.distributed carries only the
+timing max and the digest gather).  The full 65,536-instance job is 65,536/B
+such steps per GPU count.
+
+Same line: the phase breakdown (solve / DAG / wide batching / warp batching,
+CUDA events on the context stream), rooflines, the per-instance stats record
+(digest64) of the chunk, e2e through the host-buffer C-ABI call
+(recon_pipeline_batch_run_host: H2D of the grids and D2H of paths + batch
+schedule inside the timed region), the compiled reference (oracle/_ref)
+timed on this host's cores on a bounded sample, and the other BASELINE
+configs (C4 single-grid latency, the 256² red-rec batch, C3, C2) as extra keys.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 """
@@ -34,12 +41,16 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-W = H = 256
-HP = 153
-ATOMS = 39322
-SEED_BASE = 0x25600000
 METRIC = "red-rec/bird solve µs per 256×256 grid; grids/sec at 1/2/4/8 B200"
 REF_LIB = os.path.join(ROOT, "oracle", "_ref", "librecon_ref.so")
+W = H = 512
+HP = 307
+ATOMS = 157286
+SEED_BASE = 0x51200000
+WPC = (H + 63) // 64  # u64 words per column
+MOVE_STRIDE = 12_000_000  # > the largest C5 total displacement (10.82 M over the first 512 seeds)
+WORKLOAD = (f"C5: bird + batching (preset none) on {W}x{H} grids, h'={HP}, {ATOMS} atoms (eps=0.6), "
+            f"seeds {hex(SEED_BASE)} + global instance index")
 
 
 def peaks():
@@ -47,15 +58,22 @@ def peaks():
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), float(d.get("sm_max_mhz", 1965.0)), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, 1965.0, "fallback (B200_PROFILING.md)"
 
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class Clocks:
@@ -105,29 +123,34 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def gen_inputs(rank: int, batch: int):
-    from paper_2504_06182_b200.inputs import sample_grids
-    return sample_grids(SEED_BASE + rank * batch, batch, W, H, ATOMS)
+# ---- the reference arm: the compiled reference only (no repo .so is mapped) --------
+
+def ref_inputs(ref_lib, first: int, count: int) -> np.ndarray:
+    """Instances [first, first + count) from the reference's own generator,
+    Rng(seed).sample_without_replacement (rng.hpp:49-59, exported by oracle/_ref
+    as recon_ref_sample), packed into column-major occupancy bits."""
+    import ctypes as C
+    from paper_2504_06182_b200.inputs import pack_grid
+    ref_lib.recon_ref_sample.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_void_p]
+    ref_lib.recon_ref_sample.restype = None
+    out = []
+    v = np.zeros(ATOMS, np.int32)
+    for i in range(count):
+        ref_lib.recon_ref_sample(SEED_BASE + first + i, W * H, ATOMS, v.ctypes.data)
+        occ2d = np.zeros((W, H), bool)
+        occ2d[v // H, v % H] = True
+        out.append(pack_grid(occ2d))
+    return np.concatenate(out)
 
 
-def algorithmic_bytes(path_counts: np.ndarray) -> int:
-    # B = ceil(W*H/8) input bits + 8*P path list + 32 stats (no batching here)
-    n = len(path_counts)
-    return int(n * (W * H // 8) + 8 * int(path_counts.sum()) + 32 * n)
-
-
-def cpu_reference(occ: np.ndarray, count: int, solver: str = "redrec"):
-    """Times the compiled reference (oracle/_ref) on `count` grids with every host thread."""
-    from paper_2504_06182_b200.abi import ReconLib
-    ref = ReconLib(REF_LIB, "ref")
+def cpu_reference(ref, occ: np.ndarray, count: int):
+    """The compiled reference's bird + batch_moves on `count` C5 instances with
+    every host thread (std::thread pool, one instance per task)."""
     cores = os.cpu_count() or 1
     os.environ["RECON_REF_THREADS"] = str(cores)
-    wpc = (H + 63) // 64
-    sub = np.ascontiguousarray(occ[: count * W * wpc])
     t0 = time.perf_counter()
-    out = ref.grid_solve_batch(solver, sub, count, W, H, HP, host=True, with_events=False)
+    out = ref.pipeline_batch("bird", occ, count, W, H, HP, 0, MOVE_STRIDE)
     dt = time.perf_counter() - t0
-    assert (out["status"] == 0).all()
     return count / dt, cores, out
 
 
@@ -135,37 +158,42 @@ def run_reference(args):
     ws, rank, _ = dist_env()
     if ws > 1 and rank != 0:
         return
-    sample = args.ref_sample
-    occ = gen_inputs(0, sample)
+    from paper_2504_06182_b200.abi import ReconLib
+    ref = ReconLib(REF_LIB, "ref")
+    cores = os.cpu_count() or 1
+    sample = args.ref_sample or cores
+    occ = ref_inputs(ref.lib, 0, sample)
     vals = []
     for i in range(args.warmup + args.steps):
-        v, cores, _ = cpu_reference(occ, sample)
+        v, cores, _ = cpu_reference(ref, occ, sample)
         if i >= args.warmup:
             vals.append(v)
     v = statistics.median(vals)
     line = {
         "metric": METRIC, "value": v, "unit": "grids/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 * sample / v, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "impl": "reference",
-        "config": {"workload": f"red-rec {W}x{H} h'={HP} {ATOMS} atoms, batch of {sample} per step (bounded CPU sample)",
-                   "seeds": hex(SEED_BASE)},
-        "cpu_baseline": {"value": v, "unit": "grids/s", "cores": cores, "kind": "reference",
-                         "sample": f"{sample} grids per step, std::thread pool over all host threads"},
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic", "impl": "reference",
+        "config": {"workload": WORKLOAD, "batch_per_step": sample,
+                   "sample": f"the first {sample} instances of the GPU arm's chunk (bounded CPU sample)"},
+        "cpu_baseline": {"value": v, "unit": "grids/s", "cores": cores, "kind": "reference", "cpu": cpu_model(),
+                         "sample": f"{sample} C5 instances per step, bird + batch_moves of the compiled reference "
+                                   f"(oracle/_ref), std::thread pool over {cores} host threads"},
         "e2e": {"value": v, "unit": "grids/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def other_configs(lib, torch, dev, stream, reps=3):
-    """C2 (1M chains of 1024, band [256, 767]) and C3 (4096 bird 64x64 h'40 +
-    batching, preset none), each timed over `reps` runs after one warm-up."""
-    import ctypes as C
-    from paper_2504_06182_b200.abi import ChainBatch, GridBatch, PipelineBatch
-    from paper_2504_06182_b200.inputs import sample_chains, sample_grids
+# ---- extra configs (informative; the headline is C5) --------------------------------
 
-    def run(fn):
-        fn()
+def other_configs(lib, torch, dev, stream):
+    import ctypes as C
+    from paper_2504_06182_b200.abi import ChainBatch, GridBatch
+    from paper_2504_06182_b200.inputs import sample_chains, sample_grids
+    from paper_2504_06182_b200.pipeline import C3, C4, PipelineRunner
+
+    def timed(fn, reps=3, warm=1):
+        for _ in range(warm):
+            fn()
         ts = []
         for _ in range(reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -173,12 +201,48 @@ def other_configs(lib, torch, dev, stream, reps=3):
             st = fn()
             e1.record(stream)
             e1.synchronize()
-            if st != 0:
+            if st not in (None, 0):
                 raise RuntimeError(f"config run failed {st}: {lib.last_cuda_error()}")
             ts.append(e0.elapsed_time(e1))
         return statistics.median(ts)
 
     out = {}
+    # C4: red-rec on one 256x256 grid, one instance per launch (latency)
+    Wg = Hg = 256
+    lat = {}
+    for hp, seed in ((128, 256), (153, 257)):
+        o1 = torch.from_numpy(sample_grids(seed, 1, Wg, Hg, 39322).view(np.int64)).to(dev)
+        S = Wg * hp
+        bufs = [torch.empty(S, dtype=torch.int32, device=dev) for _ in range(2)]
+        i64 = torch.empty(1, dtype=torch.int64, device=dev)
+        i32 = torch.empty(3, dtype=torch.int32, device=dev)
+        g1 = GridBatch(o1.data_ptr(), 1, Wg, Hg, hp, bufs[0].data_ptr(), bufs[1].data_ptr(), None, i32.data_ptr(),
+                       i64.data_ptr(), i32.data_ptr() + 4, i32.data_ptr() + 8, None)
+        for solver, fn in (("redrec", lib.lib.recon_redrec_solve_batch), ("bird", lib.lib.recon_bird_solve_batch)):
+            lat[f"{solver}_h{hp}_seed{seed}_us"] = 1000.0 * timed(lambda: fn(lib.ctx(), C.byref(g1)), reps=5, warm=3)
+    out["c4_single_grid_latency"] = lat
+    # the 256x256 red-rec / bird batch (round 1's headline): 2,048 grids h'153
+    B = 2048
+    occ = torch.from_numpy(sample_grids(0x25600000, B, Wg, Hg, 39322).view(np.int64)).to(dev)
+    S = Wg * 153
+    src = torch.empty(B * S, dtype=torch.int32, device=dev)
+    dst = torch.empty_like(src)
+    i64 = torch.empty(B, dtype=torch.int64, device=dev)
+    i32 = torch.empty(3 * B, dtype=torch.int32, device=dev)
+    gb = GridBatch(occ.data_ptr(), B, Wg, Hg, 153, src.data_ptr(), dst.data_ptr(), None, i32.data_ptr(), i64.data_ptr(),
+                   i32.data_ptr() + 4 * B, i32.data_ptr() + 8 * B, None)
+    for solver, fn in (("redrec", lib.lib.recon_redrec_solve_batch), ("bird", lib.lib.recon_bird_solve_batch)):
+        ms = timed(lambda: fn(lib.ctx(), C.byref(gb)))
+        out[f"{solver}_256x256_h153_batch2048"] = {"ms": ms, "grids_per_s": B / ms * 1e3, "us_per_grid": ms * 1e3 / B}
+    del occ, src, dst
+    # C3: bird + batching on 4,096 64x64 grids; C4 red-rec + batching
+    for wl, n in ((C3, 4096), (C4, 64)):
+        r = PipelineRunner(lib, wl, n)
+        r.load(sample_grids(wl.seed_base, n, wl.W, wl.H, wl.atoms), n)
+        ms = timed(lambda: r.run(n, stats=False))
+        out[wl.name.split()[0].lower() + "_pipeline"] = {"instances": n, "ms": ms, "grids_per_s": n / ms * 1e3}
+        del r
+    # C2: 1M chains of 1024
     n, k, tl, th, cnt = 1024, 563, 256, 767, 1 << 20
     occ = torch.from_numpy(sample_chains(0x1D000000, cnt, n, k).view(np.int64)).to(dev)
     nt = th - tl + 1
@@ -188,41 +252,29 @@ def other_configs(lib, torch, dev, stream, reps=3):
     i32 = torch.empty(3 * cnt, dtype=torch.int32, device=dev)
     cb = ChainBatch(occ.data_ptr(), cnt, n, tl, th, src.data_ptr(), dst.data_ptr(), i64.data_ptr(), i32.data_ptr(),
                     i32.data_ptr() + 4 * cnt, i32.data_ptr() + 8 * cnt)
-    ms = run(lambda: lib.lib.recon_solve_1d_batch(lib.ctx(), C.byref(cb)))
+    ms = timed(lambda: lib.lib.recon_solve_1d_batch(lib.ctx(), C.byref(cb)))
     out["c2_1m_chains"] = {"ms": ms, "chains_per_s": cnt / ms * 1e3}
-    del occ, src, dst, i64, i32
-    W = H = 64
-    cnt = 4096
-    occ = torch.from_numpy(sample_grids(0x64000000, cnt, W, H, 2662).view(np.int64)).to(dev)
-    S, mst = W * 40, W * H * 12
-    src = torch.empty(cnt * S, dtype=torch.int32, device=dev)
-    dst = torch.empty_like(src)
-    td = torch.empty(cnt, dtype=torch.int64, device=dev)
-    i32 = torch.empty(4 * cnt, dtype=torch.int32, device=dev)
-    mb = torch.empty(cnt * mst, dtype=torch.int32, device=dev)
-    g = GridBatch(occ.data_ptr(), cnt, W, H, 40, src.data_ptr(), dst.data_ptr(), None, i32.data_ptr(), td.data_ptr(),
-                  i32.data_ptr() + 4 * cnt, i32.data_ptr() + 8 * cnt, None)
-    pb = PipelineBatch(g, 1, 0, mst, mb.data_ptr(), i32.data_ptr() + 12 * cnt)
-    ms = run(lambda: lib.lib.recon_pipeline_batch_run(lib.ctx(), C.byref(pb)))
-    out["c3_bird_batching_4096"] = {"ms": ms, "grids_per_s": cnt / ms * 1e3}
     return out
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=2048, help="grids per GPU per step")
+    ap.add_argument("--batch", type=int, default=1024, help="C5 instances per GPU per step (one HBM-resident chunk)")
+    ap.add_argument("--e2e-batch", type=int, default=256, help="instances per e2e host-API step")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--ref-sample", type=int, default=64)
+    ap.add_argument("--ref-sample", type=int, default=0, help="CPU sample (default: one instance per host thread)")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-configs", action="store_true", help="skip the C2 / C3 side measurements")
+    ap.add_argument("--no-extras", action="store_true", help="skip e2e and the other configs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args)
         return
+
+    import ctypes as C
 
     import torch
     import torch.distributed as dist
@@ -230,245 +282,201 @@ def main():
     ws, rank, local = dist_env()
     if ws > 1:
         # RECON_BENCH_BACKEND=gloo: functional runs with more ranks than GPUs
-        # (NCCL refuses two ranks on one device); timing values then mean nothing
         backend = os.environ.get("RECON_BENCH_BACKEND", "nccl" if torch.cuda.is_available() else "gloo")
         dist.init_process_group(backend)
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     from paper_2504_06182_b200 import load_native
-    from paper_2504_06182_b200.abi import GridBatch
-    import ctypes as C
+    from paper_2504_06182_b200.abi import STATS_DTYPE, GridBatch, PipelineBatch
+    from paper_2504_06182_b200.inputs import sample_grids
+    from paper_2504_06182_b200.pipeline import C5, PipelineRunner, algorithmic_bytes
 
     lib = load_native()
     lib.ctx(local)
-    stream_ptr = lib.lib.recon_ctx_stream(lib.ctx())
-    stream = torch.cuda.ExternalStream(stream_ptr)
-
-    B = args.batch
-    wpc = (H + 63) // 64
-    occ_h = gen_inputs(rank, B)
     dev = torch.device("cuda", local)
-    occ_d = torch.from_numpy(occ_h.view(np.int64)).to(dev)
-    stride = W * HP
-    bufs = {k: torch.empty(B * stride, dtype=torch.int32, device=dev) for k in ("src", "dst")}
-    pcount = torch.empty(B, dtype=torch.int32, device=dev)
-    tdisp = torch.empty(B, dtype=torch.int64, device=dev)
-    status = torch.empty(B, dtype=torch.int32, device=dev)
-    detail = torch.empty(B, dtype=torch.int32, device=dev)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
+    B = args.batch
+    first = rank * B
+    runner = PipelineRunner(lib, C5, B, device=local)
+    stream = runner.stream
+    occ_h = sample_grids(SEED_BASE + first, B, W, H, ATOMS)
+    runner.load(occ_h, B)
 
-    def batch_struct():
-        return GridBatch(occ_d.data_ptr(), B, W, H, HP, bufs["src"].data_ptr(), bufs["dst"].data_ptr(), None,
-                         pcount.data_ptr(), tdisp.data_ptr(), status.data_ptr(), detail.data_ptr(), None)
+    def step():
+        runner.run(B, stats=False)
 
-    gb = batch_struct()
-
-    def solve(fn):
-        st = fn(lib.ctx(), C.byref(gb))
-        if st != 0:
-            raise RuntimeError(f"solve failed {st}: {lib.last_cuda_error()}")
-
-    ktimes = []  # (planner ms, executor ms) per timed step, CUDA events on the context stream
-
-    def timed(fn, steps, warmup, kernels=False):
-        times = []
-        lib.set_kernel_timing(kernels)
-        for i in range(warmup + steps):
-            with torch.cuda.stream(stream):
-                flush.fill_(i)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            solve(fn)
-            e1.record(stream)
-            e1.synchronize()
-            if i >= warmup:
-                times.append(e0.elapsed_time(e1))
-                if kernels:
-                    ktimes.append(lib.kernel_times())
-        lib.set_kernel_timing(False)
-        return times
-
-    # warm-up + correctness status
-    solve(lib.lib.recon_redrec_solve_batch)
+    # warm-up (W untimed steps), then K timed steps bracketed by barrier + sync
+    for _ in range(args.warmup):
+        step()
     torch.cuda.synchronize()
-    assert int((status != 0).sum()) == 0, "solver statuses"
-
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = lib.launch_count()
+    times = []
     with Clocks(local) as clk:
-        times = timed(lib.lib.recon_redrec_solve_batch, args.steps, args.warmup)
-    launches = lib.launch_count() - launches0
-    # per-kernel breakdown in a separate pass: events between the planner and
-    # the executor serialise them (no programmatic dependent launch), so the
-    # headline above is timed without them
-    timed(lib.lib.recon_redrec_solve_batch, args.steps, args.warmup, kernels=True)
+        for _ in range(args.steps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
     torch.cuda.synchronize()
+    launches = lib.launch_count() - launches0  # every kernel of the library in the timed region
     if ws > 1:
         dist.barrier()
-    ms = sum(times) / len(times)
+    ms = statistics.mean(times)
     if ws > 1:
         t = torch.tensor([ms], device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    counts = pcount.cpu().numpy()
-    alg_bytes = algorithmic_bytes(counts)
-    hbm_peak, peak_kind = peaks()
-    plan_ms = sum(k[0] for k in ktimes) / len(ktimes)
-    exec_ms = sum(k[1] for k in ktimes) / len(ktimes)
-    achieved_gbs = alg_bytes / (exec_ms * 1e-3) / 1e9  # dominant kernel: the executor
-    traffic = warp_inst = None
+    value = ws * B / (ms * 1e-3)
+
+    # phase breakdown in separate steps (events between the phases)
+    lib.set_kernel_timing(True)
+    phases = []
+    for _ in range(2):
+        step()
+        ph = (C.c_float * 4)()
+        lib.lib.recon_ctx_phase_times(lib.ctx(), ph, 4)
+        phases.append(list(ph))
+    lib.set_kernel_timing(False)
+    ph = [statistics.mean(p[i] for p in phases) for i in range(4)]
+    solve_ms, dag_ms, wide_ms, warp_ms = ph
+
+    # the chunk's per-instance stats record (digest64), outside the timed region
+    runner.run(B, stats=True)
+    st = runner.stats(B)
+    ok = st["status"] == 0
+    alg = algorithmic_bytes(st, C5)
+    alg_solve = algorithmic_bytes(st, C5, batching=False)
+    alg_sched = alg - alg_solve
+    hbm, sm_max_mhz, peak_kind = peaks()
+    batch_ms = wide_ms + warp_ms
+    nb_mean = float(st["batch_count"][ok].mean()) if ok.any() else 0.0
+    clocks = clk.summary()
+    mhz = clocks.get("sm_mhz") or sm_max_mhz
+    traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            tr = json.load(f).get("redrec_kernel", {})
-        if tr.get("batch") == B and tr.get("workload_seed") == hex(SEED_BASE):
-            traffic = tr.get("dram_bytes")
-            warp_inst = tr.get("warp_inst")
-    value = ws * B / (ms * 1e-3)
-
-    # bird on the same grids (secondary)
-    bird_times = timed(lib.lib.recon_bird_solve_batch, max(2, args.steps // 2), 1)
-    bird_ms = sum(bird_times) / len(bird_times)
-
-    # e2e through the host-buffer C-ABI call (pinned host memory)
-    pin = {k: torch.empty(B * stride, dtype=torch.int32).pin_memory() for k in ("src", "dst")}
-    occ_pin = torch.from_numpy(occ_h.view(np.int64)).pin_memory()
-    h_cnt = torch.empty(B, dtype=torch.int32).pin_memory()
-    h_td = torch.empty(B, dtype=torch.int64).pin_memory()
-    h_st = torch.empty(B, dtype=torch.int32).pin_memory()
-    h_det = torch.empty(B, dtype=torch.int32).pin_memory()
-    hb = GridBatch(occ_pin.data_ptr(), B, W, H, HP, pin["src"].data_ptr(), pin["dst"].data_ptr(), None,
-                   h_cnt.data_ptr(), h_td.data_ptr(), h_st.data_ptr(), h_det.data_ptr(), None)
-    e2e = []
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        st = lib.lib.recon_redrec_solve_batch_host(lib.ctx(), C.byref(hb))
-        dt = time.perf_counter() - t0
-        assert st == 0
-        if i >= args.warmup:
-            e2e.append(dt)
-    e2e_s = statistics.median(e2e)
-    # the same call with the packed path list (src | dst << 16, 4 bytes per
-    # path over the host link instead of 8): the headline e2e
-    packed_pin = torch.empty(B * stride, dtype=torch.int32).pin_memory()
-    cnt_unpacked = h_cnt.clone()
-    hp_b = GridBatch(occ_pin.data_ptr(), B, W, H, HP, None, None, None,
-                     h_cnt.data_ptr(), h_td.data_ptr(), h_st.data_ptr(), h_det.data_ptr(), None)
-    e2e_p = []
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        st = lib.lib.recon_redrec_solve_batch_host_packed(lib.ctx(), C.byref(hp_b), packed_pin.data_ptr())
-        dt = time.perf_counter() - t0
-        assert st == 0
-        if i >= args.warmup:
-            e2e_p.append(dt)
-    # same paths as the unpacked call (first and last instance)
-    assert torch.equal(cnt_unpacked, h_cnt)
-    for i in (0, B - 1):
-        c0, n0 = i * stride, int(h_cnt[i])
-        pk = packed_pin[c0:c0 + n0]
-        assert torch.equal(pk & 0xFFFF, pin["src"][c0:c0 + n0]) and torch.equal((pk >> 16) & 0xFFFF, pin["dst"][c0:c0 + n0])
-    e2e_p_s = statistics.median(e2e_p)
-    # the host link's own device-to-host rate into pinned memory (the bound of
-    # the e2e call): one copy of the packed path lists' size, CUDA events
-    link = []
-    dsrc = bufs["src"].view(torch.int32)
-    for i in range(4):
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-            packed_pin.copy_(dsrc, non_blocking=True)
-            e1.record(stream)
-        e1.synchronize()
-        if i:
-            link.append(packed_pin.numel() * 4 / (e0.elapsed_time(e1) * 1e-3) / 1e9)
-    link_gbs = statistics.median(link)
+            tr = json.load(f).get("c5_batching", {})
+        if tr.get("batch") == B:
+            traffic = tr.get("dram_bytes_per_step")
+    digests = st["digest"]
+    job = {"instances": [first, first + B], "digest_sum": int(np.sum(digests, dtype=np.uint64)),
+           "statuses": {str(k): int(v) for k, v in zip(*np.unique(st["status"], return_counts=True))}}
     if ws > 1:
-        t = torch.tensor([e2e_s, e2e_p_s], device=dev if dist.get_backend() == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s, e2e_p_s = float(t[0].item()), float(t[1].item())
-    h2d = B * W * wpc * 8
-    d2h = B * stride * 4 * 2 + B * (4 + 8 + 4 + 4)
-    d2h_p = B * stride * 4 + B * (4 + 8 + 4 + 4)
+        parts = [None] * ws
+        dist.all_gather_object(parts, (first, digests.tolist(), st["status"].tolist()))
+        if rank == 0:
+            parts.sort()
+            alld = np.array([d for p in parts for d in p[1]], np.uint64)
+            job = {"instances": [0, ws * B], "digest_sum": int(np.sum(alld, dtype=np.uint64)),
+                   "statuses": {str(k): int(v) for k, v in
+                                zip(*np.unique(np.array([s for p in parts for s in p[2]]), return_counts=True))}}
 
-    # single-grid latency (C4: one instance per launch)
-    lat = {}
-    for hp, seed in ((128, 256), (153, 257)):
-        from paper_2504_06182_b200.inputs import sample_grids
-        o1 = torch.from_numpy(sample_grids(seed, 1, W, H, ATOMS).view(np.int64)).to(dev)
-        g1 = GridBatch(o1.data_ptr(), 1, W, H, hp, bufs["src"].data_ptr(), bufs["dst"].data_ptr(), None,
-                       pcount.data_ptr(), tdisp.data_ptr(), status.data_ptr(), detail.data_ptr(), None)
-        ts = []
-        for i in range(8):
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            assert lib.lib.recon_redrec_solve_batch(lib.ctx(), C.byref(g1)) == 0
-            e1.record(stream)
-            e1.synchronize()
-            if i >= 3:
-                ts.append(e0.elapsed_time(e1) * 1000.0)
-        lat[f"h{hp}_seed{seed}_us"] = statistics.median(ts)
-
-    # the other BASELINE configs at their own sizes (device-resident inputs,
-    # CUDA events on the context stream; informative, the headline is above)
+    # e2e: the host-buffer C-ABI call over pinned host memory, H2D + D2H inside
+    e2e = None
     others = None
-    if rank == 0 and ws == 1 and not args.no_configs:
-        others = other_configs(lib, torch, dev, stream)
+    if not args.no_extras:
+        E = min(args.e2e_batch, B)
+        S = W * HP
+        h_occ = torch.from_numpy(occ_h[: E * W * WPC].view(np.int64)).pin_memory()
+        h_src = torch.empty(E * S, dtype=torch.int32).pin_memory()
+        h_dst = torch.empty(E * S, dtype=torch.int32).pin_memory()
+        h_i32 = torch.empty(4 * E, dtype=torch.int32).pin_memory()
+        h_td = torch.empty(E, dtype=torch.int64).pin_memory()
+        h_mb = torch.empty(E * MOVE_STRIDE, dtype=torch.int32).pin_memory()
+        g = GridBatch(h_occ.data_ptr(), E, W, H, HP, h_src.data_ptr(), h_dst.data_ptr(), None, h_i32.data_ptr(),
+                      h_td.data_ptr(), h_i32.data_ptr() + 4 * E, h_i32.data_ptr() + 8 * E, None)
+        pb = PipelineBatch(g, 1, 0, MOVE_STRIDE, h_mb.data_ptr(), h_i32.data_ptr() + 12 * E)
+        ts = []
+        ke = max(2, min(args.steps, 3))
+        for i in range(1 + ke):
+            t0 = time.perf_counter()
+            r = lib.lib.recon_pipeline_batch_run_host(lib.ctx(), C.byref(pb))
+            dt = time.perf_counter() - t0
+            if r != 0:
+                raise RuntimeError(f"host pipeline failed {r}: {lib.last_cuda_error()}")
+            if i >= 1:
+                ts.append(dt)
+        e2e_s = statistics.median(ts)
+        # the host call returns the device path's results (first instances of the chunk)
+        assert np.array_equal(h_i32[E:2 * E].numpy(), st["status"][:E])
+        assert np.array_equal(h_td.numpy()[ok[:E]], st["total_displacement"][:E][ok[:E]])
+        d2h = int(E * S * 8 + E * 24 + 4 * int(h_td.numpy().clip(0).sum()))
+        if ws > 1:
+            t = torch.tensor([e2e_s], device=dev if dist.get_backend() == "nccl" else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": ws * E / e2e_s, "unit": "grids/s", "h2d_bytes_per_step": E * W * WPC * 8,
+               "d2h_bytes_per_step": d2h, "instances_per_step": E,
+               "call": "recon_pipeline_batch_run_host (pinned host buffers; paths + per-instance [0, D) of the "
+                       "batch schedule copied back, overlapped with the next sub-chunk)",
+               "achieved_d2h_gbs": d2h / e2e_s / 1e9}
+        del h_mb, h_src, h_dst
+        if rank == 0 and ws == 1:
+            del runner
+            torch.cuda.empty_cache()
+            others = other_configs(lib, torch, dev, stream)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        v, cores, _ = cpu_reference(occ_h, args.ref_sample)
-        cpu = {"value": v, "unit": "grids/s", "cores": cores, "kind": "reference",
-               "sample": f"first {args.ref_sample} grids of the batch, compiled reference red_rec "
-                         f"(oracle/_ref), std::thread pool over all host threads"}
-
-    # the executor is latency / issue bound, not HBM bound: its instruction
-    # issue rate against the SMs' peak (4 warp-instructions per SM per clock)
-    # says how close it runs to that ceiling
-    issue = None
-    clocks = clk.summary()
-    if warp_inst and clocks.get("sm_mhz"):
-        sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        peak_i = sms * 4 * clocks["sm_mhz"] * 1e6
-        ach_i = warp_inst / (exec_ms * 1e-3)
-        issue = {"warp_inst_per_launch": warp_inst, "achieved_ginst_s": ach_i / 1e9, "peak_ginst_s": peak_i / 1e9,
-                 "frac": ach_i / peak_i, "source": "ncu smsp__inst_executed.sum of the same launch (profiles/traffic.json)"}
+        from paper_2504_06182_b200.abi import ReconLib
+        ref = ReconLib(REF_LIB, "ref")
+        cores = os.cpu_count() or 1
+        sample = args.ref_sample or cores
+        v, cores, out = cpu_reference(ref, occ_h[: sample * W * WPC], sample)
+        # the reference's outputs on the sample equal the device's
+        assert np.array_equal(out["status"], st["status"][:sample])
+        assert np.array_equal(out["batch_count"][ok[:sample]], st["batch_count"][:sample][ok[:sample]])
+        cpu = {"value": v, "unit": "grids/s", "cores": cores, "kind": "reference", "cpu": cpu_model(),
+               "sample": f"first {sample} instances of the chunk, bird + batch_moves of the compiled reference "
+                         f"(oracle/_ref), std::thread pool over {cores} host threads; statuses and batch counts "
+                         f"equal the device's"}
 
     if rank == 0:
+        step_s = ms * 1e-3
         line = {
             "metric": METRIC, "value": value, "unit": "grids/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": f"red-rec {W}x{H} h'={HP}, {ATOMS} atoms (eps=0.6), batch {B} grids/GPU/step",
-                       "seeds": f"{hex(SEED_BASE)} + global index", "parallelism": f"instances sharded over {ws} GPU(s)",
-                       "l2": "flushed between steps (256 MiB write)"},
+            "config": {"workload": WORKLOAD, "batch_per_gpu_per_step": B,
+                       "step": "one HBM-resident chunk per GPU: recon_pipeline_batch_run (solve -> DAG -> batching)",
+                       "job": f"65,536 instances = {65536 // (ws * B)} steps at {ws} GPU(s)",
+                       "parallelism": f"instances sharded over {ws} GPU(s), no collective on the data path",
+                       "l2": "no flush: a chunk's inputs + outputs + workspace (~100 GB) dwarf the 126 MB L2"},
             "us_per_grid": ms * 1000.0 / B,
             "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved_gbs / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "rb::redrec_kernel (executor)", "kernel_ms": exec_ms,
-                         "algorithmic_bytes_per_launch": alg_bytes,
-                         "planner_kernel_ms": plan_ms, "issue": issue},
-            "e2e": {"value": ws * B / e2e_p_s, "unit": "grids/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h_p, "call": "recon_redrec_solve_batch_host_packed (pinned host buffers)",
-                    "path_format": "u32 src | dst << 16 per path",
-                    "link_d2h_gbs": link_gbs, "achieved_d2h_gbs": d2h_p / e2e_p_s / 1e9,
-                    "link_frac": d2h_p / e2e_p_s / 1e9 / link_gbs},
-            "e2e_unpacked": {"value": ws * B / e2e_s, "unit": "grids/s", "h2d_bytes_per_step": h2d,
-                             "d2h_bytes_per_step": d2h, "call": "recon_redrec_solve_batch_host (pinned host buffers)",
-                             "path_format": "i32 path_src[] + i32 path_dst[]"},
-            "bird": {"grids_per_s": ws * B / (bird_ms * 1e-3), "ms_per_step": bird_ms},
-            "latency_single_grid": lat,
-            "other_configs": others,
+            "phases_ms": {"solve": solve_ms, "dag": dag_ms, "batching_wide": wide_ms, "batching_warp": warp_ms},
+            "roofline": {
+                "bound": "hbm", "achieved": alg_sched / (batch_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                "frac": alg_sched / (batch_ms * 1e-3) / 1e9 / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                "kernel": "batching phase: rb::batch_wide_kernel + rb::batch_pipeline_kernel<16> (leap)",
+                "algorithmic_bytes_per_launch": alg_sched,
+                "algorithmic_bytes_rule": "4 B per elementary move of the batch schedule (SURVEY §8(d) 4*D)",
+                "kernel_ms": batch_ms,
+                "whole_step": {"algorithmic_bytes": alg, "achieved_gbs": alg / step_s / 1e9,
+                               "frac": alg / step_s / 1e9 / hbm,
+                               "rule": "ceil(W*H/8) + 8*P + 32 + 4*D per instance (SURVEY §8(d)), P/D the instances' own"},
+                "solve_phase": {"algorithmic_bytes": alg_solve, "ms": solve_ms,
+                                "achieved_gbs": alg_solve / (solve_ms * 1e-3) / 1e9,
+                                "frac": alg_solve / (solve_ms * 1e-3) / 1e9 / hbm},
+                "latency": {"batches_per_instance": nb_mean,
+                            "cycles_per_batch": batch_ms * 1e-3 * mhz * 1e6 / nb_mean if nb_mean else None,
+                            "note": "batching phase time x SM clock / mean batch count: every instance of the chunk "
+                                    "runs its dependent batch chain concurrently"}},
+            "stats": job,
             "clocks": clocks,
         }
+        if e2e:
+            line["e2e"] = e2e
         if cpu:
             line["cpu_baseline"] = cpu
+        if others:
+            line["other_configs"] = others
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()

@@ -123,6 +123,10 @@ int64_t recon_ctx_launch_count(recon_ctx *ctx);
    planner, ms[1] = red-rec executor or bird kernel (0 when not launched). */
 recon_status recon_ctx_set_kernel_timing(recon_ctx *ctx, int32_t enable);
 recon_status recon_ctx_kernel_times(recon_ctx *ctx, float *ms, int32_t n);
+/* With kernel timing on: the last device pipeline run's phases in ms (CUDA
+ * events on the context stream): [0] solve, [1] occupancy DAG + path records,
+ * [2] wide batching phase, [3] warp batching phase.  Zeros otherwise. */
+recon_status recon_ctx_phase_times(recon_ctx *ctx, float *ms, int32_t n);
 
 /* ------------------------------------------------------------------------- */
 /* Grid solvers (red-rec, bird): single instance, host buffers                */

@@ -2160,3 +2160,10 @@ recon_status recon_pipeline_stats(recon_ctx *ctx, const recon_pipeline_batch *pb
     (void)ctx;
     return recon_dg_stats(pb, stats);
 }
+
+/* no device phases on the CPU checker */
+recon_status recon_ctx_phase_times(recon_ctx *ctx, float *ms, int32_t n) {
+    (void)ctx;
+    for (int32_t i = 0; ms && i < n; ++i) ms[i] = 0.0f;
+    return RECON_OK;
+}

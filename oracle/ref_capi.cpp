@@ -882,3 +882,9 @@ extern "C" recon_status recon_sim_run_host(recon_ctx *, const recon_sim_batch *b
 extern "C" recon_status recon_pipeline_stats(recon_ctx *, const recon_pipeline_batch *pb, recon_instance_stats *stats) {
     return recon_dg_stats(pb, stats);
 }
+
+// no device phases on the CPU checker
+extern "C" recon_status recon_ctx_phase_times(recon_ctx *, float *ms, int32_t n) {
+    for (int32_t i = 0; ms && i < n; ++i) ms[i] = 0.0f;
+    return RECON_OK;
+}

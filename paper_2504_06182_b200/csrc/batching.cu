@@ -743,7 +743,7 @@ size_t pipeline_temp_bytes(int64_t n) {
     return t;
 }
 
-cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *counts_host) {
+cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *counts_host, int64_t *launches) {
     const int64_t S = (int64_t)a.W * a.k, WH = (int64_t)a.W * a.H, N = (int64_t)a.count * S;
     if (a.small_dag) {
         const int64_t smem = pipeline_small_dag_smem(a.W, a.H, a.k);
@@ -751,6 +751,7 @@ cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *
         cudaFuncSetAttribute(pl_dag_small_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const int grid = (int)std::min<int64_t>(a.count, 148 * 16);
         pl_dag_small_kernel<0><<<grid, 256, smem, st>>>(a);
+        *launches += 3;  // + two scans
         cudaMemsetAsync(a.inst_edges + a.count, 0, 8, st);
         cudaMemsetAsync(a.inst_moves + a.count, 0, 8, st);
         size_t tb = a.temp_bytes;
@@ -773,6 +774,7 @@ cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *
     cudaMemsetAsync(a.fill, 0, (size_t)N * 4, st);
     const int blocks = 148 * 8;
     pl_mark2_kernel<<<blocks, 256, 0, st>>>(a, mc, mr);
+    *launches += 5;  // mark, walk, widen, two scans
     pl_walk_warp_kernel<0><<<blocks, 256, 0, st>>>(a, (const int2 *)mc, (const int2 *)mr);
     // soff = exclusive scan of the out-degrees (rule 1 + rule 2); mbase = exclusive scan of lengths
     sum2_widen_kernel<<<blocks, 256, 0, st>>>(N, a.outdeg, a.mfr, a.soff);
@@ -1879,7 +1881,7 @@ __global__ void __launch_bounds__(256, (MODE & 2) ? 4 : 1) batch_pipeline_kernel
     }
 }
 
-cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t st) {
+cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t st, cudaEvent_t *pev, int64_t *launches) {
     const int64_t S = (int64_t)a.W * a.k, N = (int64_t)a.count * S, nwb = ((int64_t)a.W * a.H + 31) / 32;
     const int blocks = 148 * 8;
     if (a.small_dag) {
@@ -1891,9 +1893,11 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
     }
     if (a.prec) prec_kernel<<<blocks, 256, 0, st>>>(a);
     occ_to_vertex_bits<<<blocks, 256, 0, st>>>(a.count, a.W, a.H, a.grid_occ, a.occ);
+    *launches += a.prec ? 3 : 2;  // dag fill (+ path records) + bitmap
     cudaMemsetAsync(a.inb, 0, (size_t)a.count * nwb * 4, st);
     cudaMemsetAsync(a.counter, 0, (size_t)a.count * 4, st);
     (void)N;
+    if (pev) cudaEventRecord(pev[2], st);
     if (a.wide) {
         // wide phase first: the batches whose ready set exceeds a warp
         int rmax = 0, hbits = 0;
@@ -1908,6 +1912,7 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
             cudaMemsetAsync(a.vmin, 0x7f, (size_t)a.count * a.W * a.H * 4, st);
             cudaError_t e = launch_batch_wide(a, sms, rmax, hbits, wsmem, st);
             if (e != cudaSuccess) return e;
+            *launches += 1;
         } else {
             cudaMemsetAsync(a.wstate, 0, (size_t)a.count * 32, st);
         }
@@ -1960,7 +1965,10 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
                                : batch_pipeline_kernel<7>;
     if (smem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int grid = (int)std::min<int64_t>(((int64_t)a.count + warps - 1) / warps, (int64_t)sms * 32);
+    if (pev) cudaEventRecord(pev[3], st);
     kern<<<grid, warps * 32, smem, st>>>(a);
+    *launches += 1;
+    if (pev) cudaEventRecord(pev[4], st);
     return cudaGetLastError();
 }
 

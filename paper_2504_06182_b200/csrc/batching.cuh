@@ -97,8 +97,9 @@ struct PipelineArgs {
 
 size_t pipeline_temp_bytes(int64_t n);
 // counts_host[0] = DAG edges, counts_host[1] = elementary moves (all instances)
-cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *counts_host);
-cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t st);
+cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *counts_host, int64_t *launches);
+// pev (may be null): events [2] after the DAG, [3] after the wide phase, [4] after batching
+cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t st, cudaEvent_t *pev, int64_t *launches);
 // shared memory of the per-instance DAG builder, or 0 when an instance does not fit
 int64_t pipeline_small_dag_smem(int W, int H, int k);
 

@@ -167,8 +167,23 @@ recon_status recon_ctx_set_kernel_timing(recon_ctx *ctx, int32_t enable) {
             cudaError_t err = cudaEventCreate(&e);
             if (err != cudaSuccess) return cuda_fail(err, "cudaEventCreate", nullptr);
         }
+        for (auto &e : c->pev) {
+            cudaError_t err = cudaEventCreate(&e);
+            if (err != cudaSuccess) return cuda_fail(err, "cudaEventCreate", nullptr);
+        }
     }
     c->timing = enable != 0;
+    return RECON_OK;
+}
+
+recon_status recon_ctx_phase_times(recon_ctx *ctx, float *ms, int32_t n) {
+    Ctx *c = resolve(ctx);
+    if (!c || !ms) return RECON_ERR_ARGUMENT;
+    for (int32_t i = 0; i < n; ++i) ms[i] = 0.0f;
+    if (!c->pev[0] || !c->timed_pipeline) return RECON_OK;
+    cudaError_t e = cudaEventSynchronize(c->pev[4]);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize", nullptr);
+    for (int32_t i = 0; i < n && i < 4; ++i) cudaEventElapsedTime(&ms[i], c->pev[i], c->pev[i + 1]);
     return RECON_OK;
 }
 

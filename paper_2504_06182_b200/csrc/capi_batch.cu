@@ -25,7 +25,7 @@ __global__ void copy_i32(int64_t n, const int32_t *a, int32_t *b) {
         b[i] = a[i];
 }
 
-recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool host) {
+recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb) {
     int32_t *detail = nullptr;
     if (!pb) return RECON_ERR_ARGUMENT;
     const recon_grid_batch *b = &pb->grid;
@@ -36,27 +36,19 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool 
     Ctx *c = resolve(ctx);
     if (!c) return RECON_ERR_CUDA;
     CK(cudaSetDevice(c->device), "cudaSetDevice");
-    // 1. solve on device (host variant stages through the context)
+    // 1. solve on device
     recon_grid_batch g = *b;
     const size_t n = (size_t)b->count, S = (size_t)b->width * b->h_prime, WH = (size_t)b->width * b->height;
-    const int wpc = (b->height + 63) / 64;
-    std::vector<int32_t> h_status;
-    if (host) {
-        g.occ = c->dev<uint64_t>(S_OCC, n * b->width * wpc);
-        g.path_src = c->dev<int32_t>(S_PSRC, n * S);
-        g.path_dst = c->dev<int32_t>(S_PDST, n * S);
-        g.path_event = b->path_event ? c->dev<int32_t>(S_PEV, n * S) : nullptr;
-        g.path_count = c->dev<int32_t>(S_PCNT, n);
-        g.total_displacement = c->dev<int64_t>(S_TDISP, n);
-        g.status = c->dev<int32_t>(S_STATUS, n);
-        g.detail = c->dev<int32_t>(S_DETAIL, n);
-        g.events = nullptr;
-        if (!g.occ || !g.path_src || !g.path_dst || !g.path_count || !g.total_displacement || !g.status || !g.detail)
-            return cuda_fail(cudaErrorMemoryAllocation, "pipeline workspace", detail);
-        CK(cudaMemcpyAsync((void *)g.occ, b->occ, n * b->width * wpc * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
-    }
+    cudaEvent_t *pev = (c->timing && c->pev[0]) ? c->pev : nullptr;
+    c->timed_pipeline = pev != nullptr;
+    if (pev) cudaEventRecord(pev[0], c->stream);
+    // (a timed pipeline keeps the solve's own planner/executor events off)
+    const bool kt = c->timing;
+    if (pev) c->timing = false;
     recon_status st = pb->solver == 1 ? recon_bird_solve_batch(ctx, &g) : recon_redrec_solve_batch(ctx, &g);
+    c->timing = kt;
     if (st != RECON_OK) return st;
+    if (pev) cudaEventRecord(pev[1], c->stream);
     // 2. DAG + batching scratch
     PipelineArgs a{};
     a.count = b->count;
@@ -107,12 +99,11 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool 
     int64_t *i64 = c->dev<int64_t>(S_BM_AUX1, (n * S + 1) * 2 + 4 * (n + 1) + 4);
     uint32_t *bits = c->dev<uint32_t>(S_BM_AUX2, n * nwb * 2 + 4);
     int4 *rec = c->dev<int4>(S_BM_AUX7, n * S * 2 + 4);
-    int32_t *mb = host ? c->dev<int32_t>(S_BM_OUT, n * (size_t)pb->move_stride) : pb->move_batch;
-    int32_t *bc = host ? c->dev<int32_t>(S_BM_AUX4, n * 3) : pb->batch_count;
-    int32_t *bst = host ? bc + n : g.status;  // batching status (device variant reuses solve status)
-    int32_t *bdet = host ? bc + 2 * n : g.detail;
-    if (!i32 || !i64 || !bits || !rec || !mb || !bc) return cuda_fail(cudaErrorMemoryAllocation, "pipeline", detail);
-    if (host) CK(cudaMemsetAsync(mb, 0xff, n * (size_t)pb->move_stride * 4, c->stream), "memset");
+    int32_t *mb = pb->move_batch;
+    int32_t *bc = pb->batch_count;
+    int32_t *bst = g.status;  // batching status (overwrites the solve status)
+    int32_t *bdet = g.detail;
+    if (!i32 || !i64 || !bits || !rec) return cuda_fail(cudaErrorMemoryAllocation, "pipeline", detail);
     a.source_of = maps ? i32 : nullptr;  // int2 maps (batching.cu pl_mark2_kernel)
     a.target_of = nullptr;
     int32_t *q = i32 + maps;
@@ -144,8 +135,7 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool 
     a.temp = c->get(S_TEMP, a.temp_bytes);
     if (!a.temp) return cuda_fail(cudaErrorMemoryAllocation, "pipeline temp", detail);
     int64_t counts[2] = {0, 0};
-    CK(pipeline_dag_count(a, c->stream, counts), "pipeline dag");
-    c->launches += 5;
+    CK(pipeline_dag_count(a, c->stream, counts, &c->launches), "pipeline dag");
     const int64_t edges = counts[0];
     a.succ = c->dev<int32_t>(S_BM_AUX5, (size_t)edges + 1);
     a.edge_capacity = edges;
@@ -165,20 +155,129 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, bool 
         a.mlog = c->dev<int2>(S_BM_AUX6, (size_t)counts[1] + 1);
         if (!a.mlog) return cuda_fail(cudaErrorMemoryAllocation, "pipeline move log", detail);
     }
-    CK(pipeline_run_batching(a, c->sms, c->stream), "pipeline batching");
-    c->launches += 3;
-    if (!host) return RECON_OK;
-    CK(cudaMemcpyAsync(b->path_src, g.path_src, n * S * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    CK(cudaMemcpyAsync(b->path_dst, g.path_dst, n * S * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    if (b->path_event)
-        CK(cudaMemcpyAsync(b->path_event, g.path_event, n * S * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    CK(cudaMemcpyAsync(b->path_count, g.path_count, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    CK(cudaMemcpyAsync(b->total_displacement, g.total_displacement, n * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    CK(cudaMemcpyAsync(b->status, bst, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    if (b->detail) CK(cudaMemcpyAsync(b->detail, bdet, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    CK(cudaMemcpyAsync(pb->batch_count, bc, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    CK(cudaMemcpyAsync(pb->move_batch, mb, n * (size_t)pb->move_stride * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    CK(cudaStreamSynchronize(c->stream), "pipeline");
+    CK(pipeline_run_batching(a, c->sms, c->stream, pev, &c->launches), "pipeline batching");
+    return RECON_OK;
+}
+
+// Host buffers: the instances go through the device pipeline in sub-chunks
+// sized to free HBM.  Each sub-chunk's outputs sit in one of
+// two device slots; its device-to-host copies (per instance only the used
+// [0, D) of the schedule) run on the copy stream while the next sub-chunk is
+// solved and batched on the context stream.
+recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *pb) {
+    int32_t *detail = nullptr;
+    if (!pb) return RECON_ERR_ARGUMENT;
+    const recon_grid_batch *b = &pb->grid;
+    if (!b->occ || !b->path_src || !b->path_dst || !b->path_count || !b->total_displacement || !b->status ||
+        !pb->move_batch || !pb->batch_count)
+        return RECON_ERR_ARGUMENT;
+    if (b->count <= 0) return RECON_OK;
+    Ctx *c = resolve(ctx);
+    if (!c) return RECON_ERR_CUDA;
+    CK(cudaSetDevice(c->device), "cudaSetDevice");
+    if (!c->copy_stream) CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "copy stream");
+    cudaStream_t cs = c->copy_stream;
+    const size_t S = (size_t)b->width * b->h_prime, WH = (size_t)b->width * b->height;
+    const int wpc = (b->height + 63) / 64;
+    const size_t occ_words = (size_t)b->width * wpc;
+    // sub-chunk: what free memory holds (two output slots + the pipeline
+    // workspace, ~48 successor edges per path); RECON_PIPE_HOST_CHUNK forces
+    const size_t per = 2 * (occ_words * 8 + 8 * S + 32 + (size_t)pb->move_stride * 4) +
+                       (16 * WH + 36 * S + 16 * S + 32 * S + 16 * S + WH / 4 + 4 * WH + 192 * S);
+    static const int env_chunk = [] {
+        const char *e = getenv("RECON_PIPE_HOST_CHUNK");
+        return e ? atoi(e) : 0;
+    }();
+    size_t sub = env_chunk > 0 ? (size_t)env_chunk : 0;
+    if (!sub) {
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
+        sub = std::max<size_t>(1, (size_t)(0.8 * (double)fr) / per);
+        // two sub-chunks at least, so that copies overlap the next solve
+        if ((size_t)b->count > 1) sub = std::min(sub, ((size_t)b->count + 1) / 2);
+    }
+    sub = std::min(sub, (size_t)b->count);
+    // the two device output slots
+    struct Slot {
+        uint64_t *occ;
+        int32_t *src, *dst, *ev, *i32, *mb;
+        int64_t *i64;
+        cudaEvent_t done = nullptr;  // its copies are finished
+    } sl[2];
+    for (int k = 0; k < 2; ++k) {
+        sl[k].occ = c->dev<uint64_t>(S_PH_OCC0 + k, sub * occ_words);
+        sl[k].src = c->dev<int32_t>(S_PH_SRC0 + k, sub * S);
+        sl[k].dst = c->dev<int32_t>(S_PH_DST0 + k, sub * S);
+        sl[k].ev = b->path_event ? c->dev<int32_t>(S_PH_EV0 + k, sub * S) : nullptr;
+        sl[k].i32 = c->dev<int32_t>(S_PH_I32_0 + k, sub * 4);  // path_count | status | detail | batch_count
+        sl[k].i64 = c->dev<int64_t>(S_PH_I64_0 + k, sub);
+        sl[k].mb = c->dev<int32_t>(S_PH_MB0 + k, sub * (size_t)pb->move_stride);
+        if (!sl[k].occ || !sl[k].src || !sl[k].dst || (b->path_event && !sl[k].ev) || !sl[k].i32 || !sl[k].i64 ||
+            !sl[k].mb)
+            return cuda_fail(cudaErrorMemoryAllocation, "pipeline host slots", detail);
+    }
+    std::vector<int64_t> hD(sub);
+    // on any failure after copies were issued: drain both streams before returning
+    auto fail = [&](recon_status st) {
+        cudaStreamSynchronize(cs);
+        cudaStreamSynchronize(c->stream);
+        return st;
+    };
+#define CKF(call, where)                                                         \
+    do {                                                                         \
+        cudaError_t e_ = (call);                                                 \
+        if (e_ != cudaSuccess) return fail(cuda_fail(e_, where, detail));        \
+    } while (0)
+    int k = 0;
+    for (size_t j0 = 0; j0 < (size_t)b->count; j0 += sub, k ^= 1) {
+        const size_t n = std::min(sub, (size_t)b->count - j0);
+        Slot &o = sl[k];
+        if (o.done) CKF(cudaStreamWaitEvent(c->stream, o.done, 0), "wait slot");
+        CKF(cudaMemcpyAsync(o.occ, b->occ + j0 * occ_words, n * occ_words * 8, cudaMemcpyHostToDevice, c->stream),
+            "H2D");
+        recon_pipeline_batch d = *pb;
+        d.grid.occ = o.occ;
+        d.grid.count = (int32_t)n;
+        d.grid.path_src = o.src;
+        d.grid.path_dst = o.dst;
+        d.grid.path_event = o.ev;
+        d.grid.path_count = o.i32;
+        d.grid.status = o.i32 + n;
+        d.grid.detail = o.i32 + 2 * n;
+        d.grid.total_displacement = o.i64;
+        d.grid.events = nullptr;
+        d.batch_count = o.i32 + 3 * n;
+        d.move_batch = o.mb;
+        const recon_status st = pipeline_impl(ctx, &d);
+        if (st != RECON_OK) return fail(st);
+        // every instance's displacement, then only [0, D) of its schedule
+        CKF(cudaMemcpyAsync(hD.data(), o.i64, n * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        CKF(cudaStreamSynchronize(c->stream), "pipeline sub-chunk");
+        cudaEvent_t solved = c->chunk_event();
+        if (!solved) return fail(cuda_fail(cudaErrorUnknown, "event", detail));
+        CKF(cudaEventRecord(solved, c->stream), "event");
+        CKF(cudaStreamWaitEvent(cs, solved, 0), "wait");
+        CKF(cudaMemcpyAsync(b->path_src + j0 * S, o.src, n * S * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        CKF(cudaMemcpyAsync(b->path_dst + j0 * S, o.dst, n * S * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        if (b->path_event) CKF(cudaMemcpyAsync(b->path_event + j0 * S, o.ev, n * S * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        CKF(cudaMemcpyAsync(b->path_count + j0, o.i32, n * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        CKF(cudaMemcpyAsync(b->status + j0, o.i32 + n, n * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        if (b->detail) CKF(cudaMemcpyAsync(b->detail + j0, o.i32 + 2 * n, n * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        CKF(cudaMemcpyAsync(pb->batch_count + j0, o.i32 + 3 * n, n * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        CKF(cudaMemcpyAsync(b->total_displacement + j0, o.i64, n * 8, cudaMemcpyDeviceToHost, cs), "D2H");
+        for (size_t i = 0; i < n; ++i) {
+            const int64_t D = std::min<int64_t>(std::max<int64_t>(hD[i], 0), pb->move_stride);
+            if (D > 0)
+                CKF(cudaMemcpyAsync(pb->move_batch + (j0 + i) * (size_t)pb->move_stride,
+                                    o.mb + i * (size_t)pb->move_stride, (size_t)D * 4, cudaMemcpyDeviceToHost, cs),
+                    "D2H");
+        }
+        o.done = c->chunk_event();
+        if (!o.done) return fail(cuda_fail(cudaErrorUnknown, "event", detail));
+        CKF(cudaEventRecord(o.done, cs), "event");
+    }
+#undef CKF
+    CK(cudaStreamSynchronize(cs), "pipeline copies");
     return RECON_OK;
 }
 
@@ -324,11 +423,11 @@ recon_status recon_batch_moves(recon_ctx *ctx, int32_t width, int32_t height, co
 }
 
 recon_status recon_pipeline_batch_run(recon_ctx *ctx, const recon_pipeline_batch *pb) {
-    return pipeline_impl(ctx, pb, false);
+    return pipeline_impl(ctx, pb);
 }
 
 recon_status recon_pipeline_batch_run_host(recon_ctx *ctx, const recon_pipeline_batch *pb) {
-    return pipeline_impl(ctx, pb, true);
+    return pipeline_host_chunked(ctx, pb);
 }
 
 }  // extern "C"

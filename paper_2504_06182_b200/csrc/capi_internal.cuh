@@ -30,6 +30,8 @@ enum Slot {
     S_SIM_OCC, S_SIM_CUR, S_SIM_NXT, S_SIM_CYC, S_SIM_ST, S_SIM_SUC, S_SIM_ACC, S_SIM_EL, S_SIM_LIVE, S_SIM_CODE,
     S_SIM_CEL, S_SIM_PDEC, S_SIM_SRC, S_SIM_DST, S_SIM_PC, S_SIM_PST, S_SIM_DET, S_SIM_NB, S_SIM_TD, S_SIM_OFF,
     S_SIM_MB, S_SIM_BCNT, S_SIM_RUN, S_SIM_ALLC, S_PPACK, S_BM_WSTATE, S_BM_VMIN, S_BM_PREC,
+    S_PH_OCC0, S_PH_OCC1, S_PH_SRC0, S_PH_SRC1, S_PH_DST0, S_PH_DST1, S_PH_EV0, S_PH_EV1, S_PH_I32_0, S_PH_I32_1,
+    S_PH_I64_0, S_PH_I64_1, S_PH_MB0, S_PH_MB1,
     S_NSLOTS
 };
 
@@ -41,6 +43,8 @@ struct Ctx {
     bool timing = false;          // recon_ctx_set_kernel_timing
     bool timed_plan = false;      // the last timed solve launched the planner
     cudaEvent_t tev[3] = {};      // before planner, before executor, after executor
+    cudaEvent_t pev[5] = {};      // pipeline phases: solve | dag | wide | batching (recon_ctx_phase_times)
+    bool timed_pipeline = false;
     cudaStream_t copy_stream = nullptr;  // device-to-host copies overlapping the next chunk's solve
     cudaEvent_t cev[64] = {};            // chunk-done events (reused round robin)
     int cev_next = 0;
