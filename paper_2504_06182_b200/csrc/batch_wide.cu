@@ -37,11 +37,14 @@
 
 namespace rb {
 
+// phase cycle counters of the wide kernel (experiments: -DRECON_BATCH_PROF)
+__device__ unsigned long long g_wide_prof[8];
+
 namespace {
 
 constexpr int WT = 512;  // threads per CTA
 constexpr int NW = WT / 32;
-constexpr int G = 8;  // successor edges per thread in flight
+constexpr int G = 4;  // chunks of 32 successor ids per warp in flight
 constexpr int32_t VMIN_EMPTY = 0x7f7f7f7f;  // memset(0x7f) of the per-vertex min array
 
 __device__ __forceinline__ int vtx(int H, int k, int xs, int ys, int xt, int yt) {
@@ -156,7 +159,6 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
         }
         const int64_t o = (int64_t)inst * S;
         const int P = a.path_count[inst];
-        const int32_t *src = a.path_src + o, *dst = a.path_dst + o;
         const int64_t *mbase = a.mbase + o, *soff = a.soff + o;
         const int64_t mb0 = mbase[0], e0 = soff[0];
         const int64_t moves = mbase[P] - mb0;
@@ -166,6 +168,7 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
         }
         int32_t *blk = a.indeg + o;
         int32_t *mb = a.move_batch + (int64_t)inst * a.move_stride;
+        const int4 *prec = a.prec + (int64_t)inst * (S + 1);  // path records (batching.cu prec_kernel)
         int4 *stg = a.rec2 + o;  // hand-off staging (and overflow past rmax)
         int32_t *stb = a.rb2 + o;
         const int32_t *succ = a.succ + e0;
@@ -184,16 +187,15 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
         long long myleft = 0;
         int zero_len = 0;
         for (int p = tid; p < P; p += WT) {
-            const int s = src[p], t = dst[p];
-            const int xs = s / H, ys = s - xs * H, xt = t / H, yt = t - xt * H;
-            const int len = abs(xt - xs) + abs(yt - ys);
+            const int4 r = prec[p];
+            const int len = abs((r.y & 0xffff) - (r.x & 0xffff)) + abs((r.y >> 16) - (r.x >> 16));
             myleft += len;
             if (len == 0) {
                 zero_len = 1;  // zero-length paths: the warp kernel's init releases them
             } else if (blk[p] == 0) {
                 const int i = atomicAdd(&s_cnt[1], 1);  // [1]: batch 0 appends to [0]
-                wide_put(bufs(0), i, rmax, stg, stb, make_int4(p, len << 16, xs | (ys << 16), xt | (yt << 16)),
-                         (int)(mbase[p] - mb0), (int)(soff[p] - e0), (int)(soff[p + 1] - soff[p]), &s_ovf);
+                wide_put(bufs(0), i, rmax, stg, stb, make_int4(p, len << 16, r.x, r.y), r.z, r.w, prec[p + 1].w - r.w,
+                         &s_ovf);
             }
         }
         if (zero_len) s_ovf = 1;
@@ -210,6 +212,17 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
             continue;
         }
         int cur = 0, nb = 0, status = RECON_OK;
+#ifdef RECON_BATCH_PROF
+        long long wp[4] = {0, 0, 0, 0}, wt = clock64();
+#define WPROF(i)                          \
+    do {                                  \
+        const long long t_ = clock64();   \
+        wp[i] += t_ - wt;                 \
+        wt = t_;                          \
+    } while (0)
+#else
+#define WPROF(i) (void)0
+#endif
         for (;;) {
             const int par = nb & 1;
             const WideBufs A = bufs(cur), B = bufs(cur ^ 1);
@@ -240,6 +253,7 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
                 eflag[e] = f;
             }
             __syncthreads();
+            WPROF(0);
             if (tid == 0) {  // next batch's counters (their last readers passed the barrier above)
                 s_cnt[par ^ 1] = 0;
                 s_nacc[par ^ 1] = 0;
@@ -280,15 +294,17 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
             // batch index, finished paths to the release list, live paths to
             // the next list
             int nacc = 0;
-            for (int e = tid; e < R; e += WT) {
-                const unsigned char f = eflag[e];
-                int4 r = A.rec[e];
-                bool won = false;
+            for (int e0 = 0; e0 < R; e0 += WT) {  // (warp-uniform trip count: the appends are warp-aggregated)
+                const int e = e0 + tid;
+                const bool valid = e < R;
+                const unsigned char f = valid ? eflag[e] : 0;
+                int4 r = valid ? A.rec[e] : make_int4(0, 0, 0, 0);
+                bool fin = false;
                 if (f & F_CAND) {
                     if (eslot[e] >= 0) hash[eslot[e]] = 0u;
                     const int fr = vtx(H, r.y & 0xffff, r.z & 0xffff, r.z >> 16, r.w & 0xffff, r.w >> 16);
                     const int to = vtx(H, (r.y & 0xffff) + 1, r.z & 0xffff, r.z >> 16, r.w & 0xffff, r.w >> 16);
-                    won = contend ? (f & F_WON) != 0 : true;
+                    bool won = contend ? (f & F_WON) != 0 : true;
                     if (won && a.preset != 0) won = compatible_w(a.preset, H, fr, to, s_ff, s_ft);
                     if (won) {
                         atomicXor(&occ[fr >> 5], 1u << (fr & 31));
@@ -297,20 +313,31 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
                         __stcs(mb + A.base[e] + k, nb);
                         r.y = (k + 1) | (len << 16);
                         ++nacc;
-                        if (k + 1 == len) {
-                            const int i = atomicAdd(&s_nf[par], 1);
-                            fq0[i] = A.q0[e];
-                            fqn[i] = A.qn[e];
-                            continue;
-                        }
+                        fin = k + 1 == len;
+                        // one move left: its successor list into L2 for the release
+                        if (k + 2 == len) prefetch_l2(succ + A.q0[e], A.qn[e] * 4);
                     }
                 }
-                const int i = atomicAdd(&s_cnt[par], 1);
-                wide_put(B, i, rmax, stg, stb, r, A.base[e], A.q0[e], A.qn[e], &s_ovf);
+                const bool live = valid && !fin;
+                const unsigned lm = __ballot_sync(FULL, live), fm = __ballot_sync(FULL, fin);
+                int lb = 0, fb = 0;
+                if (lane == 0) {
+                    if (lm) lb = atomicAdd(&s_cnt[par], __popc(lm));
+                    if (fm) fb = atomicAdd(&s_nf[par], __popc(fm));
+                }
+                lb = __shfl_sync(FULL, lb, 0);
+                fb = __shfl_sync(FULL, fb, 0);
+                if (live) wide_put(B, lb + __popc(lm & lanemask_lt()), rmax, stg, stb, r, A.base[e], A.q0[e], A.qn[e], &s_ovf);
+                if (fin) {
+                    const int i = fb + __popc(fm & lanemask_lt());
+                    fq0[i] = A.q0[e];
+                    fqn[i] = A.qn[e];
+                }
             }
             nacc = warp_sum(nacc);
             if (lane == 0 && nacc) atomicAdd(&s_nacc[par], nacc);
             __syncthreads();
+            WPROF(1);
             const int nacc_all = s_nacc[par];
             if (nacc_all == 0) {
                 status = RECON_ERR_INPUT;  // batching.cpp:127-128
@@ -319,48 +346,61 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
             left -= nacc_all;
             ++nb;
             // ---- 3. release (for the next batch): warp w takes finished paths
-            // w, w + NW, ... (lane l the l-th of them), its lanes walk their
-            // concatenated successor lists, loads first, then decrements; a
-            // released path joins the next list
+            // w, w + NW, ...; its lanes load 32 successor ids of one finished
+            // path at a time into G register slots, then decrement them all;
+            // a released path joins the next list from its path record
             const int nf = s_nf[par];
-            for (int g0 = 0; g0 < nf; g0 += 32 * NW) {
-                const int fi = g0 + warp + NW * lane;
-                const int myq0 = fi < nf ? fq0[fi] : 0, myqn = fi < nf ? fqn[fi] : 0;
-                int tot;
-                const int bse = warp_excl_scan(myqn, &tot);
-                for (int t0 = 0; t0 < tot; t0 += 32 * G) {
-                    int sc[G];
+            {
+                int sc[G];
+                int nsl = 0;  // filled slots (warp-uniform)
+                auto flush = [&]() {
+                    bool rel[G];
+                    int4 pr[G];
+                    int qe[G];
 #pragma unroll
                     for (int c = 0; c < G; ++c) {
-                        const int t = t0 + c * 32 + lane;
-                        int owner = 0;  // largest lane with bse <= t
-#pragma unroll
-                        for (int stp = 16; stp > 0; stp >>= 1) {
-                            const int cl = owner + stp;
-                            if (__shfl_sync(FULL, bse, cl) <= t) owner = cl;
+                        rel[c] = false;
+                        if (c < nsl && sc[c] >= 0) {
+                            pr[c] = __ldg(prec + sc[c]);
+                            qe[c] = __ldg(&prec[sc[c] + 1].w);
+                            rel[c] = atomicSub(&blk[sc[c]], 1) == 1;
                         }
-                        const int oq0 = __shfl_sync(FULL, myq0, owner), ob = __shfl_sync(FULL, bse, owner);
-                        sc[c] = t < tot ? __ldg(succ + oq0 + (t - ob)) : -1;
                     }
 #pragma unroll
                     for (int c = 0; c < G; ++c) {
-                        if (sc[c] < 0 || atomicSub(&blk[sc[c]], 1) != 1) continue;
-                        const int p = sc[c];
-                        const int s = src[p], t = dst[p];
-                        const int64_t mbp = mbase[p], s0 = soff[p], s1 = soff[p + 1];
-                        const int xs = s / H, ys = s - xs * H, xt = t / H, yt = t - xt * H;
-                        const int len = abs(xt - xs) + abs(yt - ys);
+                        if (!rel[c]) continue;
+                        const int len = abs((pr[c].y & 0xffff) - (pr[c].x & 0xffff)) + abs((pr[c].y >> 16) - (pr[c].x >> 16));
                         const int i = atomicAdd(&s_cnt[par], 1);
-                        wide_put(B, i, rmax, stg, stb, make_int4(p, len << 16, xs | (ys << 16), xt | (yt << 16)),
-                                 (int)(mbp - mb0), (int)(s0 - e0), (int)(s1 - s0), &s_ovf);
+                        wide_put(B, i, rmax, stg, stb,
+                                 make_int4(sc[c], len << 16, pr[c].x, pr[c].y), pr[c].z, pr[c].w, qe[c] - pr[c].w, &s_ovf);
+                    }
+                    nsl = 0;
+                };
+                for (int f = warp; f < nf; f += NW) {
+                    const int fq = fq0[f], fn = fqn[f];
+                    for (int j0 = 0; j0 < fn; j0 += 32) {
+                        const int v = j0 + lane < fn ? __ldg(succ + fq + j0 + lane) : -1;
+#pragma unroll
+                        for (int c = 0; c < G; ++c)
+                            if (c == nsl) sc[c] = v;
+                        if (++nsl == G) flush();
                     }
                 }
+                if (nsl) flush();
             }
             __syncthreads();
+            WPROF(2);
             R = s_cnt[par];
             cur ^= 1;
             if (left == 0 || R <= 32 || s_ovf) break;
         }
+#ifdef RECON_BATCH_PROF
+        if (tid == 0) {
+            for (int i = 0; i < 3; ++i) atomicAdd(&g_wide_prof[i], (unsigned long long)wp[i]);
+            atomicAdd(&g_wide_prof[3], (unsigned long long)nb);
+            atomicAdd(&g_wide_prof[4], 1ull);
+        }
+#endif
         // ---- hand-off to the warp kernel, or the instance's result
         if (status == RECON_OK && left > 0) {
             // the ready set as records ranked by id into the warp kernel's
@@ -429,3 +469,13 @@ cudaError_t launch_batch_wide(const PipelineArgs &a, int sms, int rmax, int hbit
 }
 
 }  // namespace rb
+
+// experiments: the wide kernel's phase counters (zero unless built with -DRECON_BATCH_PROF)
+extern "C" int recon_debug_wide_prof(unsigned long long *out, int reset) {
+    if (cudaMemcpyFromSymbol(out, rb::g_wide_prof, sizeof(rb::g_wide_prof)) != cudaSuccess) return -1;
+    if (reset) {
+        static const unsigned long long z[8] = {};
+        if (cudaMemcpyToSymbol(rb::g_wide_prof, z, sizeof(z)) != cudaSuccess) return -1;
+    }
+    return 0;
+}

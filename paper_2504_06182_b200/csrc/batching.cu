@@ -470,6 +470,14 @@ __global__ void occ_to_vertex_bits(int count, int W, int H, const uint64_t *occ,
     }
 }
 
+// packed coordinates x | y << 16 (path records)
+__device__ __forceinline__ bool on_path2p(int ps, int pt, int x, int y) {
+    const int xs = ps & 0xffff, ys = ps >> 16, xt = pt & 0xffff, yt = pt >> 16;
+    if (y == ys && x >= min(xs, xt) && x <= max(xs, xt)) return true;
+    if (x == xt && y >= min(ys, yt) && y <= max(ys, yt)) return true;
+    return false;
+}
+
 __device__ __forceinline__ bool on_path2(int H, int32_t s, int32_t t, int32_t v) {
     const int xs = s / H, ys = s % H, xt = t / H, yt = t % H, x = v / H, y = v % H;
     if (y == ys && x >= min(xs, xt) && x <= max(xs, xt)) return true;
@@ -497,6 +505,8 @@ __global__ void pl_mark2_kernel(PipelineArgs a, int32_t *mc, int32_t *mr) {
         const int s = a.path_src[t], d = a.path_dst[t];
         const int xs = s / a.H, ys = s - xs * a.H, xd = d / a.H, yd = d - xd * a.H;
         int32_t *c = mc + inst * WH * 2, *r = mr + inst * WH * 2;
+        int2 *pc = reinterpret_cast<int2 *>(a.prec + inst * (S + 1) + p);  // {xs|ys<<16, xd|yd<<16} (prec .x/.y)
+        *pc = make_int2(xs | (ys << 16), xd | (yd << 16));
         c[2 * (int64_t)s] = p;
         c[2 * (int64_t)d + 1] = p;
         r[2 * ((int64_t)ys * a.W + xs)] = p;
@@ -510,6 +520,7 @@ __global__ void __launch_bounds__(256) pl_walk_warp_kernel(PipelineArgs a, const
     const int W = a.W, H = a.H;
     const int64_t S = (int64_t)W * a.k, WH = (int64_t)W * H, N = (int64_t)a.count * S;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    unsigned long long *fillp = reinterpret_cast<unsigned long long *>(a.rec);  // PASS 1: next free slot per path
     for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp_id(); t < N; t += nwarps) {
         const int64_t inst = t / S, o = inst * S;
         const int i = (int)(t - o);
@@ -520,9 +531,9 @@ __global__ void __launch_bounds__(256) pl_walk_warp_kernel(PipelineArgs a, const
             }
             continue;
         }
-        const int32_t *src = a.path_src + o, *dst = a.path_dst + o;
-        const int s = src[i], d = dst[i];
-        const int xs = s / H, ys = s - xs * H, xt = d / H, yt = d - xt * H;
+        const int4 *pc = a.prec + inst * (S + 1);  // packed coordinates in .x / .y
+        const int2 me = *reinterpret_cast<const int2 *>(pc + i);
+        const int xs = me.x & 0xffff, ys = me.x >> 16, xt = me.y & 0xffff, yt = me.y >> 16;
         const int dx = abs(xt - xs), len = dx + abs(yt - ys), sx = xt > xs ? 1 : -1, sy = yt > ys ? 1 : -1;
         const int2 *mci = mc + inst * WH, *mri = mr + inst * WH;
         int in1 = 0, out2 = 0;
@@ -533,14 +544,17 @@ __global__ void __launch_bounds__(256) pl_walk_warp_kernel(PipelineArgs a, const
             if (j <= len) m = j <= dx ? mri[(int64_t)ys * W + xs + sx * j] : mci[(int64_t)xt * H + ys + sy * (j - dx)];
             const bool r1 = m.x >= 0 && m.x != i;  // (m.x, i): i crosses source(m.x)
             bool r2 = m.y >= 0 && m.y != i;        // (i, m.y): i crosses target(m.y) ...
-            if (r2) r2 = !on_path2(H, src[m.y], dst[m.y], s);  // ... unless rule 1 already gives it
+            if (r2) {                              // ... unless rule 1 already gives it
+                const int2 q = *reinterpret_cast<const int2 *>(pc + m.y);
+                r2 = !on_path2p(q.x, q.y, xs, ys);
+            }
             if (PASS == 0) {
                 if (r1) atomicAdd(&a.outdeg[o + m.x], 1);
                 if (r2) atomicAdd(&a.indeg[o + m.y], 1);
                 in1 += r1;
                 out2 += r2;
             } else {
-                if (r1) a.succ[a.soff[o + m.x] + a.mfr[o + m.x] + atomicAdd(&a.fill[o + m.x], 1)] = i;
+                if (r1) a.succ[atomicAdd(&fillp[o + m.x], 1ull)] = i;
                 const unsigned b2 = __ballot_sync(FULL, r2);
                 if (r2) a.succ[my_off + out2 + __popc(b2 & lanemask_lt())] = m.y;
                 out2 += __popc(b2);
@@ -558,8 +572,16 @@ __global__ void __launch_bounds__(256) pl_walk_warp_kernel(PipelineArgs a, const
     }
 }
 
-// per-path records for leap mode: {src, dst, move base, successor offset},
-// relative to the instance; entry P closes the last path's ranges
+// rule-1 fill pointers: path i's rule-1 successors start after its rule-2 ones
+__global__ void fillptr_kernel(int64_t n, const int64_t *soff, const int32_t *out2, unsigned long long *fp) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        fp[i] = (unsigned long long)(soff[i] + out2[i]);
+}
+
+// per-path records for the batching kernels: {xs | ys << 16, xt | yt << 16,
+// move base, successor offset} relative to the instance (coordinates already
+// split, so no division by H on the release path); entry P closes the last
+// path's ranges
 __global__ void prec_kernel(PipelineArgs a) {
     const int64_t S = (int64_t)a.W * a.k, S1 = S + 1;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)a.count * S1;
@@ -570,8 +592,14 @@ __global__ void prec_kernel(PipelineArgs a) {
         if (p > P) continue;
         const int64_t o = inst * S;
         const int64_t e0 = a.soff[o], m0 = a.mbase[o];
-        a.prec[t] = make_int4(p < P ? a.path_src[o + p] : 0, p < P ? a.path_dst[o + p] : 0,
-                              (int)(a.mbase[o + p] - m0), (int)(a.soff[o + p] - e0));
+        int ps = 0, pd = 0;
+        if (p < P) {
+            const int s = a.path_src[o + p], d = a.path_dst[o + p];
+            const int xs = s / a.H, xd = d / a.H;
+            ps = xs | ((s - xs * a.H) << 16);
+            pd = xd | ((d - xd * a.H) << 16);
+        }
+        a.prec[t] = make_int4(ps, pd, (int)(a.mbase[o + p] - m0), (int)(a.soff[o + p] - e0));
     }
 }
 
@@ -771,10 +799,9 @@ cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *
     cudaMemsetAsync(mc, 0xff, (size_t)a.count * WH * 16, st);
     cudaMemsetAsync(a.outdeg, 0, (size_t)N * 4, st);
     cudaMemsetAsync(a.indeg, 0, (size_t)N * 4, st);
-    cudaMemsetAsync(a.fill, 0, (size_t)N * 4, st);
     const int blocks = 148 * 8;
     pl_mark2_kernel<<<blocks, 256, 0, st>>>(a, mc, mr);
-    *launches += 5;  // mark, walk, widen, two scans
+    *launches += 6;  // mark, walk, widen, two scans, fill pointers
     pl_walk_warp_kernel<0><<<blocks, 256, 0, st>>>(a, (const int2 *)mc, (const int2 *)mr);
     // soff = exclusive scan of the out-degrees (rule 1 + rule 2); mbase = exclusive scan of lengths
     sum2_widen_kernel<<<blocks, 256, 0, st>>>(N, a.outdeg, a.mfr, a.soff);
@@ -784,6 +811,7 @@ cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *
     cudaMemsetAsync(a.mbase + N, 0, 8, st);
     tb = a.temp_bytes;
     cub::DeviceScan::ExclusiveSum(a.temp, tb, a.mbase, a.mbase, (int)(N + 1), st);
+    fillptr_kernel<<<blocks, 256, 0, st>>>(N, a.soff, a.mfr, reinterpret_cast<unsigned long long *>(a.rec));
     cudaError_t e = cudaMemcpyAsync(counts_host, a.soff + N, 8, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) return e;
     e = cudaMemcpyAsync(counts_host + 1, a.mbase + N, 8, cudaMemcpyDeviceToHost, st);
@@ -1052,7 +1080,7 @@ __device__ __forceinline__ int release_successors_buf(const BatchJob &J, const B
 
 // Leap-mode finish: the finished lanes' successors are released as in
 // release_successors_buf, and every successor's path record
-// {src, dst, move base, successor offset} (prec, built with the dag) is loaded
+// {source, target coordinates, move base, successor offset} (prec) is loaded
 // together with its blocker decrement, so a released path needs no further
 // round trip: it goes straight into an empty lane (lanes are not kept in id
 // order in leap mode).  Released ids also go to `buf` for the rare spill.
@@ -1106,14 +1134,13 @@ __device__ __forceinline__ int release_into_lanes(const BatchJob &J, const BL &b
                                      __shfl_sync(FULL, pr[c].z, srcl), __shfl_sync(FULL, pr[c].w, srcl));
             const int e = __shfl_sync(FULL, qe[c], srcl);
             if (take) {
-                const int H = J.H;
                 took = true;
                 lp.p = np;
                 lp.k = 0;
-                lp.xs = r.x / H;
-                lp.ys = r.x - lp.xs * H;
-                lp.xt = r.y / H;
-                lp.yt = r.y - lp.xt * H;
+                lp.xs = r.x & 0xffff;
+                lp.ys = r.x >> 16;
+                lp.xt = r.y & 0xffff;
+                lp.yt = r.y >> 16;
                 lp.len = abs(lp.xt - lp.xs) + abs(lp.yt - lp.ys);
                 lp.base = r.z;
                 lp.q0 = J.e0 + r.w;
@@ -1416,6 +1443,8 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
                 // batches nb .. nb+delta-1 move every mover one vertex each
                 // (frozen lanes stay put)
                 const bool valid = (movers >> lane) & 1u;
+                // lanes finishing with this leap: successor lists into L2 now
+                if (valid && lp.len - lp.k == delta) prefetch_l2(J.succ + lp.q0, (int)(lp.q1 - lp.q0) * 4);
                 const unsigned vm = movers;
                 for (unsigned m = vm; m; m &= m - 1) {
                     const int o = __ffs(m) - 1;

@@ -31,7 +31,7 @@ struct BatchJob {
     int P, W, H, preset, edge_level;
     const int64_t *soff;  // [P+1] successor CSR offsets (global edge index)
     const int32_t *succ;
-    const int4 *prec;     // pipeline: [P+1] {src, dst, move base, soff - e0} per path
+    const int4 *prec;     // pipeline: [P+1] {xs|ys<<16, xt|yt<<16, move base, soff - e0} per path
     int64_t e0;           // pipeline: soff[0]
     const int64_t *in_off;  // edge-level only: incoming CSR
     const int32_t *in_src;
@@ -87,7 +87,7 @@ struct PipelineArgs {
     // their exclusive scans over instances, [count + 1] each
     int small_dag;
     int4 *rec, *rec2;    // [count * W*k] ready-path records (batch_warp_pipe)
-    int4 *prec;          // [count * (W*k + 1)] path records {src, dst, move base, soff} (leap mode)
+    int4 *prec;          // [count * (W*k + 1)] path records {xs|ys<<16, xt|yt<<16, move base, soff} (leap / wide)
     int32_t *rb, *rb2;   // [count * W*k] their move bases
     int64_t *inst_edges, *inst_moves, *ebase, *mvbase;
     const uint64_t *grid_occ;            // [count * W * wpc] initial occupancy (occ bits)

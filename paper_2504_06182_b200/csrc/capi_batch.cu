@@ -76,11 +76,10 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb) {
         return e ? atoi(e) : -1;
     }();
     a.wide = wide_env >= 0 ? wide_env : (S >= 16384 ? 1 : 0);
-    a.prec = nullptr;
-    if (a.leap) {
-        a.prec = c->dev<int4>(S_BM_PREC, n * (S + 1));
-        if (!a.prec) return cuda_fail(cudaErrorMemoryAllocation, "pipeline prec", detail);
-    }
+    // path records (packed coordinates, move base, successor offset): the DAG
+    // walk, the wide phase and leap mode read them
+    a.prec = c->dev<int4>(S_BM_PREC, n * (S + 1));
+    if (!a.prec) return cuda_fail(cudaErrorMemoryAllocation, "pipeline prec", detail);
     if (a.wide) {
         a.wstate = c->dev<int64_t>(S_BM_WSTATE, n * 4);
         a.vmin = c->dev<int32_t>(S_BM_VMIN, n * WH);

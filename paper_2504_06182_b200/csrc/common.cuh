@@ -36,6 +36,12 @@ __device__ __forceinline__ int warp_excl_scan(int v, int *total) {
     return x - v;
 }
 
+// pulls [p, p + bytes) into L2 ahead of use (no register result, never stalls)
+__device__ __forceinline__ void prefetch_l2(const void *p, int bytes) {
+    const char *c = static_cast<const char *>(p);
+    for (int o = 0; o < bytes; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(c + o));
+}
+
 __device__ __forceinline__ int warp_sum(int v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);

@@ -26,12 +26,16 @@ n = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 solver, W, H, hp, k, seed, preset, ms = CASES[name]
 occ = sample_grids(seed, n, W, H, k)
 buf = (C.c_ulonglong * 16)()
+wbuf = (C.c_ulonglong * 8)()
 gpu.lib.recon_debug_batch_prof(buf, 1)
+gpu.lib.recon_debug_wide_prof(wbuf, 1)
 t = time.time()
 g = gpu.pipeline_batch(solver, occ, n, W, H, hp, preset, ms)
 dt = time.time() - t
 gpu.lib.recon_debug_batch_prof(buf, 1)
+gpu.lib.recon_debug_wide_prof(wbuf, 1)
 v = list(buf)
+wv = list(wbuf)
 names = ["leap_delta", "leap_apply", "literal", "finish", "general", "n_leap", "n_literal", "n_general", "n_finish",
          "total"]
 out = {names[i]: v[i] for i in range(10)}
@@ -41,4 +45,8 @@ print("counts per instance:", {k2: out[k2] / n for k2 in names[5:9]})
 for a, b in (("leap_delta", "n_leap"), ("literal", "n_literal"), ("general", "n_general"), ("finish", "n_finish")):
     if out[b]:
         print(f"  {a}: {out[a] / max(1, out[b] if a != 'leap_delta' else out['n_leap'] + out['n_literal']):.0f} cycles per")
+if wv[4]:
+    nbw = wv[3]
+    print(f"wide: {wv[4]} instances, {nbw / wv[4]:.0f} batches each; cycles per batch: "
+          f"candidates {wv[0] / nbw:.0f}, apply {wv[1] / nbw:.0f}, release {wv[2] / nbw:.0f}")
 print("batch_count", g["batch_count"][:4], "status", np.unique(g["status"]))
