@@ -15,9 +15,12 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "build")
+# RECON_BUILD_TAG=checked: a separate object dir and library (the checked
+# build of tools/checked_run.sh); the product library is untouched
+TAG = os.environ.get("RECON_BUILD_TAG", "")
+OBJ = os.path.join(PKG, "build" + (f"_{TAG}" if TAG else ""))
 LIB_DIR = os.path.join(PKG, "lib")
-LIB = os.path.join(LIB_DIR, "librecon_b200.so")
+LIB = os.path.join(LIB_DIR, f"librecon_b200{'_' + TAG if TAG else ''}.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC]

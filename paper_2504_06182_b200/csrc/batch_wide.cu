@@ -235,7 +235,8 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
                 if (!((occ[to >> 5] >> (to & 31)) & 1u)) {
                     f = F_CAND;
                     unsigned h = hslot(to, hbits);
-                    for (;;) {
+                    for (int probes = 0;; ++probes) {
+                        RB_CHECK(probes < hsize, "wide: claim table full");
                         const uint32_t old = atomicCAS(&hash[h], 0u, (uint32_t)to + 1u);
                         if (old == 0u) {
                             slot = (int)h;
@@ -330,6 +331,7 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
                 if (live) wide_put(B, lb + __popc(lm & lanemask_lt()), rmax, stg, stb, r, A.base[e], A.q0[e], A.qn[e], &s_ovf);
                 if (fin) {
                     const int i = fb + __popc(fm & lanemask_lt());
+                    RB_CHECK(i < rmax, "wide: finished list overflow");
                     fq0[i] = A.q0[e];
                     fqn[i] = A.qn[e];
                 }
@@ -390,6 +392,7 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
             }
             __syncthreads();
             WPROF(2);
+            RB_CHECK(s_cnt[par] <= S, "wide: ready list larger than the path count");
             R = s_cnt[par];
             cur ^= 1;
             if (left == 0 || R <= 32 || s_ovf) break;

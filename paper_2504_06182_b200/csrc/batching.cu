@@ -1124,6 +1124,7 @@ __device__ __forceinline__ int release_into_lanes(const BatchJob &J, const BL &b
             if (c >= nsl) break;
             const unsigned rm = __ballot_sync(FULL, rel[c]);
             if (!rm) continue;
+            RB_CHECK(buf != sm || nnew + __popc(rm) <= cap, "released ids overflow the shared buffer");
             if (rel[c]) buf[nnew + __popc(rm & lanemask_lt())] = sc[c];
             // the empty lane of rank e takes released item e - nnew of this chunk
             const int j = erank - nnew;
@@ -1445,6 +1446,25 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
                 const bool valid = (movers >> lane) & 1u;
                 // lanes finishing with this leap: successor lists into L2 now
                 if (valid && lp.len - lp.k == delta) prefetch_l2(J.succ + lp.q0, (int)(lp.q1 - lp.q0) * 4);
+#ifdef RECON_CHECKED
+                // the leap invariant: no token outside the movers blocks a
+                // mover's next `delta` vertices (frozen tokens are fixed
+                // obstacles, stationary ones cannot lie on a route)
+                for (unsigned m = movers; m; m &= m - 1) {
+                    const int o = __ffs(m) - 1;
+                    LanePath q = shfl_lane(lp, o, false);
+                    for (int t0 = 0; t0 < delta; t0 += 32) {
+                        const int t = t0 + lane;
+                        const int32_t v = t < delta ? q.v(H, q.k + t + 1) : -1;
+                        bool mover_token = false;  // a mover's current vertex: it leaves at offset 0
+                        for (unsigned mm = movers; mm; mm &= mm - 1) {
+                            const int32_t c = __shfl_sync(FULL, fr, __ffs(mm) - 1);
+                            mover_token |= c == v && t >= 1;
+                        }
+                        RB_CHECK(v < 0 || !occ.get(v) || mover_token, "leap: a stationary token blocks a mover");
+                    }
+                }
+#endif
                 const unsigned vm = movers;
                 for (unsigned m = vm; m; m &= m - 1) {
                     const int o = __ffs(m) - 1;

@@ -6,11 +6,28 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include "recon_b200.h"
 
 namespace rb {
+
+// Device-side invariant checks of the checked build (-DRECON_CHECKED,
+// tools/checked_run.sh): a failed check prints and traps, so the launch
+// fails loudly.  They compile to nothing in the product build.
+#ifdef RECON_CHECKED
+#define RB_CHECK(cond, what)                                                                          \
+    do {                                                                                              \
+        if (!(cond)) {                                                                                \
+            printf("RB_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__,       \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                \
+            __trap();                                                                                 \
+        }                                                                                             \
+    } while (0)
+#else
+#define RB_CHECK(cond, what) (void)0
+#endif
 
 constexpr unsigned FULL = 0xffffffffu;
 

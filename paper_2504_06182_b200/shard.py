@@ -1,14 +1,15 @@
 """Multi-GPU sharding of independent instances.
 
-Instances are independent pure functions of their seed, so a batch is split
-into contiguous per-rank ranges and every rank solves its range on its own
-GPU; there is no collective on the data path.  torch.distributed only
-carries the final host gather of per-instance results (digests + stats) and
-the max-over-ranks timing.
+Instances are independent pure functions of their seed, so a job is split
+into contiguous per-rank ranges [g*N/G, (g+1)*N/G) and every rank runs its
+range on its own GPU, chunk by chunk (pipeline.PipelineRunner); there is no
+collective on the data path.  torch.distributed only carries the final host
+gather of the per-instance stats records (status, P, D, batch count,
+digest64 — computed on the device by recon_pipeline_stats) and the
+max-over-ranks timing.  The gathered records are identical for every GPU
+count (tests/test_shard_gpu.py, tests/test_shard_gloo.py).
 """
 from __future__ import annotations
-
-import hashlib
 
 import numpy as np
 
@@ -18,31 +19,30 @@ def shard_range(count: int, world: int, rank: int) -> tuple[int, int]:
     return count * rank // world, count * (rank + 1) // world
 
 
-def instance_digests(out: dict, count: int, stride: int) -> np.ndarray:
-    """64-bit digest of each instance's canonical path list (+ status)."""
-    d = np.zeros(count, np.uint64)
-    for i in range(count):
-        c = int(out["path_count"][i])
-        h = hashlib.blake2b(digest_size=8)
-        h.update(np.int32(out["status"][i]).tobytes())
-        h.update(out["path_src"][i * stride:i * stride + c].tobytes())
-        h.update(out["path_dst"][i * stride:i * stride + c].tobytes())
-        d[i] = np.frombuffer(h.digest(), np.uint64)[0]
-    return d
+def run_shard(lib, wl, count: int, world: int, rank: int, chunk: int = 1024, device: int = 0):
+    """This rank's shard of the workload's first `count` instances on the
+    product library (GPU): returns (start, stats records)."""
+    from .pipeline import PipelineRunner
+    s, e = shard_range(count, world, rank)
+    r = PipelineRunner(lib, wl, max(1, min(chunk, e - s)), device=device)
+    return s, r.run_range(s, e - s)
 
 
-def solve_shard(lib, solver: str, seed_base: int, count: int, W: int, H: int, hp: int, k: int,
-                world: int, rank: int):
-    """Solves this rank's shard of `count` seeded instances; returns (start, digests, total displacement)."""
+def run_shard_host(lib, wl, count: int, world: int, rank: int):
+    """The same through a host-memory library (the CPU checkers): the
+    pipeline via recon_pipeline_batch_run_host, the records via
+    recon_pipeline_stats over the host outputs."""
     from .inputs import sample_grids
     s, e = shard_range(count, world, rank)
-    occ = sample_grids(seed_base + s, e - s, W, H, k)
-    out = lib.grid_solve_batch(solver, occ, e - s, W, H, hp, host=True, with_events=False)
-    return s, instance_digests(out, e - s, W * hp), out["total_displacement"].copy()
+    n = e - s
+    occ = sample_grids(wl.seed_base + s, n, wl.W, wl.H, wl.atoms)
+    out = lib.pipeline_batch(wl.solver, occ, n, wl.W, wl.H, wl.h_prime, wl.preset, wl.move_stride)
+    return s, lib.pipeline_stats_host(out, n, wl.W, wl.h_prime, wl.move_stride)
 
 
 def gather_to_rank0(dist, arr: np.ndarray, count: int, start: int):
-    """Host gather (gloo or nccl object gather) of per-instance arrays, concatenated in instance order."""
+    """Host gather (gloo or nccl object gather) of per-instance arrays,
+    concatenated in instance order on rank 0 (None elsewhere)."""
     parts = [None] * dist.get_world_size()
     dist.all_gather_object(parts, (start, arr))
     if dist.get_rank() != 0:
