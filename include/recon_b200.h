@@ -220,7 +220,7 @@ recon_status recon_bird_solve_batch_host(recon_ctx *ctx, const recon_grid_batch 
  * otherwise); batch->path_src / path_dst are not used and may be NULL.  The
  * device-to-host copy of the path lists bounds the host call (8 bytes per
  * path over the host link), and this halves it.  Same paths, same order:
- * the reference-side shim widens them back into Path (redrec.hpp:67). */
+ * a caller decodes src = v & 0xffff, dst = v >> 16. */
 recon_status recon_redrec_solve_batch_host_packed(recon_ctx *ctx, const recon_grid_batch *batch,
                                                   uint32_t *path_packed);
 recon_status recon_bird_solve_batch_host_packed(recon_ctx *ctx, const recon_grid_batch *batch,

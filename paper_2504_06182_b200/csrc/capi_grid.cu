@@ -270,9 +270,22 @@ recon_status grid_batch(int solver, recon_ctx *ctx, const recon_grid_batch *b, b
     const size_t chunk_max = std::max<size_t>(wave, (n + 7) / 8);
     size_t chunk = std::min<size_t>(std::max(c->sms, 1), chunk_max);
     cudaStream_t cs = c->copy_stream;
+    // any failure after the first copy: drain both streams before returning, so
+    // no device-to-host copy of an earlier chunk is still writing into the
+    // caller's buffers when the call returns
+    auto drain = [&](recon_status st) {
+        cudaStreamSynchronize(cs);
+        cudaStreamSynchronize(c->stream);
+        return st;
+    };
+#define CKD(call, where)                                                          \
+    do {                                                                          \
+        cudaError_t e_ = (call);                                                  \
+        if (e_ != cudaSuccess) return drain(cuda_fail(e_, where, detail));        \
+    } while (0)
     for (size_t i0 = 0, m = 0; i0 < n; i0 += m, chunk = std::min(chunk * 2, chunk_max)) {
         m = std::min(chunk, n - i0);
-        CK(cudaMemcpyAsync(d_occ + i0 * words, b->occ + i0 * words, m * words * 8, cudaMemcpyHostToDevice, c->stream),
+        CKD(cudaMemcpyAsync(d_occ + i0 * words, b->occ + i0 * words, m * words * 8, cudaMemcpyHostToDevice, c->stream),
            "occ H2D");
         GridParams q = p;
         q.count = (int)m;
@@ -292,35 +305,36 @@ recon_status grid_batch(int solver, recon_ctx *ctx, const recon_grid_batch *b, b
         q.status = p.status + i0;
         q.detail = p.detail + i0;
         q.events = p.events ? p.events + i0 * b->width * per : nullptr;
-        CK(launch(c, solver, q, grid_blocks(c, solver, sq, (int)m)), "grid kernel launch");
+        CKD(launch(c, solver, q, grid_blocks(c, solver, sq, (int)m)), "grid kernel launch");
         if (packed) {
             pack_paths_kernel<<<c->sms * 8, 256, 0, c->stream>>>(q.path_src, q.path_dst, d_pack + i0 * stride, m * stride);
             ++c->launches;
-            CK(cudaGetLastError(), "pack kernel launch");
+            CKD(cudaGetLastError(), "pack kernel launch");
         }
         cudaEvent_t ev = c->chunk_event();
-        if (!ev) return cuda_fail(cudaErrorMemoryAllocation, "chunk event", detail);
-        CK(cudaEventRecord(ev, c->stream), "event");
-        CK(cudaStreamWaitEvent(cs, ev, 0), "wait");
+        if (!ev) return drain(cuda_fail(cudaErrorMemoryAllocation, "chunk event", detail));
+        CKD(cudaEventRecord(ev, c->stream), "event");
+        CKD(cudaStreamWaitEvent(cs, ev, 0), "wait");
         if (packed) {
-            CK(cudaMemcpyAsync(packed + i0 * stride, d_pack + i0 * stride, m * stride * 4, cudaMemcpyDeviceToHost, cs),
+            CKD(cudaMemcpyAsync(packed + i0 * stride, d_pack + i0 * stride, m * stride * 4, cudaMemcpyDeviceToHost, cs),
                "D2H");
         } else {
-            CK(cudaMemcpyAsync(b->path_src + i0 * stride, q.path_src, m * stride * 4, cudaMemcpyDeviceToHost, cs), "D2H");
-            CK(cudaMemcpyAsync(b->path_dst + i0 * stride, q.path_dst, m * stride * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+            CKD(cudaMemcpyAsync(b->path_src + i0 * stride, q.path_src, m * stride * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+            CKD(cudaMemcpyAsync(b->path_dst + i0 * stride, q.path_dst, m * stride * 4, cudaMemcpyDeviceToHost, cs), "D2H");
         }
         if (b->path_event)
-            CK(cudaMemcpyAsync(b->path_event + i0 * stride, q.path_event, m * stride * 4, cudaMemcpyDeviceToHost, cs),
+            CKD(cudaMemcpyAsync(b->path_event + i0 * stride, q.path_event, m * stride * 4, cudaMemcpyDeviceToHost, cs),
                "D2H");
-        CK(cudaMemcpyAsync(b->path_count + i0, q.path_count, m * 4, cudaMemcpyDeviceToHost, cs), "D2H");
-        CK(cudaMemcpyAsync(b->total_displacement + i0, q.total_displacement, m * 8, cudaMemcpyDeviceToHost, cs), "D2H");
-        CK(cudaMemcpyAsync(b->status + i0, q.status, m * 4, cudaMemcpyDeviceToHost, cs), "D2H");
-        if (b->detail) CK(cudaMemcpyAsync(b->detail + i0, q.detail, m * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        CKD(cudaMemcpyAsync(b->path_count + i0, q.path_count, m * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        CKD(cudaMemcpyAsync(b->total_displacement + i0, q.total_displacement, m * 8, cudaMemcpyDeviceToHost, cs), "D2H");
+        CKD(cudaMemcpyAsync(b->status + i0, q.status, m * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        if (b->detail) CKD(cudaMemcpyAsync(b->detail + i0, q.detail, m * 4, cudaMemcpyDeviceToHost, cs), "D2H");
         if (b->events)
-            CK(cudaMemcpyAsync(b->events + i0 * b->width * per, q.events, m * b->width * per * 4,
+            CKD(cudaMemcpyAsync(b->events + i0 * b->width * per, q.events, m * b->width * per * 4,
                                cudaMemcpyDeviceToHost, cs),
                "D2H");
     }
+#undef CKD
     CK(cudaStreamSynchronize(c->stream), "grid batch");
     CK(cudaStreamSynchronize(cs), "grid batch D2H");
     return RECON_OK;

@@ -12,6 +12,7 @@ pytestmark = pytest.mark.gpu
 
 def _cmp_pipeline(a, b, stride_moves):
     assert np.array_equal(a["status"], b["status"])
+    assert np.array_equal(a["detail"], b["detail"])
     assert np.array_equal(a["batch_count"], b["batch_count"])
     assert np.array_equal(a["path_count"], b["path_count"])
     assert np.array_equal(a["total_displacement"], b["total_displacement"])
@@ -134,3 +135,19 @@ def test_pipeline_many_instances_matches_reference(gpu, ref, solver, W, hp, k, n
     r = ref.pipeline_batch(solver, occ, n, W, W, hp, preset, ms)
     _cmp_pipeline(g, r, ms)
     assert (g["status"] == 0).sum() > n // 2
+
+
+def test_pipeline_failed_instances_report_detail(gpu, ref):
+    """the host pipeline returns each failed instance's detail —
+    InfeasibleError from the solve (problem.hpp:115) and the batching
+    no-progress InputError (batching.cpp:127-128) — next to solved ones."""
+    W = H = 64
+    occ = np.concatenate([sample_grids(0x64000000, 30, W, H, 2662), sample_grids(7, 1, W, H, 2000),
+                          sample_grids(0x6400001d, 1, W, H, 2662)])
+    ms = W * H * 12
+    g = gpu.pipeline_batch("bird", occ, 32, W, H, 40, 0, ms)
+    r = ref.pipeline_batch("bird", occ, 32, W, H, 40, 0, ms)
+    _cmp_pipeline(g, r, ms)
+    assert g["status"][30] == 2 and g["detail"][30] != 0  # InfeasibleError
+    assert g["status"][31] == 1 and g["detail"][31] != 0  # no progress
+    assert (g["detail"][g["status"] == 0] == 0).all()
