@@ -538,26 +538,38 @@ __global__ void __launch_bounds__(256) pl_walk_warp_kernel(PipelineArgs a, const
         const int2 *mci = mc + inst * WH, *mri = mr + inst * WH;
         int in1 = 0, out2 = 0;
         const int64_t my_off = PASS == 1 ? a.soff[t] : 0;
-        for (int j0 = 0; j0 <= len; j0 += 32) {
-            const int j = j0 + lane;
-            int2 m = make_int2(-1, -1);
-            if (j <= len) m = j <= dx ? mri[(int64_t)ys * W + xs + sx * j] : mci[(int64_t)xt * H + ys + sy * (j - dx)];
-            const bool r1 = m.x >= 0 && m.x != i;  // (m.x, i): i crosses source(m.x)
-            bool r2 = m.y >= 0 && m.y != i;        // (i, m.y): i crosses target(m.y) ...
-            if (r2) {                              // ... unless rule 1 already gives it
-                const int2 q = *reinterpret_cast<const int2 *>(pc + m.y);
-                r2 = !on_path2p(q.x, q.y, xs, ys);
+        // the route's owner maps, up to RG chunks of 32 vertices loaded at once
+        constexpr int RG = 4;
+        for (int g0 = 0; g0 <= len; g0 += 32 * RG) {
+            int2 m[RG];
+#pragma unroll
+            for (int c = 0; c < RG; ++c) {
+                const int j = g0 + 32 * c + lane;
+                m[c] = make_int2(-1, -1);
+                if (j <= len)
+                    m[c] = j <= dx ? mri[(int64_t)ys * W + xs + sx * j] : mci[(int64_t)xt * H + ys + sy * (j - dx)];
             }
-            if (PASS == 0) {
-                if (r1) atomicAdd(&a.outdeg[o + m.x], 1);
-                if (r2) atomicAdd(&a.indeg[o + m.y], 1);
-                in1 += r1;
-                out2 += r2;
-            } else {
-                if (r1) a.succ[atomicAdd(&fillp[o + m.x], 1ull)] = i;
-                const unsigned b2 = __ballot_sync(FULL, r2);
-                if (r2) a.succ[my_off + out2 + __popc(b2 & lanemask_lt())] = m.y;
-                out2 += __popc(b2);
+            int2 q[RG];  // the targets' paths' coordinates (rule-2 dedup)
+#pragma unroll
+            for (int c = 0; c < RG; ++c)
+                q[c] = (m[c].y >= 0 && m[c].y != i) ? *reinterpret_cast<const int2 *>(pc + m[c].y) : make_int2(0, 0);
+#pragma unroll
+            for (int c = 0; c < RG; ++c) {
+                if (g0 + 32 * c > len) break;
+                const bool r1 = m[c].x >= 0 && m[c].x != i;  // (m.x, i): i crosses source(m.x)
+                // (i, m.y): i crosses target(m.y), unless rule 1 already gives it
+                const bool r2 = m[c].y >= 0 && m[c].y != i && !on_path2p(q[c].x, q[c].y, xs, ys);
+                if (PASS == 0) {
+                    if (r1) atomicAdd(&a.outdeg[o + m[c].x], 1);
+                    if (r2) atomicAdd(&a.indeg[o + m[c].y], 1);
+                    in1 += r1;
+                    out2 += r2;
+                } else {
+                    if (r1) a.succ[atomicAdd(&fillp[o + m[c].x], 1ull)] = i;
+                    const unsigned b2 = __ballot_sync(FULL, r2);
+                    if (r2) a.succ[my_off + out2 + __popc(b2 & lanemask_lt())] = m[c].y;
+                    out2 += __popc(b2);
+                }
             }
         }
         if (PASS == 0) {
