@@ -169,9 +169,10 @@ def test_c4_variants(env):
 
 
 @pytest.mark.parametrize("env", [
-    {"RECON_BATCH_LEAP": "0"},
+    {"RECON_BATCH_LEAP": "2"},                                  # leap mode on small grids (shared-memory bitmaps)
     {"RECON_BATCH_LEAP": "0", "RECON_BATCH_LOG": "0", "RECON_BATCH_BSM": "0"},
     {"RECON_BATCH_WIDE": "1"},
+    {"RECON_BATCH_WIDE": "1", "RECON_BATCH_LEAP": "2"},
     {"RECON_SMALL_DAG": "0"},
 ])
 def test_c3_variants(env):

@@ -17,6 +17,7 @@ for FAM in solves chains pipeline stats validators wire sim; do
 done
 RECON_BATCH_WIDE=1 timeout 900 python tools/sanitize_cases.py pipeline > "$OUT/pipeline_wide.log" 2>&1; echo "pipeline (wide forced) rc=$?" | tee -a "$OUT/summary.txt"
 RECON_BATCH_LEAP=0 timeout 900 python tools/sanitize_cases.py pipeline > "$OUT/pipeline_noleap.log" 2>&1; echo "pipeline (leap off) rc=$?" | tee -a "$OUT/summary.txt"
+RECON_BATCH_LEAP=2 timeout 900 python tools/sanitize_cases.py pipeline > "$OUT/pipeline_leap.log" 2>&1; echo "pipeline (leap forced on small grids) rc=$?" | tee -a "$OUT/summary.txt"
 timeout 1800 python -m pytest tests/test_batching_scale_gpu.py tests/test_batching_gpu.py tests/test_grid_gpu.py -q -x > "$OUT/pytest.log" 2>&1; echo "pytest scale+batching+grid (checked lib) rc=$?: $(tail -1 $OUT/pytest.log)" | tee -a "$OUT/summary.txt"
 grep -h "RB_CHECK failed" "$OUT"/*.log | sort | uniq -c | tee -a "$OUT/summary.txt"
 echo "RB_CHECK failures: $(grep -h 'RB_CHECK failed' "$OUT"/*.log | wc -l)" | tee -a "$OUT/summary.txt"

@@ -176,6 +176,9 @@ CASES = {
     "c5_pipeline_512": lambda: pipeline("bird", 512, 512, 307, 157286, 0x51200000, 512, 0, 11_000_000),
     "c5_pipeline_256": lambda: pipeline("bird", 512, 512, 307, 157286, 0x51200000, 256, 0, 11_000_000),
     "c5_pipeline_4": lambda: pipeline("bird", 512, 512, 307, 157286, 0x51200000, 4, 0, 12_000_000),
+    "c5_pipeline_64": lambda: pipeline("bird", 512, 512, 307, 157286, 0x51200000, 64, 0, 12_000_000),
+    "c5_pipeline_1024": lambda: pipeline("bird", 512, 512, 307, 157286, 0x51200000, 1024, 0, 12_000_000),
+    "c5_pipeline_64_validate": lambda: pipeline("bird", 512, 512, 307, 157286, 0x51200000, 64, 0, 12_000_000, True),
     "c5_pipeline_4_validate": lambda: pipeline("bird", 512, 512, 307, 157286, 0x51200000, 4, 0, 12_000_000, True),
     "c3_pipeline_validate": lambda: pipeline("bird", 64, 64, 40, 2662, 0x64000000, 4096, 0, None, True),
     "c4_pipeline_redrec_64_validate": lambda: pipeline("redrec", 256, 256, 153, 39322, 257, 64, 0, 1_500_000, True),
