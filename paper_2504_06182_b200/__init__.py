@@ -2,8 +2,10 @@
 
 The product is the in-tree shared library lib/librecon_b200.so (sm_100a
 kernels behind the C-ABI in include/recon_b200.h).  This package holds the
-build script, the ctypes binding (abi.py) and a thin Python mirror of the
-reference's C++ API (api.py) used by the tests and the bench.
+build script (build_native.py), the ctypes binding of the C-ABI (abi.py),
+the chunked device pipeline driver (pipeline.py), the multi-GPU sharding
+(shard.py) and the input generator (inputs.py); the reference's own C++ API
+is served by the C++ shim (shim/recon_shim.cpp).
 """
 from __future__ import annotations
 
