@@ -263,7 +263,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=1024, help="C5 instances per GPU per step (one HBM-resident chunk)")
-    ap.add_argument("--e2e-batch", type=int, default=256, help="instances per e2e host-API step")
+    ap.add_argument("--e2e-batch", type=int, default=512, help="instances per e2e host-API step")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--ref-sample", type=int, default=0, help="CPU sample (default: one instance per host thread)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -378,47 +378,68 @@ def main():
                                 zip(*np.unique(np.array([s for p in parts for s in p[2]]), return_counts=True))}}
 
     # e2e: the host-buffer C-ABI call over pinned host memory, H2D + D2H inside
-    e2e = None
+    # the timed region: recon_pipeline_batch_run_host_runs (paths + the batch
+    # schedule as runs), then the same with the per-move schedule on fewer
+    # instances (e2e_move_batch)
+    e2e = e2e_mb = None
     others = None
     if not args.no_extras:
-        E = min(args.e2e_batch, B)
+        from paper_2504_06182_b200.abi import ScheduleRuns
+        del runner
+        torch.cuda.empty_cache()
         S = W * HP
-        h_occ = torch.from_numpy(occ_h[: E * W * WPC].view(np.int64)).pin_memory()
-        h_src = torch.empty(E * S, dtype=torch.int32).pin_memory()
-        h_dst = torch.empty(E * S, dtype=torch.int32).pin_memory()
-        h_i32 = torch.empty(4 * E, dtype=torch.int32).pin_memory()
-        h_td = torch.empty(E, dtype=torch.int64).pin_memory()
-        h_mb = torch.empty(E * MOVE_STRIDE, dtype=torch.int32).pin_memory()
-        g = GridBatch(h_occ.data_ptr(), E, W, H, HP, h_src.data_ptr(), h_dst.data_ptr(), None, h_i32.data_ptr(),
-                      h_td.data_ptr(), h_i32.data_ptr() + 4 * E, h_i32.data_ptr() + 8 * E, None)
-        pb = PipelineBatch(g, 1, 0, MOVE_STRIDE, h_mb.data_ptr(), h_i32.data_ptr() + 12 * E)
-        ts = []
-        ke = max(2, min(args.steps, 3))
-        for i in range(1 + ke):
-            t0 = time.perf_counter()
-            r = lib.lib.recon_pipeline_batch_run_host(lib.ctx(), C.byref(pb))
-            dt = time.perf_counter() - t0
-            if r != 0:
-                raise RuntimeError(f"host pipeline failed {r}: {lib.last_cuda_error()}")
-            if i >= 1:
-                ts.append(dt)
-        e2e_s = statistics.median(ts)
-        # the host call returns the device path's results (first instances of the chunk)
-        assert np.array_equal(h_i32[E:2 * E].numpy(), st["status"][:E])
-        assert np.array_equal(h_td.numpy()[ok[:E]], st["total_displacement"][:E][ok[:E]])
-        d2h = int(E * S * 8 + E * 24 + 4 * int(h_td.numpy().clip(0).sum()))
+        RST = S + 65536
+
+        def host_call(E, runs_format):
+            h_occ = torch.from_numpy(occ_h[: E * W * WPC].view(np.int64)).pin_memory()
+            h_src = torch.empty(E * S, dtype=torch.int32).pin_memory()
+            h_dst = torch.empty(E * S, dtype=torch.int32).pin_memory()
+            h_i32 = torch.empty(4 * E, dtype=torch.int32).pin_memory()
+            h_td = torch.empty(E, dtype=torch.int64).pin_memory()
+            g = GridBatch(h_occ.data_ptr(), E, W, H, HP, h_src.data_ptr(), h_dst.data_ptr(), None, h_i32.data_ptr(),
+                          h_td.data_ptr(), h_i32.data_ptr() + 4 * E, h_i32.data_ptr() + 8 * E, None)
+            if runs_format:
+                h_rs = torch.empty(2 * E * RST, dtype=torch.int32).pin_memory()
+                h_rc = torch.empty(E, dtype=torch.int64).pin_memory()
+                pb = PipelineBatch(g, 1, 0, MOVE_STRIDE, None, h_i32.data_ptr() + 12 * E)
+                rr = ScheduleRuns(RST, h_rs.data_ptr(), h_rs.data_ptr() + 4 * E * RST, h_rc.data_ptr())
+                call = lambda: lib.lib.recon_pipeline_batch_run_host_runs(lib.ctx(), C.byref(pb), C.byref(rr))  # noqa: E731
+            else:
+                h_mb = torch.empty(E * MOVE_STRIDE, dtype=torch.int32).pin_memory()
+                pb = PipelineBatch(g, 1, 0, MOVE_STRIDE, h_mb.data_ptr(), h_i32.data_ptr() + 12 * E)
+                call = lambda: lib.lib.recon_pipeline_batch_run_host(lib.ctx(), C.byref(pb))  # noqa: E731
+            ts = []
+            ke = max(2, min(args.steps, 3)) if runs_format else 1
+            for i in range(1 + ke):
+                t0 = time.perf_counter()
+                r = call()
+                dt = time.perf_counter() - t0
+                if r != 0:
+                    raise RuntimeError(f"host pipeline failed {r}: {lib.last_cuda_error()}")
+                if i >= 1:
+                    ts.append(dt)
+            # the host call returns the device path's results (first instances of the chunk)
+            assert np.array_equal(h_i32[E:2 * E].numpy(), st["status"][:E])
+            assert np.array_equal(h_i32[3 * E:4 * E].numpy()[ok[:E]], st["batch_count"][:E][ok[:E]])
+            sched = int(8 * h_rc.numpy().sum()) if runs_format else int(4 * h_td.numpy().clip(0)[ok[:E]].sum())
+            return statistics.median(ts), int(E * S * 8 + E * 28 + sched)
+
+        E = min(args.e2e_batch, B)
+        e2e_s, d2h = host_call(E, True)
+        mb_s, mb_d2h = host_call(min(128, E), False)
         if ws > 1:
             t = torch.tensor([e2e_s], device=dev if dist.get_backend() == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
         e2e = {"value": ws * E / e2e_s, "unit": "grids/s", "h2d_bytes_per_step": E * W * WPC * 8,
                "d2h_bytes_per_step": d2h, "instances_per_step": E,
-               "call": "recon_pipeline_batch_run_host (pinned host buffers; paths + per-instance [0, D) of the "
-                       "batch schedule copied back, overlapped with the next sub-chunk)",
+               "call": "recon_pipeline_batch_run_host_runs (pinned host buffers): paths + the batch schedule as "
+                       "runs of consecutive batch indices (recon_schedule_runs, lossless; tests expand it back)",
                "achieved_d2h_gbs": d2h / e2e_s / 1e9}
-        del h_mb, h_src, h_dst
+        e2e_mb = {"value": ws * min(128, E) / mb_s, "unit": "grids/s", "instances_per_step": min(128, E),
+                  "d2h_bytes_per_step": mb_d2h,
+                  "call": "recon_pipeline_batch_run_host (pinned): one int32 batch index per move copied back"}
         if rank == 0 and ws == 1:
-            del runner
             torch.cuda.empty_cache()
             others = other_configs(lib, torch, dev, stream)
 
@@ -473,6 +494,7 @@ def main():
         }
         if e2e:
             line["e2e"] = e2e
+            line["e2e_move_batch"] = e2e_mb
         if cpu:
             line["cpu_baseline"] = cpu
         if others:

@@ -368,6 +368,31 @@ typedef struct recon_instance_stats {
     uint64_t digest;             /* digest64 */
 } recon_instance_stats;
 
+/*
+ * Run-length form of a batch schedule (a lossless wire format of move_batch,
+ * SURVEY.md §8(f) 3): the path-major move list of an instance split into
+ * maximal runs whose batch indices rise by one per move.  Run r covers moves
+ * [run_slot[r], run_slot[r+1]) (the last run ends at the instance's total
+ * displacement D), and move j of it is in batch run_batch[r] + (j - run_slot[r]).
+ * A path that never waits is one run, so an instance needs about P runs
+ * (~1.3 MB for C5) instead of D batch indices (~43 MB).  Instances whose
+ * status is not RECON_OK have 0 runs.
+ */
+typedef struct recon_schedule_runs {
+    int64_t run_stride;   /* run capacity per instance */
+    int32_t *run_slot;    /* [count * run_stride] first move of each run */
+    int32_t *run_batch;   /* [count * run_stride] its batch index */
+    int64_t *run_count;   /* [count] runs per instance (> run_stride: RECON_ERR_CAPACITY) */
+} recon_schedule_runs;
+
+/* Runs of a finished recon_pipeline_batch_run (device pointers in both). */
+recon_status recon_pipeline_schedule_runs(recon_ctx *ctx, const recon_pipeline_batch *batch, recon_schedule_runs *runs);
+/* recon_pipeline_batch_run_host returning the schedule as runs (host pointers;
+ * batch->move_batch may be NULL): the host link carries ~P runs instead of D
+ * batch indices per instance. */
+recon_status recon_pipeline_batch_run_host_runs(recon_ctx *ctx, const recon_pipeline_batch *batch,
+                                                recon_schedule_runs *runs);
+
 /* Stats of a finished recon_pipeline_batch_run: `batch` holds the run's device
  * pointers, `stats` is a device array of batch->grid.count records.  Enqueued
  * on the context's stream. */

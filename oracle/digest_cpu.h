@@ -63,4 +63,29 @@ static inline recon_status recon_dg_stats(const recon_pipeline_batch *pb, recon_
     return RECON_OK;
 }
 
+/* recon_pipeline_schedule_runs over host pointers */
+static inline recon_status recon_dg_runs(const recon_pipeline_batch *pb, recon_schedule_runs *runs) {
+    if (!pb || !runs || !runs->run_slot || !runs->run_batch || !runs->run_count || !pb->move_batch ||
+        !pb->grid.status || !pb->grid.total_displacement)
+        return RECON_ERR_ARGUMENT;
+    int over = 0;
+    for (int32_t inst = 0; inst < pb->grid.count; ++inst) {
+        const int64_t D = pb->grid.status[inst] == RECON_OK ? pb->grid.total_displacement[inst] : 0;
+        const int32_t *mb = pb->move_batch + inst * pb->move_stride;
+        int32_t *rs = runs->run_slot + inst * runs->run_stride, *rb = runs->run_batch + inst * runs->run_stride;
+        int64_t r = 0;
+        for (int64_t j = 0; j < D; ++j)
+            if (j == 0 || mb[j] != mb[j - 1] + 1) {
+                if (r < runs->run_stride) {
+                    rs[r] = (int32_t)j;
+                    rb[r] = mb[j];
+                }
+                ++r;
+            }
+        runs->run_count[inst] = r;
+        over |= r > runs->run_stride;
+    }
+    return over ? RECON_ERR_CAPACITY : RECON_OK;
+}
+
 #endif

@@ -2167,3 +2167,25 @@ recon_status recon_ctx_phase_times(recon_ctx *ctx, float *ms, int32_t n) {
     for (int32_t i = 0; ms && i < n; ++i) ms[i] = 0.0f;
     return RECON_OK;
 }
+
+recon_status recon_pipeline_schedule_runs(recon_ctx *ctx, const recon_pipeline_batch *pb, recon_schedule_runs *runs) {
+    (void)ctx;
+    return recon_dg_runs(pb, runs);
+}
+
+/* the pipeline into a temporary schedule, then its runs */
+recon_status recon_pipeline_batch_run_host_runs(recon_ctx *ctx, const recon_pipeline_batch *pb,
+                                                recon_schedule_runs *runs) {
+    if (!pb || !runs) return RECON_ERR_ARGUMENT;
+    recon_pipeline_batch q = *pb;
+    int32_t *tmp = NULL;
+    if (!q.move_batch) {
+        tmp = (int32_t *)malloc((size_t)pb->grid.count * (size_t)pb->move_stride * sizeof(int32_t));
+        if (!tmp) return RECON_ERR_CAPACITY;
+        q.move_batch = tmp;
+    }
+    recon_status st = recon_pipeline_batch_run_host(ctx, &q);
+    if (st == RECON_OK) st = recon_dg_runs(&q, runs);
+    free(tmp);
+    return st;
+}

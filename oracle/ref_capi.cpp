@@ -888,3 +888,23 @@ extern "C" recon_status recon_ctx_phase_times(recon_ctx *, float *ms, int32_t n)
     for (int32_t i = 0; ms && i < n; ++i) ms[i] = 0.0f;
     return RECON_OK;
 }
+
+extern "C" recon_status recon_pipeline_schedule_runs(recon_ctx *, const recon_pipeline_batch *pb,
+                                                     recon_schedule_runs *runs) {
+    return recon_dg_runs(pb, runs);
+}
+
+// the pipeline into a temporary schedule, then its runs
+extern "C" recon_status recon_pipeline_batch_run_host_runs(recon_ctx *c, const recon_pipeline_batch *pb,
+                                                           recon_schedule_runs *runs) {
+    if (!pb || !runs) return RECON_ERR_ARGUMENT;
+    recon_pipeline_batch q = *pb;
+    std::vector<int32_t> tmp;
+    if (!q.move_batch) {
+        tmp.resize(static_cast<size_t>(pb->grid.count) * static_cast<size_t>(pb->move_stride));
+        q.move_batch = tmp.data();
+    }
+    recon_status st = recon_pipeline_batch_run_host(c, &q);
+    if (st == RECON_OK) st = recon_dg_runs(&q, runs);
+    return st;
+}

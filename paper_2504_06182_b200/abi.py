@@ -165,6 +165,22 @@ STATS_DTYPE = np.dtype([("status", np.int32), ("detail", np.int32), ("path_count
 assert STATS_DTYPE.itemsize == C.sizeof(InstanceStats) == 40
 
 
+class ScheduleRuns(C.Structure):
+    """recon_schedule_runs (include/recon_b200.h)."""
+    _fields_ = [("run_stride", C.c_int64), ("run_slot", C.c_void_p), ("run_batch", C.c_void_p),
+                ("run_count", C.c_void_p)]
+
+
+def expand_runs(run_slot, run_batch, nruns: int, D: int) -> np.ndarray:
+    """move_batch[0, D) of one instance from its runs."""
+    out = np.empty(D, np.int32)
+    s = np.asarray(run_slot[:nruns], np.int64)
+    ends = np.append(s[1:], D)
+    for a, e, b in zip(s, ends, np.asarray(run_batch[:nruns], np.int64)):
+        out[a:e] = b + np.arange(e - a)
+    return out
+
+
 class ValidateBatch(C.Structure):
     _fields_ = [
         ("occ", C.c_void_p), ("count", C.c_int32), ("width", C.c_int32), ("height", C.c_int32),
@@ -319,6 +335,10 @@ class ReconLib:
             f.restype = C.c_int
         L.recon_pipeline_stats.argtypes = [C.c_void_p, C.POINTER(PipelineBatch), C.c_void_p]
         L.recon_pipeline_stats.restype = C.c_int
+        for fn in ("recon_pipeline_schedule_runs", "recon_pipeline_batch_run_host_runs"):
+            f = getattr(L, fn)
+            f.argtypes = [C.c_void_p, C.POINTER(PipelineBatch), C.POINTER(ScheduleRuns)]
+            f.restype = C.c_int
         for fn in ("recon_solution_json", "recon_solution_json_host"):
             f = getattr(L, fn)
             f.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -664,6 +684,31 @@ class ReconLib:
         r = self.lib.recon_pipeline_stats(None, C.byref(pb), st.ctypes.data)
         self._check(r, 0)
         return st
+
+    def pipeline_batch_runs(self, solver: str, occ, count, width, height, h_prime, preset, move_stride,
+                            run_stride=None):
+        """recon_pipeline_batch_run_host_runs: the pipeline_batch outputs with the
+        schedule as runs (run_slot, run_batch, run_count) instead of move_batch."""
+        stride = width * h_prime
+        run_stride = run_stride or stride + 4096
+        out = {
+            "path_src": np.zeros(count * stride, np.int32), "path_dst": np.zeros(count * stride, np.int32),
+            "path_count": np.zeros(count, np.int32), "total_displacement": np.zeros(count, np.int64),
+            "status": np.zeros(count, np.int32), "detail": np.zeros(count, np.int32),
+            "batch_count": np.zeros(count, np.int32), "run_slot": np.zeros(count * run_stride, np.int32),
+            "run_batch": np.zeros(count * run_stride, np.int32), "run_count": np.zeros(count, np.int64),
+        }
+        occ = np.ascontiguousarray(occ, np.uint64)
+        g = GridBatch(_vp(occ).value, count, width, height, h_prime, _vp(out["path_src"]).value,
+                      _vp(out["path_dst"]).value, None, _vp(out["path_count"]).value,
+                      _vp(out["total_displacement"]).value, _vp(out["status"]).value, _vp(out["detail"]).value, None)
+        pb = PipelineBatch(g, 1 if solver == "bird" else 0, preset, move_stride, None, _vp(out["batch_count"]).value)
+        runs = ScheduleRuns(run_stride, _vp(out["run_slot"]).value, _vp(out["run_batch"]).value,
+                            _vp(out["run_count"]).value)
+        st = self.lib.recon_pipeline_batch_run_host_runs(self.ctx(), C.byref(pb), C.byref(runs))
+        self._check(st, 0)
+        out["run_stride"] = run_stride
+        return out
 
     def pipeline_batch(self, solver: str, occ, count, width, height, h_prime, preset, move_stride):
         stride = width * h_prime

@@ -165,12 +165,16 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb) {
 // two device slots; its device-to-host copies (per instance only the used
 // [0, D) of the schedule) run on the copy stream while the next sub-chunk is
 // solved and batched on the context stream.
-recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *pb) {
+// runs != NULL: the schedule comes back as runs (recon_schedule_runs, host
+// pointers) instead of move_batch, which may then be NULL.
+recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *pb, recon_schedule_runs *runs) {
     int32_t *detail = nullptr;
     if (!pb) return RECON_ERR_ARGUMENT;
     const recon_grid_batch *b = &pb->grid;
     if (!b->occ || !b->path_src || !b->path_dst || !b->path_count || !b->total_displacement || !b->status ||
-        !pb->move_batch || !pb->batch_count)
+        (!pb->move_batch && !runs) || !pb->batch_count)
+        return RECON_ERR_ARGUMENT;
+    if (runs && (!runs->run_slot || !runs->run_batch || !runs->run_count || runs->run_stride <= 0))
         return RECON_ERR_ARGUMENT;
     if (b->count <= 0) return RECON_OK;
     Ctx *c = resolve(ctx);
@@ -195,14 +199,16 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
         CK(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
         sub = std::max<size_t>(1, (size_t)(0.8 * (double)fr) / per);
         // two sub-chunks at least, so that copies overlap the next solve
-        if ((size_t)b->count > 1) sub = std::min(sub, ((size_t)b->count + 1) / 2);
+        // (runs: the copies are small, one sub-chunk pays the batching
+        // latency once)
+        if ((size_t)b->count > 1 && !runs) sub = std::min(sub, ((size_t)b->count + 1) / 2);
     }
     sub = std::min(sub, (size_t)b->count);
     // the two device output slots
     struct Slot {
         uint64_t *occ;
-        int32_t *src, *dst, *ev, *i32, *mb;
-        int64_t *i64;
+        int32_t *src, *dst, *ev, *i32, *mb, *rs, *rb;
+        int64_t *i64, *rc;
         cudaEvent_t done = nullptr;  // its copies are finished
     } sl[2];
     for (int k = 0; k < 2; ++k) {
@@ -213,11 +219,19 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
         sl[k].i32 = c->dev<int32_t>(S_PH_I32_0 + k, sub * 4);  // path_count | status | detail | batch_count
         sl[k].i64 = c->dev<int64_t>(S_PH_I64_0 + k, sub);
         sl[k].mb = c->dev<int32_t>(S_PH_MB0 + k, sub * (size_t)pb->move_stride);
+        sl[k].rs = sl[k].rb = nullptr;
+        sl[k].rc = nullptr;
+        if (runs) {
+            sl[k].rs = c->dev<int32_t>(S_PH_RS0 + k, sub * (size_t)runs->run_stride * 2);
+            sl[k].rb = sl[k].rs ? sl[k].rs + sub * (size_t)runs->run_stride : nullptr;
+            sl[k].rc = c->dev<int64_t>(S_PH_RC0 + k, sub);
+        }
         if (!sl[k].occ || !sl[k].src || !sl[k].dst || (b->path_event && !sl[k].ev) || !sl[k].i32 || !sl[k].i64 ||
-            !sl[k].mb)
+            !sl[k].mb || (runs && (!sl[k].rs || !sl[k].rc)))
             return cuda_fail(cudaErrorMemoryAllocation, "pipeline host slots", detail);
     }
-    std::vector<int64_t> hD(sub);
+    std::vector<int64_t> hD(sub), hR(sub);
+    bool over = false;  // some instance had more runs than run_stride
     // on any failure after copies were issued: drain both streams before returning
     auto fail = [&](recon_status st) {
         cudaStreamSynchronize(cs);
@@ -251,6 +265,13 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
         d.move_batch = o.mb;
         const recon_status st = pipeline_impl(ctx, &d);
         if (st != RECON_OK) return fail(st);
+        recon_schedule_runs dr{};
+        if (runs) {
+            dr = recon_schedule_runs{runs->run_stride, o.rs, o.rb, o.rc};
+            CKF(launch_schedule_runs(d, dr, c->sms, c->stream), "schedule runs");
+            ++c->launches;
+            CKF(cudaMemcpyAsync(hR.data(), o.rc, n * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        }
         // every instance's displacement, then only [0, D) of its schedule
         CKF(cudaMemcpyAsync(hD.data(), o.i64, n * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
         CKF(cudaStreamSynchronize(c->stream), "pipeline sub-chunk");
@@ -266,12 +287,25 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
         if (b->detail) CKF(cudaMemcpyAsync(b->detail + j0, o.i32 + 2 * n, n * 4, cudaMemcpyDeviceToHost, cs), "D2H");
         CKF(cudaMemcpyAsync(pb->batch_count + j0, o.i32 + 3 * n, n * 4, cudaMemcpyDeviceToHost, cs), "D2H");
         CKF(cudaMemcpyAsync(b->total_displacement + j0, o.i64, n * 8, cudaMemcpyDeviceToHost, cs), "D2H");
-        for (size_t i = 0; i < n; ++i) {
+        for (size_t i = 0; i < n && pb->move_batch; ++i) {
             const int64_t D = std::min<int64_t>(std::max<int64_t>(hD[i], 0), pb->move_stride);
             if (D > 0)
                 CKF(cudaMemcpyAsync(pb->move_batch + (j0 + i) * (size_t)pb->move_stride,
                                     o.mb + i * (size_t)pb->move_stride, (size_t)D * 4, cudaMemcpyDeviceToHost, cs),
                     "D2H");
+        }
+        if (runs) {
+            const size_t rst = (size_t)runs->run_stride;
+            CKF(cudaMemcpyAsync(runs->run_count + j0, o.rc, n * 8, cudaMemcpyDeviceToHost, cs), "D2H");
+            for (size_t i = 0; i < n; ++i) {
+                over |= hR[i] > runs->run_stride;
+                const int64_t R = std::min<int64_t>(hR[i], runs->run_stride);
+                if (R <= 0) continue;
+                CKF(cudaMemcpyAsync(runs->run_slot + (j0 + i) * rst, o.rs + i * rst, (size_t)R * 4,
+                                    cudaMemcpyDeviceToHost, cs), "D2H");
+                CKF(cudaMemcpyAsync(runs->run_batch + (j0 + i) * rst, o.rb + i * rst, (size_t)R * 4,
+                                    cudaMemcpyDeviceToHost, cs), "D2H");
+            }
         }
         o.done = c->chunk_event();
         if (!o.done) return fail(cuda_fail(cudaErrorUnknown, "event", detail));
@@ -279,7 +313,7 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
     }
 #undef CKF
     CK(cudaStreamSynchronize(cs), "pipeline copies");
-    return RECON_OK;
+    return over ? RECON_ERR_CAPACITY : RECON_OK;
 }
 
 }  // namespace
@@ -428,7 +462,13 @@ recon_status recon_pipeline_batch_run(recon_ctx *ctx, const recon_pipeline_batch
 }
 
 recon_status recon_pipeline_batch_run_host(recon_ctx *ctx, const recon_pipeline_batch *pb) {
-    return pipeline_host_chunked(ctx, pb);
+    return pipeline_host_chunked(ctx, pb, nullptr);
+}
+
+recon_status recon_pipeline_batch_run_host_runs(recon_ctx *ctx, const recon_pipeline_batch *pb,
+                                                recon_schedule_runs *runs) {
+    if (!runs) return RECON_ERR_ARGUMENT;
+    return pipeline_host_chunked(ctx, pb, runs);
 }
 
 }  // extern "C"

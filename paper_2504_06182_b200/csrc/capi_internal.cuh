@@ -31,7 +31,7 @@ enum Slot {
     S_SIM_CEL, S_SIM_PDEC, S_SIM_SRC, S_SIM_DST, S_SIM_PC, S_SIM_PST, S_SIM_DET, S_SIM_NB, S_SIM_TD, S_SIM_OFF,
     S_SIM_MB, S_SIM_BCNT, S_SIM_RUN, S_SIM_ALLC, S_PPACK, S_BM_WSTATE, S_BM_VMIN, S_BM_PREC,
     S_PH_OCC0, S_PH_OCC1, S_PH_SRC0, S_PH_SRC1, S_PH_DST0, S_PH_DST1, S_PH_EV0, S_PH_EV1, S_PH_I32_0, S_PH_I32_1,
-    S_PH_I64_0, S_PH_I64_1, S_PH_MB0, S_PH_MB1,
+    S_PH_I64_0, S_PH_I64_1, S_PH_MB0, S_PH_MB1, S_PH_RS0, S_PH_RS1, S_PH_RC0, S_PH_RC1,
     S_NSLOTS
 };
 
@@ -65,6 +65,9 @@ struct Ctx {
 };
 
 Ctx *resolve(recon_ctx *ctx);
+// stats.cu: the run-length schedule of a device pipeline batch, enqueued on st
+cudaError_t launch_schedule_runs(const recon_pipeline_batch &pb, const recon_schedule_runs &runs, int sms,
+                                 cudaStream_t st);
 void set_cuda_error(cudaError_t e, const char *where);
 recon_status cuda_fail(cudaError_t e, const char *where, int32_t *detail);
 

@@ -8,6 +8,8 @@
 // reduction order.  SURVEY.md §5 / §8(d): the 32-byte stats record, plus the
 // digest that cross-GPU-count identity is checked with.
 
+#include <climits>
+
 #include "capi_internal.cuh"
 #include "common.cuh"
 
@@ -88,7 +90,89 @@ __global__ void __launch_bounds__(ST) pipeline_stats_kernel(recon_pipeline_batch
     }
 }
 
+// ---- run-length schedule: one CTA per instance, RI consecutive moves per
+// thread, a run starts where the batch index does not continue the previous
+// move's (+1); a block scan over the run-start counts places the runs
+constexpr int RI = 8;
+
+__global__ void __launch_bounds__(ST) schedule_runs_kernel(recon_pipeline_batch pb, recon_schedule_runs runs) {
+    __shared__ int wsum[ST / 32];
+    __shared__ long long s_base;
+    const recon_grid_batch &g = pb.grid;
+    const int lane = lane_id(), warp = warp_id();
+    for (int inst = blockIdx.x; inst < g.count; inst += gridDim.x) {
+        const int64_t D = g.status[inst] == RECON_OK ? g.total_displacement[inst] : 0;
+        const int32_t *mb = pb.move_batch + inst * pb.move_stride;
+        int32_t *rs = runs.run_slot + inst * runs.run_stride, *rb = runs.run_batch + inst * runs.run_stride;
+        if (threadIdx.x == 0) s_base = 0;
+        __syncthreads();
+        for (int64_t t0 = 0; t0 < D; t0 += (int64_t)ST * RI) {
+            const int64_t j0 = t0 + (int64_t)threadIdx.x * RI;
+            int32_t v[RI + 1];
+            v[0] = (j0 > 0 && j0 - 1 < D) ? __ldcs(mb + j0 - 1) : INT_MIN;
+#pragma unroll
+            for (int i = 0; i < RI; ++i) v[i + 1] = j0 + i < D ? __ldcs(mb + j0 + i) : 0;
+            unsigned starts = 0;
+#pragma unroll
+            for (int i = 0; i < RI; ++i)
+                if (j0 + i < D && (j0 + i == 0 || v[i + 1] != v[i] + 1)) starts |= 1u << i;
+            const int cnt = __popc(starts);
+            int tot;
+            int ex = warp_excl_scan(cnt, &tot);
+            if (lane == 0) wsum[warp] = tot;
+            __syncthreads();
+            int before = 0, all = 0;
+#pragma unroll
+            for (int w = 0; w < ST / 32; ++w) {
+                before += w < warp ? wsum[w] : 0;
+                all += wsum[w];
+            }
+            int64_t at = s_base + before + ex;
+            for (int i = 0; i < RI; ++i)
+                if ((starts >> i) & 1u) {
+                    if (at < runs.run_stride) {
+                        rs[at] = (int32_t)(j0 + i);
+                        rb[at] = v[i + 1];
+                    }
+                    ++at;
+                }
+            __syncthreads();
+            if (threadIdx.x == 0) s_base += all;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) runs.run_count[inst] = s_base;
+        __syncthreads();
+    }
+}
+
 }  // namespace
+
+namespace rb {
+// enqueues the run extraction of a device pipeline batch on `st`
+cudaError_t launch_schedule_runs(const recon_pipeline_batch &pb, const recon_schedule_runs &runs, int sms,
+                                 cudaStream_t st) {
+    const int grid = pb.grid.count < sms * 8 ? pb.grid.count : sms * 8;
+    schedule_runs_kernel<<<grid, ST, 0, st>>>(pb, runs);
+    return cudaGetLastError();
+}
+}  // namespace rb
+
+extern "C" recon_status recon_pipeline_schedule_runs(recon_ctx *ctx, const recon_pipeline_batch *pb,
+                                                     recon_schedule_runs *runs) {
+    int32_t *detail = nullptr;
+    if (!pb || !runs || !runs->run_slot || !runs->run_batch || !runs->run_count || !pb->move_batch ||
+        !pb->grid.status || !pb->grid.total_displacement)
+        return RECON_ERR_ARGUMENT;
+    if (pb->grid.count <= 0) return RECON_OK;
+    Ctx *c = resolve(ctx);
+    if (!c) return RECON_ERR_CUDA;
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice", detail);
+    e = launch_schedule_runs(*pb, *runs, c->sms, c->stream);
+    c->launches += 1;
+    if (e != cudaSuccess) return cuda_fail(e, "schedule runs", detail);
+    return RECON_OK;
+}
 
 extern "C" recon_status recon_pipeline_stats(recon_ctx *ctx, const recon_pipeline_batch *pb, recon_instance_stats *stats) {
     int32_t *detail = nullptr;

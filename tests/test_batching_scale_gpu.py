@@ -18,6 +18,7 @@ import pytest
 
 from conftest import ROOT
 from digest import pipeline_digests
+from paper_2504_06182_b200.abi import expand_runs
 from paper_2504_06182_b200.inputs import sample_grids
 from paper_2504_06182_b200.pipeline import C3, C4, C5, PipelineRunner
 
@@ -123,6 +124,26 @@ def test_c5_full_outputs_vs_live_reference(gpu, ref):
     d_np = pipeline_digests(o, 2, C5.paths, C5.move_stride)
     assert np.array_equal(stats["digest"], d_np)
     assert np.array_equal(ref.pipeline_stats_host(o, 2, 512, 307, C5.move_stride)["digest"], d_np)
+    # the run-length schedule of the host call expands to the reference's schedule
+    rr = gpu.pipeline_batch_runs("bird", occ, 2, 512, 512, 307, 0, C5.move_stride)
+    assert int(rr["run_count"][0]) < P + 10_000 and int(rr["run_count"][1]) == 0
+    assert np.array_equal(expand_runs(rr["run_slot"], rr["run_batch"], int(rr["run_count"][0]), D), o["move_batch"][:D])
+
+
+def test_schedule_runs_device_equals_oracle(gpu, oracle):
+    """recon_pipeline_batch_run_host_runs on the device == the C oracle's, run
+    for run, on 256 C3 instances (both presets) and 4 C4 instances."""
+    for wl, n in ((C3, 256), (C4, 4)):
+        occ = sample_grids(wl.seed_base, n, wl.W, wl.H, wl.atoms)
+        for preset in (0, 1):
+            g = gpu.pipeline_batch_runs(wl.solver, occ, n, wl.W, wl.H, wl.h_prime, preset, wl.move_stride)
+            o = oracle.pipeline_batch_runs(wl.solver, occ, n, wl.W, wl.H, wl.h_prime, preset, wl.move_stride)
+            assert np.array_equal(g["run_count"], o["run_count"]) and np.array_equal(g["status"], o["status"])
+            rs = g["run_stride"]
+            for i in range(n):
+                k = int(g["run_count"][i])
+                assert np.array_equal(g["run_slot"][i * rs:i * rs + k], o["run_slot"][i * rs:i * rs + k])
+                assert np.array_equal(g["run_batch"][i * rs:i * rs + k], o["run_batch"][i * rs:i * rs + k])
 
 
 def test_device_stats_record(gpu, oracle):
