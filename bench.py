@@ -262,7 +262,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=1024, help="C5 instances per GPU per step (one HBM-resident chunk)")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="C5 instances per GPU per step (one HBM-resident chunk; default: what HBM holds, <= 1536)")
     ap.add_argument("--e2e-batch", type=int, default=512, help="instances per e2e host-API step")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--ref-sample", type=int, default=0, help="CPU sample (default: one instance per host thread)")
@@ -295,6 +296,12 @@ def main():
     lib.ctx(local)
     dev = torch.device("cuda", local)
     B = args.batch
+    if not B:
+        # the largest chunk HBM holds (device buffers + the library workspace
+        # ~100 MB per instance), capped: the batching latency is paid once per step
+        from paper_2504_06182_b200.pipeline import bytes_per_instance
+        free, _ = torch.cuda.mem_get_info(dev)
+        B = int(max(64, min(1536, (free - (6 << 30)) // bytes_per_instance(C5))) // 64 * 64)
     first = rank * B
     runner = PipelineRunner(lib, C5, B, device=local)
     stream = runner.stream
