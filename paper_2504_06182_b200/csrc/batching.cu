@@ -495,49 +495,165 @@ __device__ __forceinline__ bool on_path2(int H, int32_t s, int32_t t, int32_t v)
 // need a fill counter (virtual_line.cpp:241-268 edge rules; order inside a
 // list is irrelevant to batching).
 
-__global__ void pl_mark2_kernel(PipelineArgs a, int32_t *mc, int32_t *mr) {
-    const int64_t S = (int64_t)a.W * a.k, WH = (int64_t)a.W * a.H;
+// Per-vertex route coverage (how many routes contain a vertex) and target
+// bitmaps give every path's out-degree without walking (below).  Coverage is
+// counted as a horizontal part (row y, columns [x0, x1], the bend included)
+// and a vertical part (column x, the rows past the bend): difference arrays
+// rowc[y][W+1] and colc[x][H+1] per instance, prefix-summed by cover_scan_kernel.
+struct CoverArrays {
+    int32_t *rowc;     // [count * H * (W + 1)]
+    int32_t *colc;     // [count * W * (H + 1)]
+    uint32_t *rowT;    // [count * ceil(W*H/32)] target bits, row-major (y*W + x)
+    uint32_t *colT;    // [count * ceil(W*H/32)] target bits, column-major (x*H + y)
+};
+
+// the cover arrays live after the two int2 maps (capi_batch.cu sizes the region)
+static inline CoverArrays pipeline_cover_arrays(const PipelineArgs &a) {
+    const size_t WH = (size_t)a.W * a.H;
+    int32_t *base = a.source_of + (size_t)a.count * WH * 4;
+    CoverArrays cv;
+    cv.rowc = base;
+    cv.colc = base + (size_t)a.count * a.H * (a.W + 1);
+    cv.colT = a.occ;
+    cv.rowT = a.inb;
+    return cv;
+}
+
+__global__ void pl_mark2_kernel(PipelineArgs a, int32_t *mc, int32_t *mr, CoverArrays cv) {
+    const int64_t S = (int64_t)a.W * a.k, WH = (int64_t)a.W * a.H, nwb = (WH + 31) / 32;
+    const int W = a.W, H = a.H;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)a.count * S;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t inst = t / S;
         const int p = (int)(t % S);
         if (a.solve_status[inst] != 0 || p >= a.path_count[inst]) continue;
         const int s = a.path_src[t], d = a.path_dst[t];
-        const int xs = s / a.H, ys = s - xs * a.H, xd = d / a.H, yd = d - xd * a.H;
+        const int xs = s / H, ys = s - xs * H, xd = d / H, yd = d - xd * H;
         int32_t *c = mc + inst * WH * 2, *r = mr + inst * WH * 2;
         int2 *pc = reinterpret_cast<int2 *>(a.prec + inst * (S + 1) + p);  // {xs|ys<<16, xd|yd<<16} (prec .x/.y)
         *pc = make_int2(xs | (ys << 16), xd | (yd << 16));
         c[2 * (int64_t)s] = p;
         c[2 * (int64_t)d + 1] = p;
-        r[2 * ((int64_t)ys * a.W + xs)] = p;
-        r[2 * ((int64_t)yd * a.W + xd) + 1] = p;
+        r[2 * ((int64_t)ys * W + xs)] = p;
+        r[2 * ((int64_t)yd * W + xd) + 1] = p;
+        // coverage: horizontal part, then the vertical part past the bend
+        int32_t *rc = cv.rowc + inst * (int64_t)H * (W + 1) + (int64_t)ys * (W + 1);
+        atomicAdd(rc + min(xs, xd), 1);
+        atomicSub(rc + max(xs, xd) + 1, 1);
+        if (yd != ys) {
+            int32_t *cc = cv.colc + inst * (int64_t)W * (H + 1) + (int64_t)xd * (H + 1);
+            const int y0 = yd > ys ? ys + 1 : yd, y1 = yd > ys ? yd : ys - 1;
+            atomicAdd(cc + y0, 1);
+            atomicSub(cc + y1 + 1, 1);
+        }
+        const int64_t vr = (int64_t)yd * W + xd;
+        atomicOr(cv.rowT + inst * nwb + (vr >> 5), 1u << (vr & 31));
+        atomicOr(cv.colT + inst * nwb + ((int64_t)d >> 5), 1u << (d & 31));
     }
 }
 
-template <int PASS>
-__global__ void __launch_bounds__(256) pl_walk_warp_kernel(PipelineArgs a, const int2 *mc, const int2 *mr) {
+// in-place inclusive prefix sums of every row (length W+1) of rowc and every
+// column (length H+1) of colc: one warp per line
+__global__ void cover_scan_kernel(int count, int W, int H, CoverArrays cv) {
+    const int lane = lane_id();
+    const int64_t lines = (int64_t)count * (H + W);
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t l = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp_id(); l < lines; l += nwarps) {
+        const int64_t inst = l / (H + W), j = l % (H + W);
+        int32_t *a;
+        int n;
+        if (j < H) {
+            a = cv.rowc + inst * (int64_t)H * (W + 1) + j * (W + 1);
+            n = W + 1;
+        } else {
+            a = cv.colc + inst * (int64_t)W * (H + 1) + (j - H) * (H + 1);
+            n = H + 1;
+        }
+        int carry = 0;
+        for (int i0 = 0; i0 < n; i0 += 32) {
+            const int i = i0 + lane;
+            int v = i < n ? a[i] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(FULL, v, o);
+                if (lane >= o) v += y;
+            }
+            v += carry;
+            if (i < n) a[i] = v;
+            carry = __shfl_sync(FULL, v, 31);
+        }
+    }
+}
+
+__device__ __forceinline__ int cover_at(const CoverArrays &cv, int64_t inst, int W, int H, int x, int y) {
+    return cv.rowc[inst * (int64_t)H * (W + 1) + (int64_t)y * (W + 1) + x] +
+           cv.colc[inst * (int64_t)W * (H + 1) + (int64_t)x * (H + 1) + y];
+}
+
+// set bits of bitmap b over bit positions [lo, hi]
+__device__ __forceinline__ int popc_range(const uint32_t *b, int64_t lo, int64_t hi) {
+    int c = 0;
+    for (int64_t w = lo >> 5; w <= (hi >> 5); ++w) {
+        uint32_t m = b[w];
+        if (w == (lo >> 5)) m &= ~0u << (lo & 31);
+        if (w == (hi >> 5)) m &= ~0u >> (31 - (hi & 31));
+        c += __popc(m);
+    }
+    return c;
+}
+
+// per path: rule-1 out-degree = the routes through its source but its own;
+// rule-2 capacity = the targets on its route but its own (the rule-1
+// duplicates among them become holes, -1); move count
+__global__ void pl_degree_kernel(PipelineArgs a, CoverArrays cv) {
+    const int64_t S = (int64_t)a.W * a.k, WH = (int64_t)a.W * a.H, nwb = (WH + 31) / 32;
+    const int W = a.W, H = a.H;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)a.count * S;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t inst = t / S;
+        const int p = (int)(t % S);
+        if (a.solve_status[inst] != 0 || p >= a.path_count[inst]) {
+            a.outdeg[t] = 0;
+            a.mfr[t] = 0;
+            a.mbase[t] = 0;
+            continue;
+        }
+        const int2 me = *reinterpret_cast<const int2 *>(a.prec + inst * (S + 1) + p);
+        const int xs = me.x & 0xffff, ys = me.x >> 16, xt = me.y & 0xffff, yt = me.y >> 16;
+        a.outdeg[t] = cover_at(cv, inst, W, H, xs, ys) - 1;
+        int tg = popc_range(cv.rowT + inst * nwb, (int64_t)ys * W + min(xs, xt), (int64_t)ys * W + max(xs, xt));
+        if (yt != ys) {
+            const int y0 = yt > ys ? ys + 1 : yt, y1 = yt > ys ? yt : ys - 1;
+            tg += popc_range(cv.colT + inst * nwb, (int64_t)xt * H + y0, (int64_t)xt * H + y1);
+        }
+        a.mfr[t] = tg - 1;
+        a.mbase[t] = abs(xt - xs) + abs(yt - ys);
+    }
+}
+
+// Path i's out-list is [rule-1 edges (i, j), appended through i's fill
+// pointer by the paths j that cross source(i) | rule-2 edges (i, pb), written
+// by i itself, then -1 holes up to its capacity].  The same walk counts i's
+// in-degree: the sources on its route (rule 1) plus the routes through its
+// target (rule 2) minus the pairs both rules give.
+__global__ void __launch_bounds__(256) pl_walk_warp_kernel(PipelineArgs a, const int2 *mc, const int2 *mr,
+                                                            CoverArrays cv) {
     const int lane = lane_id();
     const int W = a.W, H = a.H;
     const int64_t S = (int64_t)W * a.k, WH = (int64_t)W * H, N = (int64_t)a.count * S;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    unsigned long long *fillp = reinterpret_cast<unsigned long long *>(a.rec);  // PASS 1: next free slot per path
+    unsigned long long *fillp = reinterpret_cast<unsigned long long *>(a.rec);  // next free rule-1 slot per path
     for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp_id(); t < N; t += nwarps) {
         const int64_t inst = t / S, o = inst * S;
         const int i = (int)(t - o);
-        if (a.solve_status[inst] != 0 || i >= a.path_count[inst]) {
-            if (PASS == 0 && lane == 0) {
-                a.mbase[t] = 0;
-                a.mfr[t] = 0;
-            }
-            continue;
-        }
+        if (a.solve_status[inst] != 0 || i >= a.path_count[inst]) continue;
         const int4 *pc = a.prec + inst * (S + 1);  // packed coordinates in .x / .y
         const int2 me = *reinterpret_cast<const int2 *>(pc + i);
         const int xs = me.x & 0xffff, ys = me.x >> 16, xt = me.y & 0xffff, yt = me.y >> 16;
         const int dx = abs(xt - xs), len = dx + abs(yt - ys), sx = xt > xs ? 1 : -1, sy = yt > ys ? 1 : -1;
         const int2 *mci = mc + inst * WH, *mri = mr + inst * WH;
-        int in1 = 0, out2 = 0;
-        const int64_t my_off = PASS == 1 ? a.soff[t] : 0;
+        int in1 = 0, dup = 0, out2 = 0;
+        const int64_t r2base = a.soff[t] + a.outdeg[t];
         // the route's owner maps, up to RG chunks of 32 vertices loaded at once
         constexpr int RG = 4;
         for (int g0 = 0; g0 <= len; g0 += 32 * RG) {
@@ -549,45 +665,42 @@ __global__ void __launch_bounds__(256) pl_walk_warp_kernel(PipelineArgs a, const
                 if (j <= len)
                     m[c] = j <= dx ? mri[(int64_t)ys * W + xs + sx * j] : mci[(int64_t)xt * H + ys + sy * (j - dx)];
             }
-            int2 q[RG];  // the targets' paths' coordinates (rule-2 dedup)
+            int2 q1[RG], q2[RG];  // coordinates of the source's / the target's path (duplicate pairs)
 #pragma unroll
-            for (int c = 0; c < RG; ++c)
-                q[c] = (m[c].y >= 0 && m[c].y != i) ? *reinterpret_cast<const int2 *>(pc + m[c].y) : make_int2(0, 0);
+            for (int c = 0; c < RG; ++c) {
+                q1[c] = (m[c].x >= 0 && m[c].x != i) ? *reinterpret_cast<const int2 *>(pc + m[c].x) : make_int2(0, 0);
+                q2[c] = (m[c].y >= 0 && m[c].y != i) ? *reinterpret_cast<const int2 *>(pc + m[c].y) : make_int2(0, 0);
+            }
 #pragma unroll
             for (int c = 0; c < RG; ++c) {
                 if (g0 + 32 * c > len) break;
-                const bool r1 = m[c].x >= 0 && m[c].x != i;  // (m.x, i): i crosses source(m.x)
-                // (i, m.y): i crosses target(m.y), unless rule 1 already gives it
-                const bool r2 = m[c].y >= 0 && m[c].y != i && !on_path2p(q[c].x, q[c].y, xs, ys);
-                if (PASS == 0) {
-                    if (r1) atomicAdd(&a.outdeg[o + m[c].x], 1);
-                    if (r2) atomicAdd(&a.indeg[o + m[c].y], 1);
-                    in1 += r1;
-                    out2 += r2;
-                } else {
-                    if (r1) a.succ[atomicAdd(&fillp[o + m[c].x], 1ull)] = i;
-                    const unsigned b2 = __ballot_sync(FULL, r2);
-                    if (r2) a.succ[my_off + out2 + __popc(b2 & lanemask_lt())] = m[c].y;
-                    out2 += __popc(b2);
+                // (m.x, i): i crosses source(m.x); both rules give it when m.x crosses target(i)
+                const bool r1 = m[c].x >= 0 && m[c].x != i;
+                if (r1) {
+                    a.succ[atomicAdd(&fillp[o + m[c].x], 1ull)] = i;
+                    ++in1;
+                    dup += on_path2p(q1[c].x, q1[c].y, xt, yt);
                 }
+                // (i, m.y): i crosses target(m.y), unless rule 1 already gives it
+                const bool r2 = m[c].y >= 0 && m[c].y != i && !on_path2p(q2[c].x, q2[c].y, xs, ys);
+                const unsigned b2 = __ballot_sync(FULL, r2);
+                if (r2) a.succ[r2base + out2 + __popc(b2 & lanemask_lt())] = m[c].y;
+                out2 += __popc(b2);
             }
         }
-        if (PASS == 0) {
-            in1 = warp_sum(in1);
-            out2 = warp_sum(out2);
-            if (lane == 0) {
-                if (in1) atomicAdd(&a.indeg[t], in1);
-                a.mfr[t] = out2;  // rule-2 out-degree, written only by i
-                a.mbase[t] = len;
-            }
-        }
+        // holes: the rule-2 capacity the duplicates did not use
+        const int cap2 = a.mfr[t];
+        for (int r = out2 + lane; r < cap2; r += 32) a.succ[r2base + r] = -1;
+        in1 = warp_sum(in1);
+        dup = warp_sum(dup);
+        if (lane == 0) a.indeg[t] = in1 + cover_at(cv, inst, W, H, xt, yt) - 1 - dup;
     }
 }
 
-// rule-1 fill pointers: path i's rule-1 successors start after its rule-2 ones
-__global__ void fillptr_kernel(int64_t n, const int64_t *soff, const int32_t *out2, unsigned long long *fp) {
+// rule-1 fill pointers: each list starts with its rule-1 part
+__global__ void fillptr_kernel(int64_t n, const int64_t *soff, unsigned long long *fp) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        fp[i] = (unsigned long long)(soff[i] + out2[i]);
+        fp[i] = (unsigned long long)soff[i];
 }
 
 // per-path records for the batching kernels: {xs | ys << 16, xt | yt << 16,
@@ -806,16 +919,21 @@ cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *
         if (e != cudaSuccess) return e;
         return cudaGetLastError();
     }
-    // maps: {source owner, target owner} per vertex, column-major then row-major
+    // maps: {source owner, target owner} per vertex, column-major then row-major;
+    // coverage difference arrays after them; target bitmaps in occ / inb
+    // (rewritten by pipeline_run_batching before the batching reads them)
     int32_t *mc = a.source_of, *mr = a.source_of + (size_t)a.count * WH * 2;
+    const CoverArrays cv = pipeline_cover_arrays(a);
     cudaMemsetAsync(mc, 0xff, (size_t)a.count * WH * 16, st);
-    cudaMemsetAsync(a.outdeg, 0, (size_t)N * 4, st);
-    cudaMemsetAsync(a.indeg, 0, (size_t)N * 4, st);
+    cudaMemsetAsync(cv.rowc, 0, (size_t)a.count * ((size_t)a.H * (a.W + 1) + (size_t)a.W * (a.H + 1)) * 4, st);
+    cudaMemsetAsync(cv.rowT, 0, (size_t)a.count * ((WH + 31) / 32) * 4, st);
+    cudaMemsetAsync(cv.colT, 0, (size_t)a.count * ((WH + 31) / 32) * 4, st);
     const int blocks = 148 * 8;
-    pl_mark2_kernel<<<blocks, 256, 0, st>>>(a, mc, mr);
-    *launches += 6;  // mark, walk, widen, two scans, fill pointers
-    pl_walk_warp_kernel<0><<<blocks, 256, 0, st>>>(a, (const int2 *)mc, (const int2 *)mr);
-    // soff = exclusive scan of the out-degrees (rule 1 + rule 2); mbase = exclusive scan of lengths
+    pl_mark2_kernel<<<blocks, 256, 0, st>>>(a, mc, mr, cv);
+    cover_scan_kernel<<<blocks, 256, 0, st>>>(a.count, a.W, a.H, cv);
+    pl_degree_kernel<<<blocks, 256, 0, st>>>(a, cv);
+    *launches += 7;  // mark, cover scan, degrees, widen, two scans, fill pointers
+    // soff = exclusive scan of the list capacities (rule 1 + rule 2); mbase = exclusive scan of lengths
     sum2_widen_kernel<<<blocks, 256, 0, st>>>(N, a.outdeg, a.mfr, a.soff);
     cudaMemsetAsync(a.soff + N, 0, 8, st);
     size_t tb = a.temp_bytes;
@@ -823,7 +941,7 @@ cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *
     cudaMemsetAsync(a.mbase + N, 0, 8, st);
     tb = a.temp_bytes;
     cub::DeviceScan::ExclusiveSum(a.temp, tb, a.mbase, a.mbase, (int)(N + 1), st);
-    fillptr_kernel<<<blocks, 256, 0, st>>>(N, a.soff, a.mfr, reinterpret_cast<unsigned long long *>(a.rec));
+    fillptr_kernel<<<blocks, 256, 0, st>>>(N, a.soff, reinterpret_cast<unsigned long long *>(a.rec));
     cudaError_t e = cudaMemcpyAsync(counts_host, a.soff + N, 8, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) return e;
     e = cudaMemcpyAsync(counts_host + 1, a.mbase + N, 8, cudaMemcpyDeviceToHost, st);
@@ -933,7 +1051,7 @@ __device__ __forceinline__ int release_successors(const BatchJob &J, const BL &b
         int sc = -1;
         if (t < tot) {
             sc = J.succ[oq0 + (t - ob)];
-            released = blockers.release(sc);
+            released = sc >= 0 && blockers.release(sc);  // (-1: a hole of the list)
         }
         const unsigned rm = __ballot_sync(FULL, released);
         if (released) newly[nnew + __popc(rm & lanemask_lt())] = sc;
@@ -1391,7 +1509,8 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
         const int len = paths.len(p);
         left += len;
         if (len == 0)
-            for (int64_t q = J.soff[p]; q < J.soff[p + 1]; ++q) blk.release(J.succ[q]);
+            for (int64_t q = J.soff[p]; q < J.soff[p + 1]; ++q)
+                if (J.succ[q] >= 0) blk.release(J.succ[q]);  // (-1: a hole of the list)
     }
     if (!resumed) left = warp_sum64(left);
     __syncwarp();
@@ -1950,7 +2069,7 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
         pl_dag_small_kernel<1><<<(int)std::min<int64_t>(a.count, 148 * 16), 256, smem, st>>>(a);
     } else {
         const int32_t *mc = a.source_of, *mr = a.source_of + (size_t)a.count * a.W * a.H * 2;
-        pl_walk_warp_kernel<1><<<blocks, 256, 0, st>>>(a, (const int2 *)mc, (const int2 *)mr);
+        pl_walk_warp_kernel<<<blocks, 256, 0, st>>>(a, (const int2 *)mc, (const int2 *)mr, pipeline_cover_arrays(a));
     }
     if (a.prec) prec_kernel<<<blocks, 256, 0, st>>>(a);
     occ_to_vertex_bits<<<blocks, 256, 0, st>>>(a.count, a.W, a.H, a.grid_occ, a.occ);

@@ -95,7 +95,8 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb) {
     a.small_dag = small_env && pipeline_small_dag_smem(a.W, a.H, a.k) > 0;
     // per-instance vertex maps only for the global DAG walk: {source, target}
     // owner per vertex, column-major and row-major
-    const size_t maps = a.small_dag ? 0 : n * WH * 4;
+    // + the coverage difference arrays (batching.cu pl_mark2_kernel)
+    const size_t maps = a.small_dag ? 0 : n * WH * 4 + n * ((size_t)b->height * (b->width + 1) + (size_t)b->width * (b->height + 1));
     int32_t *i32 = c->dev<int32_t>(S_BM_AUX0, maps + n * S * 9 + n * 2 + 8);
     int64_t *i64 = c->dev<int64_t>(S_BM_AUX1, (n * S + 1) * 2 + 4 * (n + 1) + 4);
     uint32_t *bits = c->dev<uint32_t>(S_BM_AUX2, n * nwb * 2 + 4);
