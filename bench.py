@@ -264,7 +264,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=0,
                     help="C5 instances per GPU per step (one HBM-resident chunk; default: what HBM holds, <= 1536)")
-    ap.add_argument("--e2e-batch", type=int, default=512, help="instances per e2e host-API step")
+    ap.add_argument("--e2e-batch", type=int, default=0, help="instances per e2e host-API step (default: the chunk)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--ref-sample", type=int, default=0, help="CPU sample (default: one instance per host thread)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -417,13 +417,13 @@ def main():
                 call = lambda: lib.lib.recon_pipeline_batch_run_host(lib.ctx(), C.byref(pb))  # noqa: E731
             ts = []
             ke = max(2, min(args.steps, 3)) if runs_format else 1
-            for i in range(1 + ke):
+            for i in range(2 + ke):
                 t0 = time.perf_counter()
                 r = call()
                 dt = time.perf_counter() - t0
                 if r != 0:
                     raise RuntimeError(f"host pipeline failed {r}: {lib.last_cuda_error()}")
-                if i >= 1:
+                if i >= 2:
                     ts.append(dt)
             # the host call returns the device path's results (first instances of the chunk)
             assert np.array_equal(h_i32[E:2 * E].numpy(), st["status"][:E])
@@ -431,7 +431,7 @@ def main():
             sched = int(8 * h_rc.numpy().sum()) if runs_format else int(4 * h_td.numpy().clip(0)[ok[:E]].sum())
             return statistics.median(ts), int(E * S * 8 + E * 28 + sched)
 
-        E = min(args.e2e_batch, B)
+        E = min(args.e2e_batch or B, B)
         e2e_s, d2h = host_call(E, True)
         mb_s, mb_d2h = host_call(min(128, E), False)
         if ws > 1:

@@ -2,6 +2,8 @@
 // batching pipeline over device-resident instances.
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cub/device/device_scan.cuh>
 #include <vector>
@@ -188,8 +190,14 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
     const size_t occ_words = (size_t)b->width * wpc;
     // sub-chunk: what free memory holds (two output slots + the pipeline
     // workspace, ~48 successor edges per path); RECON_PIPE_HOST_CHUNK forces
-    const size_t per = 2 * (occ_words * 8 + 8 * S + 32 + (size_t)pb->move_stride * 4) +
-                       (16 * WH + 36 * S + 16 * S + 32 * S + 16 * S + WH / 4 + 4 * WH + 192 * S);
+    // runs: the copies are small, so one output slot (the next sub-chunk waits
+    // for them); per-move schedules: two slots, copies overlap the next solve
+    const int nslots = runs ? 1 : 2;
+    // the pipeline workspace (grow-only) counts only when it must still grow:
+    // the ready-record slot holds 32 B per path slot
+    const bool warm = c->buf[S_BM_AUX7].bytes >= (size_t)b->count * S * 32;
+    const size_t per = nslots * (occ_words * 8 + 8 * S + 32 + (size_t)pb->move_stride * 4) +
+                       (warm ? 0 : (16 * WH + 36 * S + 16 * S + 32 * S + 16 * S + WH / 4 + 4 * WH + 192 * S));
     static const int env_chunk = [] {
         const char *e = getenv("RECON_PIPE_HOST_CHUNK");
         return e ? atoi(e) : 0;
@@ -198,7 +206,10 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
     if (!sub) {
         size_t fr = 0, tot = 0;
         CK(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
-        sub = std::max<size_t>(1, (size_t)(0.8 * (double)fr) / per);
+        // the output slots this context already holds count as available
+        size_t have = 0;
+        for (int sl_ = S_PH_OCC0; sl_ <= S_PH_RC1; ++sl_) have += c->buf[sl_].bytes;
+        sub = std::max<size_t>(1, (size_t)(0.8 * (double)fr + (double)have) / per);
         // two sub-chunks at least, so that copies overlap the next solve
         // (runs: the copies are small, one sub-chunk pays the batching
         // latency once)
@@ -212,7 +223,7 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
         int64_t *i64, *rc;
         cudaEvent_t done = nullptr;  // its copies are finished
     } sl[2];
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < nslots; ++k) {
         sl[k].occ = c->dev<uint64_t>(S_PH_OCC0 + k, sub * occ_words);
         sl[k].src = c->dev<int32_t>(S_PH_SRC0 + k, sub * S);
         sl[k].dst = c->dev<int32_t>(S_PH_DST0 + k, sub * S);
@@ -245,7 +256,7 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
         if (e_ != cudaSuccess) return fail(cuda_fail(e_, where, detail));        \
     } while (0)
     int k = 0;
-    for (size_t j0 = 0; j0 < (size_t)b->count; j0 += sub, k ^= 1) {
+    for (size_t j0 = 0; j0 < (size_t)b->count; j0 += sub, k = (k + 1) % nslots) {
         const size_t n = std::min(sub, (size_t)b->count - j0);
         Slot &o = sl[k];
         if (o.done) CKF(cudaStreamWaitEvent(c->stream, o.done, 0), "wait slot");
@@ -264,8 +275,17 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
         d.grid.events = nullptr;
         d.batch_count = o.i32 + 3 * n;
         d.move_batch = o.mb;
+        static const bool trace = getenv("RECON_PIPE_HOST_TRACE") != nullptr;
+        auto stamp = [&](const char *what) {
+            if (!trace) return;
+            cudaStreamSynchronize(c->stream);
+            fprintf(stderr, "[pipe host] sub-chunk %zu (n=%zu): %s %.3f ms\n", j0, n, what,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count());
+        };
+        stamp("start");
         const recon_status st = pipeline_impl(ctx, &d);
         if (st != RECON_OK) return fail(st);
+        stamp("pipeline");
         recon_schedule_runs dr{};
         if (runs) {
             dr = recon_schedule_runs{runs->run_stride, o.rs, o.rb, o.rc};
@@ -276,6 +296,7 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
         // every instance's displacement, then only [0, D) of its schedule
         CKF(cudaMemcpyAsync(hD.data(), o.i64, n * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
         CKF(cudaStreamSynchronize(c->stream), "pipeline sub-chunk");
+        stamp("runs + counts");
         cudaEvent_t solved = c->chunk_event();
         if (!solved) return fail(cuda_fail(cudaErrorUnknown, "event", detail));
         CKF(cudaEventRecord(solved, c->stream), "event");
@@ -314,6 +335,9 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
     }
 #undef CKF
     CK(cudaStreamSynchronize(cs), "pipeline copies");
+    if (getenv("RECON_PIPE_HOST_TRACE"))
+        fprintf(stderr, "[pipe host] copies done %.3f ms (sub=%zu)\n",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(), sub);
     return over ? RECON_ERR_CAPACITY : RECON_OK;
 }
 
