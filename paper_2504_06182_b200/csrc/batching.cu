@@ -510,7 +510,7 @@ struct CoverArrays {
 // the cover arrays live after the two int2 maps (capi_batch.cu sizes the region)
 static inline CoverArrays pipeline_cover_arrays(const PipelineArgs &a) {
     const size_t WH = (size_t)a.W * a.H;
-    int32_t *base = a.source_of + (size_t)a.count * WH * 4;
+    int32_t *base = a.source_of + (size_t)a.count * WH * 8;
     CoverArrays cv;
     cv.rowc = base;
     cv.colc = base + (size_t)a.count * a.H * (a.W + 1);
@@ -529,13 +529,21 @@ __global__ void pl_mark2_kernel(PipelineArgs a, int32_t *mc, int32_t *mr, CoverA
         if (a.solve_status[inst] != 0 || p >= a.path_count[inst]) continue;
         const int s = a.path_src[t], d = a.path_dst[t];
         const int xs = s / H, ys = s - xs * H, xd = d / H, yd = d - xd * H;
-        int32_t *c = mc + inst * WH * 2, *r = mr + inst * WH * 2;
-        int2 *pc = reinterpret_cast<int2 *>(a.prec + inst * (S + 1) + p);  // {xs|ys<<16, xd|yd<<16} (prec .x/.y)
-        *pc = make_int2(xs | (ys << 16), xd | (yd << 16));
-        c[2 * (int64_t)s] = p;
-        c[2 * (int64_t)d + 1] = p;
-        r[2 * ((int64_t)ys * W + xs)] = p;
-        r[2 * ((int64_t)yd * W + xd) + 1] = p;
+        // owner maps, 16 B per vertex: {source owner, target owner, the source
+        // owner's target coordinates, the target owner's source coordinates},
+        // so the walk's duplicate-edge checks need no gather
+        int32_t *c = mc + inst * WH * 4, *r = mr + inst * WH * 4;
+        const int ps = xs | (ys << 16), pd = xd | (yd << 16);
+        int2 *pc = reinterpret_cast<int2 *>(a.prec + inst * (S + 1) + p);  // (prec .x/.y)
+        *pc = make_int2(ps, pd);
+        c[4 * (int64_t)s] = p;
+        c[4 * (int64_t)s + 2] = pd;
+        c[4 * (int64_t)d + 1] = p;
+        c[4 * (int64_t)d + 3] = ps;
+        r[4 * ((int64_t)ys * W + xs)] = p;
+        r[4 * ((int64_t)ys * W + xs) + 2] = pd;
+        r[4 * ((int64_t)yd * W + xd) + 1] = p;
+        r[4 * ((int64_t)yd * W + xd) + 3] = ps;
         // coverage: horizontal part, then the vertical part past the bend
         int32_t *rc = cv.rowc + inst * (int64_t)H * (W + 1) + (int64_t)ys * (W + 1);
         atomicAdd(rc + min(xs, xd), 1);
@@ -636,8 +644,11 @@ __global__ void pl_degree_kernel(PipelineArgs a, CoverArrays cv) {
 // by i itself, then -1 holes up to its capacity].  The same walk counts i's
 // in-degree: the sources on its route (rule 1) plus the routes through its
 // target (rule 2) minus the pairs both rules give.
-__global__ void __launch_bounds__(256) pl_walk_warp_kernel(PipelineArgs a, const int2 *mc, const int2 *mr,
-                                                            CoverArrays cv) {
+#ifndef RECON_WALK_MINB
+#define RECON_WALK_MINB 4
+#endif
+__global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_warp_kernel(PipelineArgs a, const int4 *mc, const int4 *mr,
+                                                                             CoverArrays cv) {
     const int lane = lane_id();
     const int W = a.W, H = a.H;
     const int64_t S = (int64_t)W * a.k, WH = (int64_t)W * H, N = (int64_t)a.count * S;
@@ -651,38 +662,39 @@ __global__ void __launch_bounds__(256) pl_walk_warp_kernel(PipelineArgs a, const
         const int2 me = *reinterpret_cast<const int2 *>(pc + i);
         const int xs = me.x & 0xffff, ys = me.x >> 16, xt = me.y & 0xffff, yt = me.y >> 16;
         const int dx = abs(xt - xs), len = dx + abs(yt - ys), sx = xt > xs ? 1 : -1, sy = yt > ys ? 1 : -1;
-        const int2 *mci = mc + inst * WH, *mri = mr + inst * WH;
+        const int4 *mci = mc + inst * WH, *mri = mr + inst * WH;
         int in1 = 0, dup = 0, out2 = 0;
         const int64_t r2base = a.soff[t] + a.outdeg[t];
         // the route's owner maps, up to RG chunks of 32 vertices loaded at once
-        constexpr int RG = 4;
+#ifndef RECON_WALK_RG
+#define RECON_WALK_RG 4
+#endif
+        constexpr int RG = RECON_WALK_RG;
         for (int g0 = 0; g0 <= len; g0 += 32 * RG) {
-            int2 m[RG];
+            int4 m[RG];
+            int pv[RG];  // the route vertex's packed coordinates
 #pragma unroll
             for (int c = 0; c < RG; ++c) {
                 const int j = g0 + 32 * c + lane;
-                m[c] = make_int2(-1, -1);
-                if (j <= len)
-                    m[c] = j <= dx ? mri[(int64_t)ys * W + xs + sx * j] : mci[(int64_t)xt * H + ys + sy * (j - dx)];
-            }
-            int2 q1[RG], q2[RG];  // coordinates of the source's / the target's path (duplicate pairs)
-#pragma unroll
-            for (int c = 0; c < RG; ++c) {
-                q1[c] = (m[c].x >= 0 && m[c].x != i) ? *reinterpret_cast<const int2 *>(pc + m[c].x) : make_int2(0, 0);
-                q2[c] = (m[c].y >= 0 && m[c].y != i) ? *reinterpret_cast<const int2 *>(pc + m[c].y) : make_int2(0, 0);
+                m[c] = make_int4(-1, -1, 0, 0);
+                const int x = j <= dx ? xs + sx * j : xt, y = j <= dx ? ys : ys + sy * (j - dx);
+                pv[c] = x | (y << 16);
+                if (j <= len) m[c] = j <= dx ? mri[(int64_t)y * W + x] : mci[(int64_t)x * H + y];
             }
 #pragma unroll
             for (int c = 0; c < RG; ++c) {
                 if (g0 + 32 * c > len) break;
-                // (m.x, i): i crosses source(m.x); both rules give it when m.x crosses target(i)
+                // (m.x, i): i crosses source(m.x); both rules give it when m.x's
+                // route (from here to m.z) crosses target(i)
                 const bool r1 = m[c].x >= 0 && m[c].x != i;
                 if (r1) {
                     a.succ[atomicAdd(&fillp[o + m[c].x], 1ull)] = i;
                     ++in1;
-                    dup += on_path2p(q1[c].x, q1[c].y, xt, yt);
+                    dup += on_path2p(pv[c], m[c].z, xt, yt);
                 }
-                // (i, m.y): i crosses target(m.y), unless rule 1 already gives it
-                const bool r2 = m[c].y >= 0 && m[c].y != i && !on_path2p(q2[c].x, q2[c].y, xs, ys);
+                // (i, m.y): i crosses target(m.y), unless m.y's route (from m.w to
+                // here) crosses source(i), which rule 1 already gives
+                const bool r2 = m[c].y >= 0 && m[c].y != i && !on_path2p(m[c].w, pv[c], xs, ys);
                 const unsigned b2 = __ballot_sync(FULL, r2);
                 if (r2) a.succ[r2base + out2 + __popc(b2 & lanemask_lt())] = m[c].y;
                 out2 += __popc(b2);
@@ -922,9 +934,9 @@ cudaError_t pipeline_dag_count(const PipelineArgs &a, cudaStream_t st, int64_t *
     // maps: {source owner, target owner} per vertex, column-major then row-major;
     // coverage difference arrays after them; target bitmaps in occ / inb
     // (rewritten by pipeline_run_batching before the batching reads them)
-    int32_t *mc = a.source_of, *mr = a.source_of + (size_t)a.count * WH * 2;
+    int32_t *mc = a.source_of, *mr = a.source_of + (size_t)a.count * WH * 4;
     const CoverArrays cv = pipeline_cover_arrays(a);
-    cudaMemsetAsync(mc, 0xff, (size_t)a.count * WH * 16, st);
+    cudaMemsetAsync(mc, 0xff, (size_t)a.count * WH * 32, st);
     cudaMemsetAsync(cv.rowc, 0, (size_t)a.count * ((size_t)a.H * (a.W + 1) + (size_t)a.W * (a.H + 1)) * 4, st);
     cudaMemsetAsync(cv.rowT, 0, (size_t)a.count * ((WH + 31) / 32) * 4, st);
     cudaMemsetAsync(cv.colT, 0, (size_t)a.count * ((WH + 31) / 32) * 4, st);
@@ -2068,8 +2080,8 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
         const int64_t smem = pipeline_small_dag_smem(a.W, a.H, a.k);
         pl_dag_small_kernel<1><<<(int)std::min<int64_t>(a.count, 148 * 16), 256, smem, st>>>(a);
     } else {
-        const int32_t *mc = a.source_of, *mr = a.source_of + (size_t)a.count * a.W * a.H * 2;
-        pl_walk_warp_kernel<<<blocks, 256, 0, st>>>(a, (const int2 *)mc, (const int2 *)mr, pipeline_cover_arrays(a));
+        const int32_t *mc = a.source_of, *mr = a.source_of + (size_t)a.count * a.W * a.H * 4;
+        pl_walk_warp_kernel<<<blocks, 256, 0, st>>>(a, (const int4 *)mc, (const int4 *)mr, pipeline_cover_arrays(a));
     }
     if (a.prec) prec_kernel<<<blocks, 256, 0, st>>>(a);
     occ_to_vertex_bits<<<blocks, 256, 0, st>>>(a.count, a.W, a.H, a.grid_occ, a.occ);

@@ -98,7 +98,7 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb) {
     // per-instance vertex maps only for the global DAG walk: {source, target}
     // owner per vertex, column-major and row-major
     // + the coverage difference arrays (batching.cu pl_mark2_kernel)
-    const size_t maps = a.small_dag ? 0 : n * WH * 4 + n * ((size_t)b->height * (b->width + 1) + (size_t)b->width * (b->height + 1));
+    const size_t maps = a.small_dag ? 0 : n * WH * 8 + n * ((size_t)b->height * (b->width + 1) + (size_t)b->width * (b->height + 1));
     int32_t *i32 = c->dev<int32_t>(S_BM_AUX0, maps + n * S * 9 + n * 2 + 8);
     int64_t *i64 = c->dev<int64_t>(S_BM_AUX1, (n * S + 1) * 2 + 4 * (n + 1) + 4);
     uint32_t *bits = c->dev<uint32_t>(S_BM_AUX2, n * nwb * 2 + 4);
@@ -197,7 +197,7 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
     // the ready-record slot holds 32 B per path slot
     const bool warm = c->buf[S_BM_AUX7].bytes >= (size_t)b->count * S * 32;
     const size_t per = nslots * (occ_words * 8 + 8 * S + 32 + (size_t)pb->move_stride * 4) +
-                       (warm ? 0 : (16 * WH + 36 * S + 16 * S + 32 * S + 16 * S + WH / 4 + 4 * WH + 192 * S));
+                       (warm ? 0 : (40 * WH + 36 * S + 16 * S + 32 * S + 16 * S + WH / 4 + 4 * WH + 192 * S));
     static const int env_chunk = [] {
         const char *e = getenv("RECON_PIPE_HOST_CHUNK");
         return e ? atoi(e) : 0;

@@ -48,9 +48,10 @@ def bytes_per_instance(wl: Workload) -> int:
     pipeline workspace (capi_batch.cu), rounded up."""
     S, WH = wl.paths, wl.W * wl.H
     outs = wl.W * words_per_column(wl.H) * 8 + 2 * S * 4 + wl.move_stride * 4 + 64
-    # maps 16 B/vertex, i32 scratch 9*4 B/path, i64 16 B/path, records 32 B/path,
-    # path records 16 B/path, bitmaps, vmin 4 B/vertex, successor lists (~48 per path)
-    work = 16 * WH + 36 * S + 16 * S + 32 * S + 16 * S + WH // 4 + 4 * WH + 48 * 4 * S
+    # owner maps 32 B/vertex + coverage 8 B/vertex, i32 scratch 9*4 B/path,
+    # i64 16 B/path, records 32 B/path, path records 16 B/path, bitmaps,
+    # vmin 4 B/vertex, successor lists (~48 per path)
+    work = 40 * WH + 36 * S + 16 * S + 32 * S + 16 * S + WH // 4 + 4 * WH + 48 * 4 * S
     return outs + work
 
 
