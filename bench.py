@@ -364,13 +364,17 @@ def main():
     nb_mean = float(st["batch_count"][ok].mean()) if ok.any() else 0.0
     clocks = clk.summary()
     mhz = clocks.get("sm_mhz") or sm_max_mhz
-    traffic = None
+    traffic = traffic_note = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             tr = json.load(f).get("c5_batching", {})
-        if tr.get("batch") == B:
-            traffic = tr.get("dram_bytes_per_step")
+        if tr.get("per_instance_dram_bytes"):
+            # DRAM bytes of the two batching kernels per instance (ncu --set full
+            # at 64 instances) times this chunk
+            traffic = tr["per_instance_dram_bytes"] * B
+            traffic_note = (f"ncu dram read+write of both batching kernels, {tr['per_instance_dram_bytes'] / 1e6:.0f} MB "
+                            f"per instance ({tr['source']}), x {B} instances")
     digests = st["digest"]
     job = {"instances": [first, first + B], "digest_sum": int(np.sum(digests, dtype=np.uint64)),
            "statuses": {str(k): int(v) for k, v in zip(*np.unique(st["status"], return_counts=True))}}
@@ -481,7 +485,8 @@ def main():
             "phases_ms": {"solve": solve_ms, "dag": dag_ms, "batching_wide": wide_ms, "batching_warp": warp_ms},
             "roofline": {
                 "bound": "hbm", "achieved": alg_sched / (batch_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
-                "frac": alg_sched / (batch_ms * 1e-3) / 1e9 / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                "frac": alg_sched / (batch_ms * 1e-3) / 1e9 / hbm, "traffic": traffic, "traffic_source": traffic_note,
+                "peak_kind": peak_kind,
                 "kernel": "batching phase: rb::batch_wide_kernel + rb::batch_pipeline_kernel<16> (leap)",
                 "algorithmic_bytes_per_launch": alg_sched,
                 "algorithmic_bytes_rule": "4 B per elementary move of the batch schedule (SURVEY §8(d) 4*D)",
