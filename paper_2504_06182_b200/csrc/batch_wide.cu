@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
             const int par = nb & 1;
             const WideBufs A = bufs(cur), B = bufs(cur ^ 1);
             // ---- 1. candidates and destination claims
+            const bool none = a.preset == 0;
             for (int e = tid; e < R; e += WT) {
                 const int4 r = A.rec[e];
                 const int to = vtx(H, (r.y & 0xffff) + 1, r.z & 0xffff, r.z >> 16, r.w & 0xffff, r.w >> 16);
@@ -234,24 +235,40 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
                 int slot = -1;
                 if (!((occ[to >> 5] >> (to & 31)) & 1u)) {
                     f = F_CAND;
-                    unsigned h = hslot(to, hbits);
-                    for (int probes = 0;; ++probes) {
-                        RB_CHECK(probes < hsize, "wide: claim table full");
-                        const uint32_t old = atomicCAS(&hash[h], 0u, (uint32_t)to + 1u);
-                        if (old == 0u) {
-                            slot = (int)h;
-                            break;
+                    if (!none) {  // column_direction: claims in the hash table
+                        unsigned h = hslot(to, hbits);
+                        for (int probes = 0;; ++probes) {
+                            RB_CHECK(probes < hsize, "wide: claim table full");
+                            const uint32_t old = atomicCAS(&hash[h], 0u, (uint32_t)to + 1u);
+                            if (old == 0u) {
+                                slot = (int)h;
+                                break;
+                            }
+                            if (old == (uint32_t)to + 1u) {
+                                s_contend[par] = 1;
+                                break;
+                            }
+                            h = (h + 1) & (hsize - 1);
                         }
-                        if (old == (uint32_t)to + 1u) {
-                            s_contend[par] = 1;
-                            break;
-                        }
-                        h = (h + 1) & (hsize - 1);
+                        atomicMin(&s_first[par], r.x);
                     }
-                    if (a.preset != 0) atomicMin(&s_first[par], r.x);
                 }
                 eslot[e] = (int16_t)slot;
                 eflag[e] = f;
+            }
+            if (none) {
+                // preset none: every candidate is accepted unless it shares its
+                // destination, and the destination ends up occupied either way,
+                // so candidates claim it in the occupancy bitmap itself (after
+                // every candidate has read the pre-batch bitmap): a set bit seen
+                // by a claim is a second claimer
+                __syncthreads();
+                for (int e = tid; e < R; e += WT) {
+                    if (!(eflag[e] & F_CAND)) continue;
+                    const int4 r = A.rec[e];
+                    const int to = vtx(H, (r.y & 0xffff) + 1, r.z & 0xffff, r.z >> 16, r.w & 0xffff, r.w >> 16);
+                    if (atomicOr(&occ[to >> 5], 1u << (to & 31)) & (1u << (to & 31))) s_contend[par] = 1;
+                }
             }
             __syncthreads();
             WPROF(0);
@@ -290,8 +307,9 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
                     }
                 __syncthreads();
             }
-            // ---- 2. application (a move toggles its source and destination
-            // bits: the sets are disjoint, so no ordering is needed), the move's
+            // ---- 2. application (a move toggles its source bit, and its
+            // destination bit unless the claim set it: the sets are disjoint,
+            // so no ordering is needed), the move's
             // batch index, finished paths to the release list, live paths to
             // the next list
             int nacc = 0;
@@ -309,7 +327,7 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
                     if (won && a.preset != 0) won = compatible_w(a.preset, H, fr, to, s_ff, s_ft);
                     if (won) {
                         atomicXor(&occ[fr >> 5], 1u << (fr & 31));
-                        atomicXor(&occ[to >> 5], 1u << (to & 31));
+                        if (!none) atomicXor(&occ[to >> 5], 1u << (to & 31));  // (none: claimed already)
                         const int k = r.y & 0xffff, len = r.y >> 16;
                         __stcs(mb + A.base[e] + k, nb);
                         r.y = (k + 1) | (len << 16);
