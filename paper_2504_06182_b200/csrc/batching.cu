@@ -28,6 +28,8 @@
 #include "batching.cuh"
 #include "common.cuh"
 
+#include "leap.cuh"
+
 namespace rb {
 
 struct ExplicitPaths {
@@ -1359,70 +1361,6 @@ __device__ unsigned long long g_batch_prof[16];
 // small integer solve per piece pair.  delta = min over live paths of
 // min(f_p + 1, first stall) batches are applied at once; delta == 0 runs the
 // literal batch.  Bit-identical to the literal loop (tests/test_batching_gpu.py).
-struct Seg {
-    int x0, y0, vx, vy, t0, t1;  // position (x0 + vx t, y0 + vy t) for t in [t0, t1]
-};
-
-__device__ __forceinline__ void lane_segs(int k, int len, int xs, int ys, int xt, int yt, Seg &h, Seg &v) {
-    const int dx = abs(xt - xs), sx = xt > xs ? 1 : -1, sy = yt > ys ? 1 : -1;
-    h = Seg{xs + sx * k, ys, sx, 0, 0, dx - k};
-    v = Seg{xt, ys + sy * (k - dx), 0, sy, max(0, dx - k), len - k};
-}
-
-// t / c for c in {+-1, +-2}; false when not an integer
-__device__ __forceinline__ bool div12(int r, int c, int *t) {
-    if (c & 1) {
-        *t = r * c;
-        return true;
-    }
-    if (r & 1) return false;
-    *t = (r >> 1) * (c >> 1);
-    return true;
-}
-
-// min t in [lo, hi] with (ax + avx t, ay + avy t) == (bx + bvx t, by + bvy t)
-__device__ __forceinline__ int meet(int ax, int ay, int avx, int avy, int bx, int by, int bvx, int bvy, int lo,
-                                    int hi) {
-    const int cx = avx - bvx, rx = bx - ax, cy = avy - bvy, ry = by - ay;
-    int t;
-    if (cx == 0) {
-        if (rx != 0) return INT_MAX;
-    } else {
-        if (!div12(rx, cx, &t)) return INT_MAX;
-        lo = max(lo, t);
-        hi = min(hi, t);
-    }
-    if (cy == 0) {
-        if (ry != 0) return INT_MAX;
-    } else {
-        if (!div12(ry, cy, &t)) return INT_MAX;
-        lo = max(lo, t);
-        hi = min(hi, t);
-    }
-    return lo <= hi ? lo : INT_MAX;
-}
-
-// first offset t in [0, T] at which p (pieces a) is blocked by q (pieces b):
-// P(t+1) == Q(t) (q's pre-batch vertex) or P(t+1) == Q(t+1) (same destination)
-__device__ __forceinline__ int pair_event(const Seg *a, const Seg *b, int T) {
-    int best = INT_MAX;
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int w = 0; w < 2; ++w) {
-            const Seg &A = a[u], &B = b[w];
-            int lo = max(max(A.t0 - 1, B.t0), 0), hi = min(min(A.t1 - 1, B.t1), T);
-            if (lo <= hi) best = min(best, meet(A.x0 + A.vx, A.y0 + A.vy, A.vx, A.vy, B.x0, B.y0, B.vx, B.vy, lo, hi));
-            lo = max(max(A.t0, B.t0), 1);
-            hi = min(min(A.t1, B.t1), T + 1);
-            if (lo <= hi) {
-                const int s = meet(A.x0, A.y0, A.vx, A.vy, B.x0, B.y0, B.vx, B.vy, lo, hi);
-                if (s != INT_MAX) best = min(best, s - 1);
-            }
-        }
-    return best;
-}
-
 // Deadlocked lanes.  A lane whose next vertex holds another lane's token is
 // blocked; the blocked lanes whose blocker is itself blocked, closed under
 // that relation, form cycles (head-on riders, batching.cpp:127-128's
@@ -1482,7 +1420,7 @@ __device__ __forceinline__ int leap_delta(const LanePath &lp, int H, int32_t fr,
             const int qx = qfr / H, qy = qfr - qx * H;
             if (qx >= bx0 && qx <= bx1 && qy >= by0 && qy <= by1) {
                 const Seg pt[2] = {Seg{qx, qy, 0, 0, 0, INT_MAX / 2}, Seg{qx, qy, 0, 0, 0, INT_MAX / 2}};
-                best = min(best, pair_event(mine, pt, lp.len - lp.k - 1));
+                best = min(best, pair_event(mine, pt, 0, lp.len - lp.k - 1));
             }
             continue;
         }
@@ -1491,7 +1429,7 @@ __device__ __forceinline__ int leap_delta(const LanePath &lp, int H, int32_t fr,
             const int k = qk & 0xffff, len = qk >> 16;
             Seg other[2];
             lane_segs(k, len, qxs & 0xffff, qxs >> 16, qxt & 0xffff, qxt >> 16, other[0], other[1]);
-            best = min(best, pair_event(mine, other, min(lp.len - lp.k - 1, len - k - 1)));
+            best = min(best, pair_event(mine, other, 0, min(lp.len - lp.k - 1, len - k - 1)));
         }
     }
     return __reduce_min_sync(FULL, mover ? best : INT_MAX);
@@ -2099,7 +2037,19 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
             return e ? atoi(e) : 0;
         }();
         const int64_t budget = wide_smem_env > 0 ? (int64_t)wide_smem_env * 1024 : 113 * 1024;  // 2 CTAs per SM
-        if (pipeline_wide_config(a.W, a.H, budget, &rmax, &hbits, &wsmem) ||
+        // preset none: windows of batches (RECON_WIDE_WINDOW=0: batch by batch)
+        static const int window_env = [] {
+            const char *e = getenv("RECON_WIDE_WINDOW");
+            return e ? atoi(e) : 1;
+        }();
+        if (a.preset == 0 && window_env && a.prec &&
+            (pipeline_window_config(a.W, a.H, budget, &rmax, &wsmem) ||
+             pipeline_window_config(a.W, a.H, 220 * 1024, &rmax, &wsmem))) {
+            cudaMemsetAsync(a.vmin, 0x7f, (size_t)a.count * a.W * a.H * 4, st);
+            cudaError_t e = launch_batch_window(a, sms, rmax, wsmem, st);
+            if (e != cudaSuccess) return e;
+            *launches += 1;
+        } else if (pipeline_wide_config(a.W, a.H, budget, &rmax, &hbits, &wsmem) ||
             pipeline_wide_config(a.W, a.H, 220 * 1024, &rmax, &hbits, &wsmem)) {
             cudaMemsetAsync(a.vmin, 0x7f, (size_t)a.count * a.W * a.H * 4, st);
             cudaError_t e = launch_batch_wide(a, sms, rmax, hbits, wsmem, st);

@@ -106,6 +106,9 @@ int64_t pipeline_small_dag_smem(int W, int H, int k);
 // wide phase (batch_wide.cu): CTA per instance while the ready set exceeds a warp
 bool pipeline_wide_config(int W, int H, int64_t smem_budget, int *rmax, int *hbits, size_t *smem);
 cudaError_t launch_batch_wide(const PipelineArgs &a, int sms, int rmax, int hbits, size_t smem, cudaStream_t st);
+// preset none: the wide phase in windows of batches (batch_window.cu)
+bool pipeline_window_config(int W, int H, int64_t smem_budget, int *rmax, size_t *smem);
+cudaError_t launch_batch_window(const PipelineArgs &a, int sms, int rmax, size_t smem, cudaStream_t st);
 
 // occ bits (column-major, bit y) -> vertex-id bitmap
 __global__ void occ_to_vertex_bits(int count, int W, int H, const uint64_t *occ, uint32_t *bits);

@@ -172,7 +172,10 @@ def test_device_stats_record(gpu, oracle):
     {"RECON_BATCH_LEAP": "0", "RECON_BATCH_OCC_SMEM": "0"},     # mode 0: bitmaps in global memory
     {"RECON_BATCH_WIDE": "0"},                                  # leap without the wide phase (general warp path)
     {"RECON_WIDE_SMEM_KB": "105"},                              # wide ready set outgrows shared memory mid-run
+    {"RECON_WIDE_SMEM_KB": "80"},                               # windows halved by overflowing plans
     {"RECON_WIDE_SMEM_KB": "60"},                               # ... or at batch 0 (warp kernel from scratch)
+    {"RECON_WIDE_WINDOW": "0"},                                 # the wide phase batch by batch (batch_wide.cu)
+    {"RECON_WIDE_WINDOW": "0", "RECON_WIDE_SMEM_KB": "105"},
 ])
 def test_c5_variants(env):
     # 160 instances > 148 SMs: the many-instance shapes (4-warp batch CTAs,
@@ -183,6 +186,7 @@ def test_c5_variants(env):
 
 @pytest.mark.parametrize("env", [
     {"RECON_BATCH_WIDE": "0"},
+    {"RECON_WIDE_WINDOW": "0"},
     {"RECON_BATCH_LEAP": "0", "RECON_BATCH_BSM": "0"},
     {"RECON_BATCH_LEAP": "0", "RECON_BATCH_WIDE": "0", "RECON_BATCH_LOG": "1"},
 ])
@@ -194,6 +198,7 @@ def test_c4_variants(env):
     {"RECON_BATCH_LEAP": "2"},                                  # leap mode on small grids (shared-memory bitmaps)
     {"RECON_BATCH_LEAP": "0", "RECON_BATCH_LOG": "0", "RECON_BATCH_BSM": "0"},
     {"RECON_BATCH_WIDE": "1"},
+    {"RECON_BATCH_WIDE": "1", "RECON_WIDE_WINDOW": "0"},
     {"RECON_BATCH_WIDE": "1", "RECON_BATCH_LEAP": "2"},
     {"RECON_SMALL_DAG": "0"},
 ])

@@ -27,14 +27,18 @@ solver, W, H, hp, k, seed, preset, ms = CASES[name]
 occ = sample_grids(seed, n, W, H, k)
 buf = (C.c_ulonglong * 16)()
 wbuf = (C.c_ulonglong * 8)()
+vbuf = (C.c_ulonglong * 16)()
 gpu.lib.recon_debug_batch_prof(buf, 1)
 gpu.lib.recon_debug_wide_prof(wbuf, 1)
+gpu.lib.recon_debug_window_prof(vbuf, 1)
 t = time.time()
 g = gpu.pipeline_batch(solver, occ, n, W, H, hp, preset, ms)
 dt = time.time() - t
 gpu.lib.recon_debug_batch_prof(buf, 1)
 gpu.lib.recon_debug_wide_prof(wbuf, 1)
+gpu.lib.recon_debug_window_prof(vbuf, 1)
 v = list(buf)
+vv = list(vbuf)
 wv = list(wbuf)
 names = ["leap_delta", "leap_apply", "literal", "finish", "general", "n_leap", "n_literal", "n_general", "n_finish",
          "total"]
@@ -49,4 +53,13 @@ if wv[4]:
     nbw = wv[3]
     print(f"wide: {wv[4]} instances, {nbw / wv[4]:.0f} batches each; cycles per batch: "
           f"candidates {wv[0] / nbw:.0f}, apply {wv[1] / nbw:.0f}, release {wv[2] / nbw:.0f}")
+if vv[7]:
+    ni, nbw = vv[7], max(1, vv[4])
+    print(f"window: {ni} instances; per instance: {vv[0] / ni:.0f} windows ({vv[1] / ni:.1f} stalled, "
+          f"{vv[2] / ni:.1f} overflowed), {vv[3] / ni:.1f} literal batches, {vv[4] / ni:.0f} batches; "
+          f"cycles per batch: plan {vv[5] / nbw:.0f}, replay {vv[6] / nbw:.0f}, commit {vv[11] / nbw:.0f}, "
+          f"literal+other {vv[10] / nbw:.0f}; finishers per window {vv[8] / max(1, vv[0]):.0f}, "
+          f"rounds per window {vv[9] / max(1, vv[0] + vv[2]):.2f}")
+    print(f"  plan per window: scan {vv[12] / max(1, vv[0]):.0f}, pass1 {vv[13] / max(1, vv[0]):.0f}, "
+          f"pass2 {vv[14] / max(1, vv[0]):.0f}, pass3 {vv[15] / max(1, vv[0]):.0f}, rest {vv[5] / max(1, vv[0]):.0f} cycles")
 print("batch_count", g["batch_count"][:4], "status", np.unique(g["status"]))
