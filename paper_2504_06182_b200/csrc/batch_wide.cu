@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
         int4 *stg = a.rec2 + o;  // hand-off staging (and overflow past rmax)
         int32_t *stb = a.rb2 + o;
         const int32_t *succ = a.succ + e0;
+        const int32_t *slen = a.slen ? a.slen + o : nullptr;  // list lengths (else up to the next list)
         // ---- ready set at batch 0 (read-only: on a bail-out the warp kernel
         // starts from scratch)
         if (tid == 0) {
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
                 zero_len = 1;  // zero-length paths: the warp kernel's init releases them
             } else if (blk[p] == 0) {
                 const int i = atomicAdd(&s_cnt[1], 1);  // [1]: batch 0 appends to [0]
-                wide_put(bufs(0), i, rmax, stg, stb, make_int4(p, len << 16, r.x, r.y), r.z, r.w, prec[p + 1].w - r.w,
+                wide_put(bufs(0), i, rmax, stg, stb, make_int4(p, len << 16, r.x, r.y), r.z, r.w, slen ? slen[p] : prec[p + 1].w - r.w,
                          &s_ovf);
             }
         }
@@ -382,7 +383,7 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
                         rel[c] = false;
                         if (c < nsl && sc[c] >= 0) {
                             pr[c] = __ldg(prec + sc[c]);
-                            qe[c] = __ldg(&prec[sc[c] + 1].w);
+                            qe[c] = slen ? __ldg(slen + sc[c]) : __ldg(&prec[sc[c] + 1].w);
                             rel[c] = atomicSub(&blk[sc[c]], 1) == 1;
                         }
                     }
@@ -392,7 +393,7 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
                         const int len = abs((pr[c].y & 0xffff) - (pr[c].x & 0xffff)) + abs((pr[c].y >> 16) - (pr[c].x >> 16));
                         const int i = atomicAdd(&s_cnt[par], 1);
                         wide_put(B, i, rmax, stg, stb,
-                                 make_int4(sc[c], len << 16, pr[c].x, pr[c].y), pr[c].z, pr[c].w, qe[c] - pr[c].w, &s_ovf);
+                                 make_int4(sc[c], len << 16, pr[c].x, pr[c].y), pr[c].z, pr[c].w, slen ? qe[c] : qe[c] - pr[c].w, &s_ovf);
                     }
                     nsl = 0;
                 };

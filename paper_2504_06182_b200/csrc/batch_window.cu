@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
         int4 *stg = a.rec2 + o;                               // hand-off staging (and overflow past rmax)
         int32_t *stb = a.rb2 + o;
         const int32_t *succ = a.succ + e0;
+        const int32_t *slen = a.slen ? a.slen + o : nullptr;  // list lengths (else up to the next list)
         int32_t *vmin = a.vmin + (int64_t)inst * WH;
 
         // appends entry i of list X (shared memory, or the staging area past rmax)
@@ -217,7 +218,7 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
             // successor ranges of the finishers, one thread each
             for (int f = f0 + tid; f < f1; f += WT) {
                 const int pid = F[f].x;
-                const int q0 = __ldg(&prec[pid].w), qn = __ldg(&prec[pid + 1].w) - q0;
+                const int q0 = __ldg(&prec[pid].w), qn = slen ? __ldg(slen + pid) : __ldg(&prec[pid + 1].w) - q0;
                 F[f].z = q0;
                 F[f].w = qn;
                 prefetch_l2(succ + q0, qn * 4);  // (the lists are read by warps below, twice in a plan)

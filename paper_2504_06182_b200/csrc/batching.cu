@@ -146,6 +146,11 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t *a, int n, int x) {
 
 // The general entry point (arbitrary paths, given dag): the literal
 // pairwise checks.  (The solver pipeline runs batch_warp_pipe below.)
+// end of path p's successor list
+__device__ __forceinline__ int64_t list_end(const BatchJob &J, int p) {
+    return J.slen ? J.soff[p] + J.slen[p] : J.soff[p + 1];
+}
+
 template <class Paths>
 __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
     const int lane = lane_id();
@@ -164,7 +169,7 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
     for (int p = lane; p < P; p += 32)
         if (paths.len(p) == 0) {
             s.done[p] = 1;
-            for (int64_t q = J.soff[p]; q < J.soff[p + 1]; ++q) atomicSub(&s.blockers[J.succ[q]], 1);
+            for (int64_t q = J.soff[p]; q < list_end(J, p); ++q) atomicSub(&s.blockers[J.succ[q]], 1);
         }
     __syncwarp();
     __threadfence_block();
@@ -282,7 +287,7 @@ __device__ void batch_warp(const BatchJob &J, const Paths &paths) {
                 fin = m < 0;
                 if (fin) {
                     q0 = J.soff[p];
-                    q1 = J.soff[p + 1];
+                    q1 = list_end(J, p);
                 }
             }
             nfin += __popc(__ballot_sync(FULL, fin));
@@ -643,9 +648,20 @@ __global__ void pl_degree_kernel(PipelineArgs a, CoverArrays cv) {
 
 // Path i's out-list is [rule-1 edges (i, j), appended through i's fill
 // pointer by the paths j that cross source(i) | rule-2 edges (i, pb), written
-// by i itself, then -1 holes up to its capacity].  The same walk counts i's
-// in-degree: the sources on its route (rule 1) plus the routes through its
-// target (rule 2) minus the pairs both rules give.
+// by i itself]; pl_compact_kernel then closes the gap between the two parts.
+// The same walk counts i's in-degree: the sources on its route (rule 1) plus
+// the routes through its target (rule 2) minus the pairs both rules give.
+//
+// Rule-1 edges implied by two others are dropped: the batches depend only on
+// the DAG's reachability (a path is ready once all its predecessors are done,
+// and a dropped predecessor reaches a kept one), and an edge (u, w) implied by
+// a path u -> x -> w of the full DAG can go, because by induction over the
+// edges' spans in a topological order every justifying edge is kept or
+// itself implied.  For the rule-1 edge (s_b, i) at source(s_b) on i's route,
+// x is the owner s_a of the previous (or next) source on i's route when s_a's
+// route crosses source(s_b): then (s_b, s_a) is a rule-1 edge and (s_a, i)
+// is one.  In a column of tokens that move up one after another this drops
+// all but the nearest predecessor (C5: 7.4 M -> ~3.0 M edges per instance).
 #ifndef RECON_WALK_MINB
 #define RECON_WALK_MINB 4
 #endif
@@ -667,11 +683,15 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_warp_kernel(Pipe
         const int4 *mci = mc + inst * WH, *mri = mr + inst * WH;
         int in1 = 0, dup = 0, out2 = 0;
         const int64_t r2base = a.soff[t] + a.outdeg[t];
+        const int cov = lane == 0 ? cover_at(cv, inst, W, H, xt, yt) : 0;  // (issued early, used at the end)
         // the route's owner maps, up to RG chunks of 32 vertices loaded at once
 #ifndef RECON_WALK_RG
-#define RECON_WALK_RG 4
+#define RECON_WALK_RG 2
 #endif
         constexpr int RG = RECON_WALK_RG;
+        // the last rule-1 vertex of the route so far: its packed coordinates and
+        // its owner's target (warp-uniform)
+        int cpv = -1, cz = 0;
         for (int g0 = 0; g0 <= len; g0 += 32 * RG) {
             int4 m[RG];
             int pv[RG];  // the route vertex's packed coordinates
@@ -683,15 +703,52 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_warp_kernel(Pipe
                 pv[c] = x | (y << 16);
                 if (j <= len) m[c] = j <= dx ? mri[(int64_t)y * W + x] : mci[(int64_t)x * H + y];
             }
+            unsigned b1[RG];  // rule-1 lanes of each chunk
+#pragma unroll
+            for (int c = 0; c < RG; ++c) b1[c] = __ballot_sync(FULL, m[c].x >= 0 && m[c].x != i);
 #pragma unroll
             for (int c = 0; c < RG; ++c) {
                 if (g0 + 32 * c > len) break;
                 // (m.x, i): i crosses source(m.x); both rules give it when m.x's
                 // route (from here to m.z) crosses target(i)
-                const bool r1 = m[c].x >= 0 && m[c].x != i;
+                const bool r1 = b1[c] >> lane & 1u;
+                // the neighbouring rule-1 vertices on the route (previous: this
+                // chunk or the carry; next: this chunk or the next one loaded)
+                const unsigned below = b1[c] & lanemask_lt(), above = b1[c] & ~lanemask_lt() & ~(1u << lane);
+                const int pl = below ? 31 - __clz(below) : 0;
+                int ppv = __shfl_sync(FULL, pv[c], pl), pz = __shfl_sync(FULL, m[c].z, pl);
+                if (!below) {
+                    ppv = cpv;
+                    pz = cz;
+                }
+                int npv = -1, nz = 0;
+#ifndef RECON_WALK_NONEXT
+                {
+                    const int nl = above ? __ffs(above) - 1 : (c + 1 < RG && b1[c + 1] ? __ffs(b1[c + 1]) - 1 : 0);
+                    const int v0 = __shfl_sync(FULL, pv[c], nl), z0 = __shfl_sync(FULL, m[c].z, nl);
+                    const int v1 = __shfl_sync(FULL, pv[c + 1 < RG ? c + 1 : c], nl);
+                    const int z1 = __shfl_sync(FULL, m[c + 1 < RG ? c + 1 : c].z, nl);
+                    if (above) {
+                        npv = v0;
+                        nz = z0;
+                    } else if (c + 1 < RG && b1[c + 1] && g0 + 32 * (c + 1) <= len) {
+                        npv = v1;
+                        nz = z1;
+                    }
+                }
+#endif
+                if (b1[c]) {
+                    const int last = 31 - __clz(b1[c]);
+                    cpv = __shfl_sync(FULL, pv[c], last);
+                    cz = __shfl_sync(FULL, m[c].z, last);
+                }
                 if (r1) {
-                    a.succ[atomicAdd(&fillp[o + m[c].x], 1ull)] = i;
-                    ++in1;
+                    const int bx = pv[c] & 0xffff, by = pv[c] >> 16;
+                    const bool implied = (ppv >= 0 && on_path2p(ppv, pz, bx, by)) || (npv >= 0 && on_path2p(npv, nz, bx, by));
+                    if (!implied) {
+                        a.succ[atomicAdd(&fillp[o + m[c].x], 1ull)] = i;
+                        ++in1;
+                    }
                     dup += on_path2p(pv[c], m[c].z, xt, yt);
                 }
                 // (i, m.y): i crosses target(m.y), unless m.y's route (from m.w to
@@ -702,12 +759,12 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_warp_kernel(Pipe
                 out2 += __popc(b2);
             }
         }
-        // holes: the rule-2 capacity the duplicates did not use
-        const int cap2 = a.mfr[t];
-        for (int r = out2 + lane; r < cap2; r += 32) a.succ[r2base + r] = -1;
         in1 = warp_sum(in1);
         dup = warp_sum(dup);
-        if (lane == 0) a.indeg[t] = in1 + cover_at(cv, inst, W, H, xt, yt) - 1 - dup;
+        if (lane == 0) {
+            a.indeg[t] = in1 + cov - 1 - dup;
+            a.mfr[t] = out2;  // (the compaction's rule-2 count)
+        }
     }
 }
 
@@ -715,6 +772,29 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_warp_kernel(Pipe
 __global__ void fillptr_kernel(int64_t n, const int64_t *soff, unsigned long long *fp) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         fp[i] = (unsigned long long)soff[i];
+}
+
+// closes each list's gap: the rule-2 part moves down to the end of the kept
+// rule-1 part; slen (the out-degree array, free after the walk) = the list's
+// length.  Lists stay at their offsets, so paths are independent.
+__global__ void pl_compact_kernel(PipelineArgs a) {
+    const int lane = lane_id();
+    const int64_t S = (int64_t)a.W * a.k, N = (int64_t)a.count * S;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const unsigned long long *fillp = reinterpret_cast<const unsigned long long *>(a.rec);
+    for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp_id(); t < N; t += nwarps) {
+        const int64_t inst = t / S;
+        if (a.solve_status[inst] != 0 || t - inst * S >= a.path_count[inst]) continue;
+        const int64_t s0 = a.soff[t];
+        const int n1 = (int)((int64_t)fillp[t] - s0), cap1 = a.outdeg[t], n2 = a.mfr[t];
+        if (n1 < cap1)  // (chunks in ascending order: a chunk's destination never overlaps a later source)
+            for (int r0 = 0; r0 < n2; r0 += 32) {
+                const int v = r0 + lane < n2 ? a.succ[s0 + cap1 + r0 + lane] : 0;
+                __syncwarp();
+                if (r0 + lane < n2) a.succ[s0 + n1 + r0 + lane] = v;
+            }
+        if (lane == 0) a.outdeg[t] = n1 + n2;
+    }
 }
 
 // per-path records for the batching kernels: {xs | ys << 16, xt | yt << 16,
@@ -1259,7 +1339,7 @@ __device__ __forceinline__ int release_into_lanes(const BatchJob &J, const BL &b
             qe[c] = 0;
             if (c < nsl && sc[c] >= 0) {
                 pr[c] = __ldg(J.prec + sc[c]);
-                qe[c] = __ldg(&J.prec[sc[c] + 1].w);
+                qe[c] = J.slen ? __ldg(J.slen + sc[c]) : __ldg(&J.prec[sc[c] + 1].w);
                 rel[c] = blockers.release(sc[c]);
             }
         }
@@ -1289,7 +1369,7 @@ __device__ __forceinline__ int release_into_lanes(const BatchJob &J, const BL &b
                 lp.len = abs(lp.xt - lp.xs) + abs(lp.yt - lp.ys);
                 lp.base = r.z;
                 lp.q0 = J.e0 + r.w;
-                lp.q1 = J.e0 + e;
+                lp.q1 = J.e0 + (J.slen ? r.w + e : e);
             }
             nnew += __popc(rm);
         }
@@ -1459,7 +1539,7 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
         const int len = paths.len(p);
         left += len;
         if (len == 0)
-            for (int64_t q = J.soff[p]; q < J.soff[p + 1]; ++q)
+            for (int64_t q = J.soff[p]; q < list_end(J, p); ++q)
                 if (J.succ[q] >= 0) blk.release(J.succ[q]);  // (-1: a hole of the list)
     }
     if (!resumed) left = warp_sum64(left);
@@ -1501,7 +1581,7 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
             lp = rec_lane(R.rec[lane], R.rb[lane]);
             if (LEAP) {
                 lp.q0 = J.soff[lp.p];
-                lp.q1 = J.soff[lp.p + 1];
+                lp.q1 = list_end(J, lp.p);
             }
         }
         lane_move();
@@ -1616,7 +1696,7 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
                     fin = lp.k == lp.len;
                     if (fin) {
                         q0 = LEAP ? lp.q0 : J.soff[lp.p];
-                        q1 = LEAP ? lp.q1 : J.soff[lp.p + 1];
+                        q1 = LEAP ? lp.q1 : list_end(J, lp.p);
                     }
                     // next move: horizontal steps first (virtual_line.cpp:150-173)
                     const int dx = abs(lp.xt - lp.xs);
@@ -1802,7 +1882,7 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
                 if (fin) {
                     const int p = m & 0x7fffffff;
                     q0 = J.soff[p];
-                    q1 = J.soff[p + 1];
+                    q1 = list_end(J, p);
                 }
             }
             nfin += __popc(__ballot_sync(FULL, fin));
@@ -1965,6 +2045,7 @@ __global__ void __launch_bounds__(256, (MODE & 2) ? 4 : 1) batch_pipeline_kernel
         J.prec = a.prec ? a.prec + (int64_t)inst * (S + 1) : nullptr;
         J.e0 = a.soff[o];
         J.succ = a.succ;
+        J.slen = a.slen ? a.slen + o : nullptr;
         J.s.occ = a.occ + inst * nwb;
         J.s.inb = a.inb + inst * nwb;
         const int64_t nbw = BSM ? (S + 1) / 2 : 0, nib = INB_SM ? nwb : 0, per = nwb + nib + nbw;
@@ -2020,6 +2101,8 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
     } else {
         const int32_t *mc = a.source_of, *mr = a.source_of + (size_t)a.count * a.W * a.H * 4;
         pl_walk_warp_kernel<<<blocks, 256, 0, st>>>(a, (const int4 *)mc, (const int4 *)mr, pipeline_cover_arrays(a));
+        pl_compact_kernel<<<blocks, 256, 0, st>>>(a);
+        *launches += 1;
     }
     if (a.prec) prec_kernel<<<blocks, 256, 0, st>>>(a);
     occ_to_vertex_bits<<<blocks, 256, 0, st>>>(a.count, a.W, a.H, a.grid_occ, a.occ);

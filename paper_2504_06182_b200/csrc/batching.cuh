@@ -33,6 +33,8 @@ struct BatchJob {
     const int32_t *succ;
     const int4 *prec;     // pipeline: [P+1] {xs|ys<<16, xt|yt<<16, move base, soff - e0} per path
     int64_t e0;           // pipeline: soff[0]
+    const int32_t *slen;  // pipeline (global DAG walk): list lengths, p's list = [soff[p], soff[p] + slen[p]);
+                          // null: [soff[p], soff[p + 1])
     const int64_t *in_off;  // edge-level only: incoming CSR
     const int32_t *in_src;
     const int64_t *in_need;
@@ -75,6 +77,7 @@ struct PipelineArgs {
     // scratch (device), per instance strides: maps W*H, paths W*k
     int32_t *source_of, *target_of;      // [count * W*H]
     int32_t *outdeg, *indeg, *fill;      // [count * W*k]
+    const int32_t *slen;                 // list lengths (= outdeg after pl_compact_kernel), or null (small DAG)
     int64_t *soff;                       // [count * W*k + 1]
     int64_t *mbase;                      // [count * W*k + 1]
     int32_t *succ;                       // [edge capacity]

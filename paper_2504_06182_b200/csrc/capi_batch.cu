@@ -112,6 +112,7 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb) {
     a.target_of = nullptr;
     int32_t *q = i32 + maps;
     a.outdeg = q;
+    a.slen = a.small_dag ? nullptr : a.outdeg;  // (pl_compact_kernel's list lengths)
     a.indeg = q + n * S;
     a.fill = q + 2 * n * S;
     a.newly = q + 3 * n * S;
