@@ -67,6 +67,7 @@ struct LanePath {
     int p, k, len, xs, ys, xt, yt;
     int64_t base;
     int64_t q0, q1;  // successor CSR range, prefetched when the lane is filled (leap mode)
+    int pf;          // leap mode: the successors' records and blocker counts still to prefetch
     __device__ __forceinline__ int32_t v(int H, int kk) const {
         const int dx = abs(xt - xs);
         if (kk <= dx) return (xs + (xt > xs ? kk : -kk)) * H + ys;
@@ -1077,6 +1078,7 @@ __device__ __forceinline__ LanePath rec_lane(int4 r, int base) {
     l.xt = r.w & 0xffff;
     l.yt = r.w >> 16;
     l.base = base;
+    l.pf = 1;
     return l;
 }
 
@@ -1110,6 +1112,18 @@ struct Blockers {
         return (int)((x >> ((p & 1) * 16)) & 0xffffu);
     }
     // one predecessor of p finished; true when it was the last
+    // the count before a decrement (compare with 1 later: the atomic's round
+    // trip then overlaps other work)
+    __device__ __forceinline__ int release_raw(int p) const {
+        if (!BSM) return atomicSub(&g[p], 1);
+        const uint32_t sh = (uint32_t)(p & 1) * 16u;
+        uint32_t old;
+        asm volatile("atom.shared.add.u32 %0, [%1], %2;"
+                     : "=r"(old)
+                     : "r"(sa + ((uint32_t)(p >> 1) << 2)), "r"(0u - (1u << sh))
+                     : "memory");
+        return (int)((old >> sh) & 0xffffu);
+    }
     __device__ __forceinline__ bool release(int p) const {
         if (!BSM) return atomicSub(&g[p], 1) == 1;
         const uint32_t sh = (uint32_t)(p & 1) * 16u;
@@ -1252,8 +1266,10 @@ __device__ __forceinline__ LanePath shfl_lane(const LanePath &lp, int src, bool 
     if (with_succ) {
         q.q0 = __shfl_sync(FULL, lp.q0, src);
         q.q1 = __shfl_sync(FULL, lp.q1, src);
+        q.pf = __shfl_sync(FULL, lp.pf, src);
     } else {
         q.q0 = q.q1 = 0;
+        q.pf = 0;
     }
     return q;
 }
@@ -1301,6 +1317,9 @@ __device__ __forceinline__ int release_successors_buf(const BatchJob &J, const B
     }
     return nnew;
 }
+
+// phase cycle counters of batch_warp_pipe (experiments: -DRECON_BATCH_PROF)
+__device__ unsigned long long g_batch_prof[16];
 
 // Leap-mode finish: the finished lanes' successors are released as in
 // release_successors_buf, and every successor's path record
@@ -1370,11 +1389,15 @@ __device__ __forceinline__ int release_into_lanes(const BatchJob &J, const BL &b
                 lp.base = r.z;
                 lp.q0 = J.e0 + r.w;
                 lp.q1 = J.e0 + (J.slen ? r.w + e : e);
+                lp.pf = 1;
             }
             nnew += __popc(rm);
         }
         nsl = 0;
     };
+#ifdef RECON_BATCH_PROF
+    const long long rt0 = clock64();
+#endif
     // successor ids, finished lane by finished lane, 32 at a time
     for (unsigned m = fmask; m; m &= m - 1) {
         const int f = __ffs(m) - 1;
@@ -1388,9 +1411,116 @@ __device__ __forceinline__ int release_into_lanes(const BatchJob &J, const BL &b
             if (++nsl == G) flush();
         }
     }
+#ifdef RECON_BATCH_PROF
+    const long long rt1 = clock64();
+#endif
     if (nsl) flush();
+#ifdef RECON_BATCH_PROF
+    if (lane == 0) {
+        atomicAdd(&g_batch_prof[10], (unsigned long long)(rt1 - rt0));
+        atomicAdd(&g_batch_prof[11], (unsigned long long)(clock64() - rt1));
+        atomicAdd(&g_batch_prof[12], 1ull);
+    }
+#endif
     *filled = nnew <= nempty;
     if (!*filled && took) lp.p = INT_MAX;  // the spill takes every released id from buf
+    return nnew;
+}
+
+
+// Leap-mode finish issued early: the lanes that finish with this leap are
+// known as soon as `delta` is, so their successor ids are loaded before the
+// leap's schedule stores and their blocker decrements and path records are
+// issued after them; release_fill then waits for the results.  Up to
+// 32 * EG successors (the caller falls back to release_into_lanes beyond).
+#ifndef RECON_EG
+#define RECON_EG 4
+#endif
+constexpr int EG = RECON_EG;
+struct EarlyRelease {
+    int sc[EG];
+    int4 pr[EG];
+    int qe[EG];
+    int old[EG];
+};
+
+__device__ __forceinline__ void release_load(const BatchJob &J, bool fin, int64_t q0, int64_t q1, EarlyRelease &er) {
+    const int lane = lane_id();
+    if (!fin) q0 = q1 = 0;
+    int tot;
+    const int base = warp_excl_scan((int)(q1 - q0), &tot);
+#pragma unroll
+    for (int c = 0; c < EG; ++c) {
+        const int t = c * 32 + lane;
+        int owner = 0;  // largest lane with base <= t
+#pragma unroll
+        for (int st = 16; st > 0; st >>= 1) {
+            const int cl = owner + st;
+            if (__shfl_sync(FULL, base, cl) <= t) owner = cl;
+        }
+        const int64_t oq0 = __shfl_sync(FULL, q0, owner);
+        const int ob = __shfl_sync(FULL, base, owner);
+        er.sc[c] = t < tot ? __ldcg(J.succ + oq0 + (t - ob)) : -1;
+    }
+}
+
+template <class BL>
+__device__ __forceinline__ void release_issue(const BatchJob &J, const BL &blockers, EarlyRelease &er) {
+#pragma unroll
+    for (int c = 0; c < EG; ++c) {
+        er.old[c] = 0;
+        er.pr[c] = make_int4(0, 0, 0, 0);
+        er.qe[c] = 0;
+        if (er.sc[c] >= 0) {
+            er.pr[c] = __ldcg(J.prec + er.sc[c]);
+            er.qe[c] = J.slen ? __ldcg(J.slen + er.sc[c]) : __ldcg(&J.prec[er.sc[c] + 1].w);
+            er.old[c] = blockers.release_raw(er.sc[c]);
+        }
+    }
+}
+
+// the released paths of an early release into the empty lanes (and `sm`);
+// returns the number released, *filled = whether every one got a lane
+__device__ __forceinline__ int release_fill(const BatchJob &J, const EarlyRelease &er, int32_t *sm, LanePath &lp,
+                                            bool *filled) {
+    const int lane = lane_id();
+    const unsigned empty = __ballot_sync(FULL, lp.p == INT_MAX);
+    const int erank = __popc(empty & lanemask_lt());
+    const int nempty = __popc(empty);
+    const bool is_empty = (empty >> lane) & 1u;
+    bool took = false;
+    int nnew = 0;
+#pragma unroll
+    for (int c = 0; c < EG; ++c) {
+        const bool rel = er.sc[c] >= 0 && er.old[c] == 1;
+        const unsigned rm = __ballot_sync(FULL, rel);
+        if (!rm) continue;
+        if (rel) sm[nnew + __popc(rm & lanemask_lt())] = er.sc[c];
+        const int j = erank - nnew;
+        const bool take = is_empty && j >= 0 && j < __popc(rm);
+        const int srcl = take ? (int)__fns(rm, 0, j + 1) : lane;
+        const int np = __shfl_sync(FULL, er.sc[c], srcl);
+        const int4 r = make_int4(__shfl_sync(FULL, er.pr[c].x, srcl), __shfl_sync(FULL, er.pr[c].y, srcl),
+                                 __shfl_sync(FULL, er.pr[c].z, srcl), __shfl_sync(FULL, er.pr[c].w, srcl));
+        const int e = __shfl_sync(FULL, er.qe[c], srcl);
+        if (take) {
+            took = true;
+            lp.p = np;
+            lp.k = 0;
+            lp.xs = r.x & 0xffff;
+            lp.ys = r.x >> 16;
+            lp.xt = r.y & 0xffff;
+            lp.yt = r.y >> 16;
+            lp.len = abs(lp.xt - lp.xs) + abs(lp.yt - lp.ys);
+            lp.base = r.z;
+            lp.q0 = J.e0 + r.w;
+            lp.q1 = J.e0 + (J.slen ? r.w + e : e);
+            lp.pf = 1;
+        }
+        nnew += __popc(rm);
+    }
+    *filled = nnew <= nempty;
+    if (!*filled && took) lp.p = INT_MAX;  // the spill takes every released id from sm
     return nnew;
 }
 
@@ -1402,8 +1532,6 @@ __device__ __forceinline__ void occ_toggle(const Bits<SM> &b, int v) {
     else asm volatile("red.global.xor.b32 [%0], %1;" ::"l"(b.p + (v >> 5)), "r"(1u << (v & 31)) : "memory");
 }
 
-// phase cycle counters of batch_warp_pipe (experiments: -DRECON_BATCH_PROF)
-__device__ unsigned long long g_batch_prof[16];
 #ifdef RECON_BATCH_PROF
 #define BPROF_T0() long long bp_t0_ = clock64()
 #define BPROF_ADD(i)                  \
@@ -1596,17 +1724,49 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
         if (regmode) {
             bool fin = false;
             int64_t q0 = 0, q1 = 0;
+            bool early = false;  // (uniform) the finish was issued with the leap
+            EarlyRelease er;
             BPROF_T0();
             unsigned movers = 0;
+            // a lane that entered since the last leap: its successor ids now,
+            // and after leap_delta their path records and blocker counts
+            // into L2, so its finish (>= one leap away) decrements in L2
+            int pfv0 = -1, pfv1 = -1;
+            if (LEAP) {
+                const unsigned pm = __ballot_sync(FULL, lp.p != INT_MAX && lp.pf);
+                if (pm) {
+                    const int f = __ffs(pm) - 1;
+                    const int64_t fq = __shfl_sync(FULL, lp.q0, f);
+                    const int fn = (int)(__shfl_sync(FULL, lp.q1, f) - fq);
+                    pfv0 = lane < fn ? __ldcg(J.succ + fq + lane) : -1;
+                    pfv1 = 32 + lane < fn ? __ldcg(J.succ + fq + 32 + lane) : -1;
+                    if (lane == f) lp.pf = 0;
+                }
+            }
             const int delta = LEAP ? leap_delta(lp, H, fr, to, &movers) : 0;
+            if (LEAP) {
+                auto pf1 = [&](int v) {
+                    if (v < 0) return;
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(J.prec + v));
+                    if (J.slen) asm volatile("prefetch.global.L2 [%0];" ::"l"(J.slen + v));
+                    if (!BSM) asm volatile("prefetch.global.L2 [%0];" ::"l"(s.blockers + v));
+                };
+                pf1(pfv0);
+                pf1(pfv1);
+            }
             BPROF_ADD(0);
             if (delta > 0) {
                 BPROF_CNT(5);
                 // batches nb .. nb+delta-1 move every mover one vertex each
                 // (frozen lanes stay put)
                 const bool valid = (movers >> lane) & 1u;
-                // lanes finishing with this leap: successor lists into L2 now
-                if (valid && lp.len - lp.k == delta) prefetch_l2(J.succ + lp.q0, (int)(lp.q1 - lp.q0) * 4);
+                // lanes finishing with this leap: their successor ids now,
+                // their decrements after the schedule stores (EarlyRelease)
+                const bool willfin = valid && lp.len - lp.k == delta;
+                early = LEAP && __reduce_add_sync(FULL, willfin ? (unsigned)(lp.q1 - lp.q0) : 0u) <= 32u * EG &&
+                        __any_sync(FULL, willfin);
+                if (early) release_load(J, willfin, lp.q0, lp.q1, er);
+                else if (willfin) prefetch_l2(J.succ + lp.q0, (int)(lp.q1 - lp.q0) * 4);
 #ifdef RECON_CHECKED
                 // the leap invariant: no token outside the movers blocks a
                 // mover's next `delta` vertices (frozen tokens are fixed
@@ -1632,6 +1792,7 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
                     const int64_t b = __shfl_sync(FULL, lp.base + lp.k, o);
                     for (int i = lane; i < delta; i += 32) __stcs(J.move_batch + b + i, nb + i);
                 }
+                if (early) release_issue(J, blk, er);
                 if (valid) {
                     occ_toggle(occ, fr);
                     lp.k += delta;
@@ -1714,7 +1875,20 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
                 int32_t *newly = s.newly;
                 int nnew;
                 bool filled = false;
-                if (LEAP) {
+                if (LEAP && early) {
+                    if (fin) lp.p = INT_MAX;
+#ifdef RECON_BATCH_PROF
+                    const long long ft0 = clock64();
+#endif
+                    nnew = release_fill(J, er, s.newly_sm, lp, &filled);
+#ifdef RECON_BATCH_PROF
+                    if (lane == 0) {
+                        atomicAdd(&g_batch_prof[13], (unsigned long long)(clock64() - ft0));
+                        atomicAdd(&g_batch_prof[14], 1ull);
+                    }
+#endif
+                    newly = s.newly_sm;
+                } else if (LEAP) {
                     if (fin) lp.p = INT_MAX;
                     nnew = release_into_lanes(J, blk, s.newly_sm, NEWLY_SM, s.newly, fin, q0, q1, &newly, lp, &filled);
                 } else {
@@ -2006,7 +2180,8 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
 // the general path touches it), halving a large grid's shared memory,
 // 16 = leap mode (preset none; no move log)
 template <int MODE>
-__global__ void __launch_bounds__(256, (MODE & 2) ? 4 : 1) batch_pipeline_kernel(PipelineArgs a) {
+// (mode 16, one warp per CTA: <= 168 registers keep 3 warps per SM sub-partition)
+__global__ void __launch_bounds__(MODE == 16 ? 32 : 256, MODE == 16 ? 12 : ((MODE & 2) ? 4 : 1)) batch_pipeline_kernel(PipelineArgs a) {
     constexpr bool occ_in_smem = MODE & 1, LOG = MODE & 2, BSM = MODE & 4, INB_SM = occ_in_smem && !(MODE & 8);
     constexpr bool LEAP = MODE & 16;
     static_assert(!(LEAP && LOG), "leap mode writes move_batch directly");
@@ -2167,7 +2342,9 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
             warps = 8;
             smem = (size_t)warps * per;
         } else {
-            warps = 4;
+            // one warp (instance) per CTA: ~180 registers per thread still
+            // keep 11 instances per SM resident
+            warps = 1;
         }
     } else if (occ_env && bm_bytes <= 96 * 1024) {
         mode = 1 | (a.mlog ? 2 : 0);

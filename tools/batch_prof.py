@@ -49,6 +49,10 @@ print("counts per instance:", {k2: out[k2] / n for k2 in names[5:9]})
 for a, b in (("leap_delta", "n_leap"), ("literal", "n_literal"), ("general", "n_general"), ("finish", "n_finish")):
     if out[b]:
         print(f"  {a}: {out[a] / max(1, out[b] if a != 'leap_delta' else out['n_leap'] + out['n_literal']):.0f} cycles per")
+if v[12]:
+    print(f"  finish detail: successor loads {v[10] / v[12]:.0f}, decrements+records+lanes {v[11] / v[12]:.0f} cycles per finish")
+if v[14]:
+    print(f"  early finishes: {v[14] / n:.0f} per instance, release_fill {v[13] / v[14]:.0f} cycles")
 if wv[4]:
     nbw = wv[3]
     print(f"wide: {wv[4]} instances, {nbw / wv[4]:.0f} batches each; cycles per batch: "
