@@ -378,15 +378,18 @@ __global__ void __launch_bounds__(WT, 2) batch_wide_kernel(PipelineArgs a, int r
                     bool rel[G];
                     int4 pr[G];
                     int qe[G];
+                    int old[G];
 #pragma unroll
                     for (int c = 0; c < G; ++c) {
-                        rel[c] = false;
-                        if (c < nsl && sc[c] >= 0) {
+                        const bool ok = c < nsl && sc[c] >= 0;
+                        if (ok) {
                             pr[c] = __ldg(prec + sc[c]);
                             qe[c] = slen ? __ldg(slen + sc[c]) : __ldg(&prec[sc[c] + 1].w);
-                            rel[c] = atomicSub(&blk[sc[c]], 1) == 1;
                         }
+                        old[c] = (int)atom_add_if(ok, reinterpret_cast<uint32_t *>(blk + max(sc[c], 0)), 0xffffffffu);
                     }
+#pragma unroll
+                    for (int c = 0; c < G; ++c) rel[c] = c < nsl && sc[c] >= 0 && old[c] == 1;
 #pragma unroll
                     for (int c = 0; c < G; ++c) {
                         if (!rel[c]) continue;

@@ -41,8 +41,8 @@ namespace rb {
 // [0] windows [1] stalled windows [2] overflowed plans [3] literal batches
 // [4] batches [5] plan cycles [6] replay cycles [7] instances [8] finishers
 // [9] plan rounds [10] other cycles (literal batches) [11] commit cycles
-// [12] plan: finisher scan [13] pass 1 [14] pass 2 [15] pass 3
-__device__ unsigned long long g_window_prof[16];
+// [12] plan: finisher scan [13] pass 1 [14] pass 2 [15] pass 3 [16] pass 1's successor ranges
+__device__ unsigned long long g_window_prof[20];
 
 namespace {
 
@@ -53,6 +53,10 @@ constexpr int EPT = 4;          // entries per thread in the replay: rmax <= EPT
 #define RECON_WIN_G 5
 #endif
 constexpr int G = RECON_WIN_G;  // chunks of 32 successor ids per warp in flight (experiments: -DRECON_WIN_G)
+#ifndef RECON_WIN_PC
+#define RECON_WIN_PC 8
+#endif
+constexpr int PC = RECON_WIN_PC;  // successors per piece (a thread's loads, then its decrements, in flight)
 constexpr int LMAX = 128;       // window length cap (offsets fit a byte)
 constexpr int LINIT = 16;
 constexpr int32_t VMIN_EMPTY = 0x7f7f7f7f;
@@ -103,7 +107,7 @@ struct WinBufs {
 
 __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int rmax) {
     extern __shared__ __align__(16) unsigned char wsm[];
-    __shared__ int s_cnt, s_nf, s_ovf, s_nacc, s_contend, s_maxfin;
+    __shared__ int s_cnt, s_nf, s_ovf, s_nacc, s_contend, s_maxfin, s_nx;
     __shared__ unsigned long long s_left;
     const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
     const int W = a.W, H = a.H;
@@ -140,6 +144,20 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
         const int32_t *slen = a.slen ? a.slen + o : nullptr;  // list lengths (else up to the next list)
         int32_t *vmin = a.vmin + (int64_t)inst * WH;
 
+#ifdef RECON_BATCH_PROF
+        unsigned long long wp[20] = {};
+        long long wt = clock64();
+#define WINPROF(i)                        \
+    do {                                  \
+        const long long t_ = clock64();   \
+        wp[i] += t_ - wt;                 \
+        wt = t_;                          \
+    } while (0)
+#define WINCOUNT(i, v) (wp[i] += (v))
+#else
+#define WINPROF(i) (void)0
+#define WINCOUNT(i, v) (void)0
+#endif
         // appends entry i of list X (shared memory, or the staging area past rmax)
         auto put = [&](const WinBufs &X, int i, int4 r, int base, int st) {
             if (i < rmax) {
@@ -210,99 +228,99 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
                 if ((x >> 8) == (uint32_t)v + 1) return (int)h;
             }
         };
+        // Passes 1 and 2 run a thread per finisher over pieces of PC successors
+        // (a warp per finisher spends most of its instructions gathering
+        // chunks); the pieces past a finisher's first go to the list xl and
+        // are taken by all threads after a barrier.
+        //
         // pass 1 of a release round: the successors of finishers F[f0, f1)
-        // {pid, finish offset, q0, qn} lose a blocker (global counts); a path
-        // whose count reaches 0 is appended to A as a placeholder {pid} (and
-        // in a plan, keyed into the release hash)
-        auto release_pass1 = [&](const WinBufs &A, int4 *F, int f0, int f1, bool plan, int pmax) {
-            // successor ranges of the finishers, one thread each
-            for (int f = f0 + tid; f < f1; f += WT) {
-                const int pid = F[f].x;
-                const int q0 = __ldg(&prec[pid].w), qn = slen ? __ldg(slen + pid) : __ldg(&prec[pid + 1].w) - q0;
-                F[f].z = q0;
-                F[f].w = qn;
-                prefetch_l2(succ + q0, qn * 4);  // (the lists are read by warps below, twice in a plan)
-            }
-            __syncthreads();
-            // warp w: finishers w, w + NW, ...; G chunks of 32 successor ids
-            // are gathered as addresses, then loaded together, then decremented
-            int ad[G];
-            int nsl = 0;
-            auto flush = [&]() {
-                int v[G], r[G];
+        // {pid, finish offset, q0, qn} lose a blocker (global counts, issued
+        // back to back); a path whose count reaches 0 is appended to A as a
+        // placeholder {pid} (and in a plan, keyed into the release hash)
+        auto dec_piece = [&](const WinBufs &A, int q0, int lo, int hi, bool plan, int pmax) {
+            int v[PC], r[PC];
 #pragma unroll
-                for (int c = 0; c < G; ++c) v[c] = c < nsl && ad[c] >= 0 ? __ldg(succ + ad[c]) : -1;
+            for (int c = 0; c < PC; ++c) v[c] = lo + c < hi ? __ldg(succ + q0 + lo + c) : -1;
 #pragma unroll
-                for (int c = 0; c < G; ++c)
-                    r[c] = v[c] >= 0 ? atomicSub(&b16[v[c] >> 1], (v[c] & 1) ? 0x10000u : 1u) >> ((v[c] & 1) * 16) & 0xffffu : 0;
+            for (int c = 0; c < PC; ++c)
+                r[c] = (int)atom_add_if(v[c] >= 0, &b16[max(v[c], 0) >> 1], (v[c] & 1) ? 0xffff0000u : 0xffffffffu);
 #pragma unroll
-                for (int c = 0; c < G; ++c) {
-                    if (r[c] != 1) continue;
-                    const int i = atomicAdd(&s_cnt, 1);
-                    if (i >= pmax) {
-                        s_ovf = 1;
-                    } else if (i >= rmax) {  // (literal batch) past shared memory: the staging area
-                        stg[i].x = v[c];
-                        s_ovf = 1;
-                    } else {
-                        A.rec[i].x = v[c];
-                        if (plan) {
-                            const unsigned fb = fbit(v[c]);
-                            atomicOr(&filt[fb >> 5], 1u << (fb & 31));
-                            unsigned h = hslot(v[c]);
-                            while (atomicCAS(&hk[h], 0u, (uint32_t)(v[c] + 1) << 8) != 0u)
-                                h = (h + 1) & (unsigned)(hcap - 1);
-                        }
+            for (int c = 0; c < PC; ++c) {
+                if (v[c] < 0 || ((unsigned)r[c] >> ((v[c] & 1) * 16) & 0xffffu) != 1u) continue;
+                const int i = atomicAdd(&s_cnt, 1);
+                if (i >= pmax) {
+                    s_ovf = 1;
+                } else if (i >= rmax) {  // (literal batch) past shared memory: the staging area
+                    stg[i].x = v[c];
+                    s_ovf = 1;
+                } else {
+                    A.rec[i].x = v[c];
+                    if (plan) {
+                        const unsigned fb = fbit(v[c]);
+                        atomicOr(&filt[fb >> 5], 1u << (fb & 31));
+                        unsigned h = hslot(v[c]);
+                        while (atomicCAS(&hk[h], 0u, (uint32_t)(v[c] + 1) << 8) != 0u) h = (h + 1) & (unsigned)(hcap - 1);
                     }
                 }
-                nsl = 0;
-            };
-            for (int f = f0 + warp; f < f1; f += NW) {
-                const int q0 = F[f].z, qn = F[f].w;
-                for (int j0 = 0; j0 < qn; j0 += 32) {
-                    const int x = j0 + lane < qn ? q0 + j0 + lane : -1;
-#pragma unroll
-                    for (int c = 0; c < G; ++c)
-                        if (c == nsl) ad[c] = x;
-                    if (++nsl == G) flush();
-                }
             }
-            if (nsl) flush();
         };
-        // pass 2 (plan): each released path's latest blocker finish in the
-        // window, over all finishers so far (a path released in this round
-        // may have blockers from earlier rounds)
-        auto release_pass2 = [&](const int4 *F, int f1) {
-            int ad[G], fn[G];
-            int nsl = 0;
-            auto flush = [&]() {
-                int v[G];
+        // pass 2 piece: the released successors' latest blocker finish
+        auto max_piece = [&](int q0, int lo, int hi, int fin) {
+            int v[PC];
 #pragma unroll
-                for (int c = 0; c < G; ++c) v[c] = c < nsl && ad[c] >= 0 ? __ldg(succ + ad[c]) : -1;
+            for (int c = 0; c < PC; ++c) v[c] = lo + c < hi ? __ldg(succ + q0 + lo + c) : -1;
 #pragma unroll
-                for (int c = 0; c < G; ++c) {
-                    if (v[c] < 0) continue;
-                    const unsigned fb = fbit(v[c]);
-                    if (!(filt[fb >> 5] >> (fb & 31) & 1u)) continue;
-                    const int h = hfind(v[c]);
-                    if (h >= 0) atomicMax(&hk[h], ((uint32_t)(v[c] + 1) << 8) | (uint32_t)fn[c]);
+            for (int c = 0; c < PC; ++c) {
+                if (v[c] < 0) continue;
+                const unsigned fb = fbit(v[c]);
+                if (!(filt[fb >> 5] >> (fb & 31) & 1u)) continue;
+                const int h = hfind(v[c]);
+                if (h >= 0) atomicMax(&hk[h], ((uint32_t)(v[c] + 1) << 8) | (uint32_t)fin);
+            }
+        };
+        // runs op(f, q0, lo, hi) over the pieces of finishers F[f0, f1):
+        // first pieces inline, the rest from xl[0, xcap) after a barrier
+        // (or inline when xl is full)
+        auto for_pieces = [&](int4 *F, int f0, int f1, uint32_t *xl, int xcap, bool ranges, auto op) {
+            if (tid == 0) s_nx = 0;
+            __syncthreads();
+            for (int f = f0 + tid; f < f1; f += WT) {
+                int q0, qn;
+                if (ranges) {
+                    const int pid = F[f].x;
+                    q0 = __ldg(&prec[pid].w);
+                    qn = slen ? __ldg(slen + pid) : __ldg(&prec[pid + 1].w) - q0;
+                    F[f].z = q0;
+                    F[f].w = qn;
+                } else {
+                    q0 = F[f].z;
+                    qn = F[f].w;
                 }
-                nsl = 0;
-            };
-            for (int f = warp; f < f1; f += NW) {
-                const int4 fr = F[f];
-                for (int j0 = 0; j0 < fr.w; j0 += 32) {
-                    const int x = j0 + lane < fr.w ? fr.z + j0 + lane : -1;
-#pragma unroll
-                    for (int c = 0; c < G; ++c)
-                        if (c == nsl) {
-                            ad[c] = x;
-                            fn[c] = fr.y;
-                        }
-                    if (++nsl == G) flush();
+                op(f, q0, 0, min(qn, PC));
+                for (int pc = 1; pc * PC < qn; ++pc) {
+                    const int x = atomicAdd(&s_nx, 1);
+                    if (x < xcap && pc < 256)
+                        xl[x] = (uint32_t)f << 8 | (uint32_t)pc;
+                    else
+                        op(f, q0, pc * PC, min(qn, (pc + 1) * PC));
                 }
             }
-            if (nsl) flush();
+            __syncthreads();
+            const int nx = min(s_nx, xcap);
+            for (int x = tid; x < nx; x += WT) {
+                const int f = (int)(xl[x] >> 8), pc = (int)(xl[x] & 255u);
+                const int q0 = F[f].z, qn = F[f].w;
+                op(f, q0, pc * PC, min(qn, (pc + 1) * PC));
+            }
+        };
+        auto release_pass1 = [&](const WinBufs &A, int4 *F, int f0, int f1, bool plan, int pmax, uint32_t *xl, int xcap) {
+            for_pieces(F, f0, f1, xl, xcap, true,
+                       [&](int, int q0, int lo, int hi) { dec_piece(A, q0, lo, hi, plan, pmax); });
+        };
+        // pass 2 (plan): over all finishers so far (a path released in this
+        // round may have blockers from earlier rounds)
+        auto release_pass2 = [&](int4 *F, int f1, uint32_t *xl, int xcap) {
+            for_pieces(F, 0, f1, xl, xcap, false, [&](int f, int q0, int lo, int hi) { max_piece(q0, lo, hi, F[f].y); });
         };
         // pass 3: placeholders A[i0, i1) become entries; start offset = 1 +
         // latest blocker finish in the window (plan), or 1 (literal batch);
@@ -384,20 +402,6 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
         int cur = 0, nb = 0, status = RECON_OK, L = LINIT;
         bool hand = false;  // (uniform) hand the ready set to the warp kernel
         int hand_n = 0;
-#ifdef RECON_BATCH_PROF
-        unsigned long long wp[16] = {};
-        long long wt = clock64();
-#define WINPROF(i)                        \
-    do {                                  \
-        const long long t_ = clock64();   \
-        wp[i] += t_ - wt;                 \
-        wt = t_;                          \
-    } while (0)
-#define WINCOUNT(i, v) (wp[i] += (v))
-#else
-#define WINPROF(i) (void)0
-#define WINCOUNT(i, v) (void)0
-#endif
         for (;;) {
             WinBufs A = bufs(cur), B = bufs(cur ^ 1);
             int4 *F = B.rec;  // finisher list {pid, finish offset, q0, qn}
@@ -436,13 +440,15 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
             const int pmax = min(rmax, R + hcap * 3 / 4);  // (hash load <= 3/4)
             hk = (uint32_t *)B.base;
             filt = hk + hcap;
+            uint32_t *xl = filt + hcap / 2;  // extra pieces (the rest of B's move bases)
+            const int xcap = rmax - hcap - hcap / 2;
             for (int h = tid; h < hcap + hcap / 2; h += WT) hk[h] = 0u;
             __syncthreads();
             WINPROF(12);
             while (f0 < f1) {
                 WINCOUNT(9, 1);
                 const int i0 = s_cnt;
-                release_pass1(A, F, f0, f1, true, pmax);
+                release_pass1(A, F, f0, f1, true, pmax, xl, xcap);
                 __syncthreads();
                 WINPROF(13);
                 const int i1 = min(s_cnt, pmax);
@@ -452,7 +458,7 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
                     break;
                 }
                 if (i1 > i0) {
-                    release_pass2(F, f1);
+                    release_pass2(F, f1, xl, xcap);
                     __syncthreads();
                     WINPROF(14);
                     release_pass3(A, F, i0, i1, true, L);
@@ -531,12 +537,28 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
                     for (int i = 0; i < EPT; ++i)
                         if (claimed >> i & 1u) {
                             atomicAnd(&occ[cur_v[i] >> 5], ~(1u << (cur_v[i] & 31)));
-                            __stcs(mb + base[i] + (lk[i] & 0xffff), nb + t);
                             cur_v[i] = to[i];
                             ++lk[i];
                             ++moves;
                         }
                     __syncthreads();
+                }
+                // the window's schedule: an entry moved in consecutive batches
+                // from its start offset on, so its moves are one run of
+                // consecutive slots and batch indices, stored 16 bytes at a
+                // time where aligned
+#pragma unroll
+                for (int i = 0; i < EPT; ++i) {
+                    const int e = tid + i * WT;
+                    if (e >= Rw) continue;
+                    const int klo = A.rec[e].y & 0xffff;
+                    const int n = (lk[i] & 0xffff) - klo, b0 = nb + (int)(gm[i] >> 24);
+                    int32_t *d = mb + base[i] + klo;
+                    int j = 0;
+                    for (; j < n && ((uintptr_t)(d + j) & 15u); ++j) __stcs(d + j, b0 + j);
+                    for (; j + 4 <= n; j += 4)
+                        __stcs(reinterpret_cast<int4 *>(d + j), make_int4(b0 + j, b0 + j + 1, b0 + j + 2, b0 + j + 3));
+                    for (; j < n; ++j) __stcs(d + j, b0 + j);
                 }
                 moves = warp_sum(moves);
                 if (lane == 0 && moves) atomicAdd(&s_nacc, moves);
@@ -661,7 +683,7 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
                 WINCOUNT(4, 1);
                 {
                     const int i0 = s_cnt;
-                    release_pass1(A, F, 0, s_nf, false, S);
+                    release_pass1(A, F, 0, s_nf, false, S, (uint32_t *)B.base, rmax);
                     __syncthreads();
                     release_pass3(A, F, i0, s_cnt, false, 1);
                     __syncthreads();
@@ -711,7 +733,7 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
         }
 #ifdef RECON_BATCH_PROF
         if (tid == 0) {
-            for (int i = 0; i < 16; ++i)
+            for (int i = 0; i < 20; ++i)
                 if (i != 7) atomicAdd(&g_window_prof[i], wp[i]);
             atomicAdd(&g_window_prof[7], 1ull);
         }
@@ -770,7 +792,7 @@ cudaError_t launch_batch_window(const PipelineArgs &a, int sms, int rmax, size_t
 extern "C" int recon_debug_window_prof(unsigned long long *out, int reset) {
     if (cudaMemcpyFromSymbol(out, rb::g_window_prof, sizeof(rb::g_window_prof)) != cudaSuccess) return -1;
     if (reset) {
-        static const unsigned long long z[16] = {};
+        static const unsigned long long z[20] = {};
         if (cudaMemcpyToSymbol(rb::g_window_prof, z, sizeof(z)) != cudaSuccess) return -1;
     }
     return 0;

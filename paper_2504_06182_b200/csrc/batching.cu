@@ -779,22 +779,16 @@ __global__ void fillptr_kernel(int64_t n, const int64_t *soff, unsigned long lon
 // rule-1 part; slen (the out-degree array, free after the walk) = the list's
 // length.  Lists stay at their offsets, so paths are independent.
 __global__ void pl_compact_kernel(PipelineArgs a) {
-    const int lane = lane_id();
     const int64_t S = (int64_t)a.W * a.k, N = (int64_t)a.count * S;
-    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const unsigned long long *fillp = reinterpret_cast<const unsigned long long *>(a.rec);
-    for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp_id(); t < N; t += nwarps) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t inst = t / S;
         if (a.solve_status[inst] != 0 || t - inst * S >= a.path_count[inst]) continue;
         const int64_t s0 = a.soff[t];
         const int n1 = (int)((int64_t)fillp[t] - s0), cap1 = a.outdeg[t], n2 = a.mfr[t];
-        if (n1 < cap1)  // (chunks in ascending order: a chunk's destination never overlaps a later source)
-            for (int r0 = 0; r0 < n2; r0 += 32) {
-                const int v = r0 + lane < n2 ? a.succ[s0 + cap1 + r0 + lane] : 0;
-                __syncwarp();
-                if (r0 + lane < n2) a.succ[s0 + n1 + r0 + lane] = v;
-            }
-        if (lane == 0) a.outdeg[t] = n1 + n2;
+        if (n1 < cap1)  // (ascending: a destination never overlaps a later source)
+            for (int r = 0; r < n2; ++r) a.succ[s0 + n1 + r] = a.succ[s0 + cap1 + r];
+        a.outdeg[t] = n1 + n2;
     }
 }
 
@@ -1124,6 +1118,12 @@ struct Blockers {
                      : "memory");
         return (int)((old >> sh) & 0xffffu);
     }
+    // release_raw when `pred`, else 0: global counts issue back to back
+    // (atom_add_if), so a run of these costs one round trip
+    __device__ __forceinline__ int release_raw_if(bool pred, int p) const {
+        if (!BSM) return (int)atom_add_if(pred, reinterpret_cast<uint32_t *>(g + max(p, 0)), 0xffffffffu);
+        return pred ? release_raw(p) : 0;
+    }
     __device__ __forceinline__ bool release(int p) const {
         if (!BSM) return atomicSub(&g[p], 1) == 1;
         const uint32_t sh = (uint32_t)(p & 1) * 16u;
@@ -1305,9 +1305,12 @@ __device__ __forceinline__ int release_successors_buf(const BatchJob &J, const B
             const int ob = __shfl_sync(FULL, base, owner);
             sc[c] = t < tot ? __ldg(J.succ + oq0 + (t - ob)) : -1;
         }
+        int old[G];
+#pragma unroll
+        for (int c = 0; c < G; ++c) old[c] = blockers.release_raw_if(sc[c] >= 0, sc[c]);
         bool rel[G];
 #pragma unroll
-        for (int c = 0; c < G; ++c) rel[c] = sc[c] >= 0 && blockers.release(sc[c]);
+        for (int c = 0; c < G; ++c) rel[c] = sc[c] >= 0 && old[c] == 1;
 #pragma unroll
         for (int c = 0; c < G; ++c) {
             const unsigned rm = __ballot_sync(FULL, rel[c]);
@@ -1351,17 +1354,20 @@ __device__ __forceinline__ int release_into_lanes(const BatchJob &J, const BL &b
         int4 pr[G];
         int qe[G];
         bool rel[G];
+        int old[G];
 #pragma unroll
         for (int c = 0; c < G; ++c) {
-            rel[c] = false;
+            const bool ok = c < nsl && sc[c] >= 0;
             pr[c] = make_int4(0, 0, 0, 0);
             qe[c] = 0;
-            if (c < nsl && sc[c] >= 0) {
+            if (ok) {
                 pr[c] = __ldg(J.prec + sc[c]);
                 qe[c] = J.slen ? __ldg(J.slen + sc[c]) : __ldg(&J.prec[sc[c] + 1].w);
-                rel[c] = blockers.release(sc[c]);
             }
+            old[c] = blockers.release_raw_if(ok, sc[c]);
         }
+#pragma unroll
+        for (int c = 0; c < G; ++c) rel[c] = c < nsl && sc[c] >= 0 && old[c] == 1;
 #pragma unroll
         for (int c = 0; c < G; ++c) {
             if (c >= nsl) break;
@@ -1468,14 +1474,13 @@ template <class BL>
 __device__ __forceinline__ void release_issue(const BatchJob &J, const BL &blockers, EarlyRelease &er) {
 #pragma unroll
     for (int c = 0; c < EG; ++c) {
-        er.old[c] = 0;
         er.pr[c] = make_int4(0, 0, 0, 0);
         er.qe[c] = 0;
         if (er.sc[c] >= 0) {
             er.pr[c] = __ldcg(J.prec + er.sc[c]);
             er.qe[c] = J.slen ? __ldcg(J.slen + er.sc[c]) : __ldcg(&J.prec[er.sc[c] + 1].w);
-            er.old[c] = blockers.release_raw(er.sc[c]);
         }
+        er.old[c] = blockers.release_raw_if(er.sc[c] >= 0, er.sc[c]);
     }
 }
 

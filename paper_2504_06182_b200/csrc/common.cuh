@@ -53,6 +53,19 @@ __device__ __forceinline__ int warp_excl_scan(int v, int *total) {
     return x - v;
 }
 
+// predicated atomic add that returns the old value without a branch: a run of
+// these issues back to back (a conditional atomicAdd becomes a branch, and
+// ptxas then places the first use of each result right after its atomic,
+// one round trip per atomic)
+__device__ __forceinline__ uint32_t atom_add_if(bool p, uint32_t *addr, uint32_t v) {
+    uint32_t r = 0;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q atom.global.add.u32 %0, [%1], %3;\n\t}"
+                 : "+r"(r)
+                 : "l"(addr), "r"((uint32_t)p), "r"(v)
+                 : "memory");
+    return r;
+}
+
 // pulls [p, p + bytes) into L2 ahead of use (no register result, never stalls)
 __device__ __forceinline__ void prefetch_l2(const void *p, int bytes) {
     const char *c = static_cast<const char *>(p);
