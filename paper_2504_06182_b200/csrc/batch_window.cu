@@ -56,7 +56,13 @@ constexpr int G = RECON_WIN_G;  // chunks of 32 successor ids per warp in flight
 #ifndef RECON_WIN_PC
 #define RECON_WIN_PC 8
 #endif
-constexpr int PC = RECON_WIN_PC;  // successors per piece (a thread's loads, then its decrements, in flight)
+constexpr int PC = RECON_WIN_PC;
+// release offsets through a per-path tag array raised (red.max) with each
+// decrement, instead of a second pass against a shared hash of the released ids
+#ifndef RECON_WIN_TMAX
+#define RECON_WIN_TMAX 0
+#endif
+constexpr bool TMAX = RECON_WIN_TMAX;  // successors per piece (a thread's loads, then its decrements, in flight)
 constexpr int LMAX = 128;       // window length cap (offsets fit a byte)
 constexpr int LINIT = 16;
 constexpr int32_t VMIN_EMPTY = 0x7f7f7f7f;
@@ -136,6 +142,7 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
         // random-access footprint: the counts of the ~300 instances in flight
         // then stay in L2); unpacked into blk for the warp kernel at the end
         uint32_t *b16 = (uint32_t *)(a.mto + o);
+        uint32_t *tmax = (uint32_t *)(a.mem + o);  // TMAX: window id << 8 | latest blocker finish offset
         int32_t *mb = a.move_batch + (int64_t)inst * a.move_stride;
         const int4 *prec = a.prec + (int64_t)inst * (S + 1);  // path records (batching.cu prec_kernel)
         int4 *stg = a.rec2 + o;                               // hand-off staging (and overflow past rmax)
@@ -187,6 +194,7 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
                 const int4 r = prec[p];
                 const int len = rec_len(r);
                 myleft += len;
+                if (TMAX) tmax[p] = 0u;
                 if (len == 0) {
                     zero_len = 1;  // zero-length paths: the warp kernel's init releases them
                 } else if (blk[p] == 0) {
@@ -199,6 +207,7 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
                 b16[w] = (uint32_t)lo | (uint32_t)hi << 16;
             }
             if (zero_len) s_ovf = 1;
+            if (TMAX) __threadfence();
             myleft = warp_sum64(myleft);
             if (lane == 0) atomicAdd(&s_left, (unsigned long long)myleft);
             for (int64_t w = tid; w < nwb; w += WT) occ[w] = a.occ[(int64_t)inst * nwb + w];
@@ -237,10 +246,14 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
         // {pid, finish offset, q0, qn} lose a blocker (global counts, issued
         // back to back); a path whose count reaches 0 is appended to A as a
         // placeholder {pid} (and in a plan, keyed into the release hash)
-        auto dec_piece = [&](const WinBufs &A, int q0, int lo, int hi, bool plan, int pmax) {
+        auto dec_piece = [&](const WinBufs &A, int q0, int lo, int hi, bool plan, int pmax, uint32_t tag) {
             int v[PC], r[PC];
 #pragma unroll
             for (int c = 0; c < PC; ++c) v[c] = lo + c < hi ? __ldg(succ + q0 + lo + c) : -1;
+            if (TMAX && plan)
+#pragma unroll
+                for (int c = 0; c < PC; ++c)
+                    if (v[c] >= 0) asm volatile("red.global.max.u32 [%0], %1;" ::"l"(tmax + v[c]), "r"(tag) : "memory");
 #pragma unroll
             for (int c = 0; c < PC; ++c)
                 r[c] = (int)atom_add_if(v[c] >= 0, &b16[max(v[c], 0) >> 1], (v[c] & 1) ? 0xffff0000u : 0xffffffffu);
@@ -255,7 +268,7 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
                     s_ovf = 1;
                 } else {
                     A.rec[i].x = v[c];
-                    if (plan) {
+                    if (plan && !TMAX) {
                         const unsigned fb = fbit(v[c]);
                         atomicOr(&filt[fb >> 5], 1u << (fb & 31));
                         unsigned h = hslot(v[c]);
@@ -285,6 +298,9 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
             if (tid == 0) s_nx = 0;
             __syncthreads();
             for (int f = f0 + tid; f < f1; f += WT) {
+#ifdef RECON_BATCH_PROF
+                const long long pt0 = clock64();
+#endif
                 int q0, qn;
                 if (ranges) {
                     const int pid = F[f].x;
@@ -296,7 +312,17 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
                     q0 = F[f].z;
                     qn = F[f].w;
                 }
+#ifdef RECON_BATCH_PROF
+                const long long pt1 = clock64();
+#endif
                 op(f, q0, 0, min(qn, PC));
+#ifdef RECON_BATCH_PROF
+                if (ranges && tid == 0) {
+                    wp[17] += (unsigned long long)(pt1 - pt0);
+                    wp[18] += (unsigned long long)(clock64() - pt1);
+                    wp[19] += 1;
+                }
+#endif
                 for (int pc = 1; pc * PC < qn; ++pc) {
                     const int x = atomicAdd(&s_nx, 1);
                     if (x < xcap && pc < 256)
@@ -313,9 +339,11 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
                 op(f, q0, pc * PC, min(qn, (pc + 1) * PC));
             }
         };
-        auto release_pass1 = [&](const WinBufs &A, int4 *F, int f0, int f1, bool plan, int pmax, uint32_t *xl, int xcap) {
+        auto release_pass1 = [&](const WinBufs &A, int4 *F, int f0, int f1, bool plan, int pmax, uint32_t *xl, int xcap,
+                                 uint32_t wtag) {
             for_pieces(F, f0, f1, xl, xcap, true,
-                       [&](int, int q0, int lo, int hi) { dec_piece(A, q0, lo, hi, plan, pmax); });
+                       [&](int f, int q0, int lo, int hi) { dec_piece(A, q0, lo, hi, plan, pmax, wtag | (uint32_t)F[f].y); });
+            if (TMAX && plan) __threadfence();  // the raises before pass 3 reads them (after a barrier)
         };
         // pass 2 (plan): over all finishers so far (a path released in this
         // round may have blockers from earlier rounds)
@@ -325,13 +353,17 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
         // pass 3: placeholders A[i0, i1) become entries; start offset = 1 +
         // latest blocker finish in the window (plan), or 1 (literal batch);
         // plan releases that finish inside [0, L) join F (the cascade)
-        auto release_pass3 = [&](const WinBufs &A, int4 *F, int i0, int i1, bool plan, int L) {
+        auto release_pass3 = [&](const WinBufs &A, int4 *F, int i0, int i1, bool plan, int L, uint32_t wtag) {
             for (int i = i0 + tid; i < i1; i += WT) {
                 const int j = i < rmax ? A.rec[i].x : stg[i].x;
                 const int4 pr = __ldg(prec + j);
                 const int len = rec_len(pr);
                 int tj = 1;
-                if (plan) {
+                if (plan && TMAX) {
+                    const unsigned tm = __ldcg(tmax + j);
+                    RB_CHECK((tm & ~0xffu) == wtag, "window: release tag of another window");
+                    tj = (int)(tm & 0xffu) + 1;
+                } else if (plan) {
                     const int h = hfind(j);
                     RB_CHECK(h >= 0, "window: released path missing from the hash");
                     tj = (int)(hk[h] & 0xffu) + 1;
@@ -400,6 +432,7 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
         };
 
         int cur = 0, nb = 0, status = RECON_OK, L = LINIT;
+        unsigned wid = 0;  // plan id (TMAX tags; < 2^24)
         bool hand = false;  // (uniform) hand the ready set to the warp kernel
         int hand_n = 0;
         for (;;) {
@@ -437,18 +470,20 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
             __syncthreads();
             int f0 = 0, f1 = s_nf, ovf = 0;
             __syncthreads();
-            const int pmax = min(rmax, R + hcap * 3 / 4);  // (hash load <= 3/4)
+            ++wid;
+            const int pmax = TMAX ? rmax : min(rmax, R + hcap * 3 / 4);  // (hash load <= 3/4)
             hk = (uint32_t *)B.base;
             filt = hk + hcap;
-            uint32_t *xl = filt + hcap / 2;  // extra pieces (the rest of B's move bases)
-            const int xcap = rmax - hcap - hcap / 2;
-            for (int h = tid; h < hcap + hcap / 2; h += WT) hk[h] = 0u;
+            uint32_t *xl = TMAX ? hk : filt + hcap / 2;  // extra pieces (the rest of B's move bases)
+            const int xcap = TMAX ? rmax : rmax - hcap - hcap / 2;
+            if (!TMAX)
+                for (int h = tid; h < hcap + hcap / 2; h += WT) hk[h] = 0u;
             __syncthreads();
             WINPROF(12);
             while (f0 < f1) {
                 WINCOUNT(9, 1);
                 const int i0 = s_cnt;
-                release_pass1(A, F, f0, f1, true, pmax, xl, xcap);
+                release_pass1(A, F, f0, f1, true, pmax, xl, xcap, wid << 8);
                 __syncthreads();
                 WINPROF(13);
                 const int i1 = min(s_cnt, pmax);
@@ -458,10 +493,12 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
                     break;
                 }
                 if (i1 > i0) {
-                    release_pass2(F, f1, xl, xcap);
-                    __syncthreads();
+                    if (!TMAX) {
+                        release_pass2(F, f1, xl, xcap);
+                        __syncthreads();
+                    }
                     WINPROF(14);
-                    release_pass3(A, F, i0, i1, true, L);
+                    release_pass3(A, F, i0, i1, true, L, wid << 8);
                     __syncthreads();
                     WINPROF(15);
                 }
@@ -683,9 +720,9 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
                 WINCOUNT(4, 1);
                 {
                     const int i0 = s_cnt;
-                    release_pass1(A, F, 0, s_nf, false, S, (uint32_t *)B.base, rmax);
+                    release_pass1(A, F, 0, s_nf, false, S, (uint32_t *)B.base, rmax, 0u);
                     __syncthreads();
-                    release_pass3(A, F, i0, s_cnt, false, 1);
+                    release_pass3(A, F, i0, s_cnt, false, 1, 0u);
                     __syncthreads();
                 }
                 const int Rl = s_cnt, lovf = s_ovf;
@@ -719,7 +756,7 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
                 if (left == 0) break;
             } else {
                 // next window length: double while the releases leave room
-                const int nrel = Rw - R0, relcap = min(rmax - rmax / 8 - R, hcap * 5 / 8);
+                const int nrel = Rw - R0, relcap = TMAX ? rmax - rmax / 8 - R : min(rmax - rmax / 8 - R, hcap * 5 / 8);
                 if (L < LMAX && 2 * nrel + 32 < relcap)
                     L = min(LMAX, 2 * L);
                 else if (L > 1 && nrel > relcap)

@@ -530,10 +530,10 @@ static inline CoverArrays pipeline_cover_arrays(const PipelineArgs &a) {
 __global__ void pl_mark2_kernel(PipelineArgs a, int32_t *mc, int32_t *mr, CoverArrays cv) {
     const int64_t S = (int64_t)a.W * a.k, WH = (int64_t)a.W * a.H, nwb = (WH + 31) / 32;
     const int W = a.W, H = a.H;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)a.count * S;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t inst = t / S;
-        const int p = (int)(t % S);
+    for (InstIter it(blockIdx.x * (int64_t)blockDim.x + threadIdx.x, S, (int64_t)gridDim.x * blockDim.x);
+         it.t < (int64_t)a.count * S; it.next()) {
+        const int64_t t = it.t, inst = it.inst;
+        const int p = it.i;
         if (a.solve_status[inst] != 0 || p >= a.path_count[inst]) continue;
         const int s = a.path_src[t], d = a.path_dst[t];
         const int xs = s / H, ys = s - xs * H, xd = d / H, yd = d - xd * H;
@@ -624,10 +624,10 @@ __device__ __forceinline__ int popc_range(const uint32_t *b, int64_t lo, int64_t
 __global__ void pl_degree_kernel(PipelineArgs a, CoverArrays cv) {
     const int64_t S = (int64_t)a.W * a.k, WH = (int64_t)a.W * a.H, nwb = (WH + 31) / 32;
     const int W = a.W, H = a.H;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)a.count * S;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t inst = t / S;
-        const int p = (int)(t % S);
+    for (InstIter it(blockIdx.x * (int64_t)blockDim.x + threadIdx.x, S, (int64_t)gridDim.x * blockDim.x);
+         it.t < (int64_t)a.count * S; it.next()) {
+        const int64_t t = it.t, inst = it.inst;
+        const int p = it.i;
         if (a.solve_status[inst] != 0 || p >= a.path_count[inst]) {
             a.outdeg[t] = 0;
             a.mfr[t] = 0;
@@ -673,9 +673,9 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_warp_kernel(Pipe
     const int64_t S = (int64_t)W * a.k, WH = (int64_t)W * H, N = (int64_t)a.count * S;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
     unsigned long long *fillp = reinterpret_cast<unsigned long long *>(a.rec);  // next free rule-1 slot per path
-    for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp_id(); t < N; t += nwarps) {
-        const int64_t inst = t / S, o = inst * S;
-        const int i = (int)(t - o);
+    for (InstIter it(blockIdx.x * (int64_t)(blockDim.x >> 5) + warp_id(), S, nwarps); it.t < N; it.next()) {
+        const int64_t t = it.t, inst = it.inst, o = inst * S;
+        const int i = it.i;
         if (a.solve_status[inst] != 0 || i >= a.path_count[inst]) continue;
         const int4 *pc = a.prec + inst * (S + 1);  // packed coordinates in .x / .y
         const int2 me = *reinterpret_cast<const int2 *>(pc + i);
@@ -781,9 +781,10 @@ __global__ void fillptr_kernel(int64_t n, const int64_t *soff, unsigned long lon
 __global__ void pl_compact_kernel(PipelineArgs a) {
     const int64_t S = (int64_t)a.W * a.k, N = (int64_t)a.count * S;
     const unsigned long long *fillp = reinterpret_cast<const unsigned long long *>(a.rec);
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t inst = t / S;
-        if (a.solve_status[inst] != 0 || t - inst * S >= a.path_count[inst]) continue;
+    for (InstIter it(blockIdx.x * (int64_t)blockDim.x + threadIdx.x, S, (int64_t)gridDim.x * blockDim.x); it.t < N;
+         it.next()) {
+        const int64_t t = it.t, inst = it.inst;
+        if (a.solve_status[inst] != 0 || it.i >= a.path_count[inst]) continue;
         const int64_t s0 = a.soff[t];
         const int n1 = (int)((int64_t)fillp[t] - s0), cap1 = a.outdeg[t], n2 = a.mfr[t];
         if (n1 < cap1)  // (ascending: a destination never overlaps a later source)
@@ -798,10 +799,10 @@ __global__ void pl_compact_kernel(PipelineArgs a) {
 // path's ranges
 __global__ void prec_kernel(PipelineArgs a) {
     const int64_t S = (int64_t)a.W * a.k, S1 = S + 1;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)a.count * S1;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t inst = t / S1;
-        const int p = (int)(t - inst * S1);
+    for (InstIter it(blockIdx.x * (int64_t)blockDim.x + threadIdx.x, S1, (int64_t)gridDim.x * blockDim.x);
+         it.t < (int64_t)a.count * S1; it.next()) {
+        const int64_t t = it.t, inst = it.inst;
+        const int p = it.i;
         const int P = a.solve_status[inst] != 0 ? 0 : a.path_count[inst];
         if (p > P) continue;
         const int64_t o = inst * S;
@@ -1700,6 +1701,7 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
     bool regmode = false;
     LanePath lp;
     lp.p = INT_MAX;
+    lp.pf = 0;
     // the lane's current move (fr -> to), advanced incrementally on acceptance
     int32_t fr = -1, to = -1;
     auto lane_move = [&]() {
@@ -1736,16 +1738,16 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
             // a lane that entered since the last leap: its successor ids now,
             // and after leap_delta their path records and blocker counts
             // into L2, so its finish (>= one leap away) decrements in L2
-            int pfv0 = -1, pfv1 = -1;
+            int pfv0 = -1, pfv1 = -1, pff = -1, pfn = 0;  // (pff: the lane, pfn: its successor count)
             if (LEAP) {
                 const unsigned pm = __ballot_sync(FULL, lp.p != INT_MAX && lp.pf);
                 if (pm) {
-                    const int f = __ffs(pm) - 1;
-                    const int64_t fq = __shfl_sync(FULL, lp.q0, f);
-                    const int fn = (int)(__shfl_sync(FULL, lp.q1, f) - fq);
-                    pfv0 = lane < fn ? __ldcg(J.succ + fq + lane) : -1;
-                    pfv1 = 32 + lane < fn ? __ldcg(J.succ + fq + 32 + lane) : -1;
-                    if (lane == f) lp.pf = 0;
+                    pff = __ffs(pm) - 1;
+                    const int64_t fq = __shfl_sync(FULL, lp.q0, pff);
+                    pfn = (int)(__shfl_sync(FULL, lp.q1, pff) - fq);
+                    pfv0 = lane < pfn ? __ldcg(J.succ + fq + lane) : -1;
+                    pfv1 = 32 + lane < pfn ? __ldcg(J.succ + fq + 32 + lane) : -1;
+                    if (lane == pff) lp.pf = 0;
                 }
             }
             const int delta = LEAP ? leap_delta(lp, H, fr, to, &movers) : 0;
@@ -1792,10 +1794,13 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
                 }
 #endif
                 const unsigned vm = movers;
-                for (unsigned m = vm; m; m &= m - 1) {
-                    const int o = __ffs(m) - 1;
-                    const int64_t b = __shfl_sync(FULL, lp.base + lp.k, o);
-                    for (int i = lane; i < delta; i += 32) __stcs(J.move_batch + b + i, nb + i);
+                if (valid) {  // the mover's run of `delta` slots, 16 bytes at a time where aligned
+                    int32_t *d = J.move_batch + lp.base + lp.k;
+                    int j = 0;
+                    for (; j < delta && ((uintptr_t)(d + j) & 15u); ++j) __stcs(d + j, nb + j);
+                    for (; j + 4 <= delta; j += 4)
+                        __stcs(reinterpret_cast<int4 *>(d + j), make_int4(nb + j, nb + j + 1, nb + j + 2, nb + j + 3));
+                    for (; j < delta; ++j) __stcs(d + j, nb + j);
                 }
                 if (early) release_issue(J, blk, er);
                 if (valid) {

@@ -66,6 +66,29 @@ __device__ __forceinline__ uint32_t atom_add_if(bool p, uint32_t *addr, uint32_t
     return r;
 }
 
+// grid-stride position over count x S items as (instance, index), advanced
+// without a 64-bit division per step
+struct InstIter {
+    int64_t t, inst, S, q;  // q, r: the stride in instances and items
+    int i, r;
+    int64_t stride;
+    __device__ __forceinline__ InstIter(int64_t start, int64_t S_, int64_t stride_) : t(start), S(S_), stride(stride_) {
+        inst = start / S_;
+        i = (int)(start - inst * S_);
+        q = stride_ / S_;
+        r = (int)(stride_ - q * S_);
+    }
+    __device__ __forceinline__ void next() {
+        t += stride;
+        inst += q;
+        i += r;
+        if (i >= S) {
+            i -= (int)S;
+            ++inst;
+        }
+    }
+};
+
 // pulls [p, p + bytes) into L2 ahead of use (no register result, never stalls)
 __device__ __forceinline__ void prefetch_l2(const void *p, int bytes) {
     const char *c = static_cast<const char *>(p);

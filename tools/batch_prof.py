@@ -27,7 +27,7 @@ solver, W, H, hp, k, seed, preset, ms = CASES[name]
 occ = sample_grids(seed, n, W, H, k)
 buf = (C.c_ulonglong * 16)()
 wbuf = (C.c_ulonglong * 8)()
-vbuf = (C.c_ulonglong * 16)()
+vbuf = (C.c_ulonglong * 20)()
 gpu.lib.recon_debug_batch_prof(buf, 1)
 gpu.lib.recon_debug_wide_prof(wbuf, 1)
 gpu.lib.recon_debug_window_prof(vbuf, 1)
@@ -64,6 +64,8 @@ if vv[7]:
           f"cycles per batch: plan {vv[5] / nbw:.0f}, replay {vv[6] / nbw:.0f}, commit {vv[11] / nbw:.0f}, "
           f"literal+other {vv[10] / nbw:.0f}; finishers per window {vv[8] / max(1, vv[0]):.0f}, "
           f"rounds per window {vv[9] / max(1, vv[0] + vv[2]):.2f}")
+    if vv[19]:
+        print(f"  pass1 first piece (thread 0): ranges {vv[17] / vv[19]:.0f}, piece {vv[18] / vv[19]:.0f} cycles")
     print(f"  plan per window: scan {vv[12] / max(1, vv[0]):.0f}, pass1 {vv[13] / max(1, vv[0]):.0f}, "
-          f"pass2 {vv[14] / max(1, vv[0]):.0f}, pass3 {vv[15] / max(1, vv[0]):.0f}, rest {vv[5] / max(1, vv[0]):.0f} cycles")
+          f"(ranges {vv[16] / max(1, vv[0]):.0f}), pass2 {vv[14] / max(1, vv[0]):.0f}, pass3 {vv[15] / max(1, vv[0]):.0f}, rest {vv[5] / max(1, vv[0]):.0f} cycles")
 print("batch_count", g["batch_count"][:4], "status", np.unique(g["status"]))
