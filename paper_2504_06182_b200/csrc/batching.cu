@@ -537,21 +537,18 @@ __global__ void pl_mark2_kernel(PipelineArgs a, int32_t *mc, int32_t *mr, CoverA
         if (a.solve_status[inst] != 0 || p >= a.path_count[inst]) continue;
         const int s = a.path_src[t], d = a.path_dst[t];
         const int xs = s / H, ys = s - xs * H, xd = d / H, yd = d - xd * H;
-        // owner maps, 16 B per vertex: {source owner, target owner, the source
-        // owner's target coordinates, the target owner's source coordinates},
+        // owner maps, 16 B per vertex: {source owner, the source owner's
+        // target coordinates, target owner, the target owner's source
+        // coordinates},
         // so the walk's duplicate-edge checks need no gather
-        int32_t *c = mc + inst * WH * 4, *r = mr + inst * WH * 4;
+        int2 *c = reinterpret_cast<int2 *>(mc + inst * WH * 4), *r = reinterpret_cast<int2 *>(mr + inst * WH * 4);
         const int ps = xs | (ys << 16), pd = xd | (yd << 16);
         int2 *pc = reinterpret_cast<int2 *>(a.prec + inst * (S + 1) + p);  // (prec .x/.y)
         *pc = make_int2(ps, pd);
-        c[4 * (int64_t)s] = p;
-        c[4 * (int64_t)s + 2] = pd;
-        c[4 * (int64_t)d + 1] = p;
-        c[4 * (int64_t)d + 3] = ps;
-        r[4 * ((int64_t)ys * W + xs)] = p;
-        r[4 * ((int64_t)ys * W + xs) + 2] = pd;
-        r[4 * ((int64_t)yd * W + xd) + 1] = p;
-        r[4 * ((int64_t)yd * W + xd) + 3] = ps;
+        c[2 * (int64_t)s] = make_int2(p, pd);
+        c[2 * (int64_t)d + 1] = make_int2(p, ps);
+        r[2 * ((int64_t)ys * W + xs)] = make_int2(p, pd);
+        r[2 * ((int64_t)yd * W + xd) + 1] = make_int2(p, ps);
         // coverage: horizontal part, then the vertical part past the bend
         int32_t *rc = cv.rowc + inst * (int64_t)H * (W + 1) + (int64_t)ys * (W + 1);
         atomicAdd(rc + min(xs, xd), 1);
@@ -699,7 +696,7 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_warp_kernel(Pipe
 #pragma unroll
             for (int c = 0; c < RG; ++c) {
                 const int j = g0 + 32 * c + lane;
-                m[c] = make_int4(-1, -1, 0, 0);
+                m[c] = make_int4(-1, 0, -1, 0);  // {source owner, its target, target owner, its source}
                 const int x = j <= dx ? xs + sx * j : xt, y = j <= dx ? ys : ys + sy * (j - dx);
                 pv[c] = x | (y << 16);
                 if (j <= len) m[c] = j <= dx ? mri[(int64_t)y * W + x] : mci[(int64_t)x * H + y];
@@ -717,7 +714,7 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_warp_kernel(Pipe
                 // chunk or the carry; next: this chunk or the next one loaded)
                 const unsigned below = b1[c] & lanemask_lt(), above = b1[c] & ~lanemask_lt() & ~(1u << lane);
                 const int pl = below ? 31 - __clz(below) : 0;
-                int ppv = __shfl_sync(FULL, pv[c], pl), pz = __shfl_sync(FULL, m[c].z, pl);
+                int ppv = __shfl_sync(FULL, pv[c], pl), pz = __shfl_sync(FULL, m[c].y, pl);
                 if (!below) {
                     ppv = cpv;
                     pz = cz;
@@ -726,9 +723,9 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_warp_kernel(Pipe
 #ifndef RECON_WALK_NONEXT
                 {
                     const int nl = above ? __ffs(above) - 1 : (c + 1 < RG && b1[c + 1] ? __ffs(b1[c + 1]) - 1 : 0);
-                    const int v0 = __shfl_sync(FULL, pv[c], nl), z0 = __shfl_sync(FULL, m[c].z, nl);
+                    const int v0 = __shfl_sync(FULL, pv[c], nl), z0 = __shfl_sync(FULL, m[c].y, nl);
                     const int v1 = __shfl_sync(FULL, pv[c + 1 < RG ? c + 1 : c], nl);
-                    const int z1 = __shfl_sync(FULL, m[c + 1 < RG ? c + 1 : c].z, nl);
+                    const int z1 = __shfl_sync(FULL, m[c + 1 < RG ? c + 1 : c].y, nl);
                     if (above) {
                         npv = v0;
                         nz = z0;
@@ -741,7 +738,7 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_warp_kernel(Pipe
                 if (b1[c]) {
                     const int last = 31 - __clz(b1[c]);
                     cpv = __shfl_sync(FULL, pv[c], last);
-                    cz = __shfl_sync(FULL, m[c].z, last);
+                    cz = __shfl_sync(FULL, m[c].y, last);
                 }
                 if (r1) {
                     const int bx = pv[c] & 0xffff, by = pv[c] >> 16;
@@ -750,13 +747,13 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_warp_kernel(Pipe
                         a.succ[atomicAdd(&fillp[o + m[c].x], 1ull)] = i;
                         ++in1;
                     }
-                    dup += on_path2p(pv[c], m[c].z, xt, yt);
+                    dup += on_path2p(pv[c], m[c].y, xt, yt);
                 }
                 // (i, m.y): i crosses target(m.y), unless m.y's route (from m.w to
                 // here) crosses source(i), which rule 1 already gives
-                const bool r2 = m[c].y >= 0 && m[c].y != i && !on_path2p(m[c].w, pv[c], xs, ys);
+                const bool r2 = m[c].z >= 0 && m[c].z != i && !on_path2p(m[c].w, pv[c], xs, ys);
                 const unsigned b2 = __ballot_sync(FULL, r2);
-                if (r2) a.succ[r2base + out2 + __popc(b2 & lanemask_lt())] = m[c].y;
+                if (r2) a.succ[r2base + out2 + __popc(b2 & lanemask_lt())] = m[c].z;
                 out2 += __popc(b2);
             }
         }
