@@ -224,6 +224,7 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
         int64_t *i64, *rc;
         cudaEvent_t done = nullptr;  // its copies are finished
     } sl[2];
+    // (out of memory: release the output slots and halve the sub-chunk)
     for (int k = 0; k < nslots; ++k) {
         sl[k].occ = c->dev<uint64_t>(S_PH_OCC0 + k, sub * occ_words);
         sl[k].src = c->dev<int32_t>(S_PH_SRC0 + k, sub * S);
@@ -240,8 +241,16 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
             sl[k].rc = c->dev<int64_t>(S_PH_RC0 + k, sub);
         }
         if (!sl[k].occ || !sl[k].src || !sl[k].dst || (b->path_event && !sl[k].ev) || !sl[k].i32 || !sl[k].i64 ||
-            !sl[k].mb || (runs && (!sl[k].rs || !sl[k].rc)))
-            return cuda_fail(cudaErrorMemoryAllocation, "pipeline host slots", detail);
+            !sl[k].mb || (runs && (!sl[k].rs || !sl[k].rc))) {
+            if (sub == 1) return cuda_fail(cudaErrorMemoryAllocation, "pipeline host slots", detail);
+            for (int sl_ = S_PH_OCC0; sl_ <= S_PH_RC1; ++sl_) {
+                if (c->buf[sl_].p) cudaFree(c->buf[sl_].p);
+                c->buf[sl_].p = nullptr;
+                c->buf[sl_].bytes = 0;
+            }
+            sub = (sub + 1) / 2;
+            k = -1;  // (the loop's ++k restarts at slot 0)
+        }
     }
     std::vector<int64_t> hD(sub), hR(sub);
     bool over = false;  // some instance had more runs than run_stride
