@@ -15,7 +15,7 @@ no collective runs on the data path — torch.distributed carries only the
 timing max and the digest gather).  The full 65,536-instance job is 65,536/B
 such steps per GPU count.
 
-Same line: the phase breakdown (solve / DAG / wide batching / warp batching,
+Same line: the phase breakdown (solve / DAG / wide batching in windows / warp batching,
 CUDA events on the context stream), rooflines, the per-instance stats record
 (digest64) of the chunk, e2e through the host-buffer C-ABI call
 (recon_pipeline_batch_run_host: H2D of the grids and D2H of paths + batch
@@ -482,12 +482,14 @@ def main():
                        "l2": "no flush: a chunk's inputs + outputs + workspace (~100 GB) dwarf the 126 MB L2"},
             "us_per_grid": ms * 1000.0 / B,
             "gpu_launches": launches,
-            "phases_ms": {"solve": solve_ms, "dag": dag_ms, "batching_wide": wide_ms, "batching_warp": warp_ms},
+            "phases_ms": {"solve": solve_ms, "dag": dag_ms, "batching_wide": wide_ms, "batching_warp": warp_ms,
+                          "note": "batching_wide: rb::batch_window_kernel (ready sets > 32); batching_warp: the leap "
+                                  "kernel rb::batch_pipeline_kernel<16>"},
             "roofline": {
                 "bound": "hbm", "achieved": alg_sched / (batch_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                 "frac": alg_sched / (batch_ms * 1e-3) / 1e9 / hbm, "traffic": traffic, "traffic_source": traffic_note,
                 "peak_kind": peak_kind,
-                "kernel": "batching phase: rb::batch_wide_kernel + rb::batch_pipeline_kernel<16> (leap)",
+                "kernel": "batching phase: rb::batch_window_kernel + rb::batch_pipeline_kernel<16> (leap)",
                 "algorithmic_bytes_per_launch": alg_sched,
                 "algorithmic_bytes_rule": "4 B per elementary move of the batch schedule (SURVEY §8(d) 4*D)",
                 "kernel_ms": batch_ms,
