@@ -766,6 +766,116 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_warp_kernel(Pipe
     }
 }
 
+// pl_walk_warp_kernel with a half warp per path: routes (~69 vertices on C5)
+// are walked 16 vertices at a time, so a route's last chunk idles fewer
+// lanes (80 lane slots per route instead of 96).  Same lists, counts and
+// implied-edge rule; every collective runs on the whole warp, each half
+// keeping to its own 16 bits.
+__global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_half_kernel(PipelineArgs a, const int4 *mc, const int4 *mr,
+                                                                            CoverArrays cv) {
+    const int lane = lane_id(), hl = lane & 15, hs = lane & 16;
+    const unsigned hlt = (lanemask_lt() >> hs) & 0xffffu;  // the lanes below me in my half
+    const int W = a.W, H = a.H;
+    const int64_t S = (int64_t)W * a.k, WH = (int64_t)W * H, N = (int64_t)a.count * S;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    unsigned long long *fillp = reinterpret_cast<unsigned long long *>(a.rec);
+    constexpr int RG = RECON_WALK_RG;
+    for (InstIter it(2 * (blockIdx.x * (int64_t)(blockDim.x >> 5) + warp_id()) + (hs ? 1 : 0), S, 2 * nwarps);
+         __any_sync(FULL, it.t < N); it.next()) {
+        const int64_t t = it.t, inst = it.inst, o = inst * S;
+        const int i = it.i;
+        const bool act = t < N && a.solve_status[inst] == 0 && i < a.path_count[inst];
+        int xs = 0, ys = 0, xt = 0, yt = 0, len = -1;
+        int64_t r2base = 0;
+        int cov = 0;
+        const int4 *mci = mc, *mri = mr;
+        if (act) {
+            const int2 me = *reinterpret_cast<const int2 *>(a.prec + inst * (S + 1) + i);
+            xs = me.x & 0xffff, ys = me.x >> 16, xt = me.y & 0xffff, yt = me.y >> 16;
+            len = abs(xt - xs) + abs(yt - ys);
+            r2base = a.soff[t] + a.outdeg[t];
+            if (hl == 0) cov = cover_at(cv, inst, W, H, xt, yt);
+            mci = mc + inst * WH;
+            mri = mr + inst * WH;
+        }
+        const int dx = abs(xt - xs), sx = xt > xs ? 1 : -1, sy = yt > ys ? 1 : -1;
+        const int glen = (int)__reduce_max_sync(FULL, (unsigned)(len + 1)) - 1;  // (both halves' loop)
+        int in1 = 0, dup = 0, out2 = 0;
+        int cpv = -1, cz = 0;  // the half's last rule-1 vertex so far and its owner's target
+        for (int g0 = 0; g0 <= glen; g0 += 16 * RG) {
+            int4 m[RG];
+            int pv[RG];
+#pragma unroll
+            for (int c = 0; c < RG; ++c) {
+                const int j = g0 + 16 * c + hl;
+                m[c] = make_int4(-1, 0, -1, 0);
+                const int x = j <= dx ? xs + sx * j : xt, y = j <= dx ? ys : ys + sy * (j - dx);
+                pv[c] = x | (y << 16);
+                if (j <= len) m[c] = j <= dx ? mri[(int64_t)y * W + x] : mci[(int64_t)x * H + y];
+            }
+            unsigned b1[RG];  // the half's rule-1 lanes of each chunk (16 bits)
+#pragma unroll
+            for (int c = 0; c < RG; ++c) b1[c] = (__ballot_sync(FULL, m[c].x >= 0 && m[c].x != i) >> hs) & 0xffffu;
+#pragma unroll
+            for (int c = 0; c < RG; ++c) {
+                const bool on = g0 + 16 * c <= len;  // (this half still has vertices here)
+                const bool r1 = b1[c] >> hl & 1u;
+                const unsigned below = b1[c] & hlt, above = b1[c] & ~hlt & ~(1u << hl);
+                const int pl = below ? 31 - __clz(below) : 0;
+                int ppv = __shfl_sync(FULL, pv[c], hs + pl), pz = __shfl_sync(FULL, m[c].y, hs + pl);
+                if (!below) {
+                    ppv = cpv;
+                    pz = cz;
+                }
+                int npv = -1, nz = 0;
+                {
+                    const int nl = above ? __ffs(above) - 1 : (c + 1 < RG && b1[c + 1] ? __ffs(b1[c + 1]) - 1 : 0);
+                    const int v0 = __shfl_sync(FULL, pv[c], hs + nl), z0 = __shfl_sync(FULL, m[c].y, hs + nl);
+                    const int v1 = __shfl_sync(FULL, pv[c + 1 < RG ? c + 1 : c], hs + nl);
+                    const int z1 = __shfl_sync(FULL, m[c + 1 < RG ? c + 1 : c].y, hs + nl);
+                    if (above) {
+                        npv = v0;
+                        nz = z0;
+                    } else if (c + 1 < RG && b1[c + 1] && g0 + 16 * (c + 1) <= len) {
+                        npv = v1;
+                        nz = z1;
+                    }
+                }
+                {
+                    const int last = b1[c] ? 31 - __clz(b1[c]) : 0;
+                    const int lv = __shfl_sync(FULL, pv[c], hs + last), lz = __shfl_sync(FULL, m[c].y, hs + last);
+                    if (b1[c]) {
+                        cpv = lv;
+                        cz = lz;
+                    }
+                }
+                if (r1) {
+                    const int bx = pv[c] & 0xffff, by = pv[c] >> 16;
+                    const bool implied = (ppv >= 0 && on_path2p(ppv, pz, bx, by)) || (npv >= 0 && on_path2p(npv, nz, bx, by));
+                    if (!implied) {
+                        a.succ[atomicAdd(&fillp[o + m[c].x], 1ull)] = i;
+                        ++in1;
+                    }
+                    dup += on_path2p(pv[c], m[c].y, xt, yt);
+                }
+                const bool r2 = on && m[c].z >= 0 && m[c].z != i && !on_path2p(m[c].w, pv[c], xs, ys);
+                const unsigned b2 = (__ballot_sync(FULL, r2) >> hs) & 0xffffu;
+                if (r2) a.succ[r2base + out2 + __popc(b2 & hlt)] = m[c].z;
+                out2 += __popc(b2);
+            }
+        }
+#pragma unroll
+        for (int d = 8; d > 0; d >>= 1) {
+            in1 += __shfl_xor_sync(FULL, in1, d);
+            dup += __shfl_xor_sync(FULL, dup, d);
+        }
+        if (act && hl == 0) {
+            a.indeg[t] = in1 + cov - 1 - dup;
+            a.mfr[t] = out2;
+        }
+    }
+}
+
 // rule-1 fill pointers: each list starts with its rule-1 part
 __global__ void fillptr_kernel(int64_t n, const int64_t *soff, unsigned long long *fp) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -2282,7 +2392,14 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
         pl_dag_small_kernel<1><<<(int)std::min<int64_t>(a.count, 148 * 16), 256, smem, st>>>(a);
     } else {
         const int32_t *mc = a.source_of, *mr = a.source_of + (size_t)a.count * a.W * a.H * 4;
-        pl_walk_warp_kernel<<<blocks, 256, 0, st>>>(a, (const int4 *)mc, (const int4 *)mr, pipeline_cover_arrays(a));
+        static const int half_env = [] {
+            const char *e = getenv("RECON_WALK_HALF");
+            return e ? atoi(e) : 1;
+        }();
+        if (half_env)
+            pl_walk_half_kernel<<<blocks, 256, 0, st>>>(a, (const int4 *)mc, (const int4 *)mr, pipeline_cover_arrays(a));
+        else
+            pl_walk_warp_kernel<<<blocks, 256, 0, st>>>(a, (const int4 *)mc, (const int4 *)mr, pipeline_cover_arrays(a));
         pl_compact_kernel<<<blocks, 256, 0, st>>>(a);
         *launches += 1;
     }
