@@ -766,21 +766,24 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_warp_kernel(Pipe
     }
 }
 
-// pl_walk_warp_kernel with a half warp per path: routes (~69 vertices on C5)
-// are walked 16 vertices at a time, so a route's last chunk idles fewer
-// lanes (80 lane slots per route instead of 96).  Same lists, counts and
-// implied-edge rule; every collective runs on the whole warp, each half
-// keeping to its own 16 bits.
+// pl_walk_warp_kernel with GW lanes per path (32 / GW paths per warp): a
+// route (~69 vertices on C5) is walked GW * RG vertices at a time, so a
+// route's last chunk idles fewer lanes, and a warp carries several routes'
+// independent loads and atomics.  Same lists, counts and implied-edge rule;
+// every collective runs on the whole warp, each group keeping to its own
+// GW bits.
+template <int GW>  // lanes per path (16 or 8)
 __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_half_kernel(PipelineArgs a, const int4 *mc, const int4 *mr,
                                                                             CoverArrays cv) {
-    const int lane = lane_id(), hl = lane & 15, hs = lane & 16;
-    const unsigned hlt = (lanemask_lt() >> hs) & 0xffffu;  // the lanes below me in my half
+    constexpr unsigned GM = (1u << GW) - 1u;
+    const int lane = lane_id(), hl = lane & (GW - 1), hs = lane & ~(GW - 1);
+    const unsigned hlt = (lanemask_lt() >> hs) & GM;  // the lanes below me in my group
     const int W = a.W, H = a.H;
     const int64_t S = (int64_t)W * a.k, WH = (int64_t)W * H, N = (int64_t)a.count * S;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
     unsigned long long *fillp = reinterpret_cast<unsigned long long *>(a.rec);
     constexpr int RG = RECON_WALK_RG;
-    for (InstIter it(2 * (blockIdx.x * (int64_t)(blockDim.x >> 5) + warp_id()) + (hs ? 1 : 0), S, 2 * nwarps);
+    for (InstIter it((32 / GW) * (blockIdx.x * (int64_t)(blockDim.x >> 5) + warp_id()) + hs / GW, S, (32 / GW) * nwarps);
          __any_sync(FULL, it.t < N); it.next()) {
         const int64_t t = it.t, inst = it.inst, o = inst * S;
         const int i = it.i;
@@ -802,23 +805,23 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_half_kernel(Pipe
         const int glen = (int)__reduce_max_sync(FULL, (unsigned)(len + 1)) - 1;  // (both halves' loop)
         int in1 = 0, dup = 0, out2 = 0;
         int cpv = -1, cz = 0;  // the half's last rule-1 vertex so far and its owner's target
-        for (int g0 = 0; g0 <= glen; g0 += 16 * RG) {
+        for (int g0 = 0; g0 <= glen; g0 += GW * RG) {
             int4 m[RG];
             int pv[RG];
 #pragma unroll
             for (int c = 0; c < RG; ++c) {
-                const int j = g0 + 16 * c + hl;
+                const int j = g0 + GW * c + hl;
                 m[c] = make_int4(-1, 0, -1, 0);
                 const int x = j <= dx ? xs + sx * j : xt, y = j <= dx ? ys : ys + sy * (j - dx);
                 pv[c] = x | (y << 16);
                 if (j <= len) m[c] = j <= dx ? mri[(int64_t)y * W + x] : mci[(int64_t)x * H + y];
             }
-            unsigned b1[RG];  // the half's rule-1 lanes of each chunk (16 bits)
+            unsigned b1[RG];  // the group's rule-1 lanes of each chunk (GW bits)
 #pragma unroll
-            for (int c = 0; c < RG; ++c) b1[c] = (__ballot_sync(FULL, m[c].x >= 0 && m[c].x != i) >> hs) & 0xffffu;
+            for (int c = 0; c < RG; ++c) b1[c] = (__ballot_sync(FULL, m[c].x >= 0 && m[c].x != i) >> hs) & GM;
 #pragma unroll
             for (int c = 0; c < RG; ++c) {
-                const bool on = g0 + 16 * c <= len;  // (this half still has vertices here)
+                const bool on = g0 + GW * c <= len;  // (this half still has vertices here)
                 const bool r1 = b1[c] >> hl & 1u;
                 const unsigned below = b1[c] & hlt, above = b1[c] & ~hlt & ~(1u << hl);
                 const int pl = below ? 31 - __clz(below) : 0;
@@ -836,7 +839,7 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_half_kernel(Pipe
                     if (above) {
                         npv = v0;
                         nz = z0;
-                    } else if (c + 1 < RG && b1[c + 1] && g0 + 16 * (c + 1) <= len) {
+                    } else if (c + 1 < RG && b1[c + 1] && g0 + GW * (c + 1) <= len) {
                         npv = v1;
                         nz = z1;
                     }
@@ -859,13 +862,13 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_half_kernel(Pipe
                     dup += on_path2p(pv[c], m[c].y, xt, yt);
                 }
                 const bool r2 = on && m[c].z >= 0 && m[c].z != i && !on_path2p(m[c].w, pv[c], xs, ys);
-                const unsigned b2 = (__ballot_sync(FULL, r2) >> hs) & 0xffffu;
+                const unsigned b2 = (__ballot_sync(FULL, r2) >> hs) & GM;
                 if (r2) a.succ[r2base + out2 + __popc(b2 & hlt)] = m[c].z;
                 out2 += __popc(b2);
             }
         }
 #pragma unroll
-        for (int d = 8; d > 0; d >>= 1) {
+        for (int d = GW / 2; d > 0; d >>= 1) {
             in1 += __shfl_xor_sync(FULL, in1, d);
             dup += __shfl_xor_sync(FULL, dup, d);
         }
@@ -2392,14 +2395,23 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
         pl_dag_small_kernel<1><<<(int)std::min<int64_t>(a.count, 148 * 16), 256, smem, st>>>(a);
     } else {
         const int32_t *mc = a.source_of, *mr = a.source_of + (size_t)a.count * a.W * a.H * 4;
-        static const int half_env = [] {
-            const char *e = getenv("RECON_WALK_HALF");
-            return e ? atoi(e) : 1;
+        // lanes per path of the walk (RECON_WALK_LANES: 32 = a warp per path;
+        // C5 walk time at 256 instances, ms: 40.8 / 32.8 / 28.0 / 26.0 / 27.3 /
+        // 30.0 for 32 / 16 / 8 / 4 / 2 / 1)
+        static const int lanes_env = [] {
+            const char *e = getenv("RECON_WALK_LANES");
+            return e ? atoi(e) : 4;
         }();
-        if (half_env)
-            pl_walk_half_kernel<<<blocks, 256, 0, st>>>(a, (const int4 *)mc, (const int4 *)mr, pipeline_cover_arrays(a));
-        else
-            pl_walk_warp_kernel<<<blocks, 256, 0, st>>>(a, (const int4 *)mc, (const int4 *)mr, pipeline_cover_arrays(a));
+        const CoverArrays cva = pipeline_cover_arrays(a);
+        const int4 *mc4 = (const int4 *)mc, *mr4 = (const int4 *)mr;
+        switch (lanes_env) {
+            case 1: pl_walk_half_kernel<1><<<blocks, 256, 0, st>>>(a, mc4, mr4, cva); break;
+            case 2: pl_walk_half_kernel<2><<<blocks, 256, 0, st>>>(a, mc4, mr4, cva); break;
+            case 8: pl_walk_half_kernel<8><<<blocks, 256, 0, st>>>(a, mc4, mr4, cva); break;
+            case 16: pl_walk_half_kernel<16><<<blocks, 256, 0, st>>>(a, mc4, mr4, cva); break;
+            case 32: pl_walk_warp_kernel<<<blocks, 256, 0, st>>>(a, mc4, mr4, cva); break;
+            default: pl_walk_half_kernel<4><<<blocks, 256, 0, st>>>(a, mc4, mr4, cva); break;
+        }
         pl_compact_kernel<<<blocks, 256, 0, st>>>(a);
         *launches += 1;
     }

@@ -187,7 +187,8 @@ def test_c5_variants(env):
 @pytest.mark.parametrize("env", [
     {"RECON_BATCH_WIDE": "0"},
     {"RECON_WIDE_WINDOW": "0"},
-    {"RECON_WALK_HALF": "0"},                                    # the DAG walk with a warp per path
+    {"RECON_WALK_LANES": "32"},                                 # the DAG walk with a warp per path
+    {"RECON_WALK_LANES": "16"},
     {"RECON_BATCH_LEAP": "0", "RECON_BATCH_BSM": "0"},
     {"RECON_BATCH_LEAP": "0", "RECON_BATCH_WIDE": "0", "RECON_BATCH_LOG": "1"},
 ])
@@ -202,7 +203,8 @@ def test_c4_variants(env):
     {"RECON_BATCH_WIDE": "1", "RECON_WIDE_WINDOW": "0"},
     {"RECON_BATCH_WIDE": "1", "RECON_BATCH_LEAP": "2"},
     {"RECON_SMALL_DAG": "0"},
-    {"RECON_SMALL_DAG": "0", "RECON_WALK_HALF": "0"},
+    {"RECON_SMALL_DAG": "0", "RECON_WALK_LANES": "32"},
+    {"RECON_SMALL_DAG": "0", "RECON_WALK_LANES": "1"},
 ])
 def test_c3_variants(env):
     check_variant(variant(env, "c3", 0, 4096), golden("c3_none"))
