@@ -15,10 +15,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --steps 1 --warmup 3 --no-extras --no-cpu > $O/bench_under_ncu.log 2>&1; echo "launch list rc=$?"
 python tools/launch_summary.py $O/launches_bench.csv > $O/launches_bench_summary.txt 2>&1
 timeout 1800 ncu --set full --clock-control none --import-source on \
-    -k regex:"batch_window|batch_pipeline_kernel|pl_walk_warp|pl_mark2|bird_kernel|pl_compact" -c 6 \
+    -k regex:"batch_window|batch_pipeline_kernel|pl_walk|pl_mark2|bird_kernel|pl_compact" -c 6 \
     -o $O/c5_full -f python tools/perf_probe.py c5_pipeline_64 > $O/ncu_c5.log 2>&1; echo "c5 full rc=$?"
 python tools/ncu_raw.py $O/c5_full.ncu-rep > $O/c5_full_raw.txt 2>&1
-for k in batch_window batch_pipeline_kernel pl_walk_warp_kernel pl_mark2 bird_kernel; do
+for k in batch_window batch_pipeline_kernel pl_walk pl_mark2 bird_kernel; do
     ncu -i $O/c5_full.ncu-rep --page source --csv --print-source cuda,sass -k regex:"$k" > $O/src.csv 2>/dev/null
     python tools/ncu_lines.py $O/src.csv 30 > $O/c5_lines_$k.txt 2>&1
 done
