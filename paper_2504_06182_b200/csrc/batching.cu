@@ -1563,6 +1563,18 @@ struct EarlyRelease {
 
 __device__ __forceinline__ void release_load(const BatchJob &J, bool fin, int64_t q0, int64_t q1, EarlyRelease &er) {
     const int lane = lane_id();
+    const unsigned fm = __ballot_sync(FULL, fin);
+    if (!(fm & (fm - 1))) {  // one finishing lane (the common case): no owner search
+        const int f = __ffs(fm) - 1;
+        const int64_t oq0 = __shfl_sync(FULL, q0, f);
+        const int n = (int)(__shfl_sync(FULL, q1, f) - oq0);
+#pragma unroll
+        for (int c = 0; c < EG; ++c) {
+            const int t = c * 32 + lane;
+            er.sc[c] = t < n ? __ldcg(J.succ + oq0 + t) : -1;
+        }
+        return;
+    }
     if (!fin) q0 = q1 = 0;
     int tot;
     const int base = warp_excl_scan((int)(q1 - q0), &tot);
