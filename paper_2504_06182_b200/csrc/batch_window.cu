@@ -123,7 +123,15 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
     auto bufs = [&](int q) {
         return WinBufs{(int4 *)(wsm + Lo.rec) + q * rmax, (int *)(wsm + Lo.base) + q * rmax, wsm + Lo.st + q * rmax};
     };
-    for (int inst = blockIdx.x; inst < a.count; inst += gridDim.x) {
+    // instances taken one at a time from a counter: CTAs that drew short wide
+    // phases take more, so the kernel's tail is one instance, not a wave
+    __shared__ int s_inst;
+    for (;;) {
+        __syncthreads();  // (the previous instance's shared state is read no more)
+        if (tid == 0) s_inst = atomicAdd(a.wnext, 1);
+        __syncthreads();
+        const int inst = s_inst;
+        if (inst >= a.count) break;
         int64_t *wst = a.wstate + (int64_t)inst * 4;
         if (a.solve_status[inst] != 0) {
             if (tid == 0) wst[0] = 0;  // the warp kernel reports the solve status

@@ -2452,6 +2452,7 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
             (pipeline_window_config(a.W, a.H, budget, &rmax, &wsmem) ||
              pipeline_window_config(a.W, a.H, 220 * 1024, &rmax, &wsmem))) {
             cudaMemsetAsync(a.vmin, 0x7f, (size_t)a.count * a.W * a.H * 4, st);
+            cudaMemsetAsync(a.wnext, 0, sizeof(int32_t), st);
             cudaError_t e = launch_batch_window(a, sms, rmax, wsmem, st);
             if (e != cudaSuccess) return e;
             *launches += 1;

@@ -66,6 +66,7 @@ struct PipelineArgs {
     int leap;                            // leap mode (preset none): batching.cu
     int wide;                            // wide phase first (batch_wide.cu)
     int64_t *wstate;                     // [count * 4] wide -> warp hand-off {phase, nb, left, nready}
+    int32_t *wnext;                      // window kernel: next instance to take (zeroed before the launch)
     int32_t *vmin;                       // [count * W*H] wide: per-vertex min id (0x7f7f7f7f = empty)
     const int32_t *path_src, *path_dst;  // [count * W*k] (instance stride W*k)
     const int32_t *path_count;           // [count]

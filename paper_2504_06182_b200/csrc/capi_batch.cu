@@ -85,7 +85,8 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb) {
     a.prec = c->dev<int4>(S_BM_PREC, n * (S + 1));
     if (!a.prec) return cuda_fail(cudaErrorMemoryAllocation, "pipeline prec", detail);
     if (a.wide) {
-        a.wstate = c->dev<int64_t>(S_BM_WSTATE, n * 4);
+        a.wstate = c->dev<int64_t>(S_BM_WSTATE, n * 4 + 1);
+        a.wnext = a.wstate ? reinterpret_cast<int32_t *>(a.wstate + n * 4) : nullptr;
         a.vmin = c->dev<int32_t>(S_BM_VMIN, n * WH);
         if (!a.wstate || !a.vmin) return cuda_fail(cudaErrorMemoryAllocation, "pipeline wide", detail);
     }
