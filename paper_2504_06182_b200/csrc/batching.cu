@@ -68,6 +68,7 @@ struct LanePath {
     int64_t base;
     int64_t q0, q1;  // successor CSR range, prefetched when the lane is filled (leap mode)
     int pf;          // leap mode: the successors' records and blocker counts still to prefetch
+    int pn;          // leap mode: new since the cached pair meetings (leap_delta's cache)
     __device__ __forceinline__ int32_t v(int H, int kk) const {
         const int dx = abs(xt - xs);
         if (kk <= dx) return (xs + (xt > xs ? kk : -kk)) * H + ys;
@@ -1184,6 +1185,7 @@ __device__ __forceinline__ LanePath rec_lane(int4 r, int base) {
     l.yt = r.w >> 16;
     l.base = base;
     l.pf = 1;
+    l.pn = 1;
     return l;
 }
 
@@ -1382,6 +1384,7 @@ __device__ __forceinline__ LanePath shfl_lane(const LanePath &lp, int src, bool 
         q.q0 = q.q1 = 0;
         q.pf = 0;
     }
+    q.pn = 1;
     return q;
 }
 
@@ -1507,6 +1510,7 @@ __device__ __forceinline__ int release_into_lanes(const BatchJob &J, const BL &b
                 lp.q0 = J.e0 + r.w;
                 lp.q1 = J.e0 + (J.slen ? r.w + e : e);
                 lp.pf = 1;
+                lp.pn = 1;
             }
             nnew += __popc(rm);
         }
@@ -1644,6 +1648,7 @@ __device__ __forceinline__ int release_fill(const BatchJob &J, const EarlyReleas
             lp.q0 = J.e0 + r.w;
             lp.q1 = J.e0 + (J.slen ? r.w + e : e);
             lp.pf = 1;
+            lp.pn = 1;
         }
         nnew += __popc(rm);
     }
@@ -1705,7 +1710,10 @@ __device__ __forceinline__ void occ_toggle(const Bits<SM> &b, int v) {
 // leap runs over the remaining lanes (the movers).  A lane blocked by a mover
 // only waits one batch: delta = 0 then.
 // Returns delta (0: run the batch literally) and the movers' lane mask.
-__device__ __forceinline__ int leap_delta(const LanePath &lp, int H, int32_t fr, int32_t to, unsigned *movers) {
+__device__ __forceinline__ int leap_delta(const LanePath &lp, int H, int32_t fr, int32_t to, unsigned *movers,
+                                          int *ppair, int *pwith) {
+    *ppair = INT_MAX;
+    *pwith = -1;
     const int lane = lane_id();
     const bool valid = lp.p != INT_MAX;
     const unsigned vm = __ballot_sync(FULL, valid);
@@ -1765,7 +1773,12 @@ __device__ __forceinline__ int leap_delta(const LanePath &lp, int H, int32_t fr,
             const int k = qk & 0xffff, len = qk >> 16;
             Seg other[2];
             lane_segs(k, len, qxs & 0xffff, qxs >> 16, qxt & 0xffff, qxt >> 16, other[0], other[1]);
-            best = min(best, pair_event(mine, other, 0, min(lp.len - lp.k - 1, len - k - 1)));
+            const int e = pair_event(mine, other, 0, min(lp.len - lp.k - 1, len - k - 1));
+            if (e < *ppair) {
+                *ppair = e;
+                *pwith = q;
+            }
+            best = min(best, e);
         }
     }
     return __reduce_min_sync(FULL, mover ? best : INT_MAX);
@@ -1824,6 +1837,14 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
     LanePath lp;
     lp.p = INT_MAX;
     lp.pf = 0;
+    lp.pn = 0;
+    // leap mode: each lane's earliest meeting with another lane (batches from
+    // now, or INT_MAX) and that lane, kept across leaps while no lane is
+    // frozen and no literal batch runs: every lane then moves each batch, so a
+    // meeting only shifts by the leap; lanes that enter add their pairs, a
+    // lane whose partner left holds a lower bound (pst) until it binds
+    int pm = INT_MAX, pw = -1;
+    bool pst = false, pv_ok = false;
     // the lane's current move (fr -> to), advanced incrementally on acceptance
     int32_t fr = -1, to = -1;
     auto lane_move = [&]() {
@@ -1843,6 +1864,7 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
         }
         lane_move();
         regmode = true;
+        pv_ok = false;
     };
     auto put_move = [&](int64_t slot, int rank_in_batch) {
         if (LOG) J.mlog[nlog + rank_in_batch] = make_int2((int)slot, nb);
@@ -1872,7 +1894,65 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
                     if (lane == pff) lp.pf = 0;
                 }
             }
-            const int delta = LEAP ? leap_delta(lp, H, fr, to, &movers) : 0;
+            int delta = 0;
+            bool fast = false;
+            if (LEAP && pv_ok) {
+                const bool valid_l = lp.p != INT_MAX;
+                Seg mine[2];
+                lane_segs(lp.k, lp.len, lp.xs, lp.ys, lp.xt, lp.yt, mine[0], mine[1]);
+                for (unsigned nm = __ballot_sync(FULL, valid_l && lp.pn); nm; nm &= nm - 1) {
+                    // an entered lane n: the pairs (i, n) and (n, i)
+                    const int n = __ffs(nm) - 1;
+                    const int nk = __shfl_sync(FULL, lp.k, n), nlen = __shfl_sync(FULL, lp.len, n);
+                    const int nxs = __shfl_sync(FULL, lp.xs, n), nys = __shfl_sync(FULL, lp.ys, n);
+                    const int nxt = __shfl_sync(FULL, lp.xt, n), nyt = __shfl_sync(FULL, lp.yt, n);
+                    Seg sn[2];
+                    lane_segs(nk, nlen, nxs, nys, nxt, nyt, sn[0], sn[1]);
+                    // remaining routes' bounding boxes: no meeting outside both
+                    const int nxc = sn[0].t1 >= 0 ? sn[0].x0 : nxt, nyc = sn[1].y0 + sn[1].vy * sn[1].t0;
+                    const int mxc = mine[0].t1 >= 0 ? mine[0].x0 : lp.xt, myc = mine[1].y0 + mine[1].vy * mine[1].t0;
+                    const bool olap = max(min(nxc, nxt), min(mxc, lp.xt)) <= min(max(nxc, nxt), max(mxc, lp.xt)) &&
+                                      max(min(nyc, nyt), min(myc, lp.yt)) <= min(max(nyc, nyt), max(myc, lp.yt));
+                    int en = INT_MAX;
+                    if (valid_l && lane != n && olap) {
+                        const int T = min(lp.len - lp.k - 1, nlen - nk - 1);
+                        const int e = pair_event(mine, sn, 0, T);
+                        if (e < pm) {
+                            pm = e;
+                            pw = n;
+                        }
+                        en = pair_event(sn, mine, 0, T);
+                    }
+                    const int m = (int)__reduce_min_sync(FULL, (unsigned)en);
+                    const unsigned wm = __ballot_sync(FULL, en == m && m != INT_MAX);
+                    if (lane == n) {
+                        pm = m;
+                        pw = wm ? __ffs(wm) - 1 : -1;
+                        pst = false;
+                        lp.pn = 0;
+                    }
+                }
+                const int cand = valid_l ? min(lp.len - lp.k, pm) : INT_MAX;
+                const int d0 = (int)__reduce_min_sync(FULL, (unsigned)cand);
+                if (d0 > 0 && d0 != INT_MAX && !__any_sync(FULL, valid_l && pst && pm <= d0)) {
+                    delta = d0;
+                    movers = __ballot_sync(FULL, valid_l);
+                    fast = true;
+                }
+            }
+            if (LEAP && !fast) {
+#ifdef RECON_BATCH_PROF
+                if (lane == 0) atomicAdd(&g_batch_prof[15], 1ull);
+#endif
+                int pp, pwi;
+                delta = leap_delta(lp, H, fr, to, &movers, &pp, &pwi);
+                const unsigned vmask = __ballot_sync(FULL, lp.p != INT_MAX);
+                pv_ok = delta > 0 && movers == vmask;  // (no frozen lane)
+                pm = pp;
+                pw = pwi;
+                pst = false;
+                lp.pn = 0;
+            }
             if (LEAP) {
                 auto pf1 = [&](int v) {
                     if (v < 0) return;
@@ -1940,9 +2020,11 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
                 }
                 nb += delta;
                 left -= (long long)__popc(vm) * delta;
+                if (LEAP && pm != INT_MAX) pm -= delta;
                 BPROF_ADD(1);
             } else {
                 BPROF_CNT(6);
+                pv_ok = false;
                 const bool valid = lp.p != INT_MAX;
                 bool cand;
                 if (LEAP) {
@@ -2002,6 +2084,7 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
                 BPROF_ADD(2);
             }
             const unsigned fm = __ballot_sync(FULL, fin);
+            if (LEAP && pw >= 0 && (fm >> pw & 1u)) pst = true;  // (the partner left: pm is a lower bound)
             if (fm) {
                 BPROF_CNT(8);
                 int32_t *newly = s.newly;

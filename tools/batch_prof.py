@@ -51,6 +51,8 @@ for a, b in (("leap_delta", "n_leap"), ("literal", "n_literal"), ("general", "n_
         print(f"  {a}: {out[a] / max(1, out[b] if a != 'leap_delta' else out['n_leap'] + out['n_literal']):.0f} cycles per")
 if v[12]:
     print(f"  finish detail: successor loads {v[10] / v[12]:.0f}, decrements+records+lanes {v[11] / v[12]:.0f} cycles per finish")
+if v[15]:
+    print(f"  leap_delta recomputed in full: {v[15] / n:.0f} per instance (the rest from the cached pair meetings)")
 if v[14]:
     print(f"  early finishes: {v[14] / n:.0f} per instance, release_fill {v[13] / v[14]:.0f} cycles")
 if wv[4]:
