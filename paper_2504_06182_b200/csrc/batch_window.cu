@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
                     qn = slen ? __ldg(slen + pid) : __ldg(&prec[pid + 1].w) - q0;
                     F[f].z = q0;
                     F[f].w = qn;
+                    if (qn > PC) prefetch_l2(succ + q0 + PC, (qn - PC) * 4);  // (the pieces taken after the barrier)
                 } else {
                     q0 = F[f].z;
                     qn = F[f].w;
@@ -634,6 +635,12 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
                         B.rec[j] = r;
                         B.base[j] = base[i];
                         B.st[j] = 0;
+                        // a finisher of the next window (if L holds): its successor
+                        // range's record into L2 for the plan's first load
+                        if ((lk[i] >> 16) - (lk[i] & 0xffff) <= L) {
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(prec + r.x));
+                            if (slen) asm volatile("prefetch.global.L2 [%0];" ::"l"(slen + r.x));
+                        }
                     }
                 }
             }
