@@ -49,20 +49,17 @@ namespace {
 constexpr int WT = 512;  // threads per CTA
 constexpr int NW = WT / 32;
 constexpr int EPT = 4;          // entries per thread in the replay: rmax <= EPT * WT
-#ifndef RECON_WIN_G
-#define RECON_WIN_G 5
-#endif
-constexpr int G = RECON_WIN_G;  // chunks of 32 successor ids per warp in flight (experiments: -DRECON_WIN_G)
 #ifndef RECON_WIN_PC
 #define RECON_WIN_PC 8
 #endif
-constexpr int PC = RECON_WIN_PC;
+constexpr int PC = RECON_WIN_PC;  // successors per piece (a thread's loads, then its decrements, in flight)
 // release offsets through a per-path tag array raised (red.max) with each
-// decrement, instead of a second pass against a shared hash of the released ids
+// decrement, instead of a second pass against a shared hash of the released
+// ids (measured equal; experiments: -DRECON_WIN_TMAX=1)
 #ifndef RECON_WIN_TMAX
 #define RECON_WIN_TMAX 0
 #endif
-constexpr bool TMAX = RECON_WIN_TMAX;  // successors per piece (a thread's loads, then its decrements, in flight)
+constexpr bool TMAX = RECON_WIN_TMAX;
 constexpr int LMAX = 128;       // window length cap (offsets fit a byte)
 constexpr int LINIT = 16;
 constexpr int32_t VMIN_EMPTY = 0x7f7f7f7f;
