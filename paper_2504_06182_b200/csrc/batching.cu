@@ -773,7 +773,15 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_warp_kernel(Pipe
 // independent loads and atomics.  Same lists, counts and implied-edge rule;
 // every collective runs on the whole warp, each group keeping to its own
 // GW bits.
-template <int GW>  // lanes per path (16 or 8)
+// The same implied-edge rule for rule-2 edges (C5: 2.9 M -> ~1.9 M edges,
+// identical schedules): measured the leap phase 17 ms faster per 1,536-instance
+// step but this walk 26 ms slower (its neighbour shuffles and the in-degree
+// correction atomics), so off (experiments: -DRECON_RULE2_IMPLIED=1)
+#ifndef RECON_RULE2_IMPLIED
+#define RECON_RULE2_IMPLIED 0
+#endif
+constexpr bool RULE2_IMPLIED = RECON_RULE2_IMPLIED;  // (newly: the dropped rule-2 in-edges per path, zeroed)
+template <int GW>  // lanes per path
 __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_half_kernel(PipelineArgs a, const int4 *mc, const int4 *mr,
                                                                             CoverArrays cv) {
     constexpr unsigned GM = (1u << GW) - 1u;
@@ -805,7 +813,8 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_half_kernel(Pipe
         const int dx = abs(xt - xs), sx = xt > xs ? 1 : -1, sy = yt > ys ? 1 : -1;
         const int glen = (int)__reduce_max_sync(FULL, (unsigned)(len + 1)) - 1;  // (both halves' loop)
         int in1 = 0, dup = 0, out2 = 0;
-        int cpv = -1, cz = 0;  // the half's last rule-1 vertex so far and its owner's target
+        int cpv = -1, cz = 0;  // the group's last rule-1 vertex so far and its owner's target
+        int ctw = -1, cts = 0;  // (RULE2_IMPLIED) its last target vertex and that target owner's source
         for (int g0 = 0; g0 <= glen; g0 += GW * RG) {
             int4 m[RG];
             int pv[RG];
@@ -820,6 +829,9 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_half_kernel(Pipe
             unsigned b1[RG];  // the group's rule-1 lanes of each chunk (GW bits)
 #pragma unroll
             for (int c = 0; c < RG; ++c) b1[c] = (__ballot_sync(FULL, m[c].x >= 0 && m[c].x != i) >> hs) & GM;
+            unsigned bt[RG];  // the group's lanes on another path's target
+#pragma unroll
+            for (int c = 0; c < RG; ++c) bt[c] = (__ballot_sync(FULL, m[c].z >= 0 && m[c].z != i) >> hs) & GM;
 #pragma unroll
             for (int c = 0; c < RG; ++c) {
                 const bool on = g0 + GW * c <= len;  // (this half still has vertices here)
@@ -862,7 +874,49 @@ __global__ void __launch_bounds__(256, RECON_WALK_MINB) pl_walk_half_kernel(Pipe
                     }
                     dup += on_path2p(pv[c], m[c].y, xt, yt);
                 }
-                const bool r2 = on && m[c].z >= 0 && m[c].z != i && !on_path2p(m[c].w, pv[c], xs, ys);
+                bool r2 = on && m[c].z >= 0 && m[c].z != i && !on_path2p(m[c].w, pv[c], xs, ys);
+                if (RULE2_IMPLIED) {
+                    // (i, t1) at target(t1) is implied by (i, t2) and (t2, t1) when t2,
+                    // the owner of the previous or next target on i's route, passes
+                    // target(t1) on its way (from its source to its target); t1's
+                    // in-degree (counted from the routes through its target) loses it
+                    const unsigned tb = bt[c] & hlt, ta = bt[c] & ~hlt & ~(1u << hl);
+                    const int tl = tb ? 31 - __clz(tb) : 0;
+                    int pw2 = __shfl_sync(FULL, pv[c], hs + tl), ps2 = __shfl_sync(FULL, m[c].w, hs + tl);
+                    if (!tb) {
+                        pw2 = ctw;
+                        ps2 = cts;
+                    }
+                    int nw2 = -1, ns2 = 0;
+                    {
+                        const int nl = ta ? __ffs(ta) - 1 : (c + 1 < RG && bt[c + 1] ? __ffs(bt[c + 1]) - 1 : 0);
+                        const int v0 = __shfl_sync(FULL, pv[c], hs + nl), s0 = __shfl_sync(FULL, m[c].w, hs + nl);
+                        const int v1 = __shfl_sync(FULL, pv[c + 1 < RG ? c + 1 : c], hs + nl);
+                        const int s1 = __shfl_sync(FULL, m[c + 1 < RG ? c + 1 : c].w, hs + nl);
+                        if (ta) {
+                            nw2 = v0;
+                            ns2 = s0;
+                        } else if (c + 1 < RG && bt[c + 1] && g0 + GW * (c + 1) <= len) {
+                            nw2 = v1;
+                            ns2 = s1;
+                        }
+                    }
+                    {
+                        const int last = bt[c] ? 31 - __clz(bt[c]) : 0;
+                        const int lw = __shfl_sync(FULL, pv[c], hs + last), ls = __shfl_sync(FULL, m[c].w, hs + last);
+                        if (bt[c]) {
+                            ctw = lw;
+                            cts = ls;
+                        }
+                    }
+                    if (r2) {
+                        const int bx = pv[c] & 0xffff, by = pv[c] >> 16;
+                        if ((pw2 >= 0 && on_path2p(ps2, pw2, bx, by)) || (nw2 >= 0 && on_path2p(ns2, nw2, bx, by))) {
+                            atomicAdd(&a.newly[o + m[c].z], 1);
+                            r2 = false;
+                        }
+                    }
+                }
                 const unsigned b2 = (__ballot_sync(FULL, r2) >> hs) & GM;
                 if (r2) a.succ[r2base + out2 + __popc(b2 & hlt)] = m[c].z;
                 out2 += __popc(b2);
@@ -898,6 +952,7 @@ __global__ void pl_compact_kernel(PipelineArgs a) {
         if (a.solve_status[inst] != 0 || it.i >= a.path_count[inst]) continue;
         const int64_t s0 = a.soff[t];
         const int n1 = (int)((int64_t)fillp[t] - s0), cap1 = a.outdeg[t], n2 = a.mfr[t];
+        a.indeg[t] -= a.newly[t];  // (rule-2 in-edges the walk dropped; zero for the warp-per-path walk)
         if (n1 < cap1)  // (ascending: a destination never overlaps a later source)
             for (int r = 0; r < n2; ++r) a.succ[s0 + n1 + r] = a.succ[s0 + cap1 + r];
         a.outdeg[t] = n1 + n2;
@@ -2498,6 +2553,7 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
             return e ? atoi(e) : 4;
         }();
         const CoverArrays cva = pipeline_cover_arrays(a);
+        cudaMemsetAsync(a.newly, 0, (size_t)a.count * (size_t)a.W * a.k * sizeof(int32_t), st);
         const int4 *mc4 = (const int4 *)mc, *mr4 = (const int4 *)mr;
         switch (lanes_env) {
             case 1: pl_walk_half_kernel<1><<<blocks, 256, 0, st>>>(a, mc4, mr4, cva); break;
