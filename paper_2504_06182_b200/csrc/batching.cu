@@ -1939,9 +1939,9 @@ __device__ void batch_warp_pipe(const BatchJob &J, const ImplicitPaths &paths, P
             // into L2, so its finish (>= one leap away) decrements in L2
             int pfv0 = -1, pfv1 = -1, pff = -1, pfn = 0;  // (pff: the lane, pfn: its successor count)
             if (LEAP) {
-                const unsigned pm = __ballot_sync(FULL, lp.p != INT_MAX && lp.pf);
-                if (pm) {
-                    pff = __ffs(pm) - 1;
+                const unsigned pfm = __ballot_sync(FULL, lp.p != INT_MAX && lp.pf);
+                if (pfm) {
+                    pff = __ffs(pfm) - 1;
                     const int64_t fq = __shfl_sync(FULL, lp.q0, pff);
                     pfn = (int)(__shfl_sync(FULL, lp.q1, pff) - fq);
                     pfv0 = lane < pfn ? __ldcg(J.succ + fq + lane) : -1;
