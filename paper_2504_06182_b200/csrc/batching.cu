@@ -531,11 +531,17 @@ static inline CoverArrays pipeline_cover_arrays(const PipelineArgs &a) {
 __global__ void pl_mark2_kernel(PipelineArgs a, int32_t *mc, int32_t *mr, CoverArrays cv) {
     const int64_t S = (int64_t)a.W * a.k, WH = (int64_t)a.W * a.H, nwb = (WH + 31) / 32;
     const int W = a.W, H = a.H;
+    int64_t cinst = -1;  // the instance whose path count is held in cP
+    int cP = 0;
     for (InstIter it(blockIdx.x * (int64_t)blockDim.x + threadIdx.x, S, (int64_t)gridDim.x * blockDim.x);
          it.t < (int64_t)a.count * S; it.next()) {
         const int64_t t = it.t, inst = it.inst;
         const int p = it.i;
-        if (a.solve_status[inst] != 0 || p >= a.path_count[inst]) continue;
+        if (inst != cinst) {
+            cinst = inst;
+            cP = a.solve_status[inst] != 0 ? 0 : a.path_count[inst];
+        }
+        if (p >= cP) continue;
         const int s = a.path_src[t], d = a.path_dst[t];
         const int xs = s / H, ys = s - xs * H, xd = d / H, yd = d - xd * H;
         // owner maps, 16 B per vertex: {source owner, the source owner's
