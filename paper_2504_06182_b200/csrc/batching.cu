@@ -1616,7 +1616,7 @@ __device__ __forceinline__ int release_into_lanes(const BatchJob &J, const BL &b
 // issued after them; release_fill then waits for the results.  Up to
 // 32 * EG successors (the caller falls back to release_into_lanes beyond).
 #ifndef RECON_EG
-#define RECON_EG 4
+#define RECON_EG 6
 #endif
 constexpr int EG = RECON_EG;
 struct EarlyRelease {
