@@ -534,32 +534,53 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
             // ---------------- 2. replay [0, L) in shared memory
             int t_exec = Lrun, moves = 0;  // (then: the window's moves)
             {
-                // per entry: vertex, k | len << 16, dx | right << 16 | up << 17 | start << 24, move base
-                int cur_v[EPT], lk[EPT], base[EPT], to[EPT];
-                unsigned gm[EPT];
+                // per entry: vertex, claimed vertex, and its batch times in
+                // the window: start | end << 8 | turn << 16 | right << 24 | up << 25
+                // (it moves in batches [start, end), horizontally before
+                // `turn`); slots past the list are skipped a warp at a time
+                int cur_v[EPT], to[EPT];
+                unsigned pk[EPT];
+                const int wb = tid & ~31;
+                const int nsl = Rw > wb ? min(EPT, (Rw - wb + WT - 1) / WT) : 0;
 #pragma unroll
                 for (int i = 0; i < EPT; ++i) {
                     const int e = tid + i * WT;
-                    lk[i] = 0;  // k = len = 0: never active
-                    cur_v[i] = gm[i] = base[i] = to[i] = 0;
+                    cur_v[i] = to[i] = 0;
+                    pk[i] = 0;  // start = end = 0: never active
                     if (e < Rw) {
                         const int4 r = A.rec[e];
                         const int xs = r.z & 0xffff, ys = r.z >> 16, xt = r.w & 0xffff, yt = r.w >> 16;
-                        lk[i] = r.y;
-                        gm[i] = (unsigned)abs(xt - xs) | (unsigned)(xt > xs) << 16 | (unsigned)(yt > ys) << 17 |
-                                (unsigned)A.st[e] << 24;
-                        cur_v[i] = wvtx(H, r.y & 0xffff, xs, ys, xt, yt);
-                        base[i] = A.base[e];
+                        const int k = r.y & 0xffff, len = r.y >> 16, s0 = A.st[e];
+                        const int en = min(s0 + len - k, 255), tt = min(s0 + max(abs(xt - xs) - k, 0), 255);
+                        pk[i] = (unsigned)s0 | (unsigned)en << 8 | (unsigned)tt << 16 | (unsigned)(xt > xs) << 24 |
+                                (unsigned)(yt > ys) << 25;
+                        cur_v[i] = wvtx(H, k, xs, ys, xt, yt);
                     }
                 }
+                // One barrier per batch: batch t's vacated vertices are
+                // released in the same phase as batch t+1's claims, so a claim
+                // can find a vertex still held by an entry that left it in t
+                // (an entry following another, rare: ~1e-4 of the moves).
+                // Such failures get a second chance after the barrier, when
+                // every release of t is done; only a claim that fails again
+                // (occupied before the batch, or claimed twice) is a stall.
+                unsigned pend = 0;  // entries that moved in the previous batch
                 for (int t = 0; t < Lrun; ++t) {
                     bool fail = false;
-                    unsigned claimed = 0;
+                    unsigned claimed = 0, act = 0;
+#pragma unroll
+                    for (int i = 0; i < EPT; ++i)
+                        if (pend >> i & 1u) {
+                            atomicAnd(&occ[cur_v[i] >> 5], ~(1u << (cur_v[i] & 31)));
+                            cur_v[i] = to[i];
+                        }
 #pragma unroll
                     for (int i = 0; i < EPT; ++i) {
-                        const int k = lk[i] & 0xffff;
-                        if ((int)(gm[i] >> 24) <= t && k < (lk[i] >> 16)) {
-                            const int step = k < (int)(gm[i] & 0xffffu) ? ((gm[i] >> 16 & 1u) ? H : -H) : ((gm[i] >> 17 & 1u) ? 1 : -1);
+                        if (i >= nsl) break;
+                        if ((int)(pk[i] & 0xffu) <= t && t < (int)(pk[i] >> 8 & 0xffu)) {
+                            act |= 1u << i;
+                            const int step = t < (int)(pk[i] >> 16 & 0xffu) ? ((pk[i] >> 24 & 1u) ? H : -H)
+                                                                             : ((pk[i] >> 25 & 1u) ? 1 : -1);
                             to[i] = cur_v[i] + step;
                             const uint32_t bit = 1u << (to[i] & 31);
                             if (atomicOr(&occ[to[i] >> 5], bit) & bit)
@@ -569,34 +590,44 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
                         }
                     }
                     if (__syncthreads_or(fail)) {
-                        // a stall at t: t is not applied (its claims are undone)
+                        fail = false;
 #pragma unroll
                         for (int i = 0; i < EPT; ++i)
-                            if (claimed >> i & 1u) atomicAnd(&occ[to[i] >> 5], ~(1u << (to[i] & 31)));
-                        t_exec = t;
-                        break;
-                    }
+                            if ((act & ~claimed) >> i & 1u) {
+                                const uint32_t bit = 1u << (to[i] & 31);
+                                if (atomicOr(&occ[to[i] >> 5], bit) & bit)
+                                    fail = true;
+                                else
+                                    claimed |= 1u << i;
+                            }
+                        if (__syncthreads_or(fail)) {
+                            // a stall at t: t is not applied (its claims are undone)
 #pragma unroll
-                    for (int i = 0; i < EPT; ++i)
-                        if (claimed >> i & 1u) {
-                            atomicAnd(&occ[cur_v[i] >> 5], ~(1u << (cur_v[i] & 31)));
-                            cur_v[i] = to[i];
-                            ++lk[i];
-                            ++moves;
+                            for (int i = 0; i < EPT; ++i)
+                                if (claimed >> i & 1u) atomicAnd(&occ[to[i] >> 5], ~(1u << (to[i] & 31)));
+                            t_exec = t;
+                            claimed = 0;
                         }
-                    __syncthreads();
+                    }
+                    pend = claimed;
+                    if (t_exec == t) break;
                 }
-                // the window's schedule: an entry moved in consecutive batches
-                // from its start offset on, so its moves are one run of
-                // consecutive slots and batch indices, stored 16 bytes at a
-                // time where aligned
+#pragma unroll
+                for (int i = 0; i < EPT; ++i)
+                    if (pend >> i & 1u) atomicAnd(&occ[cur_v[i] >> 5], ~(1u << (cur_v[i] & 31)));
+                // each entry moved in every batch of [start, min(end, t_exec));
+                // the window's schedule: its moves are one run of consecutive
+                // slots and batch indices, stored 16 bytes at a time where aligned
+                int moved[EPT];
 #pragma unroll
                 for (int i = 0; i < EPT; ++i) {
                     const int e = tid + i * WT;
+                    moved[i] = max(0, min(t_exec, (int)(pk[i] >> 8 & 0xffu)) - (int)(pk[i] & 0xffu));
+                    moves += moved[i];
                     if (e >= Rw) continue;
                     const int klo = A.rec[e].y & 0xffff;
-                    const int n = (lk[i] & 0xffff) - klo, b0 = nb + (int)(gm[i] >> 24);
-                    int32_t *d = mb + base[i] + klo;
+                    const int n = moved[i], b0 = nb + (int)(pk[i] & 0xffu);
+                    int32_t *d = mb + A.base[e] + klo;
                     int j = 0;
                     for (; j < n && ((uintptr_t)(d + j) & 15u); ++j) __stcs(d + j, b0 + j);
                     for (; j + 4 <= n; j += 4)
@@ -620,21 +651,24 @@ __global__ void __launch_bounds__(WT, 2) batch_window_kernel(PipelineArgs a, int
 #pragma unroll
                 for (int i = 0; i < EPT; ++i) {
                     const int e = tid + i * WT;
-                    const bool keep = e < Rw && (lk[i] & 0xffff) < (lk[i] >> 16) && (int)(gm[i] >> 24) <= t_exec;
+                    int4 r = make_int4(0, 0, 0, 0);
+                    if (e < Rw) {
+                        r = A.rec[e];
+                        r.y += moved[i];
+                    }
+                    const bool keep = e < Rw && (r.y & 0xffff) < (r.y >> 16) && (int)(pk[i] & 0xffu) <= t_exec;
                     const unsigned km = __ballot_sync(FULL, keep);
                     int kb = 0;
                     if (lane == 0 && km) kb = atomicAdd(&s_cnt, __popc(km));
                     kb = __shfl_sync(FULL, kb, 0);
                     if (keep) {
-                        int4 r = A.rec[e];
-                        r.y = lk[i];
                         const int j = kb + __popc(km & lanemask_lt());
                         B.rec[j] = r;
-                        B.base[j] = base[i];
+                        B.base[j] = A.base[e];
                         B.st[j] = 0;
                         // a finisher of the next window (if L holds): its successor
                         // range's record into L2 for the plan's first load
-                        if ((lk[i] >> 16) - (lk[i] & 0xffff) <= L) {
+                        if ((r.y >> 16) - (r.y & 0xffff) <= L) {
                             asm volatile("prefetch.global.L2 [%0];" ::"l"(prec + r.x));
                             if (slen) asm volatile("prefetch.global.L2 [%0];" ::"l"(slen + r.x));
                         }
