@@ -2553,7 +2553,10 @@ cudaError_t pipeline_run_batching(const PipelineArgs &a, int sms, cudaStream_t s
         const int32_t *mc = a.source_of, *mr = a.source_of + (size_t)a.count * a.W * a.H * 4;
         // lanes per path of the walk (RECON_WALK_LANES: 32 = a warp per path;
         // C5 walk time at 256 instances, ms: 40.8 / 32.8 / 28.0 / 26.0 / 27.3 /
-        // 30.0 for 32 / 16 / 8 / 4 / 2 / 1)
+        // 30.0 for 32 / 16 / 8 / 4 / 2 / 1; a lane-per-path walk whose lanes
+        // take a new path as soon as their route ends, without shuffles:
+        // 37.8 vs 26.0 ms for the 4-lane walk, its per-lane map reads touch a
+        // line each)
         static const int lanes_env = [] {
             const char *e = getenv("RECON_WALK_LANES");
             return e ? atoi(e) : 4;
