@@ -27,7 +27,9 @@ __global__ void copy_i32(int64_t n, const int32_t *a, int32_t *b) {
         b[i] = a[i];
 }
 
-recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb) {
+// solved != NULL: recorded on the context stream once the solve's outputs
+// (paths, counts, displacements) are final, before the DAG and batching
+recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, cudaEvent_t solved = nullptr) {
     int32_t *detail = nullptr;
     if (!pb) return RECON_ERR_ARGUMENT;
     const recon_grid_batch *b = &pb->grid;
@@ -51,6 +53,7 @@ recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb) {
     c->timing = kt;
     if (st != RECON_OK) return st;
     if (pev) cudaEventRecord(pev[1], c->stream);
+    if (solved) CK(cudaEventRecord(solved, c->stream), "event");
     // 2. DAG + batching scratch
     PipelineArgs a{};
     a.count = b->count;
@@ -294,9 +297,19 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count());
         };
         stamp("start");
-        const recon_status st = pipeline_impl(ctx, &d);
+        cudaEvent_t solved = c->chunk_event();
+        if (!solved) return fail(cuda_fail(cudaErrorUnknown, "event", detail));
+        const recon_status st = pipeline_impl(ctx, &d, solved);
         if (st != RECON_OK) return fail(st);
         stamp("pipeline");
+        // the solve's outputs are final: their copies (most of the bytes, 8 B
+        // per path slot) overlap the DAG and the batching still running
+        CKF(cudaStreamWaitEvent(cs, solved, 0), "wait");
+        CKF(cudaMemcpyAsync(b->path_src + j0 * S, o.src, n * S * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        CKF(cudaMemcpyAsync(b->path_dst + j0 * S, o.dst, n * S * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        if (b->path_event) CKF(cudaMemcpyAsync(b->path_event + j0 * S, o.ev, n * S * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        CKF(cudaMemcpyAsync(b->path_count + j0, o.i32, n * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        CKF(cudaMemcpyAsync(b->total_displacement + j0, o.i64, n * 8, cudaMemcpyDeviceToHost, cs), "D2H");
         recon_schedule_runs dr{};
         if (runs) {
             dr = recon_schedule_runs{runs->run_stride, o.rs, o.rb, o.rc};
@@ -308,18 +321,13 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
         CKF(cudaMemcpyAsync(hD.data(), o.i64, n * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
         CKF(cudaStreamSynchronize(c->stream), "pipeline sub-chunk");
         stamp("runs + counts");
-        cudaEvent_t solved = c->chunk_event();
-        if (!solved) return fail(cuda_fail(cudaErrorUnknown, "event", detail));
-        CKF(cudaEventRecord(solved, c->stream), "event");
-        CKF(cudaStreamWaitEvent(cs, solved, 0), "wait");
-        CKF(cudaMemcpyAsync(b->path_src + j0 * S, o.src, n * S * 4, cudaMemcpyDeviceToHost, cs), "D2H");
-        CKF(cudaMemcpyAsync(b->path_dst + j0 * S, o.dst, n * S * 4, cudaMemcpyDeviceToHost, cs), "D2H");
-        if (b->path_event) CKF(cudaMemcpyAsync(b->path_event + j0 * S, o.ev, n * S * 4, cudaMemcpyDeviceToHost, cs), "D2H");
-        CKF(cudaMemcpyAsync(b->path_count + j0, o.i32, n * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        cudaEvent_t batched = c->chunk_event();
+        if (!batched) return fail(cuda_fail(cudaErrorUnknown, "event", detail));
+        CKF(cudaEventRecord(batched, c->stream), "event");
+        CKF(cudaStreamWaitEvent(cs, batched, 0), "wait");
         CKF(cudaMemcpyAsync(b->status + j0, o.i32 + n, n * 4, cudaMemcpyDeviceToHost, cs), "D2H");
         if (b->detail) CKF(cudaMemcpyAsync(b->detail + j0, o.i32 + 2 * n, n * 4, cudaMemcpyDeviceToHost, cs), "D2H");
         CKF(cudaMemcpyAsync(pb->batch_count + j0, o.i32 + 3 * n, n * 4, cudaMemcpyDeviceToHost, cs), "D2H");
-        CKF(cudaMemcpyAsync(b->total_displacement + j0, o.i64, n * 8, cudaMemcpyDeviceToHost, cs), "D2H");
         for (size_t i = 0; i < n && pb->move_batch; ++i) {
             const int64_t D = std::min<int64_t>(std::max<int64_t>(hD[i], 0), pb->move_stride);
             if (D > 0)
