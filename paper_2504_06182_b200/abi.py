@@ -686,17 +686,27 @@ class ReconLib:
         return st
 
     def pipeline_batch_runs(self, solver: str, occ, count, width, height, h_prime, preset, move_stride,
-                            run_stride=None):
+                            run_stride=None, pinned=False):
         """recon_pipeline_batch_run_host_runs: the pipeline_batch outputs with the
-        schedule as runs (run_slot, run_batch, run_count) instead of move_batch."""
+        schedule as runs (run_slot, run_batch, run_count) instead of move_batch.
+        pinned: the run arrays in page-locked memory (torch), which the library
+        writes from the device instead of copying."""
         stride = width * h_prime
         run_stride = run_stride or stride + 4096
+        if pinned:
+            import torch
+            keep = torch.zeros(2 * count * run_stride, dtype=torch.int32).pin_memory()
+            both = keep.numpy()
+            run_slot, run_batch = both[:count * run_stride], both[count * run_stride:]
+        else:
+            keep = None
+            run_slot, run_batch = np.zeros(count * run_stride, np.int32), np.zeros(count * run_stride, np.int32)
         out = {
             "path_src": np.zeros(count * stride, np.int32), "path_dst": np.zeros(count * stride, np.int32),
             "path_count": np.zeros(count, np.int32), "total_displacement": np.zeros(count, np.int64),
             "status": np.zeros(count, np.int32), "detail": np.zeros(count, np.int32),
-            "batch_count": np.zeros(count, np.int32), "run_slot": np.zeros(count * run_stride, np.int32),
-            "run_batch": np.zeros(count * run_stride, np.int32), "run_count": np.zeros(count, np.int64),
+            "batch_count": np.zeros(count, np.int32), "run_slot": run_slot,
+            "run_batch": run_batch, "run_count": np.zeros(count, np.int64),
         }
         occ = np.ascontiguousarray(occ, np.uint64)
         g = GridBatch(_vp(occ).value, count, width, height, h_prime, _vp(out["path_src"]).value,
@@ -708,6 +718,7 @@ class ReconLib:
         st = self.lib.recon_pipeline_batch_run_host_runs(self.ctx(), C.byref(pb), C.byref(runs))
         self._check(st, 0)
         out["run_stride"] = run_stride
+        out["_pinned"] = keep
         return out
 
     def pipeline_batch(self, solver: str, occ, count, width, height, h_prime, preset, move_stride):

@@ -27,6 +27,32 @@ __global__ void copy_i32(int64_t n, const int32_t *a, int32_t *b) {
         b[i] = a[i];
 }
 
+// every instance's runs [0, min(count, stride)) straight into the caller's
+// page-locked host arrays (device-mapped): one launch instead of two copies
+// per instance; a CTA per instance, coalesced writes over the host link
+__global__ void runs_to_host_kernel(int64_t n, int64_t rst, const int64_t *rc, const int32_t *rs, const int32_t *rb,
+                                    int32_t *hs, int32_t *hb) {
+    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const int64_t R = min(rc[i], rst);
+        const int32_t *s = rs + i * rst, *b = rb + i * rst;
+        int32_t *ds = hs + i * rst, *db = hb + i * rst;
+        for (int64_t j = threadIdx.x; j < R; j += blockDim.x) {
+            ds[j] = s[j];
+            db[j] = b[j];
+        }
+    }
+}
+
+// the device view of a page-locked, device-mapped host pointer (else NULL)
+void *mapped_host(void *p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
 // solved != NULL: recorded on the context stream once the solve's outputs
 // (paths, counts, displacements) are final, before the DAG and batching
 recon_status pipeline_impl(recon_ctx *ctx, const recon_pipeline_batch *pb, cudaEvent_t solved = nullptr) {
@@ -257,6 +283,9 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
         }
     }
     std::vector<int64_t> hD(sub), hR(sub);
+    // page-locked, device-mapped run arrays: written by a kernel, not copied
+    int32_t *hs_map = runs ? static_cast<int32_t *>(mapped_host(runs->run_slot)) : nullptr;
+    int32_t *hb_map = runs ? static_cast<int32_t *>(mapped_host(runs->run_batch)) : nullptr;
     bool over = false;  // some instance had more runs than run_stride
     // on any failure after copies were issued: drain both streams before returning
     auto fail = [&](recon_status st) {
@@ -338,8 +367,14 @@ recon_status pipeline_host_chunked(recon_ctx *ctx, const recon_pipeline_batch *p
         if (runs) {
             const size_t rst = (size_t)runs->run_stride;
             CKF(cudaMemcpyAsync(runs->run_count + j0, o.rc, n * 8, cudaMemcpyDeviceToHost, cs), "D2H");
-            for (size_t i = 0; i < n; ++i) {
-                over |= hR[i] > runs->run_stride;
+            for (size_t i = 0; i < n; ++i) over |= hR[i] > runs->run_stride;
+            if (hs_map && hb_map) {
+                runs_to_host_kernel<<<(int)std::min<size_t>(n, (size_t)c->sms * 8), 256, 0, cs>>>(
+                    (int64_t)n, (int64_t)rst, o.rc, o.rs, o.rb, hs_map + j0 * rst, hb_map + j0 * rst);
+                CKF(cudaGetLastError(), "runs to host");
+                ++c->launches;
+            }
+            for (size_t i = 0; i < n && !(hs_map && hb_map); ++i) {
                 const int64_t R = std::min<int64_t>(hR[i], runs->run_stride);
                 if (R <= 0) continue;
                 CKF(cudaMemcpyAsync(runs->run_slot + (j0 + i) * rst, o.rs + i * rst, (size_t)R * 4,

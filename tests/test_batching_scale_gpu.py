@@ -140,6 +140,11 @@ def test_schedule_runs_device_equals_oracle(gpu, oracle):
             g = gpu.pipeline_batch_runs(wl.solver, occ, n, wl.W, wl.H, wl.h_prime, preset, wl.move_stride)
             o = oracle.pipeline_batch_runs(wl.solver, occ, n, wl.W, wl.H, wl.h_prime, preset, wl.move_stride)
             assert np.array_equal(g["run_count"], o["run_count"]) and np.array_equal(g["status"], o["status"])
+            if wl is C3 and preset == 0:  # page-locked run arrays: written by runs_to_host_kernel, not copied
+                p = gpu.pipeline_batch_runs(wl.solver, occ, n, wl.W, wl.H, wl.h_prime, preset, wl.move_stride,
+                                            pinned=True)
+                assert np.array_equal(p["run_count"], g["run_count"])
+                assert np.array_equal(p["run_slot"], g["run_slot"]) and np.array_equal(p["run_batch"], g["run_batch"])
             rs = g["run_stride"]
             for i in range(n):
                 k = int(g["run_count"][i])
