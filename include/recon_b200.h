@@ -389,7 +389,9 @@ typedef struct recon_schedule_runs {
 recon_status recon_pipeline_schedule_runs(recon_ctx *ctx, const recon_pipeline_batch *batch, recon_schedule_runs *runs);
 /* recon_pipeline_batch_run_host returning the schedule as runs (host pointers;
  * batch->move_batch may be NULL): the host link carries ~P runs instead of D
- * batch indices per instance. */
+ * batch indices per instance.  Page-locked, device-mapped run_slot/run_batch
+ * arrays (cudaHostAlloc, torch pin_memory) are written by a kernel over the host
+ * link; other host memory is filled with one copy per instance and array. */
 recon_status recon_pipeline_batch_run_host_runs(recon_ctx *ctx, const recon_pipeline_batch *batch,
                                                 recon_schedule_runs *runs);
 
