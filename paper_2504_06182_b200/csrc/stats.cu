@@ -91,57 +91,78 @@ __global__ void __launch_bounds__(ST) pipeline_stats_kernel(recon_pipeline_batch
 }
 
 // ---- run-length schedule: one CTA per instance, RI consecutive moves per
-// thread, a run starts where the batch index does not continue the previous
-// move's (+1); a block scan over the run-start counts places the runs
-constexpr int RI = 8;
+// thread (two 16-byte loads, the next tile's issued before this tile's scan),
+// a run starts where the batch index does not continue the previous move's
+// (+1); a block scan over the run-start counts places the runs (one barrier
+// per tile: the warp totals are double-buffered).  HBM-bound: 4 B read per
+// move (C5: 54 GB per 1,536-instance chunk)
+constexpr int RI = 8, RT = 1024;
 
-__global__ void __launch_bounds__(ST) schedule_runs_kernel(recon_pipeline_batch pb, recon_schedule_runs runs) {
-    __shared__ int wsum[ST / 32];
-    __shared__ long long s_base;
+// v = p[j, j + RI) (0 past D); 16-byte loads while inside [0, lim)
+__device__ __forceinline__ void load8(const int32_t *p, int64_t j, int64_t lim, int64_t D, int32_t *v) {
+    if (j + RI <= lim) {
+        const int4 x = __ldcs(reinterpret_cast<const int4 *>(p + j));
+        const int4 y = __ldcs(reinterpret_cast<const int4 *>(p + j + 4));
+        v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w, v[4] = y.x, v[5] = y.y, v[6] = y.z, v[7] = y.w;
+    } else {
+#pragma unroll
+        for (int i = 0; i < RI; ++i) v[i] = j + i < D ? p[j + i] : 0;
+    }
+}
+
+__global__ void __launch_bounds__(RT, 2) schedule_runs_kernel(recon_pipeline_batch pb, recon_schedule_runs runs) {
+    __shared__ int wsum[2][RT / 32];
     const recon_grid_batch &g = pb.grid;
     const int lane = lane_id(), warp = warp_id();
+    constexpr int64_t TILE = (int64_t)RT * RI;
     for (int inst = blockIdx.x; inst < g.count; inst += gridDim.x) {
         const int64_t D = g.status[inst] == RECON_OK ? g.total_displacement[inst] : 0;
         const int32_t *mb = pb.move_batch + inst * pb.move_stride;
         int32_t *rs = runs.run_slot + inst * runs.run_stride, *rb = runs.run_batch + inst * runs.run_stride;
-        if (threadIdx.x == 0) s_base = 0;
-        __syncthreads();
-        for (int64_t t0 = 0; t0 < D; t0 += (int64_t)ST * RI) {
+        // (vector loads only when aligned, and inside the instance's move_stride;
+        // moves past D are masked)
+        const int64_t ms4 = pb.move_stride - (pb.move_stride & 3);
+        const int64_t lim = ((uintptr_t)mb & 15u) == 0 && ms4 >= D ? ms4 : -1;
+        int64_t base = 0;
+        int32_t nx[RI];
+        if (D > 0) load8(mb, (int64_t)threadIdx.x * RI, lim, D, nx);
+        int par = 0;
+        for (int64_t t0 = 0; t0 < D; t0 += TILE, par ^= 1) {
             const int64_t j0 = t0 + (int64_t)threadIdx.x * RI;
-            int32_t v[RI + 1];
-            v[0] = (j0 > 0 && j0 - 1 < D) ? __ldcs(mb + j0 - 1) : INT_MIN;
+            int32_t v[RI];
 #pragma unroll
-            for (int i = 0; i < RI; ++i) v[i + 1] = j0 + i < D ? __ldcs(mb + j0 + i) : 0;
+            for (int i = 0; i < RI; ++i) v[i] = nx[i];
+            if (t0 + TILE < D) load8(mb, j0 + TILE, lim, D, nx);
+            // the move before this thread's first: the lane below's last, or
+            // (lane 0) the previous warp's / tile's, loaded
+            int32_t pv = __shfl_up_sync(FULL, v[RI - 1], 1);
+            if (lane == 0) pv = (j0 > 0 && j0 - 1 < D) ? mb[j0 - 1] : INT_MIN;
             unsigned starts = 0;
 #pragma unroll
-            for (int i = 0; i < RI; ++i)
-                if (j0 + i < D && (j0 + i == 0 || v[i + 1] != v[i] + 1)) starts |= 1u << i;
-            const int cnt = __popc(starts);
-            int tot;
-            int ex = warp_excl_scan(cnt, &tot);
-            if (lane == 0) wsum[warp] = tot;
-            __syncthreads();
-            int before = 0, all = 0;
-#pragma unroll
-            for (int w = 0; w < ST / 32; ++w) {
-                before += w < warp ? wsum[w] : 0;
-                all += wsum[w];
+            for (int i = 0; i < RI; ++i) {
+                const int32_t prev = i == 0 ? pv : v[i - 1];
+                if (j0 + i < D && (j0 + i == 0 || v[i] != prev + 1)) starts |= 1u << i;
             }
-            int64_t at = s_base + before + ex;
+            int tot;
+            const int ex = warp_excl_scan(__popc(starts), &tot);
+            if (lane == 0) wsum[par][warp] = tot;
+            __syncthreads();
+            int wt;
+            const int wex = warp_excl_scan(wsum[par][lane], &wt);  // (RT / 32 == 32 warps)
+            int64_t at = base + __shfl_sync(FULL, wex, warp) + ex;
+#pragma unroll
             for (int i = 0; i < RI; ++i)
                 if ((starts >> i) & 1u) {
                     if (at < runs.run_stride) {
                         rs[at] = (int32_t)(j0 + i);
-                        rb[at] = v[i + 1];
+                        rb[at] = v[i];
                     }
                     ++at;
                 }
-            __syncthreads();
-            if (threadIdx.x == 0) s_base += all;
-            __syncthreads();
+            base += wt;
         }
-        if (threadIdx.x == 0) runs.run_count[inst] = s_base;
-        __syncthreads();
+        if (threadIdx.x == 0) runs.run_count[inst] = base;
+        __syncthreads();  // (wsum of this instance's last tiles)
     }
 }
 
@@ -151,8 +172,8 @@ namespace rb {
 // enqueues the run extraction of a device pipeline batch on `st`
 cudaError_t launch_schedule_runs(const recon_pipeline_batch &pb, const recon_schedule_runs &runs, int sms,
                                  cudaStream_t st) {
-    const int grid = pb.grid.count < sms * 8 ? pb.grid.count : sms * 8;
-    schedule_runs_kernel<<<grid, ST, 0, st>>>(pb, runs);
+    const int grid = pb.grid.count < sms * 2 ? pb.grid.count : sms * 2;
+    schedule_runs_kernel<<<grid, RT, 0, st>>>(pb, runs);
     return cudaGetLastError();
 }
 }  // namespace rb
